@@ -1,0 +1,4 @@
+// Reference-compatible include path: gpuos/metrics.hpp. Declarations live in the
+// B200 library's grouped headers listed below.
+#pragma once
+#include "gpuos/scenario.hpp"

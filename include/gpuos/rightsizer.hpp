@@ -1,0 +1,4 @@
+// Reference-compatible include path: gpuos/rightsizer.hpp. Declarations live in the
+// B200 library's grouped headers listed below.
+#pragma once
+#include "gpuos/policy.hpp"
