@@ -1,0 +1,156 @@
+/*
+ * gpuos_dev.h — C ABI of the B200 TPC dispatcher (the device seam).
+ *
+ * The reference's scheduler drives a concrete C++ DeviceEngine
+ * (reference: proj/include/gpuos/device.hpp:79-121). On the B200 that seam
+ * becomes a persistent sm_100a dispatcher kernel; this header is the thin,
+ * language-neutral boundary a host scheduler (the gpuos:: C++ library in
+ * this repo, or any FFI) binds to. Plain pointers and sizes only; every
+ * function returns 0 on success or a negative GPUOS_E_* code and never
+ * throws. The mapping to the reference seam (file:line in
+ * proj/include/gpuos/device.hpp / proj/src/device.cpp):
+ *
+ *   gpuos_dev_open / _close        DeviceEngine ctor/dtor      device.hpp:81, device.cpp:74-81
+ *   gpuos_dev_get_topology         topology()                  device.hpp:84
+ *   gpuos_dev_submit_atom          submit_atom()               device.hpp:92-94, device.cpp:121-163
+ *   gpuos_dev_set_atom_paused      set_atom_paused()           device.hpp:97, device.cpp:165-171
+ *   gpuos_dev_poll                 completion handler / step() device.hpp:102-107, device.cpp:208-219,277-306
+ *   gpuos_dev_now_ns               now()                       device.hpp:83
+ *   gpuos_dev_set_tpc_fence        (new) TPC-ownership table: block-granular revocation
+ *   gpuos_dev_start / _stop        (new) persistent-kernel lifetime, CUDA-event timing
+ *   gpuos_dev_get_stats            tpc_busy_integral() etc.    device.hpp:112-118
+ *
+ * Threading: one host thread owns a handle (reference: device.hpp:76-78,
+ * SPEC.md:111-112). The persistent kernel is the only concurrent actor.
+ */
+#ifndef GPUOS_DEV_H_
+#define GPUOS_DEV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+#define GPUOS_OK 0
+#define GPUOS_E_CONFIG (-2)    /* bad argument; maps to gpuos::ConfigError   */
+#define GPUOS_E_INVARIANT (-3) /* internal state violated; InvariantError    */
+#define GPUOS_E_CUDA (-4)      /* CUDA runtime failure; InvariantError       */
+#define GPUOS_E_FULL (-5)      /* ring / atom table / TPC residency full      */
+#define GPUOS_E_STATE (-6)     /* call not valid in the current state         */
+#define GPUOS_E_TIMEOUT (-7)
+
+/* ------------------------------------------------------------------ limits */
+#define GPUOS_MAX_TPCS 128     /* logical TPC ids are < 128 (two 64-bit words) */
+#define GPUOS_RESIDENT_PER_TPC 32
+
+/* ------------------------------------------------------------ body kinds */
+/* What one block of an atom executes (args per kind).                     */
+#define GPUOS_BODY_STREAM 1u  /* args: src u32*, dst u32*, words/block (mult.
+                                 of 4, 16 B aligned), salt, chunks (0 = none)
+                                 block b covers chunk c = chunks ? b % chunks : b:
+                                 dst[i] = (src[i] ^ salt) * 0x9E3779B1 + i
+                                 for i in [c * words, (c + 1) * words)       */
+#define GPUOS_BODY_GEMM_BF16 2u /* args: A bf16 [M,K], B bf16 [N,K], C bf16
+                                   [M,N] row-major, M|N|K packed (see b200.hpp) */
+#define GPUOS_BODY_SPIN 3u    /* args: ns to spin per block (globaltimer)    */
+
+/* Launch-time configuration. Zero fields take the defaults in brackets.   */
+typedef struct gpuos_dev_config {
+  int32_t device_ordinal;   /* [0] */
+  int32_t workers_per_sm;   /* resident worker CTAs per SM [2]            */
+  int32_t logical_tpcs;     /* TPCs exposed, mapped onto physical TPCs
+                               0..n-1 (smid>>1) [all = 74 on B200]        */
+  int32_t atom_slots;       /* in-flight atom table size [4096]           */
+  int32_t ring_entries;     /* host->device submit ring [4096]            */
+  int32_t idle_sleep_ns;    /* worker back-off while idle [256]           */
+  uint32_t flags;           /* reserved, 0                                */
+  int32_t reserved;
+} gpuos_dev_config;
+
+typedef struct gpuos_dev_topology {
+  int32_t sm_count;          /* physical SMs (148 on B200)                */
+  int32_t physical_tpcs;     /* sm_count / 2                              */
+  int32_t logical_tpcs;      /* TPC ids accepted by submit_atom           */
+  int32_t workers_per_sm;
+  int32_t workers_per_tpc;   /* resident worker CTAs per logical TPC      */
+  int32_t threads_per_worker;
+  int32_t smem_per_worker;   /* bytes of dynamic shared memory            */
+  int32_t reserved;
+} gpuos_dev_topology;
+
+/* One atom: a contiguous block range [lo, hi) of a tenant kernel, bound to
+ * a TPC set at a priority (reference: submit_atom, device.cpp:121-163).    */
+typedef struct gpuos_atom_desc {
+  int64_t lo, hi;            /* block range, 0 <= lo < hi                   */
+  uint64_t tpc_mask[2];      /* logical TPC set, bit t of word t/64         */
+  int32_t priority;          /* higher wins freed slots (30 HP, 20 BE, 10
+                                stolen); clamped to [0, 254]                */
+  uint32_t body;             /* GPUOS_BODY_*                                */
+  uint64_t args[5];          /* body arguments                              */
+  uint64_t tag;              /* caller cookie, echoed in the completion     */
+  uint32_t* trace;           /* optional per-block execution trace, indexed
+                                by block id: += 0x10000 | (smid + 1)        */
+  int32_t atomized;          /* informational (the prelude is free on B200) */
+  int32_t reserved;
+} gpuos_atom_desc;
+
+typedef struct gpuos_completion {
+  uint32_t atom_id;          /* id returned by gpuos_dev_submit_atom        */
+  uint32_t blocks;           /* blocks executed                             */
+  uint64_t tag;
+  int64_t host_submit_ns;    /* gpuos_dev_now_ns() at submit                */
+  int64_t host_complete_ns;  /* gpuos_dev_now_ns() when polled              */
+  int64_t dev_first_start_ns;/* first block start, device clock, relative to open */
+  int64_t dev_last_end_ns;   /* last block end, same clock                  */
+  uint64_t tpc_touched[2];   /* logical TPCs that ran at least one block    */
+} gpuos_completion;
+
+typedef struct gpuos_dev_stats {
+  uint64_t blocks_executed;
+  uint64_t atoms_completed;
+  uint64_t worker_busy_ns;   /* summed block time over all workers          */
+  uint64_t claim_retries;    /* lost CAS races on block claims              */
+  int64_t kernel_elapsed_ns; /* CUDA-event time of the last start..stop     */
+  int64_t ingest_entries;    /* ring entries consumed by the device         */
+} gpuos_dev_stats;
+
+int gpuos_dev_open(const gpuos_dev_config* cfg, struct gpuos_dev** out);
+int gpuos_dev_close(struct gpuos_dev* dev);
+int gpuos_dev_get_topology(struct gpuos_dev* dev, gpuos_dev_topology* out);
+
+/* Launch the persistent dispatcher (ingest + worker kernels). */
+int gpuos_dev_start(struct gpuos_dev* dev);
+/* drain != 0: wait until every submitted atom completed, then stop.
+ * Returns the worker kernel's CUDA-event elapsed time in *elapsed_ms.       */
+int gpuos_dev_stop(struct gpuos_dev* dev, int drain, float* elapsed_ms);
+
+int gpuos_dev_submit_atom(struct gpuos_dev* dev, const gpuos_atom_desc* desc,
+                          uint32_t* atom_id);
+int gpuos_dev_set_atom_paused(struct gpuos_dev* dev, uint32_t atom_id,
+                              int paused);
+/* Blocks of atoms below min_priority stop starting on `tpc` (0 lifts). */
+int gpuos_dev_set_tpc_fence(struct gpuos_dev* dev, int32_t tpc,
+                            int32_t min_priority);
+/* Non-blocking; returns the number of completions written to out[0..max). */
+int gpuos_dev_poll(struct gpuos_dev* dev, gpuos_completion* out, int32_t max);
+int64_t gpuos_dev_now_ns(struct gpuos_dev* dev);
+int32_t gpuos_dev_in_flight(struct gpuos_dev* dev);
+int gpuos_dev_get_stats(struct gpuos_dev* dev, gpuos_dev_stats* out);
+
+/* Device memory helpers (stream-ordered on a side stream: safe while the
+ * persistent dispatcher runs; never synchronise the whole device).        */
+int gpuos_dev_alloc(struct gpuos_dev* dev, uint64_t bytes, void** ptr);
+int gpuos_dev_free(struct gpuos_dev* dev, void* ptr);
+int gpuos_dev_copy(struct gpuos_dev* dev, void* dst, const void* src,
+                   uint64_t bytes, int kind /* 1 H2D, 2 D2H, 3 D2D */);
+int gpuos_dev_memset(struct gpuos_dev* dev, void* dst, int value, uint64_t bytes);
+
+const char* gpuos_dev_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GPUOS_DEV_H_ */

@@ -1,0 +1,920 @@
+// Persistent sm_100a TPC dispatcher and its C ABI (include/gpuos_dev.h).
+//
+// The reference's DeviceEngine (device.cpp:74-311) models a GPU as a pool of
+// TPCs whose block slots refill from the highest-priority resident atom.
+// Here that model is executed for real:
+//
+//   host scheduler --submit ring (pinned, mapped)--> INGEST warp (1 CTA)
+//        ^                                              | writes atom slot,
+//        |                                              v inserts resident keys
+//   completion ring <--last block-- WORKER CTAs (W per SM, 148 SMs)
+//
+// * Every worker CTA reads %smid; TPC = smid >> 1 (2-CTA clusters always land
+//   on SMs {2k, 2k+1}: profiles/topology_probe_r01.json) and maps it to a
+//   logical TPC id through a device table.
+// * Each logical TPC owns a 32-entry resident list of 64-bit keys
+//   (priority << 56 | ~seq << 24 | slot). Warp 0 of a free worker reads the
+//   list (one entry per lane), keeps the atoms that still have waiting
+//   blocks, are not paused and clear the TPC's fence, and takes the maximum
+//   key: highest priority, then oldest atom -- the reference's refill rule
+//   (device.cpp:188-206). There is no lower-priority bypass: a lane-parallel
+//   max over eligible atoms picks exactly one.
+// * Lane 0 claims a block with a CAS on the atom's claim word
+//   (seq << 32 | next offset); the sequence tag makes a stale key for a
+//   recycled slot fail the CAS instead of stealing a block.
+// * All 8 warps run the body; warp 0 then accounts the block and, for the
+//   atom's last block, removes its resident keys and writes the completion
+//   record (device timestamps, TPCs touched) into host-mapped memory.
+// * Block-granular revocation: fence[tpc] is a minimum priority; raising it
+//   stops stolen atoms from starting new blocks there without a relaunch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <memory>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "bodies.cuh"
+#include "gpuos_dev.h"
+#include "ptx.cuh"
+
+namespace gpuos_dev_impl {
+
+constexpr int kResident = GPUOS_RESIDENT_PER_TPC;  // keys per TPC (one per lane)
+static_assert(kResident == 32, "one resident key per lane");
+
+enum Op : unsigned { kOpSubmit = 1, kOpPause = 2, kOpResume = 3, kOpFence = 4,
+                     kOpDrain = 5, kOpShutdown = 6 };
+
+// Device-resident atom slot. The first 32 bytes are what selecting workers
+// read; the rest is written once by the ingest warp.
+struct alignas(128) DevAtom {
+  unsigned long long claim;  // seq << 32 | next block offset
+  unsigned count;            // blocks in the atom
+  unsigned seq;
+  int prio;                  // 1..255
+  unsigned paused;
+  unsigned done;             // finished blocks
+  unsigned body;
+  long long lo;
+  unsigned atom_id;
+  unsigned pad;
+  unsigned long long args[5];
+  unsigned long long tag;
+  unsigned* trace;
+  unsigned long long mask[2];
+  unsigned long long t_first, t_last;
+  unsigned long long touched[2];
+  unsigned char entry[GPUOS_MAX_TPCS];  // resident-list index per TPC
+};
+
+struct DevCtl {
+  unsigned quit;
+  unsigned drain;
+  int outstanding;      // ingested, not yet completed
+  unsigned comp_tail;   // completion records allocated
+  unsigned long long deadline;  // globaltimer: hard stop (hang guard)
+  unsigned long long blocks, busy_ns, retries, atoms_done;
+};
+
+// 128-byte submit-ring entry: four 32-byte sectors, each = 7 data words +
+// a ticket word. The host stores every sector's data before its ticket, so
+// a sector whose ticket matches is internally consistent no matter how the
+// device read is split into PCIe requests.
+struct RingEntry {
+  unsigned w[32];
+};
+__host__ __device__ constexpr int ring_word(int d) { return (d / 7) * 8 + d % 7; }
+enum RingField : int {
+  kFOp = 0, kFSlot = 1, kFSeq = 2, kFPrio = 3, kFLo = 4 /*2*/, kFCount = 6,
+  kFBody = 7, kFMask0 = 8 /*2*/, kFMask1 = 10 /*2*/, kFAtomId = 12, kFAux = 13,
+  kFArgs = 14 /*10*/, kFTag = 24 /*2*/, kFTrace = 26 /*2*/
+};
+
+// 64-byte completion record written by the device into mapped host memory;
+// word 15 is the ticket, stored after a system-scope fence.
+struct CompRec {
+  unsigned w[16];
+};
+
+struct Params {
+  DevAtom* atoms;
+  unsigned long long* resident;  // [tpcs][32]
+  unsigned* version;             // [tpcs] bumped when a TPC's candidates change
+  int* fence;                    // [tpcs] minimum priority allowed to start
+  DevCtl* ctl;
+  const int* phys2log;           // [physical tpcs]
+  RingEntry* ring;               // mapped host memory
+  CompRec* comp;                 // mapped host memory
+  unsigned long long* consumed;  // mapped host memory
+  unsigned* alive;               // mapped host memory, one word per worker CTA
+  unsigned ring_cap;
+  unsigned comp_cap;
+  int logical_tpcs;
+  int idle_sleep_ns;
+};
+
+__device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) {
+  return static_cast<unsigned long long>(lo) | (static_cast<unsigned long long>(hi) << 32);
+}
+
+// ------------------------------------------------------------ ingest warp
+__global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
+  const unsigned lane = threadIdx.x;
+  unsigned long long head = 0;
+  for (;;) {
+    if (gtimer() > p.ctl->deadline) {
+      atomicExch(&p.ctl->quit, 1u);
+      break;
+    }
+    const RingEntry* e = p.ring + (head % p.ring_cap);
+    const unsigned w = ld_relaxed_sys(&e->w[lane]);
+    const unsigned want = static_cast<unsigned>(head + 1);
+    const bool ok = __all_sync(0xffffffffu, (lane & 7) != 7 || w == want);
+    if (!ok) {
+      __nanosleep(64);
+      continue;
+    }
+    auto get = [&](int d) { return __shfl_sync(0xffffffffu, w, ring_word(d)); };
+    const unsigned op = get(kFOp);
+    bool stop = false;
+    if (op == kOpSubmit) {
+      const unsigned slot = get(kFSlot);
+      const unsigned seq = get(kFSeq);
+      const int prio = static_cast<int>(get(kFPrio));
+      const unsigned long long mask0 = field64(get(kFMask0), get(kFMask0 + 1));
+      const unsigned long long mask1 = field64(get(kFMask1), get(kFMask1 + 1));
+      unsigned long long args[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) args[k] = field64(get(kFArgs + 2 * k), get(kFArgs + 2 * k + 1));
+      const unsigned long long tag = field64(get(kFTag), get(kFTag + 1));
+      const unsigned long long trace = field64(get(kFTrace), get(kFTrace + 1));
+      const long long lo = static_cast<long long>(field64(get(kFLo), get(kFLo + 1)));
+      const unsigned count = get(kFCount);
+      const unsigned body = get(kFBody);
+      const unsigned atom_id = get(kFAtomId);
+      DevAtom* a = p.atoms + slot;
+      if (lane == 0) {
+        // Not claimable until every resident key is in place (arming below).
+        a->claim = (static_cast<unsigned long long>(seq) << 32) | 0xffffffffull;
+        a->count = count;
+        a->seq = seq;
+        a->prio = prio;
+        a->paused = 0;
+        a->done = 0;
+        a->body = body;
+        a->lo = lo;
+        a->atom_id = atom_id;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) a->args[k] = args[k];
+        a->tag = tag;
+        a->trace = reinterpret_cast<unsigned*>(trace);
+        a->mask[0] = mask0;
+        a->mask[1] = mask1;
+        a->t_first = ~0ull;
+        a->t_last = 0;
+        a->touched[0] = 0;
+        a->touched[1] = 0;
+      }
+      __syncwarp();
+      __threadfence();
+      const unsigned long long key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
+                                     (static_cast<unsigned long long>(~seq) << 24) |
+                                     (slot & 0xffffffu);
+      for (int t = lane; t < p.logical_tpcs; t += 32) {
+        const unsigned long long m = t < 64 ? mask0 : mask1;
+        if (!((m >> (t & 63)) & 1ull)) continue;
+        unsigned long long* list = p.resident + static_cast<size_t>(t) * kResident;
+        for (;;) {  // host admission control keeps a free entry available
+          int placed = -1;
+          for (int k = 0; k < kResident; ++k) {
+            if (ld_relaxed_gpu64(list + k) == 0ull && atomicCAS(list + k, 0ull, key) == 0ull) {
+              placed = k;
+              break;
+            }
+          }
+          if (placed >= 0) {
+            a->entry[t] = static_cast<unsigned char>(placed);
+            break;
+          }
+          __nanosleep(128);
+        }
+      }
+      __syncwarp();
+      __threadfence();
+      if (lane == 0) {
+        atomicAdd(&p.ctl->outstanding, 1);
+        __threadfence();
+        atomicExch(&a->claim, static_cast<unsigned long long>(seq) << 32);  // arm
+      }
+      __syncwarp();
+      __threadfence();
+      for (int t = lane; t < p.logical_tpcs; t += 32) {
+        const unsigned long long m = t < 64 ? mask0 : mask1;
+        if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
+      }
+    } else if (op == kOpPause || op == kOpResume) {
+      DevAtom* a = p.atoms + get(kFSlot);
+      if (lane == 0) {
+        atomicExch(&a->paused, op == kOpPause ? 1u : 0u);
+        __threadfence();
+      }
+      __syncwarp();
+      if (op == kOpResume)
+        for (int t = lane; t < p.logical_tpcs; t += 32) {
+          const unsigned long long m = a->mask[t >> 6];
+          if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
+        }
+    } else if (op == kOpFence) {
+      const int t = static_cast<int>(get(kFAux));
+      if (lane == 0 && t >= 0 && t < p.logical_tpcs) {
+        atomicExch(p.fence + t, static_cast<int>(get(kFPrio)));
+        __threadfence();
+        atomicAdd(p.version + t, 1u);
+      }
+    } else if (op == kOpDrain) {
+      if (lane == 0) atomicExch(&p.ctl->drain, 1u);
+      stop = true;
+    } else if (op == kOpShutdown) {
+      if (lane == 0) atomicExch(&p.ctl->quit, 1u);
+      stop = true;
+    }
+    ++head;
+    __syncwarp();
+    if (lane == 0) st_release_sys64(p.consumed, head);
+    if (stop) break;
+  }
+}
+
+// ------------------------------------------------------------ worker CTAs
+struct WorkerShared {
+  BlockCmd cmd;
+  unsigned long long key;
+  unsigned long long t_start;
+  unsigned slot;
+  int go;
+};
+
+__global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
+  __shared__ WorkerShared sh;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const unsigned lane = tid & 31;
+  const unsigned sm = smid();
+  const int tpc = p.phys2log[sm >> 1];
+  if (tid == 0) st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 ? 0x80000000u : 0u));
+  if (tpc < 0) return;  // TPC not exposed to the scheduler
+
+  unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
+  unsigned long long n_blocks = 0, busy = 0, retries = 0;
+
+  for (;;) {
+    if (warp == 0) {
+      int go = 0;
+      for (;;) {
+        if (ld_relaxed_gpu(&p.ctl->quit)) break;
+        const unsigned ver = ld_relaxed_gpu(p.version + tpc);
+        const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
+        const unsigned long long key = ld_acquire_gpu64(list + lane);
+        bool eligible = false;
+        if (key != 0ull) {
+          const DevAtom* a = p.atoms + (key & 0xffffffull);
+          const unsigned seq = ~static_cast<unsigned>(key >> 24);
+          const unsigned long long cw = ld_relaxed_gpu64(&a->claim);
+          const int prio = static_cast<int>(key >> 56);
+          eligible = static_cast<unsigned>(cw >> 32) == seq &&
+                     static_cast<unsigned>(cw) < ld_relaxed_gpu(&a->count) &&
+                     ld_relaxed_gpu(&a->paused) == 0u && prio >= floor_prio;
+        }
+        const unsigned long long best = warp_max_u64(eligible ? key : 0ull);
+        if (best != 0ull) {
+          long long off = -1;
+          if (lane == 0) {
+            DevAtom* a = p.atoms + (best & 0xffffffull);
+            const unsigned seq = ~static_cast<unsigned>(best >> 24);
+            const unsigned count = ld_relaxed_gpu(&a->count);
+            unsigned long long cur = ld_relaxed_gpu64(&a->claim);
+            while (static_cast<unsigned>(cur >> 32) == seq &&
+                   static_cast<unsigned>(cur) < count) {
+              const unsigned long long prev = atomicCAS(&a->claim, cur, cur + 1);
+              if (prev == cur) {
+                off = static_cast<long long>(static_cast<unsigned>(cur));
+                break;
+              }
+              cur = prev;
+              ++retries;
+            }
+            if (off >= 0) {
+              __threadfence();  // acquire: see the ingest warp's slot writes
+              sh.key = best;
+              sh.slot = static_cast<unsigned>(best & 0xffffffull);
+              sh.cmd.block = a->lo + off;
+              sh.cmd.body = a->body;
+#pragma unroll
+              for (int k = 0; k < 5; ++k) sh.cmd.args[k] = a->args[k];
+              sh.t_start = gtimer();
+            }
+          }
+          off = __shfl_sync(0xffffffffu, off, 0);
+          if (off >= 0) {
+            go = 1;
+            break;
+          }
+          continue;  // lost the race for that atom's last block: reselect
+        }
+        if (ld_relaxed_gpu(&p.ctl->drain) &&
+            ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0)
+          break;
+        if (gtimer() > p.ctl->deadline) break;
+        // Idle: wait for this TPC's candidate set to change.
+        for (int k = 0; k < 64; ++k) {
+          __nanosleep(p.idle_sleep_ns);
+          if (ld_relaxed_gpu(p.version + tpc) != ver) break;
+        }
+      }
+      if (lane == 0) sh.go = go;
+    }
+    __syncthreads();
+    if (!sh.go) break;
+
+    switch (sh.cmd.body) {
+      case GPUOS_BODY_STREAM: body_stream(sh.cmd, tid); break;
+      case GPUOS_BODY_SPIN: body_spin(sh.cmd, tid); break;
+      default: break;
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+      DevAtom* a = p.atoms + sh.slot;
+      int last = 0;
+      if (lane == 0) {
+        const unsigned long long t_end = gtimer();
+        atomicMin(&a->t_first, sh.t_start);
+        atomicMax(&a->t_last, t_end);
+        atomicOr(&a->touched[tpc >> 6], 1ull << (tpc & 63));
+        if (a->trace != nullptr) atomicAdd(a->trace + sh.cmd.block, 0x10000u + sm + 1u);
+        busy += t_end - sh.t_start;
+        ++n_blocks;
+        __threadfence();
+        last = atomicAdd(&a->done, 1u) + 1u == a->count;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        const unsigned long long key = sh.key;
+        for (int t = lane; t < p.logical_tpcs; t += 32) {
+          const unsigned long long m = a->mask[t >> 6];
+          if ((m >> (t & 63)) & 1ull)
+            atomicCAS(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], key, 0ull);
+        }
+        __syncwarp();
+        __threadfence();
+        if (lane == 0) {
+          const unsigned idx = atomicAdd(&p.ctl->comp_tail, 1u);
+          CompRec* rec = p.comp + (idx % p.comp_cap);
+          const unsigned long long t0 = *reinterpret_cast<volatile unsigned long long*>(&a->t_first);
+          const unsigned long long t1 = *reinterpret_cast<volatile unsigned long long*>(&a->t_last);
+          const unsigned long long m0 = *reinterpret_cast<volatile unsigned long long*>(&a->touched[0]);
+          const unsigned long long m1 = *reinterpret_cast<volatile unsigned long long*>(&a->touched[1]);
+          st_relaxed_sys_v4(rec->w + 0, a->atom_id, a->count, static_cast<unsigned>(a->tag),
+                            static_cast<unsigned>(a->tag >> 32));
+          st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
+                            static_cast<unsigned>(t1), static_cast<unsigned>(t1 >> 32));
+          st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
+                            static_cast<unsigned>(m1), static_cast<unsigned>(m1 >> 32));
+          st_relaxed_sys_v4(rec->w + 12, sh.slot, 0u, 0u, 0u);
+          __threadfence_system();
+          st_release_sys(rec->w + 15, idx + 1u);
+          atomicAdd(&p.ctl->atoms_done, 1ull);
+          __threadfence();
+          atomicSub(&p.ctl->outstanding, 1);
+        }
+      }
+    }
+  }
+  if (tid == 0) {
+    atomicAdd(&p.ctl->blocks, n_blocks);
+    atomicAdd(&p.ctl->busy_ns, busy);
+    atomicAdd(&p.ctl->retries, retries);
+  }
+}
+
+__global__ void k_gtimer(unsigned long long* out) { *out = gtimer(); }
+
+}  // namespace gpuos_dev_impl
+
+// ====================================================================== host
+using namespace gpuos_dev_impl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                        \
+  do {                                                                        \
+    cudaError_t e_ = (expr);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(GPUOS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int64_t steady_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+struct HostAtom {
+  uint32_t atom_id = 0;
+  int64_t submit_ns = 0;
+  uint64_t mask[2] = {0, 0};
+  bool live = false;
+};
+
+}  // namespace
+
+struct gpuos_dev {
+  gpuos_dev_config cfg{};
+  gpuos_dev_topology topo{};
+  int device = 0;
+  cudaStream_t s_ingest = nullptr, s_work = nullptr, s_side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  // device tables
+  DevAtom* atoms = nullptr;
+  unsigned long long* resident = nullptr;
+  unsigned* version = nullptr;
+  int* fence = nullptr;
+  DevCtl* ctl = nullptr;
+  int* phys2log = nullptr;
+  unsigned long long* gt_scratch = nullptr;
+  // mapped host memory
+  RingEntry* ring_h = nullptr;
+  RingEntry* ring_d = nullptr;
+  CompRec* comp_h = nullptr;
+  CompRec* comp_d = nullptr;
+  unsigned long long* consumed_h = nullptr;
+  unsigned long long* consumed_d = nullptr;
+  unsigned* alive_h = nullptr;
+  unsigned* alive_d = nullptr;
+  int grid = 0;
+  // host bookkeeping
+  uint64_t ring_head = 0;  // next ring index to publish
+  uint32_t comp_head = 0;  // next completion index to consume
+  uint32_t next_seq = 1;
+  uint32_t next_atom_id = 0;
+  std::vector<uint32_t> free_slots;
+  std::vector<HostAtom> slots;
+  std::vector<int> tpc_resident;  // keys currently resident per logical TPC
+  int32_t in_flight = 0;
+  bool running = false;
+  int64_t t0_ns = 0;        // host origin
+  int64_t gt_offset = 0;    // device globaltimer - host origin-relative ns
+  float last_elapsed_ms = 0.f;
+  gpuos_dev_stats stats{};
+};
+
+namespace {
+
+int publish(gpuos_dev* d, const uint32_t* data /*28 words*/) {
+  // Back-pressure: never overwrite an entry the device has not consumed.
+  const int64_t deadline = steady_ns() + 10'000'000'000LL;
+  while (d->ring_head - __atomic_load_n(d->consumed_h, __ATOMIC_ACQUIRE) >=
+         static_cast<uint64_t>(d->cfg.ring_entries)) {
+    if (!d->running) return fail(GPUOS_E_FULL, "submit ring full and dispatcher stopped");
+    if (steady_ns() > deadline) return fail(GPUOS_E_TIMEOUT, "submit ring stalled");
+  }
+  RingEntry* e = d->ring_h + (d->ring_head % d->cfg.ring_entries);
+  const uint32_t ticket = static_cast<uint32_t>(d->ring_head + 1);
+  volatile uint32_t* w = e->w;
+  for (int sector = 0; sector < 4; ++sector) {
+    for (int k = 0; k < 7; ++k) w[sector * 8 + k] = data[sector * 7 + k];
+    __atomic_store_n(const_cast<uint32_t*>(&w[sector * 8 + 7]), ticket, __ATOMIC_RELEASE);
+  }
+  ++d->ring_head;
+  return GPUOS_OK;
+}
+
+void put64(uint32_t* data, int field, uint64_t v) {
+  data[field] = static_cast<uint32_t>(v);
+  data[field + 1] = static_cast<uint32_t>(v >> 32);
+}
+
+int map_priority(int32_t p) { return std::clamp(p, 0, 254) + 1; }
+
+}  // namespace
+
+extern "C" {
+
+const char* gpuos_dev_last_error(void) { return g_last_error.c_str(); }
+
+int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
+  if (out == nullptr) return fail(GPUOS_E_CONFIG, "null out pointer");
+  *out = nullptr;
+  gpuos_dev_config cfg{};
+  if (cfg_in) cfg = *cfg_in;
+  if (cfg.workers_per_sm <= 0) cfg.workers_per_sm = 2;
+  if (cfg.atom_slots <= 0) cfg.atom_slots = 4096;
+  if (cfg.ring_entries <= 0) cfg.ring_entries = 4096;
+  if (cfg.idle_sleep_ns <= 0) cfg.idle_sleep_ns = 256;
+  if (cfg.workers_per_sm > 8) return fail(GPUOS_E_CONFIG, "workers_per_sm must be <= 8");
+  if (cfg.atom_slots > (1 << 24)) return fail(GPUOS_E_CONFIG, "atom_slots must be < 2^24");
+
+  auto d = std::make_unique<gpuos_dev>();
+  d->cfg = cfg;
+  d->device = cfg.device_ordinal;
+  CUDA_TRY(cudaSetDevice(d->device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, d->device));
+  if (prop.major != 10)
+    return fail(GPUOS_E_CONFIG, std::string("sm_100a dispatcher needs a Blackwell B200, found ") + prop.name);
+  const int phys_tpcs = prop.multiProcessorCount / 2;
+  if (cfg.logical_tpcs <= 0) cfg.logical_tpcs = std::min(phys_tpcs, GPUOS_MAX_TPCS);
+  if (cfg.logical_tpcs > phys_tpcs || cfg.logical_tpcs > GPUOS_MAX_TPCS)
+    return fail(GPUOS_E_CONFIG, "logical_tpcs exceeds the physical TPC count");
+  d->cfg = cfg;
+
+  // Size each worker's shared memory so that exactly W workers fit per SM.
+  const int smem_sm = static_cast<int>(prop.sharedMemPerMultiprocessor);
+  int smem_worker = std::min<int>(static_cast<int>(prop.sharedMemPerBlockOptin),
+                                  smem_sm / cfg.workers_per_sm - 2048);
+  smem_worker = std::max(smem_worker - smem_worker % 1024, 0);
+  if (cfg.workers_per_sm > 1) {
+    // W+1 workers must not fit.
+    while ((cfg.workers_per_sm + 1) * (smem_worker + 1024) <= smem_sm) smem_worker += 1024;
+  }
+  d->topo.sm_count = prop.multiProcessorCount;
+  d->topo.physical_tpcs = phys_tpcs;
+  d->topo.logical_tpcs = cfg.logical_tpcs;
+  d->topo.workers_per_sm = cfg.workers_per_sm;
+  d->topo.workers_per_tpc = 2 * cfg.workers_per_sm;
+  d->topo.threads_per_worker = kWorkerThreads;
+  d->topo.smem_per_worker = smem_worker;
+  d->grid = prop.multiProcessorCount * cfg.workers_per_sm;
+
+  CUDA_TRY(cudaFuncSetAttribute(k_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_worker));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_worker, kWorkerThreads, smem_worker));
+  if (per_sm != cfg.workers_per_sm)
+    return fail(GPUOS_E_CONFIG, "worker occupancy is " + std::to_string(per_sm) +
+                                    " CTAs/SM, expected " + std::to_string(cfg.workers_per_sm));
+
+  CUDA_TRY(cudaStreamCreateWithFlags(&d->s_ingest, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&d->s_work, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&d->s_side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreate(&d->ev_start));
+  CUDA_TRY(cudaEventCreate(&d->ev_stop));
+
+  const size_t T = static_cast<size_t>(cfg.logical_tpcs);
+  CUDA_TRY(cudaMalloc(&d->atoms, sizeof(DevAtom) * cfg.atom_slots));
+  CUDA_TRY(cudaMemset(d->atoms, 0, sizeof(DevAtom) * cfg.atom_slots));
+  CUDA_TRY(cudaMalloc(&d->resident, sizeof(unsigned long long) * T * kResident));
+  CUDA_TRY(cudaMalloc(&d->version, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMalloc(&d->fence, sizeof(int) * T));
+  CUDA_TRY(cudaMalloc(&d->ctl, sizeof(DevCtl)));
+  CUDA_TRY(cudaMalloc(&d->phys2log, sizeof(int) * phys_tpcs));
+  CUDA_TRY(cudaMalloc(&d->gt_scratch, sizeof(unsigned long long)));
+  std::vector<int> p2l(phys_tpcs, -1);
+  for (int t = 0; t < cfg.logical_tpcs; ++t) p2l[t] = t;
+  CUDA_TRY(cudaMemcpy(d->phys2log, p2l.data(), sizeof(int) * phys_tpcs, cudaMemcpyHostToDevice));
+
+  CUDA_TRY(cudaHostAlloc(&d->ring_h, sizeof(RingEntry) * cfg.ring_entries, cudaHostAllocMapped));
+  CUDA_TRY(cudaHostAlloc(&d->comp_h, sizeof(CompRec) * cfg.atom_slots, cudaHostAllocMapped));
+  CUDA_TRY(cudaHostAlloc(&d->consumed_h, 128, cudaHostAllocMapped));
+  CUDA_TRY(cudaHostAlloc(&d->alive_h, sizeof(unsigned) * d->grid, cudaHostAllocMapped));
+  CUDA_TRY(cudaHostGetDevicePointer(&d->ring_d, d->ring_h, 0));
+  CUDA_TRY(cudaHostGetDevicePointer(&d->comp_d, d->comp_h, 0));
+  CUDA_TRY(cudaHostGetDevicePointer(&d->consumed_d, d->consumed_h, 0));
+  CUDA_TRY(cudaHostGetDevicePointer(&d->alive_d, d->alive_h, 0));
+
+  d->slots.assign(cfg.atom_slots, HostAtom{});
+  d->free_slots.reserve(cfg.atom_slots);
+  for (int s = cfg.atom_slots - 1; s >= 0; --s) d->free_slots.push_back(static_cast<uint32_t>(s));
+  d->tpc_resident.assign(T, 0);
+  d->t0_ns = steady_ns();
+  *out = d.release();
+  return GPUOS_OK;
+}
+
+int gpuos_dev_close(gpuos_dev* d) {
+  if (d == nullptr) return GPUOS_OK;
+  if (d->running) {
+    float ms = 0;
+    gpuos_dev_stop(d, 0, &ms);
+  }
+  cudaFree(d->atoms);
+  cudaFree(d->resident);
+  cudaFree(d->version);
+  cudaFree(d->fence);
+  cudaFree(d->ctl);
+  cudaFree(d->phys2log);
+  cudaFree(d->gt_scratch);
+  cudaFreeHost(d->ring_h);
+  cudaFreeHost(d->comp_h);
+  cudaFreeHost(d->consumed_h);
+  cudaFreeHost(d->alive_h);
+  if (d->ev_start) cudaEventDestroy(d->ev_start);
+  if (d->ev_stop) cudaEventDestroy(d->ev_stop);
+  if (d->s_ingest) cudaStreamDestroy(d->s_ingest);
+  if (d->s_work) cudaStreamDestroy(d->s_work);
+  if (d->s_side) cudaStreamDestroy(d->s_side);
+  delete d;
+  return GPUOS_OK;
+}
+
+int gpuos_dev_get_topology(gpuos_dev* d, gpuos_dev_topology* out) {
+  if (!d || !out) return fail(GPUOS_E_CONFIG, "null argument");
+  *out = d->topo;
+  return GPUOS_OK;
+}
+
+int64_t gpuos_dev_now_ns(gpuos_dev* d) { return d ? steady_ns() - d->t0_ns : 0; }
+int32_t gpuos_dev_in_flight(gpuos_dev* d) { return d ? d->in_flight : 0; }
+
+int gpuos_dev_start(gpuos_dev* d) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  if (d->running) return fail(GPUOS_E_STATE, "dispatcher already running");
+  if (d->in_flight != 0) return fail(GPUOS_E_STATE, "atoms still in flight");
+  CUDA_TRY(cudaSetDevice(d->device));
+  const size_t T = static_cast<size_t>(d->cfg.logical_tpcs);
+  CUDA_TRY(cudaMemset(d->resident, 0, sizeof(unsigned long long) * T * kResident));
+  CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
+  std::memset(d->ring_h, 0, sizeof(RingEntry) * d->cfg.ring_entries);
+  std::memset(d->comp_h, 0, sizeof(CompRec) * d->cfg.atom_slots);
+  std::memset(d->alive_h, 0, sizeof(unsigned) * d->grid);
+  *d->consumed_h = 0;
+  d->ring_head = 0;
+  d->comp_head = 0;
+  std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
+
+  // Calibrate device globaltimer against the host origin (+- half an RTT).
+  int64_t best_rtt = INT64_MAX;
+  for (int i = 0; i < 5; ++i) {
+    const int64_t h0 = gpuos_dev_now_ns(d);
+    k_gtimer<<<1, 1, 0, d->s_work>>>(d->gt_scratch);
+    unsigned long long g = 0;
+    CUDA_TRY(cudaMemcpyAsync(&g, d->gt_scratch, 8, cudaMemcpyDeviceToHost, d->s_work));
+    CUDA_TRY(cudaStreamSynchronize(d->s_work));
+    const int64_t h1 = gpuos_dev_now_ns(d);
+    if (h1 - h0 < best_rtt) {
+      best_rtt = h1 - h0;
+      d->gt_offset = static_cast<int64_t>(g) - (h0 + h1) / 2;
+    }
+  }
+  DevCtl ctl{};
+  unsigned long long g_now = 0;
+  CUDA_TRY(cudaMemcpy(&g_now, d->gt_scratch, 8, cudaMemcpyDeviceToHost));
+  ctl.deadline = g_now + 1800ull * 1000000000ull;  // hang guard: 30 min
+  CUDA_TRY(cudaMemcpy(d->ctl, &ctl, sizeof(DevCtl), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaDeviceSynchronize());
+
+  Params p{};
+  p.atoms = d->atoms;
+  p.resident = d->resident;
+  p.version = d->version;
+  p.fence = d->fence;
+  p.ctl = d->ctl;
+  p.phys2log = d->phys2log;
+  p.ring = d->ring_d;
+  p.comp = d->comp_d;
+  p.consumed = d->consumed_d;
+  p.alive = d->alive_d;
+  p.ring_cap = static_cast<unsigned>(d->cfg.ring_entries);
+  p.comp_cap = static_cast<unsigned>(d->cfg.atom_slots);
+  p.logical_tpcs = d->cfg.logical_tpcs;
+  p.idle_sleep_ns = d->cfg.idle_sleep_ns;
+
+  k_ingest<<<1, 32, 0, d->s_ingest>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
+  k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+  d->running = true;
+
+  // Every worker CTA must be resident, W per SM, 2W per logical TPC.
+  const int64_t deadline = steady_ns() + 5'000'000'000LL;
+  for (;;) {
+    int ready = 0;
+    for (int i = 0; i < d->grid; ++i)
+      ready += __atomic_load_n(d->alive_h + i, __ATOMIC_ACQUIRE) != 0u;
+    if (ready == d->grid) break;
+    if (steady_ns() > deadline) {
+      gpuos_dev_stop(d, 0, nullptr);
+      return fail(GPUOS_E_TIMEOUT, "only " + std::to_string(ready) + " of " +
+                                       std::to_string(d->grid) + " worker CTAs became resident");
+    }
+  }
+  std::vector<int> per_sm(d->topo.sm_count, 0);
+  for (int i = 0; i < d->grid; ++i) ++per_sm[(d->alive_h[i] & 0x7fffffffu) - 1];
+  for (int s = 0; s < d->topo.sm_count; ++s)
+    if (per_sm[s] != d->cfg.workers_per_sm) {
+      gpuos_dev_stop(d, 0, nullptr);
+      return fail(GPUOS_E_INVARIANT, "SM " + std::to_string(s) + " hosts " +
+                                         std::to_string(per_sm[s]) + " workers");
+    }
+  return GPUOS_OK;
+}
+
+int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  if (!d->running) return fail(GPUOS_E_STATE, "dispatcher not running");
+  uint32_t data[28] = {};
+  data[kFOp] = drain ? kOpDrain : kOpShutdown;
+  int rc = publish(d, data);
+  if (rc != GPUOS_OK) return rc;
+  // Completions keep arriving while draining; the caller polls them after.
+  const int64_t deadline = steady_ns() + 600'000'000'000LL;
+  while (cudaStreamQuery(d->s_work) == cudaErrorNotReady ||
+         cudaStreamQuery(d->s_ingest) == cudaErrorNotReady) {
+    if (steady_ns() > deadline) return fail(GPUOS_E_TIMEOUT, "dispatcher did not stop");
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  d->running = false;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(d->s_work));
+  CUDA_TRY(cudaStreamSynchronize(d->s_ingest));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, d->ev_start, d->ev_stop));
+  d->last_elapsed_ms = ms;
+  if (elapsed_ms) *elapsed_ms = ms;
+  DevCtl ctl{};
+  CUDA_TRY(cudaMemcpy(&ctl, d->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost));
+  d->stats.blocks_executed += ctl.blocks;
+  d->stats.worker_busy_ns += ctl.busy_ns;
+  d->stats.claim_retries += ctl.retries;
+  d->stats.kernel_elapsed_ns = static_cast<int64_t>(ms * 1e6);
+  d->stats.ingest_entries += static_cast<int64_t>(*d->consumed_h);
+  if (drain && ctl.outstanding != 0)
+    return fail(GPUOS_E_INVARIANT, "drained with atoms outstanding");
+  return GPUOS_OK;
+}
+
+int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom_id) {
+  if (!d || !a) return fail(GPUOS_E_CONFIG, "null argument");
+  if (!d->running) return fail(GPUOS_E_STATE, "dispatcher not running");
+  if (a->lo < 0 || a->hi <= a->lo) return fail(GPUOS_E_CONFIG, "atom block range out of bounds");
+  if (a->hi - a->lo > 0xfffffffeLL) return fail(GPUOS_E_CONFIG, "atom too large");
+  if (a->body != GPUOS_BODY_STREAM && a->body != GPUOS_BODY_SPIN)
+    return fail(GPUOS_E_CONFIG, "unknown body kind");
+  const int T = d->cfg.logical_tpcs;
+  bool any = false;
+  for (int w = 0; w < 2; ++w) {
+    const uint64_t m = a->tpc_mask[w];
+    if (m == 0) continue;
+    any = true;
+    const int top = 64 * w + 63 - __builtin_clzll(m);
+    if (top >= T) return fail(GPUOS_E_CONFIG, "TPC id out of range");
+  }
+  if (!any) return fail(GPUOS_E_CONFIG, "atom needs a non-empty TPC set");
+  for (int t = 0; t < T; ++t)
+    if (((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) && d->tpc_resident[t] >= kResident)
+      return fail(GPUOS_E_FULL, "TPC " + std::to_string(t) + " already holds 32 resident atoms");
+  if (d->free_slots.empty()) return fail(GPUOS_E_FULL, "atom table full");
+
+  const uint32_t slot = d->free_slots.back();
+  d->free_slots.pop_back();
+  const uint32_t id = d->next_atom_id++;
+  const uint32_t seq = d->next_seq++;
+  uint32_t data[28] = {};
+  data[kFOp] = kOpSubmit;
+  data[kFSlot] = slot;
+  data[kFSeq] = seq;
+  data[kFPrio] = static_cast<uint32_t>(map_priority(a->priority));
+  put64(data, kFLo, static_cast<uint64_t>(a->lo));
+  data[kFCount] = static_cast<uint32_t>(a->hi - a->lo);
+  data[kFBody] = a->body;
+  put64(data, kFMask0, a->tpc_mask[0]);
+  put64(data, kFMask1, a->tpc_mask[1]);
+  data[kFAtomId] = id;
+  for (int k = 0; k < 5; ++k) put64(data, kFArgs + 2 * k, a->args[k]);
+  put64(data, kFTag, a->tag);
+  put64(data, kFTrace, reinterpret_cast<uint64_t>(a->trace));
+  HostAtom& h = d->slots[slot];
+  h.atom_id = id;
+  h.submit_ns = gpuos_dev_now_ns(d);
+  h.mask[0] = a->tpc_mask[0];
+  h.mask[1] = a->tpc_mask[1];
+  h.live = true;
+  const int rc = publish(d, data);
+  if (rc != GPUOS_OK) {
+    h.live = false;
+    d->free_slots.push_back(slot);
+    return rc;
+  }
+  for (int t = 0; t < T; ++t)
+    if ((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) ++d->tpc_resident[t];
+  ++d->in_flight;
+  if (atom_id) *atom_id = id;
+  return GPUOS_OK;
+}
+
+int gpuos_dev_set_atom_paused(gpuos_dev* d, uint32_t atom_id, int paused) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  for (uint32_t s = 0; s < d->slots.size(); ++s) {
+    if (!d->slots[s].live || d->slots[s].atom_id != atom_id) continue;
+    uint32_t data[28] = {};
+    data[kFOp] = paused ? kOpPause : kOpResume;
+    data[kFSlot] = s;
+    return publish(d, data);
+  }
+  return GPUOS_OK;  // already finished: nothing to pause (device.cpp:167)
+}
+
+int gpuos_dev_set_tpc_fence(gpuos_dev* d, int32_t tpc, int32_t min_priority) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  if (tpc < 0 || tpc >= d->cfg.logical_tpcs) return fail(GPUOS_E_CONFIG, "TPC id out of range");
+  uint32_t data[28] = {};
+  data[kFOp] = kOpFence;
+  data[kFAux] = static_cast<uint32_t>(tpc);
+  data[kFPrio] = min_priority <= 0 ? 0u : static_cast<uint32_t>(map_priority(min_priority));
+  return publish(d, data);
+}
+
+int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
+  if (!d || (!out && max > 0)) return fail(GPUOS_E_CONFIG, "null argument");
+  int n = 0;
+  while (n < max) {
+    CompRec* rec = d->comp_h + (d->comp_head % d->cfg.atom_slots);
+    const uint32_t ticket = __atomic_load_n(&rec->w[15], __ATOMIC_ACQUIRE);
+    if (ticket != d->comp_head + 1u) break;
+    const volatile uint32_t* w = rec->w;
+    gpuos_completion& c = out[n];
+    c.atom_id = w[0];
+    c.blocks = w[1];
+    c.tag = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+    const uint64_t t_first = (uint64_t)w[4] | ((uint64_t)w[5] << 32);
+    const uint64_t t_last = (uint64_t)w[6] | ((uint64_t)w[7] << 32);
+    c.tpc_touched[0] = (uint64_t)w[8] | ((uint64_t)w[9] << 32);
+    c.tpc_touched[1] = (uint64_t)w[10] | ((uint64_t)w[11] << 32);
+    const uint32_t slot = w[12];
+    c.dev_first_start_ns = static_cast<int64_t>(t_first) - d->gt_offset;
+    c.dev_last_end_ns = static_cast<int64_t>(t_last) - d->gt_offset;
+    c.host_complete_ns = gpuos_dev_now_ns(d);
+    if (slot >= d->slots.size() || !d->slots[slot].live || d->slots[slot].atom_id != c.atom_id)
+      return fail(GPUOS_E_INVARIANT, "completion for an unknown atom");
+    HostAtom& h = d->slots[slot];
+    c.host_submit_ns = h.submit_ns;
+    for (int t = 0; t < d->cfg.logical_tpcs; ++t)
+      if ((h.mask[t >> 6] >> (t & 63)) & 1ull) --d->tpc_resident[t];
+    h.live = false;
+    d->free_slots.push_back(slot);
+    --d->in_flight;
+    ++d->stats.atoms_completed;
+    ++d->comp_head;
+    ++n;
+  }
+  return n;
+}
+
+int gpuos_dev_get_stats(gpuos_dev* d, gpuos_dev_stats* out) {
+  if (!d || !out) return fail(GPUOS_E_CONFIG, "null argument");
+  *out = d->stats;
+  return GPUOS_OK;
+}
+
+// Workspace management runs on a side stream with the stream-ordered
+// allocator: it never synchronises the device, so it is safe while the
+// persistent dispatcher is resident.
+int gpuos_dev_alloc(gpuos_dev* d, uint64_t bytes, void** ptr) {
+  if (!d || !ptr) return fail(GPUOS_E_CONFIG, "null argument");
+  CUDA_TRY(cudaSetDevice(d->device));
+  CUDA_TRY(cudaMallocAsync(ptr, bytes, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  return GPUOS_OK;
+}
+
+int gpuos_dev_free(gpuos_dev* d, void* ptr) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  CUDA_TRY(cudaFreeAsync(ptr, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  return GPUOS_OK;
+}
+
+int gpuos_dev_copy(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, int kind) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                           : kind == 2 ? cudaMemcpyDeviceToHost
+                                       : cudaMemcpyDeviceToDevice;
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, k, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  return GPUOS_OK;
+}
+
+int gpuos_dev_memset(gpuos_dev* d, void* dst, int value, uint64_t bytes) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  CUDA_TRY(cudaMemsetAsync(dst, value, bytes, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  return GPUOS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,546 @@
+// Live B200 backend and GPU mirror of the device seam (include/gpuos/b200.hpp),
+// written purely against the C ABI of the sm_100a dispatcher (gpuos_dev.h).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "gpuos/b200.hpp"
+#include "gpuos_dev.h"
+
+namespace gpuos {
+
+namespace {
+
+[[noreturn]] void raise(int rc, const char* what) {
+  std::string msg = std::string(what) + ": " + gpuos_dev_last_error();
+  if (rc == GPUOS_E_CONFIG) throw ConfigError(msg);
+  throw InvariantError(msg);
+}
+
+void check(int rc, const char* what) {
+  if (rc < 0) raise(rc, what);
+}
+
+// splitmix64: deterministic workspace contents.
+std::uint64_t mix64(std::uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+std::uint32_t salt_of(std::uint32_t workspace) {
+  return static_cast<std::uint32_t>(mix64(0xB200u + workspace)) | 1u;
+}
+
+// CPU restatement of the STREAM body (bodies.cuh), the verification oracle.
+inline std::uint32_t stream_expect(std::uint32_t x, std::uint32_t salt, std::uint64_t e) {
+  return (x ^ salt) * 0x9E3779B1u + static_cast<std::uint32_t>(e);
+}
+
+std::array<std::uint64_t, 2> mask_of(const std::vector<int>& tpcs) {
+  std::array<std::uint64_t, 2> m{0, 0};
+  for (int t : tpcs) m[t >> 6] |= 1ull << (t & 63);
+  return m;
+}
+
+}  // namespace
+
+// ================================================================ runtime
+B200Runtime::B200Runtime(int logical_tpcs, const B200Options& opt)
+    : opt_(opt), tpcs_(logical_tpcs) {
+  if (logical_tpcs < 1 || logical_tpcs > GPUOS_MAX_TPCS)
+    throw ConfigError("B200 backend supports 1..128 logical TPCs");
+  gpuos_dev_config cfg{};
+  cfg.device_ordinal = opt.device;
+  cfg.workers_per_sm = opt.workers_per_sm;
+  cfg.logical_tpcs = logical_tpcs;
+  cfg.idle_sleep_ns = opt.idle_sleep_ns;
+  check(gpuos_dev_open(&cfg, &dev_), "gpuos_dev_open");
+}
+
+B200Runtime::~B200Runtime() {
+  if (running_) {
+    float ms;
+    gpuos_dev_stop(dev_, 0, &ms);
+  }
+  for (auto& [id, w] : ws_) {
+    gpuos_dev_free(dev_, w.src);
+    gpuos_dev_free(dev_, w.dst);
+  }
+  for (auto* p : trace_chunks_) gpuos_dev_free(dev_, p);
+  gpuos_dev_close(dev_);
+}
+
+int B200Runtime::workers_per_tpc() const {
+  gpuos_dev_topology t{};
+  gpuos_dev_get_topology(dev_, &t);
+  return t.workers_per_tpc;
+}
+
+B200Runtime::Workspace& B200Runtime::workspace(std::uint32_t id, std::uint64_t words) {
+  Workspace& w = ws_[id];
+  if (w.words >= words) return w;
+  // Buffers may be referenced by atoms in flight: never reallocate.
+  if (w.src) throw ConfigError("workspace " + std::to_string(id) + " is smaller than a later kernel needs");
+  words = (words + 3) & ~3ull;
+  void* p = nullptr;
+  check(gpuos_dev_alloc(dev_, words * 4, &p), "workspace alloc");
+  w.src = static_cast<std::uint32_t*>(p);
+  check(gpuos_dev_alloc(dev_, words * 4, &p), "workspace alloc");
+  w.dst = static_cast<std::uint32_t*>(p);
+  w.words = words;
+  w.host_src.resize(words);
+  std::uint64_t s = mix64(id);
+  for (std::uint64_t i = 0; i < words; i += 2) {
+    s = mix64(s);
+    w.host_src[i] = static_cast<std::uint32_t>(s);
+    if (i + 1 < words) w.host_src[i + 1] = static_cast<std::uint32_t>(s >> 32);
+  }
+  check(gpuos_dev_copy(dev_, w.src, w.host_src.data(), words * 4, 1), "workspace upload");
+  check(gpuos_dev_memset(dev_, w.dst, 0, words * 4), "workspace clear");
+  return w;
+}
+
+void B200Runtime::ensure_trace(KernelId kid, long blocks) {
+  if (trace_of_.size() <= kid) trace_of_.resize(kid + 1, nullptr);
+  if (trace_of_[kid]) return;
+  const std::uint64_t need = static_cast<std::uint64_t>(blocks);
+  if (trace_pool_used_ + need > trace_pool_cap_) {
+    const std::uint64_t cap = std::max<std::uint64_t>(need, 16ull << 20);
+    void* p = nullptr;
+    check(gpuos_dev_alloc(dev_, cap * 4, &p), "trace alloc");
+    check(gpuos_dev_memset(dev_, p, 0, cap * 4), "trace clear");
+    trace_pool_ = static_cast<std::uint32_t*>(p);
+    trace_chunks_.push_back(trace_pool_);
+    trace_pool_used_ = 0;
+    trace_pool_cap_ = cap;
+  }
+  trace_of_[kid] = trace_pool_ + trace_pool_used_;
+  trace_pool_used_ += need;
+}
+
+B200Runtime::Resolved B200Runtime::resolve(KernelId kid, const SimKernelSpec& spec) {
+  if (has_resolved_.size() > kid && has_resolved_[kid]) return resolved_[kid];
+  Resolved r{};
+  BodyRef b = spec.body;
+  if (b.kind == BodyKind::None) {
+    // The reference's cost-only kernel: synthesise a body of the same length.
+    const double us = static_cast<double>(spec.block_duration_at_fmax) / 1000.0;
+    if (opt_.synth == B200Options::Synth::Spin) {
+      b.kind = BodyKind::Spin;
+      b.p0 = spec.block_duration_at_fmax;
+    } else {
+      long words = static_cast<long>(std::llround(us * opt_.stream_words_per_us));
+      words = std::max(opt_.stream_min_words, (words + 3) & ~3L);
+      b.kind = BodyKind::Stream;
+      b.p0 = words;
+      b.workspace = 0x100000u + static_cast<std::uint32_t>(words / 4);
+    }
+  }
+  switch (b.kind) {
+    case BodyKind::Stream: {
+      const long words = static_cast<long>(b.p0);
+      if (words <= 0 || words % 4 != 0) throw ConfigError("stream body needs words % 4 == 0");
+      const long cap = b.p2 > 0 ? static_cast<long>(b.p2) : opt_.stream_chunk_cap;
+      const long chunks = std::min<long>(spec.total_blocks, cap);
+      Workspace& w = workspace(b.workspace, static_cast<std::uint64_t>(words) * cap);
+      r.body = GPUOS_BODY_STREAM;
+      r.args[0] = reinterpret_cast<std::uint64_t>(w.src);
+      r.args[1] = reinterpret_cast<std::uint64_t>(w.dst);
+      r.args[2] = static_cast<std::uint64_t>(words);
+      r.args[3] = b.p1 != 0 ? static_cast<std::uint32_t>(b.p1) : salt_of(b.workspace);
+      r.args[4] = static_cast<std::uint64_t>(chunks);
+      r.words = words;
+      r.chunks = chunks;
+      break;
+    }
+    case BodyKind::Spin:
+      r.body = GPUOS_BODY_SPIN;
+      r.args[0] = static_cast<std::uint64_t>(b.p0);
+      break;
+    case BodyKind::GemmBf16:
+      throw ConfigError("gemm_bf16 body is not available in this build");
+    case BodyKind::None:
+      break;
+  }
+  if (opt_.trace_blocks) {
+    ensure_trace(kid, spec.total_blocks);
+    r.trace = trace_of_[kid];
+  }
+  if (resolved_.size() <= kid) {
+    resolved_.resize(kid + 1);
+    has_resolved_.resize(kid + 1, 0);
+  }
+  resolved_[kid] = r;
+  has_resolved_[kid] = 1;
+  return r;
+}
+
+void B200Runtime::reset_kernels() {
+  resolved_.clear();
+  has_resolved_.clear();
+  trace_of_.clear();
+  for (auto* p : trace_chunks_) gpuos_dev_free(dev_, p);
+  trace_chunks_.clear();
+  trace_pool_ = nullptr;
+  trace_pool_used_ = trace_pool_cap_ = 0;
+}
+
+void B200Runtime::start() {
+  check(gpuos_dev_start(dev_), "gpuos_dev_start");
+  running_ = true;
+}
+
+float B200Runtime::stop(bool drain) {
+  float ms = 0.f;
+  running_ = false;
+  check(gpuos_dev_stop(dev_, drain ? 1 : 0, &ms), "gpuos_dev_stop");
+  return ms;
+}
+
+std::uint64_t B200Runtime::workspace_bytes() const {
+  std::uint64_t b = 0;
+  for (const auto& [id, w] : ws_) b += w.words * 4;
+  return b;
+}
+
+std::uint64_t B200Runtime::upload_inputs() {
+  std::uint64_t bytes = 0;
+  for (auto& [id, w] : ws_) {
+    check(gpuos_dev_copy(dev_, w.src, w.host_src.data(), w.words * 4, 1), "upload");
+    bytes += w.words * 4;
+  }
+  return bytes;
+}
+
+std::uint64_t B200Runtime::download_digest() {
+  // The step's result as seen by a tenant: the first 64 KiB of every output.
+  std::uint64_t bytes = 0;
+  std::vector<std::uint32_t> sink;
+  for (auto& [id, w] : ws_) {
+    const std::uint64_t n = std::min<std::uint64_t>(w.words, 16384);
+    sink.resize(n);
+    check(gpuos_dev_copy(dev_, sink.data(), w.dst, n * 4, 2), "download");
+    bytes += n * 4;
+  }
+  return bytes;
+}
+
+VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs,
+                                         const std::vector<KernelPlacement>& placement) {
+  VerifyReport rep;
+  // Chunks of each workspace that some executed block wrote.
+  std::unordered_map<std::uint64_t, std::vector<char>> touched;  // args[1] -> chunks
+  std::vector<std::uint32_t> trace;
+  for (std::size_t k = 0; k < specs.size(); ++k) {
+    if (k >= has_resolved_.size() || !has_resolved_[k]) continue;
+    const Resolved& r = resolved_[k];
+    const long blocks = specs[k].total_blocks;
+    const KernelPlacement& pl = placement[k];
+    if (pl.ranges.empty()) continue;  // never dispatched
+    ++rep.kernels;
+    rep.blocks += blocks;
+    if (!r.trace) continue;
+    trace.assign(static_cast<std::size_t>(blocks), 0u);
+    check(gpuos_dev_copy(dev_, trace.data(), r.trace, blocks * 4ull, 2), "trace download");
+    std::vector<char>* tc = nullptr;
+    if (r.body == GPUOS_BODY_STREAM) {
+      auto& v = touched[r.args[1]];
+      v.resize(static_cast<std::size_t>(r.chunks), 0);
+      tc = &v;
+    }
+    for (std::size_t a = 0; a < pl.ranges.size(); ++a) {
+      for (long b = pl.ranges[a].first; b < pl.ranges[a].second; ++b) {
+        const std::uint32_t v = trace[static_cast<std::size_t>(b)];
+        const std::uint32_t count = v >> 16;
+        if (count == 0) {
+          ++rep.missing;
+          continue;
+        }
+        if (count > 1) {
+          ++rep.duplicated;
+          continue;
+        }
+        const int sm = static_cast<int>(v & 0xffffu) - 1;
+        const int tpc = sm >> 1;  // identity logical map (gpuos_dev_open)
+        if (tpc < 0 || tpc >= GPUOS_MAX_TPCS || !((pl.masks[a][tpc >> 6] >> (tpc & 63)) & 1ull))
+          ++rep.misplaced;
+        if (tc) (*tc)[static_cast<std::size_t>(b % r.chunks)] = 1;
+      }
+    }
+  }
+  // Body outputs against the CPU restatement.
+  for (auto& [id, w] : ws_) {
+    auto it = touched.find(reinterpret_cast<std::uint64_t>(w.dst));
+    if (it == touched.end()) continue;
+    // words per chunk: any kernel on this workspace shares the chunk geometry.
+    long words = 0;
+    std::uint32_t salt = 0;
+    for (std::size_t k = 0; k < resolved_.size(); ++k)
+      if (has_resolved_[k] && resolved_[k].args[1] == reinterpret_cast<std::uint64_t>(w.dst)) {
+        words = resolved_[k].words;
+        salt = static_cast<std::uint32_t>(resolved_[k].args[3]);
+        break;
+      }
+    std::vector<std::uint32_t> out(w.words);
+    check(gpuos_dev_copy(dev_, out.data(), w.dst, w.words * 4, 2), "output download");
+    const auto& chunks = it->second;
+    for (std::size_t c = 0; c < chunks.size(); ++c) {
+      if (!chunks[c]) continue;
+      const std::uint64_t base = c * static_cast<std::uint64_t>(words);
+      for (long i = 0; i < words; ++i) {
+        const std::uint64_t e = base + static_cast<std::uint64_t>(i);
+        ++rep.checked_words;
+        if (out[e] != stream_expect(w.host_src[e], salt, e)) ++rep.bad_words;
+      }
+    }
+  }
+  return rep;
+}
+
+// ============================================================ B200Device
+B200Device::B200Device(DeviceTopology topo, FrequencyDomain freq, B200Options opt)
+    : topo_(topo), freq_(std::move(freq)) {
+  topo_.validate();
+  freq_.validate();
+  rt_ = std::make_unique<B200Runtime>(topo_.total_tpcs(), opt);
+}
+
+B200Device::~B200Device() = default;
+
+void B200Device::reset_run() {
+  if (rt_->running()) throw InvariantError("reset_run while the dispatcher runs");
+  rt_->reset_kernels();
+  kernels_.clear();
+  executed_.clear();
+  atom_index_.clear();
+  timeline_.clear();
+  ready_.clear();
+  while (!timers_.empty()) timers_.pop();
+  timer_fns_.clear();
+  now_ = 0;
+  busy_tpc_ns_ = 0.0;
+  residency_.clear();
+}
+
+SimTime B200Device::host_now() const { return gpuos_dev_now_ns(rt_->handle()) - origin_; }
+
+KernelId B200Device::register_kernel(const SimKernelSpec& spec) {
+  spec.validate();
+  const KernelId kid = static_cast<KernelId>(kernels_.size());
+  kernels_.push_back(spec);
+  executed_.push_back(0);
+  rt_->resolve(kid, spec);
+  return kid;
+}
+
+AtomId B200Device::submit_atom(KernelId kernel, long lo, long hi, const std::vector<int>& tpcs,
+                               int priority, bool atomized, std::uint64_t tag) {
+  const SimKernelSpec& spec = kernels_.at(kernel);
+  if (tpcs.empty()) throw ConfigError("atom needs a non-empty TPC set");
+  if (lo < 0 || hi <= lo || hi > spec.total_blocks)
+    throw ConfigError("atom block range out of bounds");
+  for (int t : tpcs)
+    if (t < 0 || t >= topo_.total_tpcs()) throw ConfigError("TPC id out of range");
+  if (!rt_->running()) throw InvariantError("submit_atom outside run_all()");
+  const B200Runtime::Resolved r = rt_->resolve(kernel, spec);
+  const auto m = mask_of(tpcs);
+  gpuos_atom_desc d{};
+  d.lo = lo;
+  d.hi = hi;
+  d.tpc_mask[0] = m[0];
+  d.tpc_mask[1] = m[1];
+  d.priority = priority;
+  d.body = r.body;
+  std::memcpy(d.args, r.args, sizeof d.args);
+  d.tag = tag;
+  d.trace = r.trace;
+  d.atomized = atomized ? 1 : 0;
+  std::uint32_t id = 0;
+  check(gpuos_dev_submit_atom(rt_->handle(), &d, &id), "gpuos_dev_submit_atom");
+  AtomTimeline tl{};
+  tl.atom = id;
+  tl.tag = tag;
+  tl.kernel = kernel;
+  tl.lo = lo;
+  tl.hi = hi;
+  tl.priority = priority;
+  tl.mask[0] = m[0];
+  tl.mask[1] = m[1];
+  atom_index_[id] = timeline_.size();
+  timeline_.push_back(tl);
+  return id;
+}
+
+void B200Device::set_atom_paused(AtomId atom, bool paused) {
+  check(gpuos_dev_set_atom_paused(rt_->handle(), atom, paused ? 1 : 0), "pause");
+}
+
+void B200Device::set_tpc_fence(int tpc, int min_priority) {
+  if (!rt_->running()) return;
+  check(gpuos_dev_set_tpc_fence(rt_->handle(), tpc, min_priority), "fence");
+}
+
+SimTime B200Device::request_frequency(FreqMhz f) {
+  if (!freq_.supports(f)) throw ConfigError("unsupported frequency");
+  return now_;  // DVFS actuation is out of scope; clocks stay at f_max
+}
+
+void B200Device::schedule_call(SimTime t, std::function<void()> fn) {
+  if (t < now_) throw InvariantError("scheduling a call in the past");
+  const std::uint64_t seq = timer_seq_++;
+  timers_.push(Timer{t, seq});
+  timer_fns_.emplace(seq, std::move(fn));
+}
+
+void B200Device::pump() {
+  gpuos_completion buf[64];
+  const int n = gpuos_dev_poll(rt_->handle(), buf, 64);
+  if (n < 0) raise(n, "gpuos_dev_poll");
+  for (int i = 0; i < n; ++i) {
+    const gpuos_completion& c = buf[i];
+    auto it = atom_index_.find(c.atom_id);
+    if (it == atom_index_.end()) throw InvariantError("completion for unknown atom");
+    AtomTimeline& tl = timeline_[it->second];
+    tl.host_submit_ns = c.host_submit_ns - origin_;
+    tl.host_complete_ns = c.host_complete_ns - origin_;
+    tl.dev_first_start_ns = c.dev_first_start_ns - origin_;
+    tl.dev_last_end_ns = c.dev_last_end_ns - origin_;
+    tl.touched[0] = c.tpc_touched[0];
+    tl.touched[1] = c.tpc_touched[1];
+    executed_[tl.kernel] += c.blocks;
+    ready_.push_back(AtomCompletion{c.atom_id, c.tag, tl.host_submit_ns, tl.host_complete_ns});
+  }
+}
+
+bool B200Device::step() {
+  if (ready_.empty()) pump();
+  if (!ready_.empty()) {
+    const AtomCompletion c = ready_.front();
+    ready_.pop_front();
+    now_ = std::max(now_, c.complete_time);
+    if (on_complete_) on_complete_(c);
+    return true;
+  }
+  const SimTime t = host_now();
+  if (!timers_.empty() && timers_.top().t <= t) {
+    const Timer top = timers_.top();
+    timers_.pop();
+    auto node = timer_fns_.extract(top.seq);
+    now_ = std::max(now_, t);
+    node.mapped()();
+    return true;
+  }
+  const int in_flight = gpuos_dev_in_flight(rt_->handle());
+  if (timers_.empty() && in_flight == 0) return false;
+  now_ = std::max(now_, t);
+  if (in_flight == 0 && !timers_.empty()) {
+    // Nothing on the GPU: sleep towards the next arrival, wake early.
+    const SimTime gap = timers_.top().t - t;
+    if (gap > 200'000) std::this_thread::sleep_for(std::chrono::nanoseconds(gap - 100'000));
+  }
+  return true;
+}
+
+void B200Device::run_all() {
+  rt_->start();
+  origin_ = gpuos_dev_now_ns(rt_->handle());
+  now_ = 0;
+  const auto w0 = std::chrono::steady_clock::now();
+  try {
+    while (step()) {
+    }
+  } catch (...) {
+    rt_->stop(false);
+    throw;
+  }
+  last_ms_ = rt_->stop(true);
+  run_wall_ns_ = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                     std::chrono::steady_clock::now() - w0)
+                     .count();
+  pump();  // nothing should remain; keep the ring consistent regardless
+  gpuos_dev_stats st{};
+  gpuos_dev_get_stats(rt_->handle(), &st);
+  busy_tpc_ns_ = static_cast<double>(st.worker_busy_ns) / rt_->workers_per_tpc();
+  residency_[freq_.f_max()] = now_;
+}
+
+// ============================================================ MirrorDevice
+MirrorDevice::MirrorDevice(DeviceTopology topo, FrequencyDomain freq, PowerModel power,
+                           B200Options opt)
+    : replay_(topo, std::move(freq), power) {
+  opt.trace_blocks = true;
+  rt_ = std::make_unique<B200Runtime>(topo.total_tpcs(), opt);
+}
+
+MirrorDevice::~MirrorDevice() = default;
+
+KernelId MirrorDevice::register_kernel(const SimKernelSpec& spec) {
+  const KernelId kid = replay_.register_kernel(spec);
+  specs_.push_back(spec);
+  placement_.emplace_back();
+  rt_->resolve(kid, spec);
+  return kid;
+}
+
+void MirrorDevice::drain_some(bool all) {
+  gpuos_completion buf[256];
+  for (;;) {
+    const int n = gpuos_dev_poll(rt_->handle(), buf, 256);
+    if (n < 0) raise(n, "gpuos_dev_poll");
+    if (!all || gpuos_dev_in_flight(rt_->handle()) == 0) return;
+    if (n == 0) std::this_thread::yield();
+  }
+}
+
+AtomId MirrorDevice::submit_atom(KernelId kernel, long lo, long hi, const std::vector<int>& tpcs,
+                                 int priority, bool atomized, std::uint64_t tag) {
+  const AtomId id = replay_.submit_atom(kernel, lo, hi, tpcs, priority, atomized, tag);
+  if (!rt_->running()) rt_->start();
+  const B200Runtime::Resolved r = rt_->resolve(kernel, specs_.at(kernel));
+  const auto m = mask_of(tpcs);
+  gpuos_atom_desc d{};
+  d.lo = lo;
+  d.hi = hi;
+  d.tpc_mask[0] = m[0];
+  d.tpc_mask[1] = m[1];
+  d.priority = priority;
+  d.body = r.body;
+  std::memcpy(d.args, r.args, sizeof d.args);
+  d.tag = tag;
+  d.trace = r.trace;
+  std::uint32_t gid = 0;
+  for (;;) {
+    const int rc = gpuos_dev_submit_atom(rt_->handle(), &d, &gid);
+    if (rc == GPUOS_OK) break;
+    if (rc != GPUOS_E_FULL) raise(rc, "mirror submit");
+    drain_some(false);  // the GPU lags the replay clock: wait for room
+    std::this_thread::yield();
+  }
+  ++gpu_atoms_;
+  placement_[kernel].ranges.emplace_back(lo, hi);
+  placement_[kernel].masks.push_back(m);
+  drain_some(false);
+  return id;
+}
+
+void MirrorDevice::run_all() {
+  replay_.run_all();
+  if (rt_->running()) {
+    drain_some(true);
+    gpu_ms_ = rt_->stop(true);
+  }
+}
+
+VerifyReport MirrorDevice::verify() {
+  if (rt_->running()) {
+    drain_some(true);
+    gpu_ms_ = rt_->stop(true);
+  }
+  return rt_->verify_kernels(specs_, placement_);
+}
+
+}  // namespace gpuos

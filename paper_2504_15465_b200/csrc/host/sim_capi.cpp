@@ -1,0 +1,438 @@
+// C ABI of the host scheduler path (include/gpuos_sim.h): scenario sessions
+// on the replay / live B200 / mirror backends, and the pure policy functions.
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include "gpuos/b200.hpp"
+#include "gpuos/replay.hpp"
+#include "gpuos/scenario.hpp"
+#include "gpuos_sim.h"
+#include "json.hpp"
+
+using nlohmann::json;
+using namespace gpuos;
+
+namespace {
+
+thread_local std::string g_error;
+
+char* dup_text(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+std::string runs_of(const std::vector<int>& t) {
+  std::string s;
+  for (std::size_t i = 0; i < t.size();) {
+    std::size_t j = i;
+    while (j + 1 < t.size() && t[j + 1] == t[j] + 1) ++j;
+    if (!s.empty()) s += ',';
+    s += std::to_string(t[i]);
+    if (j > i) s += '-' + std::to_string(t[j]);
+    i = j + 1;
+  }
+  return s;
+}
+
+// Scheduler knobs by their scenario-JSON names (sim.cpp:206-234).
+void apply_knob(ScenarioConfig& c, const std::string& k, const json& v) {
+  SchedulerConfig& s = c.sched;
+  auto flag = [&] { return v.is_boolean() ? v.get<bool>() : v.get<double>() != 0.0; };
+  if (k == "stealing") s.stealing_enabled = flag();
+  else if (k == "atomizer") s.atomizer_enabled = flag();
+  else if (k == "rightsizer") s.rightsizer_enabled = flag();
+  else if (k == "dvfs") s.dvfs_enabled = flag();
+  else if (k == "occupancy_filter") s.occupancy_filter = flag();
+  else if (k == "block_revocation") s.block_revocation = flag();
+  else if (k == "atom_duration_us") s.atom_duration = duration_from_us(v.get<double>());
+  else if (k == "steal_horizon_us") s.steal_horizon = duration_from_us(v.get<double>());
+  else if (k == "max_outstanding_atoms") s.max_outstanding_atoms = v.get<int>();
+  else if (k == "slip_k") s.rightsizer.slip_k = v.get<double>();
+  else if (k == "probe_depth_limit") s.rightsizer.probe_depth_limit = v.get<int>();
+  else if (k == "dvfs_slip_k") s.dvfs.slip_k = v.get<double>();
+  else if (k == "ewma_beta") s.predictor.ewma_beta = v.get<double>();
+  else if (k == "default_unknown_us") s.predictor.default_unknown = duration_from_us(v.get<double>());
+  else if (k == "disable_factor") s.disable_factor = v.get<double>();
+  else if (k == "time_slice_window_us") s.time_slice_window = duration_from_us(v.get<double>());
+  else throw ConfigError("unknown scheduler knob: " + k);
+}
+
+ScenarioConfig scenario_from(const json& req) {
+  const json& sc = req.contains("scenario") ? req.at("scenario") : req;
+  ScenarioConfig cfg;
+  if (sc.contains("preset")) cfg = preset_scenario(sc.at("preset").get<std::string>());
+  else if (sc.contains("config")) cfg = parse_scenario(sc.at("config").dump());
+  else if (sc.contains("config_path")) cfg = load_scenario_file(sc.at("config_path").get<std::string>());
+  else throw ConfigError("request needs scenario.preset, scenario.config or scenario.config_path");
+  return cfg;
+}
+
+void apply_overrides(ScenarioConfig& cfg, const json& o) {
+  if (o.contains("device")) {
+    const std::string d = o.at("device").get<std::string>();
+    if (d == "b200") cfg.topo = DeviceTopology::b200();
+    else if (d == "a100-like") cfg.topo = DeviceTopology::a100_like();
+    else if (d == "h100-like") cfg.topo = DeviceTopology::h100_like();
+    else throw ConfigError("unknown device profile: " + d);
+  }
+  if (o.contains("horizon_ms")) cfg.horizon = duration_from_ms(o.at("horizon_ms").get<double>());
+  if (o.contains("policy")) cfg.sched.policy = policy_from_string(o.at("policy").get<std::string>());
+  if (o.contains("seed")) cfg.seed = o.at("seed").get<std::uint64_t>();
+  if (o.contains("set"))
+    for (const auto& [k, v] : o.at("set").items()) apply_knob(cfg, k, v);
+  if (o.contains("quota_scale")) {
+    // Rescale quotas/caps to a larger device (e.g. a100-like 54 -> B200 74).
+    const double f = o.at("quota_scale").get<double>();
+    for (AppWorkload& wl : cfg.apps) {
+      wl.spec.tpc_quota = static_cast<int>(std::floor(wl.spec.tpc_quota * f));
+      if (wl.spec.tpc_cap > 0) wl.spec.tpc_cap = static_cast<int>(std::floor(wl.spec.tpc_cap * f));
+    }
+  }
+  if (o.contains("drop_apps"))  // run a subset of tenants (e.g. "LC alone")
+    for (const auto& id : o.at("drop_apps")) {
+      const std::string name = id.get<std::string>();
+      cfg.apps.erase(std::remove_if(cfg.apps.begin(), cfg.apps.end(),
+                                    [&](const AppWorkload& a) { return a.spec.app_id == name; }),
+                     cfg.apps.end());
+    }
+  if (o.contains("time_scale")) cfg = time_scaled(cfg, o.at("time_scale").get<double>());
+}
+
+B200Options b200_options(const json& o) {
+  B200Options b;
+  if (!o.is_object()) return b;
+  b.device = o.value("device", b.device);
+  b.workers_per_sm = o.value("workers_per_sm", b.workers_per_sm);
+  b.idle_sleep_ns = o.value("idle_sleep_ns", b.idle_sleep_ns);
+  b.trace_blocks = o.value("trace", b.trace_blocks);
+  b.synth = o.value("synth", std::string("stream")) == "spin" ? B200Options::Synth::Spin
+                                                              : B200Options::Synth::Stream;
+  b.stream_words_per_us = o.value("words_per_us", b.stream_words_per_us);
+  b.stream_min_words = o.value("min_words", b.stream_min_words);
+  b.stream_chunk_cap = o.value("chunk_cap", b.stream_chunk_cap);
+  return b;
+}
+
+json verify_json(const VerifyReport& v) {
+  return json{{"kernels", v.kernels},   {"blocks", v.blocks},
+              {"missing", v.missing},   {"duplicated", v.duplicated},
+              {"misplaced", v.misplaced}, {"bad_words", v.bad_words},
+              {"checked_words", v.checked_words}, {"ok", v.ok()}};
+}
+
+}  // namespace
+
+struct gpuos_session {
+  json request;
+  std::string backend;  // replay | b200 | mirror
+  std::unique_ptr<B200Device> b200;
+};
+
+namespace {
+
+std::string run_session(gpuos_session* s, const json& overrides) {
+  json merged = s->request;
+  if (overrides.is_object())
+    for (const auto& [k, v] : overrides.items()) merged[k] = v;
+  ScenarioConfig cfg = scenario_from(merged);
+  apply_overrides(cfg, merged);
+  cfg.validate();
+  const bool want_log = merged.value("log", false);
+  const bool want_requests = merged.value("requests", false);
+  const bool want_timeline = merged.value("timeline", false);
+  const bool e2e = merged.value("e2e", false);
+
+  std::ostringstream log;
+  long hp_atoms = 0, be_atoms = 0;
+  std::vector<long> app_atoms;
+  RunHooks hooks;
+  if (want_log) {
+    hooks.on_dispatch = [&](const DispatchRecord& d) {
+      log << "D " << d.now << ' ' << d.atom << ' ' << d.app << ' ' << d.kernel << ' ' << d.lo
+          << ' ' << d.hi << ' ' << d.priority << ' ' << (d.atomized ? 1 : 0) << ' '
+          << runs_of(*d.tpcs) << '\n';
+    };
+    hooks.on_complete = [&](const AtomCompletion& c) {
+      log << "C " << c.complete_time << ' ' << c.atom << ' ' << c.tag << ' ' << c.dispatch_time
+          << '\n';
+    };
+  }
+  hooks.on_finish = [&](const Scheduler& sc) {
+    app_atoms.assign(sc.app_count(), 0);
+    for (const PredictionLogEntry& e : sc.prediction_log()) {
+      (e.high_priority ? hp_atoms : be_atoms) += 1;
+      app_atoms[e.key.queue_id] += 1;
+    }
+  };
+
+  json out;
+  RunResult res;
+  if (s->backend == "replay") {
+    DeviceEngine engine(cfg.topo, cfg.freq, cfg.power);
+    const auto t0 = std::chrono::steady_clock::now();
+    res = run_scenario_on(engine, cfg, hooks);
+    out["wall_ns"] = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                         std::chrono::steady_clock::now() - t0)
+                         .count();
+  } else if (s->backend == "mirror") {
+    MirrorDevice dev(cfg.topo, cfg.freq, cfg.power, b200_options(merged.value("b200", json::object())));
+    res = run_scenario_on(dev, cfg, hooks);
+    out["verify"] = verify_json(dev.verify());
+    out["gpu_atoms"] = dev.gpu_atoms();
+    out["gpu_kernel_ms"] = dev.gpu_kernel_ms();
+  } else if (s->backend == "b200") {
+    if (!s->b200 || s->b200->topology().total_tpcs() != cfg.topo.total_tpcs())
+      s->b200 = std::make_unique<B200Device>(cfg.topo, cfg.freq,
+                                             b200_options(merged.value("b200", json::object())));
+    B200Device& dev = *s->b200;
+    dev.reset_run();
+    std::uint64_t h2d = 0, d2h = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    // End-to-end leg: every tenant input is copied from host memory before
+    // the run and a digest of every output is read back after it.
+    if (e2e) h2d = dev.runtime().upload_inputs();
+    res = run_scenario_on(dev, cfg, hooks);
+    if (e2e) d2h = dev.runtime().download_digest();
+    const std::int64_t e2e_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                 std::chrono::steady_clock::now() - t0)
+                 .count();
+    json b;
+    b["kernel_ms"] = dev.last_kernel_ms();
+    b["run_wall_ns"] = dev.run_wall_ns();
+    b["e2e_wall_ns"] = e2e_ns;
+    b["h2d_bytes"] = h2d;
+    b["d2h_bytes"] = d2h;
+    b["workspace_bytes"] = dev.runtime().workspace_bytes();
+    b["workers_per_tpc"] = dev.runtime().workers_per_tpc();
+    b["logical_tpcs"] = cfg.topo.total_tpcs();
+    b["tpc_busy_integral"] = dev.tpc_busy_integral();
+    long blocks = 0;
+    for (std::size_t k = 0; k < dev.kernels().size(); ++k) blocks += dev.blocks_executed(static_cast<KernelId>(k));
+    b["blocks"] = blocks;
+    b["atoms"] = dev.timeline().size();
+    if (want_timeline) {
+      json tl = json::object();
+      std::vector<long long> submit, complete, first, last, lo, hi, tag, prio, kern;
+      std::vector<unsigned long long> m0, m1, t0v, t1v;
+      for (const AtomTimeline& a : dev.timeline()) {
+        submit.push_back(a.host_submit_ns);
+        complete.push_back(a.host_complete_ns);
+        first.push_back(a.dev_first_start_ns);
+        last.push_back(a.dev_last_end_ns);
+        lo.push_back(a.lo);
+        hi.push_back(a.hi);
+        tag.push_back(static_cast<long long>(a.tag));
+        prio.push_back(a.priority);
+        kern.push_back(a.kernel);
+        m0.push_back(a.mask[0]);
+        m1.push_back(a.mask[1]);
+        t0v.push_back(a.touched[0]);
+        t1v.push_back(a.touched[1]);
+      }
+      tl["submit"] = submit;
+      tl["complete"] = complete;
+      tl["dev_first"] = first;
+      tl["dev_last"] = last;
+      tl["lo"] = lo;
+      tl["hi"] = hi;
+      tl["tag"] = tag;
+      tl["prio"] = prio;
+      tl["kernel"] = kern;
+      tl["mask0"] = m0;
+      tl["mask1"] = m1;
+      tl["touched0"] = t0v;
+      tl["touched1"] = t1v;
+      std::vector<long long> words;
+      for (std::size_t k = 0; k < dev.kernels().size(); ++k)
+        words.push_back(dev.runtime().resolve(static_cast<KernelId>(k), dev.kernels()[k]).words);
+      tl["kernel_words"] = words;
+      b["timeline"] = std::move(tl);
+    }
+    if (merged.value("verify", false)) {
+      std::vector<B200Runtime::KernelPlacement> pl(dev.kernels().size());
+      for (const AtomTimeline& a : dev.timeline()) {
+        pl[a.kernel].ranges.emplace_back(a.lo, a.hi);
+        pl[a.kernel].masks.push_back({a.mask[0], a.mask[1]});
+      }
+      out["verify"] = verify_json(dev.runtime().verify_kernels(dev.kernels(), pl));
+    }
+    out["b200"] = std::move(b);
+  } else {
+    throw ConfigError("backend must be replay, b200 or mirror");
+  }
+  out["report"] = json::parse(res.report.to_json());
+  if (want_requests) out["request_log"] = res.request_log;
+  if (want_log) out["log"] = log.str();
+  out["atoms"] = json{{"hp", hp_atoms}, {"be", be_atoms}, {"per_app", app_atoms}};
+  out["horizon_ns"] = cfg.horizon;
+  out["total_tpcs"] = cfg.topo.total_tpcs();
+  return out.dump();
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ConfigError& e) {
+    g_error = e.what();
+    return 2;
+  } catch (const InvariantError& e) {
+    g_error = e.what();
+    return 3;
+  } catch (const json::exception& e) {
+    g_error = std::string("json: ") + e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return 3;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gpuos_sim_last_error(void) { return g_error.c_str(); }
+
+void gpuos_free_text(char* text) { std::free(text); }
+
+int gpuos_session_open(const char* request_json, gpuos_session** out) {
+  return guarded([&] {
+    if (!out) throw ConfigError("null out pointer");
+    auto s = std::make_unique<gpuos_session>();
+    s->request = json::parse(request_json ? request_json : "{}");
+    s->backend = s->request.value("backend", std::string("replay"));
+    if (s->backend != "replay" && s->backend != "b200" && s->backend != "mirror")
+      throw ConfigError("backend must be replay, b200 or mirror");
+    *out = s.release();
+  });
+}
+
+int gpuos_session_run(gpuos_session* s, const char* overrides_json, char** result_json) {
+  return guarded([&] {
+    if (!s || !result_json) throw ConfigError("null argument");
+    const json o = overrides_json ? json::parse(overrides_json) : json::object();
+    *result_json = dup_text(run_session(s, o));
+  });
+}
+
+int gpuos_session_close(gpuos_session* s) {
+  return guarded([&] { delete s; });
+}
+
+int gpuos_run_json(const char* request_json, char** result_json) {
+  gpuos_session* s = nullptr;
+  int rc = gpuos_session_open(request_json, &s);
+  if (rc != 0) return rc;
+  rc = gpuos_session_run(s, nullptr, result_json);
+  gpuos_session_close(s);
+  return rc;
+}
+
+// ------------------------------------------------------------ policy ABI
+int64_t gpuos_plan_atoms(int64_t n, int64_t pred, int64_t atom, int64_t minb,
+                         int64_t* out, int64_t cap) {
+  int64_t count = -2;
+  guarded([&] {
+    const auto a = plan_atoms(n, pred, atom, minb);
+    for (std::size_t i = 0; i < a.size() && static_cast<int64_t>(i) < cap; ++i) {
+      out[2 * i] = a[i].lo;
+      out[2 * i + 1] = a[i].hi;
+    }
+    count = static_cast<int64_t>(a.size());
+  });
+  return count;
+}
+
+int gpuos_should_atomize(int64_t pred, int64_t n, int64_t atom, double factor) {
+  return should_atomize(pred, n, atom, factor) ? 1 : 0;
+}
+
+int gpuos_filter_cap(int64_t n, int32_t occ, int32_t total) {
+  int r = -2;
+  guarded([&] { r = filter_cap(n, occ, total); });
+  return r;
+}
+
+int gpuos_fit_scaling(int64_t l1, int64_t lT, int32_t T, double* m, double* b, int32_t* valid) {
+  return guarded([&] {
+    const ScalingFit f = fit_scaling(l1, lT, T);
+    *m = f.m_ns;
+    *b = f.b_ns;
+    *valid = f.valid ? 1 : 0;
+  });
+}
+
+int gpuos_choose_tpcs(double m, double b, int32_t valid, int32_t t_alloc, double slip, int32_t cap) {
+  int r = -2;
+  guarded([&] { r = choose_tpcs(ScalingFit{m, b, valid != 0}, t_alloc, slip, cap); });
+  return r;
+}
+
+int gpuos_choose_tpcs_wave(double m, double b, int32_t valid, int32_t t_alloc, double slip,
+                           int64_t blocks, int32_t occ) {
+  int r = -2;
+  guarded([&] { r = choose_tpcs_wave(ScalingFit{m, b, valid != 0}, t_alloc, slip, blocks, occ); });
+  return r;
+}
+
+int64_t gpuos_block_latency(int64_t d0, double s, int32_t f) {
+  int64_t r = -2;
+  guarded([&] {
+    FrequencyDomain fd;
+    fd.supported_mhz = default_freq_table();
+    SimKernelSpec k;
+    k.block_duration_at_fmax = d0;
+    k.sensitivity_s = s;
+    r = block_latency(k, f, fd);
+  });
+  return r;
+}
+
+int64_t gpuos_reference_kernel_latency(int64_t blocks, int64_t d0, double s, int32_t occ, int32_t t,
+                                       int32_t f) {
+  int64_t r = -2;
+  guarded([&] {
+    FrequencyDomain fd;
+    fd.supported_mhz = default_freq_table();
+    SimKernelSpec k;
+    k.total_blocks = blocks;
+    k.block_duration_at_fmax = d0;
+    k.sensitivity_s = s;
+    k.occupancy_per_tpc = occ;
+    r = reference_kernel_latency(k, t, f, fd);
+  });
+  return r;
+}
+
+int32_t gpuos_select_frequency(double S, double slip) {
+  int32_t r = -2;
+  guarded([&] { r = select_frequency(S, slip, 1410, default_freq_table()); });
+  return r;
+}
+
+int gpuos_predictor_replay(const int64_t* records, int32_t n, const int64_t* queries, int32_t q,
+                           int64_t* out_latency, int32_t* out_conf) {
+  return guarded([&] {
+    LatencyPredictor p;
+    const OperatorKey key{0, 0};
+    for (int i = 0; i < n; ++i) {
+      const int64_t* r = records + 4 * i;
+      p.record(key, ObsConfig{static_cast<int>(r[0]), static_cast<FreqMhz>(r[1]), r[2]}, r[3]);
+    }
+    for (int i = 0; i < q; ++i) {
+      const int64_t* x = queries + 3 * i;
+      const Prediction pr = p.predict(key, static_cast<int>(x[0]), static_cast<FreqMhz>(x[1]), x[2]);
+      out_latency[i] = pr.latency;
+      out_conf[i] = static_cast<int32_t>(pr.confidence);
+    }
+  });
+}
+
+}  // extern "C"
