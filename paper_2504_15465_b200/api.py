@@ -178,6 +178,12 @@ class Session:
             self._lib.gpuos_session_close(self._h)
             self._h = C.c_void_p()
 
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
+
     def __enter__(self) -> "Session":
         return self
 
@@ -267,6 +273,12 @@ class Device:
         if self._h:
             self._lib.gpuos_dev_close(self._h)
             self._h = C.c_void_p()
+
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def __enter__(self) -> "Device":
         return self

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
   const unsigned lane = threadIdx.x;
   unsigned long long head = 0;
   for (;;) {
+    if (ld_relaxed_gpu(&p.ctl->quit)) break;
     if (gtimer() > p.ctl->deadline) {
       atomicExch(&p.ctl->quit, 1u);
       break;
@@ -265,15 +266,20 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const unsigned lane = tid & 31;
-  const unsigned sm = smid();
-  const int tpc = p.phys2log[sm >> 1];
+  unsigned sm = smid();
+  int tpc = p.phys2log[sm >> 1];
   if (tid == 0) st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 ? 0x80000000u : 0u));
   if (tpc < 0) return;  // TPC not exposed to the scheduler
 
-  unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
 
   for (;;) {
+    // %smid can change if the CTA is ever preempted and restored elsewhere;
+    // re-derive the TPC each round so placement stays exact.
+    sm = smid();
+    tpc = p.phys2log[sm >> 1];
+    if (tpc < 0) break;
+    unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
     if (warp == 0) {
       int go = 0;
       for (;;) {
@@ -561,6 +567,11 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   d->grid = prop.multiProcessorCount * cfg.workers_per_sm;
 
   CUDA_TRY(cudaFuncSetAttribute(k_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_worker));
+  // Both kernels must ask for the same L1/shared carveout, or the SM that
+  // hosts the ingest warp cannot also host workers (measured:
+  // csrc/tools/residency_probe.cu).
+  CUDA_TRY(cudaFuncSetAttribute(k_worker, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  CUDA_TRY(cudaFuncSetAttribute(k_ingest, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_worker, kWorkerThreads, smem_worker));
   if (per_sm != cfg.workers_per_sm)
@@ -693,12 +704,12 @@ int gpuos_dev_start(gpuos_dev* d) {
   p.logical_tpcs = d->cfg.logical_tpcs;
   p.idle_sleep_ns = d->cfg.idle_sleep_ns;
 
-  k_ingest<<<1, 32, 0, d->s_ingest>>>(p);
-  CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
   k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+  k_ingest<<<1, 32, 0, d->s_ingest>>>(p);
+  CUDA_TRY(cudaGetLastError());
   d->running = true;
 
   // Every worker CTA must be resident, W per SM, 2W per logical TPC.
@@ -715,7 +726,10 @@ int gpuos_dev_start(gpuos_dev* d) {
     }
   }
   std::vector<int> per_sm(d->topo.sm_count, 0);
-  for (int i = 0; i < d->grid; ++i) ++per_sm[(d->alive_h[i] & 0x7fffffffu) - 1];
+  for (int i = 0; i < d->grid; ++i) {
+    const unsigned sm = (d->alive_h[i] & 0x7fffffffu) - 1u;
+    if (sm < per_sm.size()) ++per_sm[sm];
+  }
   for (int s = 0; s < d->topo.sm_count; ++s)
     if (per_sm[s] != d->cfg.workers_per_sm) {
       gpuos_dev_stop(d, 0, nullptr);
@@ -731,12 +745,28 @@ int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
   uint32_t data[28] = {};
   data[kFOp] = drain ? kOpDrain : kOpShutdown;
   int rc = publish(d, data);
-  if (rc != GPUOS_OK) return rc;
+  if (rc != GPUOS_OK) drain = 0;
+  if (!drain) {
+    // Abort path: also raise the quit flag directly through the side stream,
+    // so workers stop even if the ingest warp never became resident.
+    static const unsigned one = 1;
+    cudaMemcpyAsync(&d->ctl->quit, &one, sizeof one, cudaMemcpyHostToDevice, d->s_side);
+    cudaStreamSynchronize(d->s_side);
+  }
   // Completions keep arriving while draining; the caller polls them after.
-  const int64_t deadline = steady_ns() + 600'000'000'000LL;
+  const int64_t deadline = steady_ns() + (drain ? 300'000'000'000LL : 30'000'000'000LL);
   while (cudaStreamQuery(d->s_work) == cudaErrorNotReady ||
          cudaStreamQuery(d->s_ingest) == cudaErrorNotReady) {
-    if (steady_ns() > deadline) return fail(GPUOS_E_TIMEOUT, "dispatcher did not stop");
+    if (steady_ns() > deadline) {
+      if (drain) {
+        static const unsigned one = 1;
+        cudaMemcpyAsync(&d->ctl->quit, &one, sizeof one, cudaMemcpyHostToDevice, d->s_side);
+        cudaStreamSynchronize(d->s_side);
+        drain = 0;
+        continue;
+      }
+      return fail(GPUOS_E_TIMEOUT, "dispatcher did not stop");
+    }
     std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
   d->running = false;

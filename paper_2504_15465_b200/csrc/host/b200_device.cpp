@@ -488,11 +488,14 @@ KernelId MirrorDevice::register_kernel(const SimKernelSpec& spec) {
 
 void MirrorDevice::drain_some(bool all) {
   gpuos_completion buf[256];
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(120);
   for (;;) {
     const int n = gpuos_dev_poll(rt_->handle(), buf, 256);
     if (n < 0) raise(n, "gpuos_dev_poll");
     if (!all || gpuos_dev_in_flight(rt_->handle()) == 0) return;
     if (n == 0) std::this_thread::yield();
+    if (std::chrono::steady_clock::now() > deadline)
+      throw InvariantError("mirror: GPU made no progress for 120 s");
   }
 }
 
@@ -513,12 +516,15 @@ AtomId MirrorDevice::submit_atom(KernelId kernel, long lo, long hi, const std::v
   d.tag = tag;
   d.trace = r.trace;
   std::uint32_t gid = 0;
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(120);
   for (;;) {
     const int rc = gpuos_dev_submit_atom(rt_->handle(), &d, &gid);
     if (rc == GPUOS_OK) break;
     if (rc != GPUOS_E_FULL) raise(rc, "mirror submit");
     drain_some(false);  // the GPU lags the replay clock: wait for room
     std::this_thread::yield();
+    if (std::chrono::steady_clock::now() > deadline)
+      throw InvariantError("mirror: no room on the GPU for 120 s");
   }
   ++gpu_atoms_;
   placement_[kernel].ranges.emplace_back(lo, hi);
