@@ -45,6 +45,12 @@ extern "C" {
 #define GPUOS_MAX_TPCS 128     /* logical TPC ids are < 128 (two 64-bit words) */
 #define GPUOS_RESIDENT_PER_TPC 32
 
+/* ------------------------------------------------------------ config flags */
+/* start() launches only the ingest warp; atoms submitted before
+ * gpuos_dev_launch_workers() are staged on the device, so the worker
+ * kernel's CUDA-event time covers execution alone (batch measurements).  */
+#define GPUOS_DEV_DEFER_WORKERS 1u
+
 /* ------------------------------------------------------------ body kinds */
 /* What one block of an atom executes (args per kind).                     */
 #define GPUOS_BODY_STREAM 1u  /* args: src u32*, dst u32*, words/block (mult.
@@ -65,7 +71,7 @@ typedef struct gpuos_dev_config {
   int32_t atom_slots;       /* in-flight atom table size [4096]           */
   int32_t ring_entries;     /* host->device submit ring [4096]            */
   int32_t idle_sleep_ns;    /* worker back-off while idle [256]           */
-  uint32_t flags;           /* reserved, 0                                */
+  uint32_t flags;           /* GPUOS_DEV_* flags                          */
   int32_t reserved;
 } gpuos_dev_config;
 
@@ -122,6 +128,10 @@ int gpuos_dev_get_topology(struct gpuos_dev* dev, gpuos_dev_topology* out);
 
 /* Launch the persistent dispatcher (ingest + worker kernels). */
 int gpuos_dev_start(struct gpuos_dev* dev);
+/* With GPUOS_DEV_DEFER_WORKERS: launch the worker kernel now. */
+int gpuos_dev_launch_workers(struct gpuos_dev* dev);
+/* Ring entries consumed by the device / published by the host so far. */
+int gpuos_dev_consumed(struct gpuos_dev* dev, uint64_t* consumed, uint64_t* published);
 /* drain != 0: wait until every submitted atom completed, then stop.
  * Returns the worker kernel's CUDA-event elapsed time in *elapsed_ms.       */
 int gpuos_dev_stop(struct gpuos_dev* dev, int drain, float* elapsed_ms);

@@ -32,6 +32,7 @@ GPUOS_BODY_STREAM = 1
 GPUOS_BODY_GEMM_BF16 = 2
 GPUOS_BODY_SPIN = 3
 GPUOS_E_FULL = -5
+GPUOS_DEV_DEFER_WORKERS = 1
 
 # Every symbol the C headers declare (tests check the library exports them).
 DEV_SYMBOLS = [
@@ -39,7 +40,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_stop", "gpuos_dev_submit_atom", "gpuos_dev_set_atom_paused",
     "gpuos_dev_set_tpc_fence", "gpuos_dev_poll", "gpuos_dev_now_ns", "gpuos_dev_in_flight",
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
-    "gpuos_dev_memset", "gpuos_dev_last_error",
+    "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -121,6 +122,8 @@ def library() -> C.CDLL:
         "gpuos_dev_copy": (C.c_int, [P, P, P, C.c_uint64, C.c_int]),
         "gpuos_dev_memset": (C.c_int, [P, P, C.c_int, C.c_uint64]),
         "gpuos_dev_last_error": (C.c_char_p, []),
+        "gpuos_dev_launch_workers": (C.c_int, [P]),
+        "gpuos_dev_consumed": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "gpuos_session_open": (C.c_int, [C.c_char_p, C.POINTER(P)]),
         "gpuos_session_run": (C.c_int, [P, C.c_char_p, C.POINTER(C.c_void_p)]),
         "gpuos_session_close": (C.c_int, [P]),
@@ -201,11 +204,11 @@ class Device:
     """Direct handle on the persistent dispatcher (gpuos_dev_*)."""
 
     def __init__(self, workers_per_sm: int = 2, logical_tpcs: int = 0, device: int = 0,
-                 atom_slots: int = 0, idle_sleep_ns: int = 0):
+                 atom_slots: int = 0, idle_sleep_ns: int = 0, flags: int = 0):
         self._lib = library()
         cfg = DevConfig(device_ordinal=device, workers_per_sm=workers_per_sm,
                         logical_tpcs=logical_tpcs, atom_slots=atom_slots,
-                        idle_sleep_ns=idle_sleep_ns)
+                        idle_sleep_ns=idle_sleep_ns, flags=flags)
         self._h = C.c_void_p()
         self._check(self._lib.gpuos_dev_open(C.byref(cfg), C.byref(self._h)))
         self.topology = DevTopology()
@@ -218,6 +221,14 @@ class Device:
 
     def start(self) -> None:
         self._check(self._lib.gpuos_dev_start(self._h))
+
+    def launch_workers(self) -> None:
+        self._check(self._lib.gpuos_dev_launch_workers(self._h))
+
+    def consumed(self) -> tuple[int, int]:
+        c, p = C.c_uint64(), C.c_uint64()
+        self._check(self._lib.gpuos_dev_consumed(self._h, C.byref(c), C.byref(p)))
+        return c.value, p.value
 
     def stop(self, drain: bool = True) -> float:
         ms = C.c_float()

@@ -482,6 +482,9 @@ struct gpuos_dev {
   std::vector<int> tpc_resident;  // keys currently resident per logical TPC
   int32_t in_flight = 0;
   bool running = false;
+  bool workers_launched = false;
+  bool calibrated = false;
+  Params params{};
   int64_t t0_ns = 0;        // host origin
   int64_t gt_offset = 0;    // device globaltimer - host origin-relative ns
   float last_elapsed_ms = 0.f;
@@ -667,26 +670,30 @@ int gpuos_dev_start(gpuos_dev* d) {
   d->comp_head = 0;
   std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
 
-  // Calibrate device globaltimer against the host origin (+- half an RTT).
-  int64_t best_rtt = INT64_MAX;
-  for (int i = 0; i < 5; ++i) {
-    const int64_t h0 = gpuos_dev_now_ns(d);
-    k_gtimer<<<1, 1, 0, d->s_work>>>(d->gt_scratch);
-    unsigned long long g = 0;
-    CUDA_TRY(cudaMemcpyAsync(&g, d->gt_scratch, 8, cudaMemcpyDeviceToHost, d->s_work));
-    CUDA_TRY(cudaStreamSynchronize(d->s_work));
-    const int64_t h1 = gpuos_dev_now_ns(d);
-    if (h1 - h0 < best_rtt) {
-      best_rtt = h1 - h0;
-      d->gt_offset = static_cast<int64_t>(g) - (h0 + h1) / 2;
+  // Calibrate device globaltimer against the host origin (+- half an RTT),
+  // once per handle: later runs launch nothing but the dispatcher itself.
+  if (!d->calibrated) {
+    int64_t best_rtt = INT64_MAX;
+    for (int i = 0; i < 5; ++i) {
+      const int64_t h0 = gpuos_dev_now_ns(d);
+      k_gtimer<<<1, 1, 0, d->s_work>>>(d->gt_scratch);
+      unsigned long long g = 0;
+      CUDA_TRY(cudaMemcpyAsync(&g, d->gt_scratch, 8, cudaMemcpyDeviceToHost, d->s_work));
+      CUDA_TRY(cudaStreamSynchronize(d->s_work));
+      const int64_t h1 = gpuos_dev_now_ns(d);
+      if (h1 - h0 < best_rtt) {
+        best_rtt = h1 - h0;
+        d->gt_offset = static_cast<int64_t>(g) - (h0 + h1) / 2;
+      }
     }
+    d->calibrated = true;
   }
   DevCtl ctl{};
-  unsigned long long g_now = 0;
-  CUDA_TRY(cudaMemcpy(&g_now, d->gt_scratch, 8, cudaMemcpyDeviceToHost));
-  ctl.deadline = g_now + 1800ull * 1000000000ull;  // hang guard: 30 min
-  CUDA_TRY(cudaMemcpy(d->ctl, &ctl, sizeof(DevCtl), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaDeviceSynchronize());
+  // Hang guard: every dispatcher kernel exits 30 min after start regardless.
+  ctl.deadline = static_cast<unsigned long long>(d->gt_offset + gpuos_dev_now_ns(d)) +
+                 1800ull * 1000000000ull;
+  CUDA_TRY(cudaMemcpyAsync(d->ctl, &ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
 
   Params p{};
   p.atoms = d->atoms;
@@ -704,13 +711,23 @@ int gpuos_dev_start(gpuos_dev* d) {
   p.logical_tpcs = d->cfg.logical_tpcs;
   p.idle_sleep_ns = d->cfg.idle_sleep_ns;
 
-  CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
-  k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+  d->params = p;
   k_ingest<<<1, 32, 0, d->s_ingest>>>(p);
   CUDA_TRY(cudaGetLastError());
   d->running = true;
+  d->workers_launched = false;
+  if (d->cfg.flags & GPUOS_DEV_DEFER_WORKERS) return GPUOS_OK;
+  return gpuos_dev_launch_workers(d);
+}
+
+int gpuos_dev_launch_workers(gpuos_dev* d) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  if (!d->running || d->workers_launched) return fail(GPUOS_E_STATE, "workers not launchable now");
+  CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
+  k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(d->params);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+  d->workers_launched = true;
 
   // Every worker CTA must be resident, W per SM, 2W per logical TPC.
   const int64_t deadline = steady_ns() + 5'000'000'000LL;
@@ -739,9 +756,27 @@ int gpuos_dev_start(gpuos_dev* d) {
   return GPUOS_OK;
 }
 
+int gpuos_dev_consumed(gpuos_dev* d, uint64_t* consumed, uint64_t* published) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  if (consumed) *consumed = __atomic_load_n(d->consumed_h, __ATOMIC_ACQUIRE);
+  if (published) *published = d->ring_head;
+  return GPUOS_OK;
+}
+
 int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
   if (!d) return fail(GPUOS_E_CONFIG, "null device");
   if (!d->running) return fail(GPUOS_E_STATE, "dispatcher not running");
+  if (!d->workers_launched) {
+    // Deferred workers never launched: run them now so the drain completes.
+    if (drain) {
+      const int lrc = gpuos_dev_launch_workers(d);
+      if (lrc != GPUOS_OK) return lrc;
+    } else {
+      d->workers_launched = true;  // nothing to wait for on the work stream
+      CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
+      CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+    }
+  }
   uint32_t data[28] = {};
   data[kFOp] = drain ? kOpDrain : kOpShutdown;
   int rc = publish(d, data);

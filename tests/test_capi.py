@@ -1,0 +1,78 @@
+"""The C-ABI library loads on CPU and exports every function the headers in
+include/ declare; error codes follow the reference CLI (2 config, 3
+invariant). No device calls here."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(r"\b(gpuos_\w+)\s*\(", text)))
+
+
+@pytest.mark.parametrize("header", ["gpuos_dev.h", "gpuos_sim.h"])
+def test_library_exports_every_declared_symbol(api, header):
+    lib = ctypes.CDLL(api.LIB_PATH)
+    names = declared(header)
+    assert names
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    listed = set(api.DEV_SYMBOLS + api.SIM_SYMBOLS)
+    assert set(names) <= listed
+
+
+def test_session_error_codes(api):
+    with pytest.raises(api.GpuosError) as e:
+        api.run({"scenario": {"preset": "nope"}, "backend": "replay"})
+    assert e.value.code == 2
+    with pytest.raises(api.GpuosError) as e:
+        api.run({"scenario": {"preset": "fig7"}, "backend": "warp-drive"})
+    assert e.value.code == 2
+    with pytest.raises(api.GpuosError) as e:
+        api.run({"scenario": {"preset": "fig7"}, "backend": "replay", "set": {"bogus": 1}})
+    assert e.value.code == 2
+
+
+def test_device_open_fails_loudly_without_gpu(api):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(api.GpuosError) as e:
+        api.Device()
+    assert e.value.code in (-2, -4)
+
+
+def test_b200_backend_fails_loudly_without_gpu(api):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(api.GpuosError) as e:
+        api.run({"scenario": {"preset": "fig7"}, "backend": "b200", "horizon_ms": 10})
+    assert e.value.code in (2, 3)
+
+
+def test_replay_session_reuse_is_deterministic(api):
+    with api.Session({"scenario": {"preset": "inf-train"}, "backend": "replay", "horizon_ms": 500}) as s:
+        a = s.run(log=True)
+        b = s.run(log=True)
+    assert a["log"] == b["log"] and a["report"] == b["report"]
+
+
+def test_time_scaled_scenario_scales_latencies(api):
+    base = api.run({"scenario": {"preset": "fig7"}, "backend": "replay", "horizon_ms": 1000})
+    fast = api.run({"scenario": {"preset": "fig7"}, "backend": "replay", "horizon_ms": 1000,
+                    "time_scale": 10.0})
+    hp0 = base["report"]["apps"][0]
+    hp1 = fast["report"]["apps"][0]
+    assert fast["horizon_ns"] == base["horizon_ns"] // 10
+    assert hp1["completed"] == hp0["completed"]
+    assert abs(hp1["p99_ns"] * 10 - hp0["p99_ns"]) <= 0.02 * hp0["p99_ns"]
