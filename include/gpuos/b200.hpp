@@ -121,7 +121,7 @@ class B200Runtime {
     std::uint32_t* src = nullptr;
     std::uint32_t* dst = nullptr;
     std::uint64_t words = 0;  // capacity of each buffer
-    std::vector<std::uint32_t> host_src;
+    std::uint32_t* host_src = nullptr;  // pinned tenant input
   };
   Workspace& workspace(std::uint32_t id, std::uint64_t words);
   void ensure_trace(KernelId kid, long blocks);

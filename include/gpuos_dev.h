@@ -156,6 +156,9 @@ int gpuos_dev_free(struct gpuos_dev* dev, void* ptr);
 int gpuos_dev_copy(struct gpuos_dev* dev, void* dst, const void* src,
                    uint64_t bytes, int kind /* 1 H2D, 2 D2H, 3 D2D */);
 int gpuos_dev_memset(struct gpuos_dev* dev, void* dst, int value, uint64_t bytes);
+/* Pinned host memory for tenant inputs/outputs (fast, truly async H2D/D2H). */
+int gpuos_dev_host_alloc(struct gpuos_dev* dev, uint64_t bytes, void** ptr);
+int gpuos_dev_host_free(struct gpuos_dev* dev, void* ptr);
 
 const char* gpuos_dev_last_error(void);
 

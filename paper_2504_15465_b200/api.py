@@ -41,6 +41,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_set_tpc_fence", "gpuos_dev_poll", "gpuos_dev_now_ns", "gpuos_dev_in_flight",
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
+    "gpuos_dev_host_alloc", "gpuos_dev_host_free",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -123,6 +124,8 @@ def library() -> C.CDLL:
         "gpuos_dev_memset": (C.c_int, [P, P, C.c_int, C.c_uint64]),
         "gpuos_dev_last_error": (C.c_char_p, []),
         "gpuos_dev_launch_workers": (C.c_int, [P]),
+        "gpuos_dev_host_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
+        "gpuos_dev_host_free": (C.c_int, [P, P]),
         "gpuos_dev_consumed": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "gpuos_session_open": (C.c_int, [C.c_char_p, C.POINTER(P)]),
         "gpuos_session_run": (C.c_int, [P, C.c_char_p, C.POINTER(C.c_void_p)]),

@@ -982,4 +982,16 @@ int gpuos_dev_memset(gpuos_dev* d, void* dst, int value, uint64_t bytes) {
   return GPUOS_OK;
 }
 
+int gpuos_dev_host_alloc(gpuos_dev* d, uint64_t bytes, void** ptr) {
+  if (!d || !ptr) return fail(GPUOS_E_CONFIG, "null argument");
+  CUDA_TRY(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault));
+  return GPUOS_OK;
+}
+
+int gpuos_dev_host_free(gpuos_dev* d, void* ptr) {
+  if (!d) return fail(GPUOS_E_CONFIG, "null device");
+  CUDA_TRY(cudaFreeHost(ptr));
+  return GPUOS_OK;
+}
+
 }  // extern "C"

@@ -69,6 +69,7 @@ B200Runtime::~B200Runtime() {
   for (auto& [id, w] : ws_) {
     gpuos_dev_free(dev_, w.src);
     gpuos_dev_free(dev_, w.dst);
+    gpuos_dev_host_free(dev_, w.host_src);
   }
   for (auto* p : trace_chunks_) gpuos_dev_free(dev_, p);
   gpuos_dev_close(dev_);
@@ -92,14 +93,15 @@ B200Runtime::Workspace& B200Runtime::workspace(std::uint32_t id, std::uint64_t w
   check(gpuos_dev_alloc(dev_, words * 4, &p), "workspace alloc");
   w.dst = static_cast<std::uint32_t*>(p);
   w.words = words;
-  w.host_src.resize(words);
+  check(gpuos_dev_host_alloc(dev_, words * 4, &p), "pinned input alloc");
+  w.host_src = static_cast<std::uint32_t*>(p);
   std::uint64_t s = mix64(id);
   for (std::uint64_t i = 0; i < words; i += 2) {
     s = mix64(s);
     w.host_src[i] = static_cast<std::uint32_t>(s);
     if (i + 1 < words) w.host_src[i + 1] = static_cast<std::uint32_t>(s >> 32);
   }
-  check(gpuos_dev_copy(dev_, w.src, w.host_src.data(), words * 4, 1), "workspace upload");
+  check(gpuos_dev_copy(dev_, w.src, w.host_src, words * 4, 1), "workspace upload");
   check(gpuos_dev_memset(dev_, w.dst, 0, words * 4), "workspace clear");
   return w;
 }
@@ -210,7 +212,7 @@ std::uint64_t B200Runtime::workspace_bytes() const {
 std::uint64_t B200Runtime::upload_inputs() {
   std::uint64_t bytes = 0;
   for (auto& [id, w] : ws_) {
-    check(gpuos_dev_copy(dev_, w.src, w.host_src.data(), w.words * 4, 1), "upload");
+    check(gpuos_dev_copy(dev_, w.src, w.host_src, w.words * 4, 1), "upload");
     bytes += w.words * 4;
   }
   return bytes;

@@ -150,13 +150,16 @@ std::string run_session(gpuos_session* s, const json& overrides) {
   std::ostringstream log;
   long hp_atoms = 0, be_atoms = 0;
   std::vector<long> app_atoms;
+  std::vector<long long> app_blocks(cfg.apps.size(), 0);
   RunHooks hooks;
-  if (want_log) {
-    hooks.on_dispatch = [&](const DispatchRecord& d) {
+  hooks.on_dispatch = [&](const DispatchRecord& d) {
+    app_blocks[static_cast<std::size_t>(d.app)] += d.hi - d.lo;
+    if (want_log)
       log << "D " << d.now << ' ' << d.atom << ' ' << d.app << ' ' << d.kernel << ' ' << d.lo
           << ' ' << d.hi << ' ' << d.priority << ' ' << (d.atomized ? 1 : 0) << ' '
           << runs_of(*d.tpcs) << '\n';
-    };
+  };
+  if (want_log) {
     hooks.on_complete = [&](const AtomCompletion& c) {
       log << "C " << c.complete_time << ' ' << c.atom << ' ' << c.tag << ' ' << c.dispatch_time
           << '\n';
@@ -215,6 +218,13 @@ std::string run_session(gpuos_session* s, const json& overrides) {
     for (std::size_t k = 0; k < dev.kernels().size(); ++k) blocks += dev.blocks_executed(static_cast<KernelId>(k));
     b["blocks"] = blocks;
     b["atoms"] = dev.timeline().size();
+    // Algorithmic HBM bytes of the STREAM bodies executed: 8 per word.
+    double stream_bytes = 0.0;
+    for (const AtomTimeline& a : dev.timeline()) {
+      const auto r = dev.runtime().resolve(a.kernel, dev.kernels()[a.kernel]);
+      if (r.body == 1u) stream_bytes += 8.0 * static_cast<double>(r.words) * static_cast<double>(a.hi - a.lo);
+    }
+    b["stream_bytes"] = stream_bytes;
     if (want_timeline) {
       json tl = json::object();
       std::vector<long long> submit, complete, first, last, lo, hi, tag, prio, kern;
@@ -269,6 +279,7 @@ std::string run_session(gpuos_session* s, const json& overrides) {
   if (want_requests) out["request_log"] = res.request_log;
   if (want_log) out["log"] = log.str();
   out["atoms"] = json{{"hp", hp_atoms}, {"be", be_atoms}, {"per_app", app_atoms}};
+  out["blocks_per_app"] = app_blocks;
   out["horizon_ns"] = cfg.horizon;
   out["total_tpcs"] = cfg.topo.total_tpcs();
   return out.dump();

@@ -1,0 +1,248 @@
+"""Device-level parity of the persistent sm_100a dispatcher, through the C
+ABI (include/gpuos_dev.h). Checked against the CPU oracle: every block of
+every atom runs exactly once, only on SMs of the atom's TPC set, and STREAM
+body outputs equal oracle.policy.stream_expect bit for bit. Also the
+reference engine's priority-refill, pause and revocation semantics
+(device.cpp:165-206) on real hardware."""
+from __future__ import annotations
+
+import random
+import time
+
+import numpy as np
+import pytest
+
+from oracle.policy import stream_expect
+
+pytestmark = pytest.mark.gpu
+
+
+def wait_all(dev, n, timeout=30.0):
+    done = []
+    t0 = time.time()
+    while len(done) < n:
+        done += dev.poll()
+        assert time.time() - t0 < timeout, f"only {len(done)}/{n} atoms completed"
+    return done
+
+
+def decode(trace):
+    tr = trace.cpu().numpy().view(np.uint32)
+    return tr >> 16, (tr & 0xFFFF).astype(np.int64) - 1
+
+
+@pytest.fixture()
+def torch_mod(cuda_device):
+    import torch
+
+    return torch
+
+
+def test_topology_and_residency(api, cuda_device):
+    with api.Device(workers_per_sm=2) as dev:
+        t = dev.topology
+        assert (t.sm_count, t.physical_tpcs, t.logical_tpcs) == (148, 74, 74)
+        assert t.workers_per_tpc == 4
+        dev.start()  # fails loudly unless every SM hosts exactly W workers
+        dev.stop()
+
+
+@pytest.mark.parametrize("workers_per_sm", [1, 2, 4])
+def test_stream_atoms_exactly_once_placed_bit_exact(api, torch_mod, workers_per_sm):
+    torch = torch_mod
+    rng = random.Random(workers_per_sm)
+    words, blocks = 1024, 6000
+    src = torch.randint(-2**31, 2**31 - 1, (blocks * words,), dtype=torch.int32, device="cuda")
+    dst = torch.zeros_like(src)
+    trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+    salt = 0x5EED1234
+    # Random partition into atoms with random TPC sets and priorities,
+    # including single-block atoms and the highest TPC ids.
+    cuts = sorted(rng.sample(range(1, blocks), 60))
+    ranges = list(zip([0] + cuts, cuts + [blocks]))
+    specs = []
+    for lo, hi in ranges:
+        k = rng.choice([1, 2, 5, 20, 74])
+        tpcs = sorted(rng.sample(range(74), k)) if k < 74 else list(range(74))
+        if rng.random() < 0.1:
+            tpcs = [73]
+        specs.append((lo, hi, tpcs, rng.choice([10, 20, 30])))
+    with api.Device(workers_per_sm=workers_per_sm) as dev:
+        dev.start()
+        for lo, hi, tpcs, prio in specs:
+            dev.submit(lo, hi, tpcs, prio, api.GPUOS_BODY_STREAM,
+                       [src.data_ptr(), dst.data_ptr(), words, salt, 0], trace=trace.data_ptr())
+        done = wait_all(dev, len(specs))
+        dev.stop()
+    counts, sm = decode(trace)
+    assert (counts == 1).all(), f"{int((counts == 0).sum())} missing, {int((counts > 1).sum())} duplicated"
+    for (lo, hi, tpcs, _), c in zip(specs, sorted(done, key=lambda c: c.atom_id)):
+        assert set((sm[lo:hi] >> 1).tolist()) <= set(tpcs)
+        assert c.blocks == hi - lo
+        touched = {t for t in range(74) if (c.tpc_touched[t >> 6] >> (t & 63)) & 1}
+        assert touched <= set(tpcs) and touched
+        assert c.dev_last_end_ns >= c.dev_first_start_ns
+    expect = stream_expect(src.cpu().numpy().view(np.uint32), salt, 0)
+    assert np.array_equal(dst.cpu().numpy().view(np.uint32), expect)
+
+
+def test_chunked_stream_and_block_offsets(api, torch_mod):
+    """args[4] = chunks: block b works on chunk b % chunks (bounded workspace)."""
+    torch = torch_mod
+    words, chunks, blocks = 512, 7, 500
+    src = torch.randint(-2**31, 2**31 - 1, (chunks * words,), dtype=torch.int32, device="cuda")
+    dst = torch.zeros_like(src)
+    trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+    with api.Device() as dev:
+        dev.start()
+        dev.submit(100, 500, list(range(10, 30)), 20, api.GPUOS_BODY_STREAM,
+                   [src.data_ptr(), dst.data_ptr(), words, 77, chunks], trace=trace.data_ptr())
+        dev.submit(0, 100, [0], 30, api.GPUOS_BODY_STREAM,
+                   [src.data_ptr(), dst.data_ptr(), words, 77, chunks], trace=trace.data_ptr())
+        wait_all(dev, 2)
+        dev.stop()
+    counts, sm = decode(trace)
+    assert (counts == 1).all()
+    assert set((sm[100:] >> 1).tolist()) <= set(range(10, 30))
+    assert set((sm[:100] >> 1).tolist()) == {0}
+    assert np.array_equal(dst.cpu().numpy().view(np.uint32),
+                          stream_expect(src.cpu().numpy().view(np.uint32), 77, 0))
+
+
+def test_higher_priority_takes_freed_slots_first(api, torch_mod):
+    """A late high-priority atom overtakes the waiting blocks of a resident
+    low-priority atom on the same TPC (reference refill rule,
+    device.cpp:188-206; test_device.cpp:101-115)."""
+    with api.Device(workers_per_sm=2) as dev:
+        dev.start()
+        lp = dev.submit(0, 200, [0], 5, api.GPUOS_BODY_SPIN, [200_000, 0, 0, 0, 0], tag=1)
+        time.sleep(0.002)
+        t_hp = dev.now_ns()
+        hp = dev.submit(0, 8, [0], 30, api.GPUOS_BODY_SPIN, [50_000, 0, 0, 0, 0], tag=2)
+        done = {c.atom_id: c for c in wait_all(dev, 2)}
+        dev.stop()
+    # 4 workers on TPC 0: HP waits at most one LP block (200 us) for a slot,
+    # then runs 2 waves of 50 us; LP still has ~190 blocks (~10 ms) to go.
+    assert done[hp].dev_last_end_ns - t_hp < 1_000_000
+    assert done[hp].dev_last_end_ns < done[lp].dev_last_end_ns - 5_000_000
+
+
+def test_pause_keeps_in_flight_blocks_and_resumes(api, torch_mod):
+    torch = torch_mod
+    trace = torch.zeros(400, dtype=torch.int32, device="cuda")
+    with api.Device() as dev:
+        dev.start()
+        a = dev.submit(0, 400, [3], 20, api.GPUOS_BODY_SPIN, [100_000, 0, 0, 0, 0],
+                       trace=trace.data_ptr())
+        time.sleep(0.001)
+        dev.pause(a, True)
+        time.sleep(0.003)  # let in-flight blocks finish
+        before = int((decode(trace)[0] > 0).sum())
+        time.sleep(0.005)
+        after = int((decode(trace)[0] > 0).sum())
+        assert after == before and 0 < before < 400
+        dev.pause(a, False)
+        wait_all(dev, 1)
+        dev.stop()
+    assert (decode(trace)[0] == 1).all()
+
+
+def test_fence_revokes_tpcs_mid_atom(api, torch_mod):
+    """Raising a TPC's fence stops a stolen (priority 10) atom from starting
+    new blocks there without relaunching it: block-granular revocation."""
+    torch = torch_mod
+    blocks = 800
+    trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+    with api.Device() as dev:
+        dev.start()
+        dev.submit(0, blocks, [0, 1, 2, 3], 10, api.GPUOS_BODY_SPIN, [100_000, 0, 0, 0, 0],
+                   trace=trace.data_ptr())
+        time.sleep(0.001)
+        dev.fence(0, 11)
+        dev.fence(1, 11)
+        time.sleep(0.0005)
+        frontier = int(np.nonzero(decode(trace)[0])[0].max()) + 64  # claimed before the fence took hold
+        wait_all(dev, 1)
+        dev.fence(0, 0)
+        dev.fence(1, 0)
+        dev.stop()
+    counts, sm = decode(trace)
+    assert (counts == 1).all()
+    late = sm[frontier:] >> 1
+    assert frontier < blocks - 100
+    assert set(late.tolist()) <= {2, 3}
+
+
+def test_slot_recycling_many_small_atoms(api, torch_mod):
+    """10k one-to-three-block atoms through a 64-slot atom table: slots are
+    reused while stale resident keys are still visible; the sequence-tagged
+    claim word must keep every block exactly once."""
+    torch = torch_mod
+    n_atoms = 10_000
+    trace = torch.zeros(n_atoms * 3, dtype=torch.int32, device="cuda")
+    rng = random.Random(5)
+    with api.Device(atom_slots=64) as dev:
+        dev.start()
+        sub, got, b = 0, 0, 0
+        t0 = time.time()
+        while got < n_atoms:
+            if sub < n_atoms:
+                k = rng.randint(1, 3)
+                aid = dev.try_submit(b, b + k, [rng.randrange(74)], rng.choice([10, 20, 30]),
+                                     api.GPUOS_BODY_SPIN, [0, 0, 0, 0, 0], trace=trace.data_ptr())
+                if aid is not None:
+                    sub += 1
+                    b += k
+            got += len(dev.poll())
+            assert time.time() - t0 < 60
+        dev.stop()
+    counts, _ = decode(trace)
+    assert (counts[:b] == 1).all() and (counts[b:] == 0).all()
+
+
+def test_residency_limit_is_enforced(api, torch_mod):
+    with api.Device() as dev:
+        dev.start()
+        for _ in range(32):
+            dev.submit(0, 1, [5], 20, api.GPUOS_BODY_SPIN, [2_000_000, 0, 0, 0, 0])
+        with pytest.raises(api.GpuosError) as e:
+            dev.submit(0, 1, [5], 20, api.GPUOS_BODY_SPIN, [0, 0, 0, 0, 0])
+        assert e.value.code == api.GPUOS_E_FULL
+        wait_all(dev, 32)
+        dev.stop()
+
+
+def test_bad_submissions_rejected(api, torch_mod):
+    with api.Device() as dev:
+        dev.start()
+        for lo, hi, tpcs in [(5, 5, [0]), (-1, 3, [0]), (0, 3, []), (0, 3, [74])]:
+            with pytest.raises(api.GpuosError) as e:
+                dev.submit(lo, hi, tpcs, 20, api.GPUOS_BODY_SPIN, [0, 0, 0, 0, 0])
+            assert e.value.code == -2
+        dev.stop()
+
+
+def test_batch_stream_bandwidth(api, torch_mod):
+    """Full-width atomized STREAM kernel, workers launched after staging:
+    the worker kernel's CUDA-event time is execution only."""
+    torch = torch_mod
+    words, blocks = 65536, 8192  # 256 KiB per block, 2 GiB per buffer
+    src = torch.randint(-2**31, 2**31 - 1, (blocks * words,), dtype=torch.int32, device="cuda")
+    dst = torch.zeros_like(src)
+    torch.cuda.synchronize()
+    with api.Device(flags=api.GPUOS_DEV_DEFER_WORKERS) as dev:
+        best = 0.0
+        for _ in range(3):
+            dev.start()
+            n_atoms = 32
+            per = blocks // n_atoms
+            for i in range(n_atoms):
+                dev.submit(i * per, (i + 1) * per, list(range(74)), 20, api.GPUOS_BODY_STREAM,
+                           [src.data_ptr(), dst.data_ptr(), words, 9, 0])
+            while dev.consumed()[0] < dev.consumed()[1]:
+                pass
+            dev.launch_workers()
+            ms = dev.stop(drain=True)
+            wait_all(dev, n_atoms)
+            best = max(best, blocks * words * 8 / (ms * 1e-3) / 1e9)
+    assert best > 3000, f"{best:.0f} GB/s"

@@ -1,0 +1,94 @@
+"""The gpuos:: scheduler driving the B200 through the C ABI.
+
+* Mirror backend: the replay clock drives every decision (so the
+  dispatch/completion log must equal the reference's golden log byte for
+  byte) while every atom is also executed on the B200 on exactly the TPC
+  set the scheduler chose; then every block is checked: executed once, on
+  an SM of its atom's TPC set, body output equal to the CPU oracle.
+* Live backend: the persistent dispatcher executes a time-scaled stacked
+  scenario in real time with per-block verification.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import os
+
+import pytest
+
+from conftest import GOLDEN
+from oracle.policy import percentile
+
+pytestmark = pytest.mark.gpu
+CASES = json.load(open(os.path.join(GOLDEN, "cases.json")))["cases"]
+
+MIRROR = {
+    "fig7_2s": {"scenario": {"preset": "fig7"}, "horizon_ms": 2000},
+    "inf-inf_2s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 2000},
+    "inf-train_2s": {"scenario": {"preset": "inf-train"}, "horizon_ms": 2000},
+    "inf-inf_mps_like_1s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 1000, "policy": "mps_like"},
+    "inf-inf_time_slice_1s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 1000, "policy": "time_slice"},
+    "cli_smoke": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "cli_smoke.json")}},
+    "random_7": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "random_7.json")}},
+}
+
+
+@pytest.mark.parametrize("name", sorted(MIRROR))
+def test_mirror_executes_reference_schedule_on_b200(api, cuda_device, name):
+    req = dict(MIRROR[name], backend="mirror", log=True,
+               b200={"min_words": 256, "words_per_us": 0.0, "chunk_cap": 64})
+    r = api.run(req)
+    ref = gzip.open(os.path.join(GOLDEN, "logs", name + ".log.gz")).read().decode()
+    assert r["log"].splitlines() == [line for line in ref.splitlines() if line[:1] in "DC"]
+    v = r["verify"]
+    assert v["ok"], v
+    assert v["missing"] == v["duplicated"] == v["misplaced"] == v["bad_words"] == 0
+    assert r["gpu_atoms"] == r["atoms"]["hp"] + r["atoms"]["be"]
+    assert v["checked_words"] > 0
+
+
+def live_request(**kw):
+    req = {"scenario": {"preset": "fig7"}, "backend": "b200", "device": "b200",
+           "quota_scale": 74 / 54, "time_scale": 10.0, "horizon_ms": 1000,
+           "b200": {"chunk_cap": 64}, "requests": True}
+    req.update(kw)
+    return req
+
+
+def hp_latencies(r):
+    lat = []
+    for line in r["request_log"].splitlines():
+        j = json.loads(line)
+        if j["app"] == "hp" and j["completed"]:
+            lat.append(j["latency_us"])
+    return lat
+
+
+def test_live_fig7_verified(api, cuda_device):
+    with api.Session(live_request(verify=True, timeline=True,
+                                  b200={"chunk_cap": 64, "trace": True})) as s:
+        s.run()  # warm: creates workspaces
+        r = s.run()
+    v = r["verify"]
+    assert v["ok"], v
+    hp, be = r["report"]["apps"]
+    assert hp["completed"] == hp["offered"] > 0
+    assert be["completed"] > 0
+    # Every atom ran only on TPCs of its set and touched at least one.
+    tl = r["b200"]["timeline"]
+    for m0, m1, t0, t1 in zip(tl["mask0"], tl["mask1"], tl["touched0"], tl["touched1"]):
+        assert (t0 & ~m0) == 0 and (t1 & ~m1) == 0 and (t0 | t1) != 0
+    # HP requests meet their (scaled) 8 ms SLO.
+    assert percentile(hp_latencies(r), 99) <= 8000
+
+
+def test_live_block_revocation_helps_hp_tail(api, cuda_device):
+    with api.Session(live_request()) as s:
+        s.run()
+        base = [s.run() for _ in range(2)]
+        rev = [s.run(set={"block_revocation": True}) for _ in range(2)]
+    p_base = percentile(sum((hp_latencies(r) for r in base), []), 99)
+    p_rev = percentile(sum((hp_latencies(r) for r in rev), []), 99)
+    assert p_rev <= p_base * 1.25 + 50
+    for r in rev:
+        assert r["report"]["apps"][0]["completed"] == r["report"]["apps"][0]["offered"]
