@@ -302,21 +302,13 @@ def saturation(api, local: int, args) -> dict:
     dst = torch.empty_like(src)
     torch.cuda.synchronize()
     best = 0.0
-    with api.Device(device=local, workers_per_sm=args.workers_per_sm,
-                    flags=api.GPUOS_DEV_DEFER_WORKERS) as dev:
+    n_atoms = 64
+    per = blocks // n_atoms
+    descs = [api.Device.desc(i * per, (i + 1) * per, range(74), 20, api.GPUOS_BODY_STREAM,
+                             [src.data_ptr(), dst.data_ptr(), words, 7, chunks]) for i in range(n_atoms)]
+    with api.Device(device=local, workers_per_sm=args.workers_per_sm) as dev:
         for _ in range(3):
-            dev.start()
-            n_atoms = 64
-            per = blocks // n_atoms
-            for i in range(n_atoms):
-                dev.submit(i * per, (i + 1) * per, list(range(74)), 20, api.GPUOS_BODY_STREAM,
-                           [src.data_ptr(), dst.data_ptr(), words, 7, chunks])
-            while True:
-                c, p = dev.consumed()
-                if c >= p:
-                    break
-            dev.launch_workers()
-            ms = dev.stop(drain=True)
+            ms = dev.run_batch(descs)  # single k_worker launch, CUDA events
             while dev.in_flight():
                 dev.poll()
             best = max(best, blocks * words * 8 / (ms * 1e-3) / 1e9)

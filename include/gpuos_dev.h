@@ -130,6 +130,12 @@ int gpuos_dev_get_topology(struct gpuos_dev* dev, gpuos_dev_topology* out);
 int gpuos_dev_start(struct gpuos_dev* dev);
 /* With GPUOS_DEV_DEFER_WORKERS: launch the worker kernel now. */
 int gpuos_dev_launch_workers(struct gpuos_dev* dev);
+/* Batch mode (dispatcher stopped): stage n atoms directly into the device
+ * tables and run the worker kernel alone until all complete. Returns its
+ * CUDA-event time; completions are then read with gpuos_dev_poll. A single
+ * self-contained launch: the path ncu profiles and rooflines are taken on. */
+int gpuos_dev_run_batch(struct gpuos_dev* dev, const gpuos_atom_desc* descs, int32_t n,
+                        float* elapsed_ms);
 /* Ring entries consumed by the device / published by the host so far. */
 int gpuos_dev_consumed(struct gpuos_dev* dev, uint64_t* consumed, uint64_t* published);
 /* drain != 0: wait until every submitted atom completed, then stop.

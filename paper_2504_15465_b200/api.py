@@ -41,7 +41,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_set_tpc_fence", "gpuos_dev_poll", "gpuos_dev_now_ns", "gpuos_dev_in_flight",
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
-    "gpuos_dev_host_alloc", "gpuos_dev_host_free",
+    "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -124,6 +124,7 @@ def library() -> C.CDLL:
         "gpuos_dev_memset": (C.c_int, [P, P, C.c_int, C.c_uint64]),
         "gpuos_dev_last_error": (C.c_char_p, []),
         "gpuos_dev_launch_workers": (C.c_int, [P]),
+        "gpuos_dev_run_batch": (C.c_int, [P, C.POINTER(AtomDesc), C.c_int32, C.POINTER(C.c_float)]),
         "gpuos_dev_host_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
         "gpuos_dev_host_free": (C.c_int, [P, P]),
         "gpuos_dev_consumed": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -236,6 +237,27 @@ class Device:
     def stop(self, drain: bool = True) -> float:
         ms = C.c_float()
         self._check(self._lib.gpuos_dev_stop(self._h, 1 if drain else 0, C.byref(ms)))
+        return ms.value
+
+    @staticmethod
+    def desc(lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
+             trace: int | None = None) -> AtomDesc:
+        d = AtomDesc()
+        d.lo, d.hi, d.priority, d.body, d.tag = lo, hi, priority, body, tag
+        m = [0, 0]
+        for t in tpcs:
+            m[t >> 6] |= 1 << (t & 63)
+        d.tpc_mask[0], d.tpc_mask[1] = m
+        for i, a in enumerate(args):
+            d.args[i] = int(a)
+        d.trace = trace
+        return d
+
+    def run_batch(self, descs: list[AtomDesc]) -> float:
+        """Stage `descs` and run the worker kernel alone; returns its ms."""
+        arr = (AtomDesc * len(descs))(*descs)
+        ms = C.c_float()
+        self._check(self._lib.gpuos_dev_run_batch(self._h, arr, len(descs), C.byref(ms)))
         return ms.value
 
     def submit(self, lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,

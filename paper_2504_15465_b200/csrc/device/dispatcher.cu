@@ -824,6 +824,123 @@ int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
   return GPUOS_OK;
 }
 
+// Batch mode: the host stages a whole set of atoms straight into the device
+// tables (exactly the state the ingest warp would build), then launches the
+// worker kernel alone with the drain flag raised. The kernel exits when the
+// last atom completes, so its CUDA-event time is pure execution, and it is a
+// single self-contained launch that ncu can replay.
+int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, float* elapsed_ms) {
+  if (!d || (!descs && n > 0)) return fail(GPUOS_E_CONFIG, "null argument");
+  if (d->running) return fail(GPUOS_E_STATE, "dispatcher running");
+  if (d->in_flight != 0) return fail(GPUOS_E_STATE, "atoms still in flight");
+  if (n < 1 || n > d->cfg.atom_slots) return fail(GPUOS_E_FULL, "batch larger than the atom table");
+  CUDA_TRY(cudaSetDevice(d->device));
+  const int T = d->cfg.logical_tpcs;
+  std::vector<DevAtom> atoms(static_cast<size_t>(n));
+  std::vector<unsigned long long> resident(static_cast<size_t>(T) * kResident, 0ull);
+  std::vector<int> fill(static_cast<size_t>(T), 0);
+  std::vector<uint32_t> ids(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    const gpuos_atom_desc& a = descs[i];
+    if (a.lo < 0 || a.hi <= a.lo || a.hi - a.lo > 0xfffffffeLL)
+      return fail(GPUOS_E_CONFIG, "atom block range out of bounds");
+    if (a.body != GPUOS_BODY_STREAM && a.body != GPUOS_BODY_SPIN)
+      return fail(GPUOS_E_CONFIG, "unknown body kind");
+    const uint32_t seq = d->next_seq++;
+    const int prio = map_priority(a.priority);
+    DevAtom& x = atoms[static_cast<size_t>(i)];
+    std::memset(&x, 0, sizeof x);
+    x.claim = static_cast<unsigned long long>(seq) << 32;
+    x.count = static_cast<unsigned>(a.hi - a.lo);
+    x.seq = seq;
+    x.prio = prio;
+    x.body = a.body;
+    x.lo = a.lo;
+    x.atom_id = ids[static_cast<size_t>(i)] = d->next_atom_id++;
+    std::memcpy(x.args, a.args, sizeof x.args);
+    x.tag = a.tag;
+    x.trace = a.trace;
+    x.mask[0] = a.tpc_mask[0];
+    x.mask[1] = a.tpc_mask[1];
+    x.t_first = ~0ull;
+    const unsigned long long key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
+                                   (static_cast<unsigned long long>(~seq) << 24) |
+                                   static_cast<unsigned long long>(i);
+    bool any = false;
+    for (int t = 0; t < GPUOS_MAX_TPCS; ++t) {
+      if (!((a.tpc_mask[t >> 6] >> (t & 63)) & 1ull)) continue;
+      if (t >= T) return fail(GPUOS_E_CONFIG, "TPC id out of range");
+      if (fill[t] >= kResident) return fail(GPUOS_E_FULL, "more than 32 atoms on one TPC");
+      x.entry[t] = static_cast<unsigned char>(fill[t]);
+      resident[static_cast<size_t>(t) * kResident + fill[t]++] = key;
+      any = true;
+    }
+    if (!any) return fail(GPUOS_E_CONFIG, "atom needs a non-empty TPC set");
+  }
+  // Host bookkeeping: slots 0..n-1 in flight, completions consumed by poll().
+  d->free_slots.clear();
+  for (int s = d->cfg.atom_slots - 1; s >= n; --s) d->free_slots.push_back(static_cast<uint32_t>(s));
+  const int64_t now = gpuos_dev_now_ns(d);
+  for (int i = 0; i < n; ++i) {
+    HostAtom& h = d->slots[static_cast<size_t>(i)];
+    h.atom_id = ids[static_cast<size_t>(i)];
+    h.submit_ns = now;
+    h.mask[0] = descs[i].tpc_mask[0];
+    h.mask[1] = descs[i].tpc_mask[1];
+    h.live = true;
+  }
+  std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
+  std::memset(d->comp_h, 0, sizeof(CompRec) * d->cfg.atom_slots);
+  std::memset(d->alive_h, 0, sizeof(unsigned) * d->grid);
+  d->comp_head = 0;
+  d->in_flight = n;
+
+  CUDA_TRY(cudaMemcpy(d->atoms, atoms.data(), sizeof(DevAtom) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d->resident, resident.data(), sizeof(unsigned long long) * resident.size(),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
+  DevCtl ctl{};
+  ctl.drain = 1;
+  ctl.outstanding = n;
+  ctl.deadline = ~0ull >> 1;
+  CUDA_TRY(cudaMemcpy(d->ctl, &ctl, sizeof ctl, cudaMemcpyHostToDevice));
+
+  Params p{};
+  p.atoms = d->atoms;
+  p.resident = d->resident;
+  p.version = d->version;
+  p.fence = d->fence;
+  p.ctl = d->ctl;
+  p.phys2log = d->phys2log;
+  p.ring = d->ring_d;
+  p.comp = d->comp_d;
+  p.consumed = d->consumed_d;
+  p.alive = d->alive_d;
+  p.ring_cap = static_cast<unsigned>(d->cfg.ring_entries);
+  p.comp_cap = static_cast<unsigned>(d->cfg.atom_slots);
+  p.logical_tpcs = T;
+  p.idle_sleep_ns = d->cfg.idle_sleep_ns;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
+  k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+  CUDA_TRY(cudaStreamSynchronize(d->s_work));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, d->ev_start, d->ev_stop));
+  if (elapsed_ms) *elapsed_ms = ms;
+  d->last_elapsed_ms = ms;
+  DevCtl after{};
+  CUDA_TRY(cudaMemcpy(&after, d->ctl, sizeof after, cudaMemcpyDeviceToHost));
+  d->stats.blocks_executed += after.blocks;
+  d->stats.worker_busy_ns += after.busy_ns;
+  d->stats.claim_retries += after.retries;
+  d->stats.kernel_elapsed_ns = static_cast<int64_t>(ms * 1e6);
+  if (after.outstanding != 0) return fail(GPUOS_E_INVARIANT, "batch finished with atoms outstanding");
+  return GPUOS_OK;
+}
+
 int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom_id) {
   if (!d || !a) return fail(GPUOS_E_CONFIG, "null argument");
   if (!d->running) return fail(GPUOS_E_STATE, "dispatcher not running");

@@ -223,26 +223,38 @@ def test_bad_submissions_rejected(api, torch_mod):
 
 
 def test_batch_stream_bandwidth(api, torch_mod):
-    """Full-width atomized STREAM kernel, workers launched after staging:
-    the worker kernel's CUDA-event time is execution only."""
+    """Full-width atomized STREAM kernel in batch mode (atoms staged, worker
+    kernel launched alone): its CUDA-event time is execution only."""
     torch = torch_mod
     words, blocks = 65536, 8192  # 256 KiB per block, 2 GiB per buffer
     src = torch.randint(-2**31, 2**31 - 1, (blocks * words,), dtype=torch.int32, device="cuda")
     dst = torch.zeros_like(src)
     torch.cuda.synchronize()
-    with api.Device(flags=api.GPUOS_DEV_DEFER_WORKERS) as dev:
+    n_atoms, per = 32, blocks // 32
+    descs = [api.Device.desc(i * per, (i + 1) * per, range(74), 20, api.GPUOS_BODY_STREAM,
+                             [src.data_ptr(), dst.data_ptr(), words, 9, 0]) for i in range(n_atoms)]
+    with api.Device() as dev:
         best = 0.0
         for _ in range(3):
-            dev.start()
-            n_atoms = 32
-            per = blocks // n_atoms
-            for i in range(n_atoms):
-                dev.submit(i * per, (i + 1) * per, list(range(74)), 20, api.GPUOS_BODY_STREAM,
-                           [src.data_ptr(), dst.data_ptr(), words, 9, 0])
-            while dev.consumed()[0] < dev.consumed()[1]:
-                pass
-            dev.launch_workers()
-            ms = dev.stop(drain=True)
-            wait_all(dev, n_atoms)
+            ms = dev.run_batch(descs)
+            assert len(wait_all(dev, n_atoms)) == n_atoms
             best = max(best, blocks * words * 8 / (ms * 1e-3) / 1e9)
+    expect = stream_expect(src.cpu().numpy().view(np.uint32), 9, 0)
+    assert np.array_equal(dst.cpu().numpy().view(np.uint32), expect)
     assert best > 3000, f"{best:.0f} GB/s"
+
+
+def test_batch_mode_priority_and_placement(api, torch_mod):
+    torch = torch_mod
+    trace = torch.zeros(3000, dtype=torch.int32, device="cuda")
+    descs = [api.Device.desc(i * 100, (i + 1) * 100, [i % 74, (i * 7) % 74], 10 + 10 * (i % 3),
+                             api.GPUOS_BODY_SPIN, [2000, 0, 0, 0, 0], trace=trace.data_ptr())
+             for i in range(30)]
+    with api.Device() as dev:
+        dev.run_batch(descs)
+        done = wait_all(dev, 30)
+    counts, sm = decode(trace)
+    assert (counts == 1).all()
+    for i in range(30):
+        assert set((sm[i * 100:(i + 1) * 100] >> 1).tolist()) <= {i % 74, (i * 7) % 74}
+    assert sorted(c.blocks for c in done) == [100] * 30
