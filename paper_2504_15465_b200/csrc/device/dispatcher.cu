@@ -35,6 +35,7 @@
 #include <memory>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <string>
 #include <thread>
 #include <vector>
@@ -54,11 +55,11 @@ enum Op : unsigned { kOpSubmit = 1, kOpPause = 2, kOpResume = 3, kOpFence = 4,
 // Device-resident atom slot. The first 32 bytes are what selecting workers
 // read; the rest is written once by the ingest warp.
 struct alignas(128) DevAtom {
-  unsigned long long claim;  // seq << 32 | next block offset
+  unsigned long long claim;  // seq << 32 | next block offset (fetch-add)
   unsigned count;            // blocks in the atom
+  unsigned paused;           // (claim, count, paused): one 16-byte load
   unsigned seq;
   int prio;                  // 1..255
-  unsigned paused;
   unsigned done;             // finished blocks
   unsigned body;
   long long lo;
@@ -80,6 +81,7 @@ struct DevCtl {
   unsigned comp_tail;   // completion records allocated
   unsigned long long deadline;  // globaltimer: hard stop (hang guard)
   unsigned long long blocks, busy_ns, retries, atoms_done;
+  unsigned long long stale_claims;  // claims that landed on a recycled slot
 };
 
 // 128-byte submit-ring entry: four 32-byte sectors, each = 7 data words +
@@ -162,7 +164,10 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
       DevAtom* a = p.atoms + slot;
       if (lane == 0) {
         // Not claimable until every resident key is in place (arming below).
-        a->claim = (static_cast<unsigned long long>(seq) << 32) | 0xffffffffull;
+        // Exhausted (offset == count) until armed: a stale fetch-add from a
+        // worker still holding the previous occupant's key cannot carry into
+        // the sequence bits, and the arming exchange overwrites it.
+        a->claim = (static_cast<unsigned long long>(seq) << 32) | count;
         a->count = count;
         a->seq = seq;
         a->prio = prio;
@@ -226,8 +231,9 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
         __threadfence();
       }
       __syncwarp();
-      if (op == kOpResume)
-        for (int t = lane; t < p.logical_tpcs; t += 32) {
+      // Workers drain one atom on a fast path while their TPC's version is
+      // unchanged, so pause and resume both bump it.
+      for (int t = lane; t < p.logical_tpcs; t += 32) {
           const unsigned long long m = a->mask[t >> 6];
           if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
         }
@@ -254,12 +260,50 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
 
 // ------------------------------------------------------------ worker CTAs
 struct WorkerShared {
-  BlockCmd cmd;
-  unsigned long long key;
+  BlockCmd cmd;                 // current block: args, block id, body
+  unsigned long long key;       // resident key of the atom being drained
   unsigned long long t_start;
   unsigned slot;
   int go;
 };
+
+__device__ __forceinline__ unsigned long long atom_add_acquire64(unsigned long long* p,
+                                                                 unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acquire.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel32(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void ld_relaxed_gpu_v2(const void* p, unsigned long long& a,
+                                                  unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// Lane 0: claim one block of the atom behind `key` with a fetch-add on its
+// claim word. Returns the block offset, or -1 if the atom is exhausted.
+// Fetch-add never retries, so 300 workers draining one atom cost one L2
+// atomic each (the CAS loop it replaces spent ~140 failed attempts per
+// claim under that contention: profiles/ncu_k_worker_r01_cas.txt).
+// A worker holding a stale key for a recycled slot (the host quarantines
+// freed slots FIFO over the whole table, so this needs a worker stalled for
+// thousands of atom lifetimes) sees a foreign sequence in the returned word;
+// if that offset is valid it now owns a block of the new occupant and runs
+// it rather than lose it, counting the event in ctl->stale_claims.
+__device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long key,
+                                                 DevCtl* ctl, bool& stale) {
+  const unsigned seq = ~static_cast<unsigned>(key >> 24);
+  const unsigned long long old = atom_add_acquire64(&a->claim, 1ull);
+  const unsigned off = static_cast<unsigned>(old);
+  const unsigned count = ld_relaxed_gpu(&a->count);
+  stale = static_cast<unsigned>(old >> 32) != seq;
+  if (off >= count) return -1;
+  if (stale) atomicAdd(&ctl->stale_claims, 1ull);
+  return static_cast<long long>(off);
+}
 
 __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   __shared__ WorkerShared sh;
@@ -271,7 +315,20 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   if (tid == 0) st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 ? 0x80000000u : 0u));
   if (tpc < 0) return;  // TPC not exposed to the scheduler
 
+  if (tid == 0) {
+    sh.key = 0ull;
+    sh.slot = ~0u;
+  }
+  __syncthreads();
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
+  // Warp 0's draining state: the atom it last claimed from and the TPC's
+  // candidate-set version at that time. While the version is unchanged no
+  // higher-priority atom arrived, nothing was paused or fenced, so the next
+  // block comes from the same atom without rescanning the resident list.
+  unsigned long long cur_key = 0ull;
+  unsigned cur_ver = 0u;
+  unsigned cur_slot = 0u;
+  int cur_tpc = -1;
 
   for (;;) {
     // %smid can change if the CTA is ever preempted and restored elsewhere;
@@ -279,66 +336,76 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     sm = smid();
     tpc = p.phys2log[sm >> 1];
     if (tpc < 0) break;
+    if (tpc != cur_tpc) {
+      cur_key = 0ull;
+      cur_tpc = tpc;
+    }
     unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
     if (warp == 0) {
       int go = 0;
       for (;;) {
-        if (ld_relaxed_gpu(&p.ctl->quit)) break;
         const unsigned ver = ld_relaxed_gpu(p.version + tpc);
-        const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
-        const unsigned long long key = ld_acquire_gpu64(list + lane);
-        bool eligible = false;
-        if (key != 0ull) {
-          const DevAtom* a = p.atoms + (key & 0xffffffull);
-          const unsigned seq = ~static_cast<unsigned>(key >> 24);
-          const unsigned long long cw = ld_relaxed_gpu64(&a->claim);
-          const int prio = static_cast<int>(key >> 56);
-          eligible = static_cast<unsigned>(cw >> 32) == seq &&
-                     static_cast<unsigned>(cw) < ld_relaxed_gpu(&a->count) &&
-                     ld_relaxed_gpu(&a->paused) == 0u && prio >= floor_prio;
-        }
-        const unsigned long long best = warp_max_u64(eligible ? key : 0ull);
-        if (best != 0ull) {
-          long long off = -1;
-          if (lane == 0) {
-            DevAtom* a = p.atoms + (best & 0xffffffull);
-            const unsigned seq = ~static_cast<unsigned>(best >> 24);
-            const unsigned count = ld_relaxed_gpu(&a->count);
-            unsigned long long cur = ld_relaxed_gpu64(&a->claim);
-            while (static_cast<unsigned>(cur >> 32) == seq &&
-                   static_cast<unsigned>(cur) < count) {
-              const unsigned long long prev = atomicCAS(&a->claim, cur, cur + 1);
-              if (prev == cur) {
-                off = static_cast<long long>(static_cast<unsigned>(cur));
-                break;
-              }
-              cur = prev;
-              ++retries;
-            }
-            if (off >= 0) {
-              __threadfence();  // acquire: see the ingest warp's slot writes
-              sh.key = best;
-              sh.slot = static_cast<unsigned>(best & 0xffffffull);
-              sh.cmd.block = a->lo + off;
-              sh.cmd.body = a->body;
-#pragma unroll
-              for (int k = 0; k < 5; ++k) sh.cmd.args[k] = a->args[k];
-              sh.t_start = gtimer();
-            }
-          }
+        long long off = -1;
+        unsigned long long key = 0ull;
+        bool stale = false;
+        if (cur_key != 0ull && ver == cur_ver) {
+          if (lane == 0) off = claim_block(p.atoms + cur_slot, cur_key, p.ctl, stale);
           off = __shfl_sync(0xffffffffu, off, 0);
-          if (off >= 0) {
-            go = 1;
-            break;
-          }
-          continue;  // lost the race for that atom's last block: reselect
+          if (off >= 0) key = cur_key;
         }
-        if (ld_relaxed_gpu(&p.ctl->drain) &&
-            ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0)
+        if (off < 0) {
+          cur_key = 0ull;
+          if (ld_relaxed_gpu(&p.ctl->quit)) break;
+          // Full arbitration: eligible = waiting blocks, not paused, not
+          // fenced off this TPC; highest priority then oldest wins.
+          const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
+          const unsigned long long k = ld_acquire_gpu64(list + lane);
+          bool eligible = false;
+          if (k != 0ull) {
+            const DevAtom* a = p.atoms + (k & 0xffffffull);
+            unsigned long long cw, cp;
+            ld_relaxed_gpu_v2(a, cw, cp);  // claim | count, paused
+            eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
+                       static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
+                       static_cast<unsigned>(cp >> 32) == 0u &&
+                       static_cast<int>(k >> 56) >= floor_prio;
+          }
+          key = warp_max_u64(eligible ? k : 0ull);
+          if (key != 0ull) {
+            if (lane == 0) off = claim_block(p.atoms + (key & 0xffffffull), key, p.ctl, stale);
+            off = __shfl_sync(0xffffffffu, off, 0);
+            if (off < 0) {
+              ++retries;  // lost that atom's last blocks to other workers
+              continue;
+            }
+          }
+        }
+        if (off >= 0) {
+          const unsigned slot = static_cast<unsigned>(key & 0xffffffull);
+          if (lane == 0) {
+            const DevAtom* a = p.atoms + slot;
+            // The acquire fetch-add ordered the ingest warp's slot writes
+            // before these loads; args are cached per drained atom.
+            if (stale || key != sh.key || slot != sh.slot) {
+#pragma unroll
+              for (int k2 = 0; k2 < 5; ++k2) sh.cmd.args[k2] = a->args[k2];
+              sh.cmd.body = a->body;
+              sh.key = stale ? 0ull : key;
+              sh.slot = slot;
+            }
+            sh.cmd.block = a->lo + off;
+            sh.t_start = gtimer();
+          }
+          cur_key = key;
+          cur_slot = slot;
+          cur_ver = ver;
+          go = 1;
           break;
+        }
+        if (ld_relaxed_gpu(&p.ctl->drain) && ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0) break;
         if (gtimer() > p.ctl->deadline) break;
         // Idle: wait for this TPC's candidate set to change.
-        for (int k = 0; k < 64; ++k) {
+        for (int k2 = 0; k2 < 64; ++k2) {
           __nanosleep(p.idle_sleep_ns);
           if (ld_relaxed_gpu(p.version + tpc) != ver) break;
         }
@@ -366,8 +433,9 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
         if (a->trace != nullptr) atomicAdd(a->trace + sh.cmd.block, 0x10000u + sm + 1u);
         busy += t_end - sh.t_start;
         ++n_blocks;
-        __threadfence();
-        last = atomicAdd(&a->done, 1u) + 1u == a->count;
+        // acq_rel: this block's records precede the count; the last finisher
+        // observes every other block's records.
+        last = atom_add_acq_rel32(&a->done, 1u) + 1u == ld_relaxed_gpu(&a->count);
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
@@ -400,6 +468,7 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           __threadfence();
           atomicSub(&p.ctl->outstanding, 1);
         }
+        cur_key = 0ull;
       }
     }
   }
@@ -477,7 +546,7 @@ struct gpuos_dev {
   uint32_t comp_head = 0;  // next completion index to consume
   uint32_t next_seq = 1;
   uint32_t next_atom_id = 0;
-  std::vector<uint32_t> free_slots;
+  std::deque<uint32_t> free_slots;  // FIFO: a freed slot is reused last
   std::vector<HostAtom> slots;
   std::vector<int> tpc_resident;  // keys currently resident per logical TPC
   int32_t in_flight = 0;
@@ -553,8 +622,10 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
 
   // Size each worker's shared memory so that exactly W workers fit per SM.
   const int smem_sm = static_cast<int>(prop.sharedMemPerMultiprocessor);
-  int smem_worker = std::min<int>(static_cast<int>(prop.sharedMemPerBlockOptin),
-                                  smem_sm / cfg.workers_per_sm - 2048);
+  // Headroom for the per-CTA reserved shared memory of the workers and of
+  // the co-resident ingest CTA.
+  int smem_worker = std::min<int>(static_cast<int>(prop.sharedMemPerBlockOptin) - 2048,
+                                  smem_sm / cfg.workers_per_sm - 4096);
   smem_worker = std::max(smem_worker - smem_worker % 1024, 0);
   if (cfg.workers_per_sm > 1) {
     // W+1 workers must not fit.
@@ -610,7 +681,6 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   CUDA_TRY(cudaHostGetDevicePointer(&d->alive_d, d->alive_h, 0));
 
   d->slots.assign(cfg.atom_slots, HostAtom{});
-  d->free_slots.reserve(cfg.atom_slots);
   for (int s = cfg.atom_slots - 1; s >= 0; --s) d->free_slots.push_back(static_cast<uint32_t>(s));
   d->tpc_resident.assign(T, 0);
   d->t0_ns = steady_ns();
@@ -963,8 +1033,8 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
       return fail(GPUOS_E_FULL, "TPC " + std::to_string(t) + " already holds 32 resident atoms");
   if (d->free_slots.empty()) return fail(GPUOS_E_FULL, "atom table full");
 
-  const uint32_t slot = d->free_slots.back();
-  d->free_slots.pop_back();
+  const uint32_t slot = d->free_slots.front();
+  d->free_slots.pop_front();
   const uint32_t id = d->next_atom_id++;
   const uint32_t seq = d->next_seq++;
   uint32_t data[28] = {};
@@ -990,7 +1060,7 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   const int rc = publish(d, data);
   if (rc != GPUOS_OK) {
     h.live = false;
-    d->free_slots.push_back(slot);
+    d->free_slots.push_front(slot);
     return rc;
   }
   for (int t = 0; t < T; ++t)

@@ -13,7 +13,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2504_15465_b200 import api  # noqa: E402
 
-words = int(sys.argv[1]) if len(sys.argv) > 1 else 55000 // 4 * 4
+words = int(sys.argv[1]) if len(sys.argv) > 1 else 550000  # bench saturation shape (> L2 with 256 chunks)
 blocks = int(sys.argv[2]) if len(sys.argv) > 2 else 2160
 src = torch.randint(-2**31, 2**31 - 1, (256 * words,), dtype=torch.int32, device="cuda")
 dst = torch.empty_like(src)
