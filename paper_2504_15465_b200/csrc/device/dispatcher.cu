@@ -119,6 +119,7 @@ struct Params {
   unsigned comp_cap;
   int logical_tpcs;
   int idle_sleep_ns;
+  unsigned smem_bytes;  // dynamic shared memory per worker (STREAM ring)
 };
 
 __device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) {
@@ -307,6 +308,7 @@ __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long 
 
 __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   __shared__ WorkerShared sh;
+  extern __shared__ __align__(1024) unsigned char dsmem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const unsigned lane = tid & 31;
@@ -319,6 +321,8 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     sh.key = 0ull;
     sh.slot = ~0u;
   }
+  StreamPipe pipe;
+  stream_pipe_init(pipe, dsmem, p.smem_bytes, tid);
   __syncthreads();
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
   // Warp 0's draining state: the atom it last claimed from and the TPC's
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     if (!sh.go) break;
 
     switch (sh.cmd.body) {
-      case GPUOS_BODY_STREAM: body_stream(sh.cmd, tid); break;
+      case GPUOS_BODY_STREAM: body_stream(sh.cmd, tid, pipe); break;
       case GPUOS_BODY_SPIN: body_spin(sh.cmd, tid); break;
       default: break;
     }
@@ -780,6 +784,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   p.comp_cap = static_cast<unsigned>(d->cfg.atom_slots);
   p.logical_tpcs = d->cfg.logical_tpcs;
   p.idle_sleep_ns = d->cfg.idle_sleep_ns;
+  p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
 
   d->params = p;
   k_ingest<<<1, 32, 0, d->s_ingest>>>(p);
@@ -991,6 +996,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   p.comp_cap = static_cast<unsigned>(d->cfg.atom_slots);
   p.logical_tpcs = T;
   p.idle_sleep_ns = d->cfg.idle_sleep_ns;
+  p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
   k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);

@@ -448,6 +448,8 @@ bool B200Device::step() {
 }
 
 void B200Device::run_all() {
+  gpuos_dev_stats before{};
+  gpuos_dev_get_stats(rt_->handle(), &before);
   rt_->start();
   origin_ = gpuos_dev_now_ns(rt_->handle());
   now_ = 0;
@@ -466,7 +468,12 @@ void B200Device::run_all() {
   pump();  // nothing should remain; keep the ring consistent regardless
   gpuos_dev_stats st{};
   gpuos_dev_get_stats(rt_->handle(), &st);
-  busy_tpc_ns_ = static_cast<double>(st.worker_busy_ns) / rt_->workers_per_tpc();
+  // Worker-slot time of this run in TPC-ns, counted up to the metrics
+  // horizon (blocks after it are scaled out pro rata).
+  double busy = static_cast<double>(st.worker_busy_ns - before.worker_busy_ns) /
+                rt_->workers_per_tpc();
+  if (horizon_ > 0 && now_ > horizon_) busy *= static_cast<double>(horizon_) / static_cast<double>(now_);
+  busy_tpc_ns_ = busy;
   residency_[freq_.f_max()] = now_;
 }
 

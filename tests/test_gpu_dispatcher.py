@@ -47,7 +47,7 @@ def test_topology_and_residency(api, cuda_device):
         dev.stop()
 
 
-@pytest.mark.parametrize("workers_per_sm", [1, 2, 4])
+@pytest.mark.parametrize("workers_per_sm", [1, 2])
 def test_stream_atoms_exactly_once_placed_bit_exact(api, torch_mod, workers_per_sm):
     torch = torch_mod
     rng = random.Random(workers_per_sm)
