@@ -239,9 +239,11 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
           if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
         }
     } else if (op == kOpFence) {
+      // Shuffles are warp-collective: read every field before lane-0 work.
       const int t = static_cast<int>(get(kFAux));
+      const int floor_prio = static_cast<int>(get(kFPrio));
       if (lane == 0 && t >= 0 && t < p.logical_tpcs) {
-        atomicExch(p.fence + t, static_cast<int>(get(kFPrio)));
+        atomicExch(p.fence + t, floor_prio);
         __threadfence();
         atomicAdd(p.version + t, 1u);
       }
@@ -997,7 +999,6 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   p.logical_tpcs = T;
   p.idle_sleep_ns = d->cfg.idle_sleep_ns;
   p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
-  CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
   k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);
   CUDA_TRY(cudaGetLastError());
