@@ -48,6 +48,10 @@ struct B200Options {
   double stream_words_per_us = 2750.0;  // None -> Stream sizing (per worker)
   long stream_min_words = 256;
   long stream_chunk_cap = 4096;     // bound on distinct chunks per workspace
+  // Preemption quantum: blocks longer than this run as independently
+  // claimed slices, bounding how long a higher-priority atom waits for a
+  // worker slot (0: whole blocks).
+  std::int64_t quantum_ns = 0;
 };
 
 struct AtomTimeline {
@@ -91,9 +95,10 @@ class B200Runtime {
   struct Resolved {
     std::uint32_t body;
     std::uint64_t args[5];
-    std::uint32_t* trace;
+    std::uint32_t* trace;   // indexed block * parts + part
     long words;  // Stream: words per block
     long chunks;
+    std::uint32_t parts;    // preemption slices per block
   };
   Resolved resolve(KernelId kid, const SimKernelSpec& spec);
 
@@ -168,7 +173,7 @@ class B200Device final : public Device {
   const std::map<FreqMhz, Duration>& freq_residency() const override { return residency_; }
   long blocks_executed(KernelId k) const override { return executed_.at(k); }
 
-  void set_tpc_fence(int tpc, int min_priority) override;
+  void set_tpc_fence(const std::vector<int>& tpcs, int min_priority) override;
   bool preempts_stolen() const override { return true; }
 
   B200Runtime& runtime() { return *rt_; }

@@ -163,7 +163,7 @@ class Device {
   // work, so blocks of atoms below `min_priority` must stop starting there
   // (block-granular revocation). The replay backend models the reference,
   // which revokes only at atom boundaries, and ignores it.
-  virtual void set_tpc_fence(int /*tpc*/, int /*min_priority*/) {}
+  virtual void set_tpc_fence(const std::vector<int>& /*tpcs*/, int /*min_priority*/) {}
   // Live-backend hook: true when TPCs holding only foreign stolen atoms may
   // be handed back to their owner immediately (device priority arbitration
   // preempts at the next block boundary).

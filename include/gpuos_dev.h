@@ -99,7 +99,11 @@ typedef struct gpuos_atom_desc {
   uint32_t* trace;           /* optional per-block execution trace, indexed
                                 by block id: += 0x10000 | (smid + 1)        */
   int32_t atomized;          /* informational (the prelude is free on B200) */
-  int32_t reserved;
+  uint32_t parts;            /* preemption quanta per block (0/1: whole
+                                blocks). Each block runs as `parts` slices
+                                claimed independently, so a higher-priority
+                                atom waits at most one slice for a slot.
+                                trace is then indexed block * parts + part. */
 } gpuos_atom_desc;
 
 typedef struct gpuos_completion {
@@ -149,6 +153,9 @@ int gpuos_dev_set_atom_paused(struct gpuos_dev* dev, uint32_t atom_id,
 /* Blocks of atoms below min_priority stop starting on `tpc` (0 lifts). */
 int gpuos_dev_set_tpc_fence(struct gpuos_dev* dev, int32_t tpc,
                             int32_t min_priority);
+/* Same for every TPC in the mask, as one ring entry. */
+int gpuos_dev_set_fence_mask(struct gpuos_dev* dev, const uint64_t mask[2],
+                             int32_t min_priority);
 /* Non-blocking; returns the number of completions written to out[0..max). */
 int gpuos_dev_poll(struct gpuos_dev* dev, gpuos_completion* out, int32_t max);
 int64_t gpuos_dev_now_ns(struct gpuos_dev* dev);

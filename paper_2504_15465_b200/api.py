@@ -41,7 +41,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_set_tpc_fence", "gpuos_dev_poll", "gpuos_dev_now_ns", "gpuos_dev_in_flight",
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
-    "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch",
+    "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -76,7 +76,7 @@ class AtomDesc(C.Structure):
     _fields_ = [("lo", C.c_int64), ("hi", C.c_int64), ("tpc_mask", C.c_uint64 * 2),
                 ("priority", C.c_int32), ("body", C.c_uint32), ("args", C.c_uint64 * 5),
                 ("tag", C.c_uint64), ("trace", C.c_void_p), ("atomized", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("parts", C.c_uint32)]
 
 
 class Completion(C.Structure):
@@ -114,6 +114,7 @@ def library() -> C.CDLL:
         "gpuos_dev_submit_atom": (C.c_int, [P, C.POINTER(AtomDesc), C.POINTER(C.c_uint32)]),
         "gpuos_dev_set_atom_paused": (C.c_int, [P, C.c_uint32, C.c_int]),
         "gpuos_dev_set_tpc_fence": (C.c_int, [P, C.c_int32, C.c_int32]),
+        "gpuos_dev_set_fence_mask": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int32]),
         "gpuos_dev_poll": (C.c_int, [P, C.POINTER(Completion), C.c_int32]),
         "gpuos_dev_now_ns": (C.c_int64, [P]),
         "gpuos_dev_in_flight": (C.c_int32, [P]),
@@ -241,8 +242,9 @@ class Device:
 
     @staticmethod
     def desc(lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
-             trace: int | None = None) -> AtomDesc:
+             trace: int | None = None, parts: int = 1) -> AtomDesc:
         d = AtomDesc()
+        d.parts = parts
         d.lo, d.hi, d.priority, d.body, d.tag = lo, hi, priority, body, tag
         m = [0, 0]
         for t in tpcs:
@@ -261,8 +263,9 @@ class Device:
         return ms.value
 
     def submit(self, lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
-               trace: int | None = None) -> int:
+               trace: int | None = None, parts: int = 1) -> int:
         d = AtomDesc()
+        d.parts = parts
         d.lo, d.hi, d.priority, d.body, d.tag = lo, hi, priority, body, tag
         m = [0, 0]
         for t in tpcs:
@@ -288,6 +291,12 @@ class Device:
 
     def fence(self, tpc: int, min_priority: int) -> None:
         self._check(self._lib.gpuos_dev_set_tpc_fence(self._h, tpc, min_priority))
+
+    def fence_mask(self, tpcs, min_priority: int) -> None:
+        m = (C.c_uint64 * 2)()
+        for t in tpcs:
+            m[t >> 6] |= 1 << (t & 63)
+        self._check(self._lib.gpuos_dev_set_fence_mask(self._h, m, min_priority))
 
     def poll(self, max_n: int = 256) -> list[Completion]:
         buf = (Completion * max_n)()

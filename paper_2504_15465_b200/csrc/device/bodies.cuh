@@ -22,6 +22,8 @@ struct BlockCmd {
   unsigned long long args[5];
   long long block;  // absolute block index within the tenant kernel
   unsigned body;
+  unsigned part;    // preemption slice of the block, 0 .. parts-1
+  unsigned parts;
 };
 
 __device__ __forceinline__ unsigned stream_word(unsigned x, unsigned salt,
@@ -108,8 +110,13 @@ __device__ __forceinline__ void body_stream(const BlockCmd& c, int tid, StreamPi
   const unsigned long long chunk =
       chunks ? static_cast<unsigned long long>(c.block) % chunks
              : static_cast<unsigned long long>(c.block);
-  const unsigned long long first = chunk * words;
-  const unsigned long long bytes = words * 4ull;
+  // Slice `part` of the block covers a 16-byte-aligned share of its words.
+  const unsigned long long quads = words / 4;
+  const unsigned long long q0 = quads * c.part / c.parts;
+  const unsigned long long q1 = quads * (c.part + 1) / c.parts;
+  const unsigned long long first = chunk * words + 4 * q0;
+  const unsigned long long bytes = 16 * (q1 - q0);
+  if (bytes == 0) return;
   const unsigned n = static_cast<unsigned>((bytes + kTile - 1) / kTile);
   const unsigned S = P.stages;
   const unsigned long long g0 = P.used;
@@ -157,8 +164,9 @@ __device__ __forceinline__ void body_stream(const BlockCmd& c, int tid, StreamPi
 
 __device__ __forceinline__ void body_spin(const BlockCmd& c, int tid) {
   if (tid != 0) return;
+  const unsigned long long ns = c.args[0] * (c.part + 1) / c.parts - c.args[0] * c.part / c.parts;
   const unsigned long long t0 = gtimer();
-  while (gtimer() - t0 < c.args[0]) {
+  while (gtimer() - t0 < ns) {
   }
 }
 

@@ -50,7 +50,7 @@ constexpr int kResident = GPUOS_RESIDENT_PER_TPC;  // keys per TPC (one per lane
 static_assert(kResident == 32, "one resident key per lane");
 
 enum Op : unsigned { kOpSubmit = 1, kOpPause = 2, kOpResume = 3, kOpFence = 4,
-                     kOpDrain = 5, kOpShutdown = 6 };
+                     kOpDrain = 5, kOpShutdown = 6, kOpFenceMask = 7 };
 
 // Device-resident atom slot. The first 32 bytes are what selecting workers
 // read; the rest is written once by the ingest warp.
@@ -60,7 +60,8 @@ struct alignas(128) DevAtom {
   unsigned paused;           // (claim, count, paused): one 16-byte load
   unsigned seq;
   int prio;                  // 1..255
-  unsigned done;             // finished blocks
+  unsigned done;             // finished slices
+  unsigned parts;            // slices per block (count = blocks x parts)
   unsigned body;
   long long lo;
   unsigned atom_id;
@@ -159,9 +160,10 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
       const unsigned long long tag = field64(get(kFTag), get(kFTag + 1));
       const unsigned long long trace = field64(get(kFTrace), get(kFTrace + 1));
       const long long lo = static_cast<long long>(field64(get(kFLo), get(kFLo + 1)));
-      const unsigned count = get(kFCount);
+      const unsigned count = get(kFCount);  // slices = blocks x parts
       const unsigned body = get(kFBody);
       const unsigned atom_id = get(kFAtomId);
+      const unsigned parts = get(kFAux);
       DevAtom* a = p.atoms + slot;
       if (lane == 0) {
         // Not claimable until every resident key is in place (arming below).
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
         a->prio = prio;
         a->paused = 0;
         a->done = 0;
+        a->parts = parts;
         a->body = body;
         a->lo = lo;
         a->atom_id = atom_id;
@@ -246,6 +249,21 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
         atomicExch(p.fence + t, floor_prio);
         __threadfence();
         atomicAdd(p.version + t, 1u);
+      }
+    } else if (op == kOpFenceMask) {
+      const unsigned long long m0 = field64(get(kFMask0), get(kFMask0 + 1));
+      const unsigned long long m1 = field64(get(kFMask1), get(kFMask1 + 1));
+      const int floor_prio = static_cast<int>(get(kFPrio));
+      for (int t = lane; t < p.logical_tpcs; t += 32) {
+        const unsigned long long m = t < 64 ? m0 : m1;
+        if (!((m >> (t & 63)) & 1ull)) continue;
+        atomicExch(p.fence + t, floor_prio);
+      }
+      __syncwarp();
+      __threadfence();
+      for (int t = lane; t < p.logical_tpcs; t += 32) {
+        const unsigned long long m = t < 64 ? m0 : m1;
+        if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
       }
     } else if (op == kOpDrain) {
       if (lane == 0) atomicExch(&p.ctl->drain, 1u);
@@ -396,10 +414,13 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
 #pragma unroll
               for (int k2 = 0; k2 < 5; ++k2) sh.cmd.args[k2] = a->args[k2];
               sh.cmd.body = a->body;
+              sh.cmd.parts = a->parts;
               sh.key = stale ? 0ull : key;
               sh.slot = slot;
             }
-            sh.cmd.block = a->lo + off;
+            const unsigned parts = sh.cmd.parts;
+            sh.cmd.block = a->lo + off / parts;
+            sh.cmd.part = static_cast<unsigned>(off % parts);
             sh.t_start = gtimer();
           }
           cur_key = key;
@@ -436,7 +457,8 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
         atomicMin(&a->t_first, sh.t_start);
         atomicMax(&a->t_last, t_end);
         atomicOr(&a->touched[tpc >> 6], 1ull << (tpc & 63));
-        if (a->trace != nullptr) atomicAdd(a->trace + sh.cmd.block, 0x10000u + sm + 1u);
+        if (a->trace != nullptr)
+          atomicAdd(a->trace + sh.cmd.block * sh.cmd.parts + sh.cmd.part, 0x10000u + sm + 1u);
         busy += t_end - sh.t_start;
         ++n_blocks;
         // acq_rel: this block's records precede the count; the last finisher
@@ -461,7 +483,7 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           const unsigned long long t1 = *reinterpret_cast<volatile unsigned long long*>(&a->t_last);
           const unsigned long long m0 = *reinterpret_cast<volatile unsigned long long*>(&a->touched[0]);
           const unsigned long long m1 = *reinterpret_cast<volatile unsigned long long*>(&a->touched[1]);
-          st_relaxed_sys_v4(rec->w + 0, a->atom_id, a->count, static_cast<unsigned>(a->tag),
+          st_relaxed_sys_v4(rec->w + 0, a->atom_id, a->count / a->parts, static_cast<unsigned>(a->tag),
                             static_cast<unsigned>(a->tag >> 32));
           st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
                             static_cast<unsigned>(t1), static_cast<unsigned>(t1 >> 32));
@@ -919,7 +941,8 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   std::vector<uint32_t> ids(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) {
     const gpuos_atom_desc& a = descs[i];
-    if (a.lo < 0 || a.hi <= a.lo || a.hi - a.lo > 0xfffffffeLL)
+    const uint32_t parts = a.parts == 0 ? 1u : a.parts;
+    if (a.lo < 0 || a.hi <= a.lo || (a.hi - a.lo) * static_cast<int64_t>(parts) > 0xfffffffeLL)
       return fail(GPUOS_E_CONFIG, "atom block range out of bounds");
     if (a.body != GPUOS_BODY_STREAM && a.body != GPUOS_BODY_SPIN)
       return fail(GPUOS_E_CONFIG, "unknown body kind");
@@ -928,7 +951,8 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     DevAtom& x = atoms[static_cast<size_t>(i)];
     std::memset(&x, 0, sizeof x);
     x.claim = static_cast<unsigned long long>(seq) << 32;
-    x.count = static_cast<unsigned>(a.hi - a.lo);
+    x.count = static_cast<unsigned>((a.hi - a.lo) * parts);
+    x.parts = parts;
     x.seq = seq;
     x.prio = prio;
     x.body = a.body;
@@ -1022,7 +1046,10 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   if (!d || !a) return fail(GPUOS_E_CONFIG, "null argument");
   if (!d->running) return fail(GPUOS_E_STATE, "dispatcher not running");
   if (a->lo < 0 || a->hi <= a->lo) return fail(GPUOS_E_CONFIG, "atom block range out of bounds");
-  if (a->hi - a->lo > 0xfffffffeLL) return fail(GPUOS_E_CONFIG, "atom too large");
+  const uint32_t parts = a->parts == 0 ? 1u : a->parts;
+  if (parts > 4096) return fail(GPUOS_E_CONFIG, "parts must be <= 4096");
+  if ((a->hi - a->lo) * static_cast<int64_t>(parts) > 0xfffffffeLL)
+    return fail(GPUOS_E_CONFIG, "atom too large");
   if (a->body != GPUOS_BODY_STREAM && a->body != GPUOS_BODY_SPIN)
     return fail(GPUOS_E_CONFIG, "unknown body kind");
   const int T = d->cfg.logical_tpcs;
@@ -1050,7 +1077,8 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   data[kFSeq] = seq;
   data[kFPrio] = static_cast<uint32_t>(map_priority(a->priority));
   put64(data, kFLo, static_cast<uint64_t>(a->lo));
-  data[kFCount] = static_cast<uint32_t>(a->hi - a->lo);
+  data[kFCount] = static_cast<uint32_t>((a->hi - a->lo) * parts);
+  data[kFAux] = parts;
   data[kFBody] = a->body;
   put64(data, kFMask0, a->tpc_mask[0]);
   put64(data, kFMask1, a->tpc_mask[1]);
@@ -1095,6 +1123,16 @@ int gpuos_dev_set_tpc_fence(gpuos_dev* d, int32_t tpc, int32_t min_priority) {
   uint32_t data[28] = {};
   data[kFOp] = kOpFence;
   data[kFAux] = static_cast<uint32_t>(tpc);
+  data[kFPrio] = min_priority <= 0 ? 0u : static_cast<uint32_t>(map_priority(min_priority));
+  return publish(d, data);
+}
+
+int gpuos_dev_set_fence_mask(gpuos_dev* d, const uint64_t mask[2], int32_t min_priority) {
+  if (!d || !mask) return fail(GPUOS_E_CONFIG, "null argument");
+  uint32_t data[28] = {};
+  data[kFOp] = kOpFenceMask;
+  put64(data, kFMask0, mask[0]);
+  put64(data, kFMask1, mask[1]);
   data[kFPrio] = min_priority <= 0 ? 0u : static_cast<uint32_t>(map_priority(min_priority));
   return publish(d, data);
 }

@@ -168,8 +168,15 @@ B200Runtime::Resolved B200Runtime::resolve(KernelId kid, const SimKernelSpec& sp
     case BodyKind::None:
       break;
   }
+  r.parts = 1;
+  if (opt_.quantum_ns > 0) {
+    const std::int64_t block_ns = b.kind == BodyKind::Spin ? b.p0 : spec.block_duration_at_fmax;
+    std::int64_t parts = (block_ns + opt_.quantum_ns - 1) / opt_.quantum_ns;
+    if (r.body == GPUOS_BODY_STREAM) parts = std::min<std::int64_t>(parts, r.words / 4);
+    r.parts = static_cast<std::uint32_t>(std::clamp<std::int64_t>(parts, 1, 4096));
+  }
   if (opt_.trace_blocks) {
-    ensure_trace(kid, spec.total_blocks);
+    ensure_trace(kid, spec.total_blocks * static_cast<long>(r.parts));
     r.trace = trace_of_[kid];
   }
   if (resolved_.size() <= kid) {
@@ -246,8 +253,9 @@ VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs
     ++rep.kernels;
     rep.blocks += blocks;
     if (!r.trace) continue;
-    trace.assign(static_cast<std::size_t>(blocks), 0u);
-    check(gpuos_dev_copy(dev_, trace.data(), r.trace, blocks * 4ull, 2), "trace download");
+    const long parts = static_cast<long>(r.parts);
+    trace.assign(static_cast<std::size_t>(blocks * parts), 0u);
+    check(gpuos_dev_copy(dev_, trace.data(), r.trace, blocks * parts * 4ull, 2), "trace download");
     std::vector<char>* tc = nullptr;
     if (r.body == GPUOS_BODY_STREAM) {
       auto& v = touched[r.args[1]];
@@ -256,21 +264,21 @@ VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs
     }
     for (std::size_t a = 0; a < pl.ranges.size(); ++a) {
       for (long b = pl.ranges[a].first; b < pl.ranges[a].second; ++b) {
-        const std::uint32_t v = trace[static_cast<std::size_t>(b)];
-        const std::uint32_t count = v >> 16;
-        if (count == 0) {
-          ++rep.missing;
-          continue;
+        bool whole = true;
+        for (long part = 0; part < parts; ++part) {
+          const std::uint32_t v = trace[static_cast<std::size_t>(b * parts + part)];
+          const std::uint32_t count = v >> 16;
+          if (count != 1) {
+            whole = false;
+            (count == 0 ? rep.missing : rep.duplicated) += 1;
+            continue;
+          }
+          const int sm = static_cast<int>(v & 0xffffu) - 1;
+          const int tpc = sm >> 1;  // identity logical map (gpuos_dev_open)
+          if (tpc < 0 || tpc >= GPUOS_MAX_TPCS || !((pl.masks[a][tpc >> 6] >> (tpc & 63)) & 1ull))
+            ++rep.misplaced;
         }
-        if (count > 1) {
-          ++rep.duplicated;
-          continue;
-        }
-        const int sm = static_cast<int>(v & 0xffffu) - 1;
-        const int tpc = sm >> 1;  // identity logical map (gpuos_dev_open)
-        if (tpc < 0 || tpc >= GPUOS_MAX_TPCS || !((pl.masks[a][tpc >> 6] >> (tpc & 63)) & 1ull))
-          ++rep.misplaced;
-        if (tc) (*tc)[static_cast<std::size_t>(b % r.chunks)] = 1;
+        if (tc && whole) (*tc)[static_cast<std::size_t>(b % r.chunks)] = 1;
       }
     }
   }
@@ -361,6 +369,7 @@ AtomId B200Device::submit_atom(KernelId kernel, long lo, long hi, const std::vec
   d.tag = tag;
   d.trace = r.trace;
   d.atomized = atomized ? 1 : 0;
+  d.parts = r.parts;
   std::uint32_t id = 0;
   check(gpuos_dev_submit_atom(rt_->handle(), &d, &id), "gpuos_dev_submit_atom");
   AtomTimeline tl{};
@@ -381,9 +390,11 @@ void B200Device::set_atom_paused(AtomId atom, bool paused) {
   check(gpuos_dev_set_atom_paused(rt_->handle(), atom, paused ? 1 : 0), "pause");
 }
 
-void B200Device::set_tpc_fence(int tpc, int min_priority) {
-  if (!rt_->running()) return;
-  check(gpuos_dev_set_tpc_fence(rt_->handle(), tpc, min_priority), "fence");
+void B200Device::set_tpc_fence(const std::vector<int>& tpcs, int min_priority) {
+  if (!rt_->running() || tpcs.empty()) return;
+  const auto m = mask_of(tpcs);
+  const std::uint64_t mask[2] = {m[0], m[1]};
+  check(gpuos_dev_set_fence_mask(rt_->handle(), mask, min_priority), "fence");
 }
 
 SimTime B200Device::request_frequency(FreqMhz f) {
@@ -524,6 +535,7 @@ AtomId MirrorDevice::submit_atom(KernelId kernel, long lo, long hi, const std::v
   std::memcpy(d.args, r.args, sizeof d.args);
   d.tag = tag;
   d.trace = r.trace;
+  d.parts = r.parts;
   std::uint32_t gid = 0;
   const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(120);
   for (;;) {

@@ -115,6 +115,7 @@ B200Options b200_options(const json& o) {
   b.stream_words_per_us = o.value("words_per_us", b.stream_words_per_us);
   b.stream_min_words = o.value("min_words", b.stream_min_words);
   b.stream_chunk_cap = o.value("chunk_cap", b.stream_chunk_cap);
+  b.quantum_ns = static_cast<std::int64_t>(o.value("quantum_us", 0.0) * 1000.0);
   return b;
 }
 
