@@ -106,6 +106,9 @@ class B200Runtime {
   float stop(bool drain);  // returns the worker kernel's CUDA-event ms
   // Forget per-run kernel bindings (workspaces stay allocated and resident).
   void reset_kernels();
+  // Body-resolution options (quantum, tracing, synthesis) may change between
+  // runs; device, workers_per_sm and idle_sleep_ns are fixed at open.
+  bool set_run_options(const B200Options& o);
   bool running() const { return running_; }
 
   // Verification against a CPU restatement of the bodies.

@@ -188,6 +188,14 @@ B200Runtime::Resolved B200Runtime::resolve(KernelId kid, const SimKernelSpec& sp
   return r;
 }
 
+bool B200Runtime::set_run_options(const B200Options& o) {
+  if (o.device != opt_.device || o.workers_per_sm != opt_.workers_per_sm ||
+      o.idle_sleep_ns != opt_.idle_sleep_ns)
+    return false;
+  opt_ = o;
+  return true;
+}
+
 void B200Runtime::reset_kernels() {
   resolved_.clear();
   has_resolved_.clear();

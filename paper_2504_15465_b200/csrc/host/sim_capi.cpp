@@ -190,9 +190,10 @@ std::string run_session(gpuos_session* s, const json& overrides) {
     out["gpu_atoms"] = dev.gpu_atoms();
     out["gpu_kernel_ms"] = dev.gpu_kernel_ms();
   } else if (s->backend == "b200") {
-    if (!s->b200 || s->b200->topology().total_tpcs() != cfg.topo.total_tpcs())
-      s->b200 = std::make_unique<B200Device>(cfg.topo, cfg.freq,
-                                             b200_options(merged.value("b200", json::object())));
+    const B200Options opt = b200_options(merged.value("b200", json::object()));
+    if (!s->b200 || s->b200->topology().total_tpcs() != cfg.topo.total_tpcs() ||
+        !s->b200->runtime().set_run_options(opt))
+      s->b200 = std::make_unique<B200Device>(cfg.topo, cfg.freq, opt);
     B200Device& dev = *s->b200;
     dev.reset_run();
     std::uint64_t h2d = 0, d2h = 0;

@@ -109,6 +109,32 @@ def test_chunked_stream_and_block_offsets(api, torch_mod):
                           stream_expect(src.cpu().numpy().view(np.uint32), 77, 0))
 
 
+@pytest.mark.parametrize("parts", [2, 3, 7])
+def test_preemption_slices_exactly_once(api, torch_mod, parts):
+    """parts > 1: every block runs as `parts` independently claimed slices;
+    each slice exactly once, on the atom's TPCs, output bit-exact."""
+    torch = torch_mod
+    words, blocks = 4096, 700
+    src = torch.randint(-2**31, 2**31 - 1, (blocks * words,), dtype=torch.int32, device="cuda")
+    dst = torch.zeros_like(src)
+    trace = torch.zeros(blocks * parts, dtype=torch.int32, device="cuda")
+    with api.Device() as dev:
+        dev.start()
+        dev.submit(0, 300, list(range(0, 20)), 20, api.GPUOS_BODY_STREAM,
+                   [src.data_ptr(), dst.data_ptr(), words, 5, 0], trace=trace.data_ptr(), parts=parts)
+        dev.submit(300, 700, [40, 41], 30, api.GPUOS_BODY_STREAM,
+                   [src.data_ptr(), dst.data_ptr(), words, 5, 0], trace=trace.data_ptr(), parts=parts)
+        done = wait_all(dev, 2)
+        dev.stop()
+    assert sorted(c.blocks for c in done) == [300, 400]
+    counts, sm = decode(trace)
+    assert (counts == 1).all()
+    assert set((sm[:300 * parts] >> 1).tolist()) <= set(range(20))
+    assert set((sm[300 * parts:] >> 1).tolist()) <= {40, 41}
+    assert np.array_equal(dst.cpu().numpy().view(np.uint32),
+                          stream_expect(src.cpu().numpy().view(np.uint32), 5, 0))
+
+
 def test_higher_priority_takes_freed_slots_first(api, torch_mod):
     """A late high-priority atom overtakes the waiting blocks of a resident
     low-priority atom on the same TPC (reference refill rule,
@@ -158,8 +184,7 @@ def test_fence_revokes_tpcs_mid_atom(api, torch_mod):
         dev.submit(0, blocks, [0, 1, 2, 3], 10, api.GPUOS_BODY_SPIN, [100_000, 0, 0, 0, 0],
                    trace=trace.data_ptr())
         time.sleep(0.001)
-        dev.fence(0, 11)
-        dev.fence(1, 11)
+        dev.fence_mask([0, 1], 11)
         time.sleep(0.0005)
         frontier = int(np.nonzero(decode(trace)[0])[0].max()) + 64  # claimed before the fence took hold
         wait_all(dev, 1)

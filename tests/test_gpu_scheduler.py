@@ -82,13 +82,31 @@ def test_live_fig7_verified(api, cuda_device):
     assert percentile(hp_latencies(r), 99) <= 8000
 
 
-def test_live_block_revocation_helps_hp_tail(api, cuda_device):
-    with api.Session(live_request()) as s:
+def test_live_mechanisms_lc_tail_and_be_throughput(api, cuda_device):
+    """Block-granular revocation + 25 us preemption quanta: the LC tenant's
+    p99 stays near its alone p99 while BE runs far faster than a static
+    partition (north-star targets 1.2x and 1.3x; asserted with margin)."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(GOLDEN))
+    from paper_2504_15465_b200 import workloads
+
+    cfg = workloads.fig7_b200(10.0, 2000.0)
+    req = {"scenario": {"config": cfg}, "backend": "b200", "requests": True,
+           "b200": {"chunk_cap": 256, "quantum_us": 25.0}, "set": {"block_revocation": True}}
+    with api.Session(req) as s:
         s.run()
-        base = [s.run() for _ in range(2)]
-        rev = [s.run(set={"block_revocation": True}) for _ in range(2)]
-    p_base = percentile(sum((hp_latencies(r) for r in base), []), 99)
-    p_rev = percentile(sum((hp_latencies(r) for r in rev), []), 99)
-    assert p_rev <= p_base * 1.25 + 50
-    for r in rev:
-        assert r["report"]["apps"][0]["completed"] == r["report"]["apps"][0]["offered"]
+        s.run()
+        live = [s.run() for _ in range(2)]
+        alone = [s.run(scenario={"config": workloads.without_apps(cfg, "be")}) for _ in range(2)]
+        static = [s.run(scenario={"config": workloads.variant(cfg, stealing=False, atomizer=False)})
+                  for _ in range(2)]
+    p_live = percentile(sum((hp_latencies(r) for r in live), []), 99)
+    p_alone = percentile(sum((hp_latencies(r) for r in alone), []), 99)
+    assert p_live <= 1.35 * p_alone, (p_live, p_alone)
+    be = sum(r["blocks_per_app"][1] for r in live) / sum(r["b200"]["kernel_ms"] for r in live)
+    be_static = sum(r["blocks_per_app"][1] for r in static) / sum(r["b200"]["kernel_ms"] for r in static)
+    assert be >= 1.3 * be_static, (be, be_static)
+    for r in live:
+        hp = r["report"]["apps"][0]
+        assert hp["completed"] == hp["offered"]
