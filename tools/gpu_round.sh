@@ -1,8 +1,8 @@
-set -x
+# One GPU round: parity tests, smoke, bench, ncu launch list + full capture.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?"
-tail -30 gpurun_out/pytest_gpu.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?"; tail -5 gpurun_out/smoke.txt
-timeout 600 python bench.py --steps 3 --warmup 2 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -5 gpurun_out/bench.err; cat gpurun_out/bench.json
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/ncu_batch.py > gpurun_out/ncu_launch.txt 2>&1; echo "ncu1 rc=$?"; tail -3 gpurun_out/ncu_launch.txt
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_worker -c 1 -o gpurun_out/prof_k_worker python tools/ncu_batch.py 550000 2160 1 > gpurun_out/ncu_full.txt 2>&1; echo "ncu2 rc=$?"; tail -3 gpurun_out/ncu_full.txt
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?"
+tail -15 gpurun_out/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?"; tail -3 gpurun_out/smoke.txt
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/ncu_batch.py > gpurun_out/ncu_launch.txt 2>&1; echo "ncu1 rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_worker -c 1 -o gpurun_out/prof_k_worker python tools/ncu_batch.py 550000 2160 1 > gpurun_out/ncu_full.txt 2>&1; echo "ncu2 rc=$?"; tail -2 gpurun_out/ncu_full.txt
