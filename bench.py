@@ -37,7 +37,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2504_15465_b200 import workloads  # noqa: E402
+from paper_2504_15465_b200 import replicas, workloads  # noqa: E402
 
 METRIC = "LC p99 latency + BE atoms/sec per B200 under stacking; HBM/TC roofline %"
 
@@ -57,6 +57,11 @@ def nearest_rank(samples, p):
     import math
 
     return s[max(1, math.ceil(p / 100.0 * len(s))) - 1]
+
+
+def be_blocks_of(result) -> int:
+    flags = [a["high_priority"] for a in result["report"]["apps"]]
+    return sum(b for b, hp in zip(result["blocks_per_app"], flags) if not hp)
 
 
 def hp_latencies_us(result) -> list[float]:
@@ -113,58 +118,49 @@ class ClockSampler:
 
 
 def dist_init():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("gloo")
-    return rank, world, local
+    r = replicas.init_from_env("gloo")
+    return r.rank, r.world, r.local
 
 
 def allreduce(values: list[float], op: str) -> list[float]:
-    if int(os.environ.get("WORLD_SIZE", "1")) == 1:
-        return values
-    import torch
-    import torch.distributed as dist
-
-    t = torch.tensor(values, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
-    return t.tolist()
+    return replicas.reduce(values, op)
 
 
 def barrier():
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
+    replicas.barrier()
 
 
-def reference_arm(args, cfg: dict, rank: int, world: int) -> None:
+def reference_arm(args, cfgs: list[dict], rank: int, world: int) -> None:
+    """The unmodified reference on this box's host cores (rank 0 only): every
+    rank's scenario, each as parallel replicas over an equal share of cores."""
     if rank != 0:
         return
-    ref_dir = os.path.join(ROOT, "oracle", "_ref")
-    exe = os.path.join(ref_dir, "ref_bench")
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
     if not os.path.exists(exe) and os.path.isdir("/root/reference/proj"):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
     if not os.path.exists(exe):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
         return
     cores = os.cpu_count() or 1
-    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
-        json.dump(cfg, f)
-        path = f.name
-    def one(reps):
-        r = subprocess.run([exe, "--config", path, "--threads", str(cores), "--reps", str(reps)],
-                           capture_output=True, text=True, check=True)
-        return json.loads(r.stdout)
-    # Size a step to ~5 s of wall time on all cores.
-    probe = one(1)
-    reps = max(1, int(5.0 / max(probe["wall_s"], 1e-3)))
+    per = max(1, cores // len(cfgs))
+    paths = []
+    for c in cfgs:
+        with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+            json.dump(c, f)
+            paths.append(f.name)
+
+    def step(reps):
+        procs = [subprocess.Popen([exe, "--config", p, "--threads", str(per), "--reps", str(reps)],
+                                  stdout=subprocess.PIPE, text=True) for p in paths]
+        outs = [json.loads(p.communicate()[0]) for p in procs]
+        return {"be_atoms": sum(o["be_atoms"] for o in outs), "wall_s": max(o["wall_s"] for o in outs),
+                "hp_p99_ns": max(o["hp_p99_ns"] for o in outs)}
+
+    probe = step(1)
+    reps = max(1, int(5.0 / max(probe["wall_s"], 1e-3)))  # ~5 s of wall time per step
     for _ in range(args.warmup):
-        one(1)
-    steps = [one(reps) for _ in range(args.steps)]
+        step(1)
+    steps = [step(reps) for _ in range(args.steps)]
     be = sum(s["be_atoms"] for s in steps)
     wall = sum(s["wall_s"] for s in steps)
     value = be / wall
@@ -173,10 +169,11 @@ def reference_arm(args, cfg: dict, rank: int, world: int) -> None:
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": cfg["name"], "tenants": [a["id"] for a in cfg["apps"]],
-                   "tpcs": cfg["device"]["gpc_count"] * cfg["device"]["tpcs_per_gpc"]},
-        "cpu_baseline": {"value": value, "unit": "BE atoms/s", "cores": cores, "kind": "reference",
-                         "sample": f"{reps} x {cores} replicas of the scenario per step "
+        "config": {"workload": ", ".join(c["name"] for c in cfgs),
+                   "tenants": [a["id"] for a in cfgs[0]["apps"]],
+                   "tpcs": cfgs[0]["device"]["gpc_count"] * cfgs[0]["device"]["tpcs_per_gpc"]},
+        "cpu_baseline": {"value": value, "unit": "BE atoms/s", "cores": per * len(cfgs), "kind": "reference",
+                         "sample": f"{reps} x {per} replicas of each of {len(cfgs)} scenario(s) per step "
                                    f"(reference discrete-event simulator, wall clock)"},
         "e2e": {"value": value, "unit": "BE atoms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "lc_p99_ms_simulated": steps[-1]["hp_p99_ns"] / 1e6,
@@ -231,15 +228,15 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     barrier()
     dev_ms = sum(s["b200"]["kernel_ms"] for s in steps)
     be_atoms = sum(s["atoms"]["be"] for s in steps)
-    be_blocks = sum(s["blocks_per_app"][1] for s in steps)
+    be_blocks = sum(be_blocks_of(s) for s in steps)
     stream_bytes = sum(s["b200"]["stream_bytes"] for s in steps)
-    lat = sum((hp_latencies_us(s) for s in steps), [])
+    lat = replicas.gather_samples(sum((hp_latencies_us(s) for s in steps), []))
     max_ms, = allreduce([dev_ms], "max")
     be_atoms_all, be_blocks_all = allreduce([float(be_atoms), float(be_blocks)], "sum")
     value = be_atoms_all / (max_ms * 1e-3)
 
     # ---- comparisons on the same device: LC alone, static partition
-    alone_cfg = workloads.without_apps(cfg, "be")
+    alone_cfg = workloads.without_apps(cfg, *[a["id"] for a in cfg["apps"] if a["priority"] == "be"])
     static_cfg = workloads.variant(cfg, stealing=False, atomizer=False)
     alone = [sess.run(scenario={"config": alone_cfg}) for _ in range(args.steps)]
     static = [sess.run(scenario={"config": static_cfg}) for _ in range(args.steps)]
@@ -247,10 +244,10 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     # boundary revocation, whole blocks).
     ref_sem = [sess.run(set={"block_revocation": False}, b200=dict(b200, quantum_us=0.0))
                for _ in range(args.steps)]
-    lat_alone = sum((hp_latencies_us(s) for s in alone), [])
-    lat_ref_sem = sum((hp_latencies_us(s) for s in ref_sem), [])
+    lat_alone = replicas.gather_samples(sum((hp_latencies_us(s) for s in alone), []))
+    lat_ref_sem = replicas.gather_samples(sum((hp_latencies_us(s) for s in ref_sem), []))
     ref_sem_ms = sum(s["b200"]["kernel_ms"] for s in ref_sem)
-    static_blocks = sum(s["blocks_per_app"][1] for s in static)
+    static_blocks = sum(be_blocks_of(s) for s in static)
     static_ms = sum(s["b200"]["kernel_ms"] for s in static)
 
     # ---- end to end through the C-ABI session call with host buffers
@@ -264,6 +261,8 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
 
     # ---- saturated roofline: the BE tenant's atomized kernel alone at full width
     sat = saturation(api, local, args)
+    probe = api.probe_dispatch(device=local, workers_per_sm=args.workers_per_sm, serial=2000,
+                               pipelined=20000, depth=16)
 
     if rank != 0:
         return
@@ -275,7 +274,9 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (reference Figure-7 trace, time-scaled; STREAM bodies over seeded u32 workspaces)",
-        "config": {"workload": cfg["name"] + " (BASELINE config #1)", "tenants": ["hp (LC)", "be (BE)"],
+        "config": {"workload": cfg["name"] + (" (BASELINE config #5, per GPU)" if args.workload == "box8"
+                                              else " (BASELINE config #1)"),
+                   "tenants": [a["id"] + (" (LC)" if a["priority"] == "hp" else " (BE)") for a in cfg["apps"]],
                    "tpcs": 74, "time_scale": args.time_scale, "horizon_ms": cfg["horizon_ms"],
                    "workers_per_sm": args.workers_per_sm,
                    "l2": "inputs larger than L2 (STREAM workspaces >> 126 MB)",
@@ -291,12 +292,17 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
             "lc_p99_ms": nearest_rank(lat_ref_sem, 99) / 1e3,
             "lc_p99_vs_alone": nearest_rank(lat_ref_sem, 99) / nearest_rank(lat_alone, 99),
             "be_atoms_per_s": sum(s["atoms"]["be"] for s in ref_sem) / (ref_sem_ms * 1e-3),
-            "be_blocks_per_s": sum(s["blocks_per_app"][1] for s in ref_sem) / (ref_sem_ms * 1e-3)},
+            "be_blocks_per_s": sum(be_blocks_of(s) for s in ref_sem) / (ref_sem_ms * 1e-3)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": None,
                      "kernel": "k_worker (persistent dispatcher, stacked run, CUDA events)",
                      "peak_source": pk["source"]},
         "roofline_saturated": sat,
+        "dispatcher_overhead": {
+            "serial_roundtrip_us_p50": probe["serial_roundtrip_ns"]["p50"] / 1e3,
+            "publish_to_first_block_us_p50": probe["publish_to_first_block_ns"]["p50"] / 1e3,
+            "pipelined_ns_per_atom": probe["pipelined_ns_per_atom"],
+            "note": "empty one-block atoms through the live ring (gpuos_probe_dispatch)"},
         "cpu_baseline": cpu_baseline(cfg) if world == 1 else None,
         "e2e": {"value": e2e_atoms_all / e2e_s_max, "unit": "BE atoms/s",
                 "h2d_bytes_per_step": e2e[0]["b200"]["h2d_bytes"],
@@ -346,11 +352,18 @@ def main():
     ap.add_argument("--horizon-ms", type=float, default=2000.0, help="reference-scale horizon")
     ap.add_argument("--workers-per-sm", type=int, default=2)
     ap.add_argument("--chunk-cap", type=int, default=256)
+    ap.add_argument("--workload", choices=["fig7", "box8"], default="fig7",
+                    help="fig7: BASELINE config #1; box8: config #5 (8 tenants per GPU)")
     args = ap.parse_args()
     rank, world, local = dist_init()
-    cfg = workloads.fig7_b200(args.time_scale, args.horizon_ms)
+    if args.workload == "box8":
+        cfg = workloads.tenant_set(rank, args.time_scale, args.horizon_ms)
+    else:
+        cfg = workloads.fig7_b200(args.time_scale, args.horizon_ms)
     if args.impl == "reference":
-        reference_arm(args, cfg, rank, world)
+        cfgs = ([workloads.tenant_set(r, args.time_scale, args.horizon_ms) for r in range(world)]
+                if args.workload == "box8" else [cfg])
+        reference_arm(args, cfgs, rank, world)
     else:
         ours(args, cfg, rank, world, local)
 

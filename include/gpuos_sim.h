@@ -39,6 +39,10 @@ int gpuos_session_close(gpuos_session* s);
 /* One-shot convenience: open + run + close. */
 int gpuos_run_json(const char* request_json, char** result_json);
 void gpuos_free_text(char* text);
+/* Dispatcher overhead probe on the live path (serial round trips of empty
+ * atoms, publish -> first block start, pipelined empty-atom rate); options
+ * {"serial", "pipelined", "depth", "tpc", "device", "workers_per_sm"}.    */
+int gpuos_probe_dispatch(const char* opts_json, char** result_json);
 const char* gpuos_sim_last_error(void);
 
 /* ---- pure policy functions (parity against the reference's vectors) ---- */

@@ -48,7 +48,7 @@ SIM_SYMBOLS = [
     "gpuos_free_text", "gpuos_sim_last_error", "gpuos_plan_atoms", "gpuos_should_atomize",
     "gpuos_filter_cap", "gpuos_fit_scaling", "gpuos_choose_tpcs", "gpuos_choose_tpcs_wave",
     "gpuos_block_latency", "gpuos_reference_kernel_latency", "gpuos_select_frequency",
-    "gpuos_predictor_replay",
+    "gpuos_predictor_replay", "gpuos_probe_dispatch",
 ]
 
 
@@ -135,6 +135,7 @@ def library() -> C.CDLL:
         "gpuos_run_json": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
         "gpuos_free_text": (None, [C.c_void_p]),
         "gpuos_sim_last_error": (C.c_char_p, []),
+        "gpuos_probe_dispatch": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
         "gpuos_plan_atoms": (C.c_int64, [C.c_int64] * 4 + [C.POINTER(C.c_int64), C.c_int64]),
         "gpuos_should_atomize": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_double]),
         "gpuos_filter_cap": (C.c_int, [C.c_int64, C.c_int32, C.c_int32]),
@@ -197,6 +198,19 @@ class Session:
 
     def __exit__(self, *exc: Any) -> None:
         self.close()
+
+
+def probe_dispatch(**opts: Any) -> dict[str, Any]:
+    """Live-path dispatcher overhead (gpuos_probe_dispatch)."""
+    lib = library()
+    out = C.c_void_p()
+    rc = lib.gpuos_probe_dispatch(json.dumps(opts).encode(), C.byref(out))
+    if rc != 0:
+        raise GpuosError(rc, lib.gpuos_sim_last_error().decode())
+    try:
+        return json.loads(C.string_at(out.value).decode())
+    finally:
+        lib.gpuos_free_text(out)
 
 
 def run(request: dict[str, Any]) -> dict[str, Any]:

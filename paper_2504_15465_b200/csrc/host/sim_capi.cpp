@@ -10,6 +10,7 @@
 #include "gpuos/b200.hpp"
 #include "gpuos/replay.hpp"
 #include "gpuos/scenario.hpp"
+#include "gpuos_dev.h"
 #include "gpuos_sim.h"
 #include "json.hpp"
 
@@ -346,6 +347,80 @@ int gpuos_run_json(const char* request_json, char** result_json) {
   rc = gpuos_session_run(s, nullptr, result_json);
   gpuos_session_close(s);
   return rc;
+}
+
+// ------------------------------------------------------------ dispatch probe
+// Dispatcher overhead on the live path, measured in C against the C ABI:
+//  * serial: n one-block SPIN(0) atoms, each submitted after the previous
+//    completion was polled -> host round trip (submit .. completion seen)
+//    and publish -> first block start (device clock, calibrated);
+//  * pipelined: empty atoms kept `depth` deep in flight on one TPC set ->
+//    sustained atoms/s; per-atom overhead = 1 / rate.
+int gpuos_probe_dispatch(const char* opts_json, char** result_json) {
+  return guarded([&] {
+    const json o = json::parse(opts_json ? opts_json : "{}");
+    const int n = o.value("serial", 2000);
+    const int m = o.value("pipelined", 20000);
+    const int depth = o.value("depth", 16);
+    const int tpc = o.value("tpc", 0);
+    gpuos_dev_config cfg{};
+    cfg.device_ordinal = o.value("device", 0);
+    cfg.workers_per_sm = o.value("workers_per_sm", 2);
+    gpuos_dev* d = nullptr;
+    if (gpuos_dev_open(&cfg, &d) != GPUOS_OK) throw InvariantError(gpuos_dev_last_error());
+    std::unique_ptr<gpuos_dev, int (*)(gpuos_dev*)> guard(d, gpuos_dev_close);
+    auto must = [&](int rc) {
+      if (rc < 0) throw InvariantError(gpuos_dev_last_error());
+      return rc;
+    };
+    gpuos_atom_desc a{};
+    a.lo = 0;
+    a.hi = 1;
+    a.tpc_mask[tpc >> 6] = 1ull << (tpc & 63);
+    a.priority = 20;
+    a.body = GPUOS_BODY_SPIN;
+    must(gpuos_dev_start(d));
+    std::vector<double> rtt, to_start, to_end;
+    gpuos_completion c{};
+    for (int i = 0; i < n + 50; ++i) {
+      std::uint32_t id = 0;
+      must(gpuos_dev_submit_atom(d, &a, &id));
+      while (must(gpuos_dev_poll(d, &c, 1)) == 0) {
+      }
+      if (i < 50) continue;  // warm-up
+      rtt.push_back(static_cast<double>(c.host_complete_ns - c.host_submit_ns));
+      to_start.push_back(static_cast<double>(c.dev_first_start_ns - c.host_submit_ns));
+      to_end.push_back(static_cast<double>(c.host_complete_ns - c.dev_last_end_ns));
+    }
+    // Pipelined: keep `depth` empty atoms in flight.
+    gpuos_completion buf[64];
+    int sent = 0, got = 0;
+    const std::int64_t t0 = gpuos_dev_now_ns(d);
+    while (got < m) {
+      while (sent < m && sent - got < depth) {
+        std::uint32_t id = 0;
+        must(gpuos_dev_submit_atom(d, &a, &id));
+        ++sent;
+      }
+      got += must(gpuos_dev_poll(d, buf, 64));
+    }
+    const double secs = static_cast<double>(gpuos_dev_now_ns(d) - t0) * 1e-9;
+    float ms = 0.f;
+    must(gpuos_dev_stop(d, 1, &ms));
+    auto pct = [](std::vector<double> v, double p) {
+      std::sort(v.begin(), v.end());
+      return v[static_cast<std::size_t>(p / 100.0 * (v.size() - 1))];
+    };
+    json out;
+    out["serial_roundtrip_ns"] = {{"p50", pct(rtt, 50)}, {"p90", pct(rtt, 90)}, {"p99", pct(rtt, 99)}};
+    out["publish_to_first_block_ns"] = {{"p50", pct(to_start, 50)}, {"p90", pct(to_start, 90)},
+                                        {"p99", pct(to_start, 99)}};
+    out["last_block_to_host_ns"] = {{"p50", pct(to_end, 50)}, {"p90", pct(to_end, 90)}};
+    out["pipelined_atoms_per_s"] = m / secs;
+    out["pipelined_ns_per_atom"] = secs * 1e9 / m;
+    out["depth"] = depth;
+    *result_json = dup_text(out.dump());
+  });
 }
 
 // ------------------------------------------------------------ policy ABI
