@@ -62,6 +62,7 @@ struct AtomTimeline {
   int priority;
   std::int64_t host_submit_ns, host_complete_ns;
   std::int64_t dev_first_start_ns, dev_last_end_ns;
+  std::int64_t dev_ingest_ns, dev_armed_ns;  // ingest warp saw / armed the atom
   std::uint64_t touched[2];
   std::uint64_t mask[2];
 };

@@ -115,6 +115,8 @@ typedef struct gpuos_completion {
   int64_t dev_first_start_ns;/* first block start, device clock, relative to open */
   int64_t dev_last_end_ns;   /* last block end, same clock                  */
   uint64_t tpc_touched[2];   /* logical TPCs that ran at least one block    */
+  int64_t dev_ingest_ns;     /* ingest warp read the ring entry (device clock) */
+  int64_t dev_armed_ns;      /* atom claimable on every TPC of its set      */
 } gpuos_completion;
 
 typedef struct gpuos_dev_stats {

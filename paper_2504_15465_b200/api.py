@@ -83,7 +83,8 @@ class Completion(C.Structure):
     _fields_ = [("atom_id", C.c_uint32), ("blocks", C.c_uint32), ("tag", C.c_uint64),
                 ("host_submit_ns", C.c_int64), ("host_complete_ns", C.c_int64),
                 ("dev_first_start_ns", C.c_int64), ("dev_last_end_ns", C.c_int64),
-                ("tpc_touched", C.c_uint64 * 2)]
+                ("tpc_touched", C.c_uint64 * 2), ("dev_ingest_ns", C.c_int64),
+                ("dev_armed_ns", C.c_int64)]
 
 
 class DevStats(C.Structure):

@@ -72,6 +72,7 @@ struct alignas(128) DevAtom {
   unsigned long long mask[2];
   unsigned long long t_first, t_last;
   unsigned long long touched[2];
+  unsigned long long t_seen, t_armed;   // ingest instrumentation (globaltimer)
   unsigned char entry[GPUOS_MAX_TPCS];  // resident-list index per TPC
 };
 
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
       continue;
     }
     auto get = [&](int d) { return __shfl_sync(0xffffffffu, w, ring_word(d)); };
+    const unsigned long long t_seen = gtimer();
     const unsigned op = get(kFOp);
     bool stop = false;
     if (op == kOpSubmit) {
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
         a->t_last = 0;
         a->touched[0] = 0;
         a->touched[1] = 0;
+        a->t_seen = t_seen;
       }
       __syncwarp();
       __threadfence();
@@ -219,6 +222,7 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
       __threadfence();
       if (lane == 0) {
         atomicAdd(&p.ctl->outstanding, 1);
+        a->t_armed = gtimer();
         __threadfence();
         atomicExch(&a->claim, static_cast<unsigned long long>(seq) << 32);  // arm
       }
@@ -489,7 +493,11 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
                             static_cast<unsigned>(t1), static_cast<unsigned>(t1 >> 32));
           st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
                             static_cast<unsigned>(m1), static_cast<unsigned>(m1 >> 32));
-          st_relaxed_sys_v4(rec->w + 12, sh.slot, 0u, 0u, 0u);
+          const unsigned long long ts = *reinterpret_cast<volatile unsigned long long*>(&a->t_seen);
+          const unsigned long long ta = *reinterpret_cast<volatile unsigned long long*>(&a->t_armed);
+          // t_seen / t_armed as ns before t_first (0 in batch mode).
+          st_relaxed_sys_v4(rec->w + 12, sh.slot, ts ? static_cast<unsigned>(t0 - ts) : 0u,
+                            ta ? static_cast<unsigned>(t0 - ta) : 0u, 0u);
           __threadfence_system();
           st_release_sys(rec->w + 15, idx + 1u);
           atomicAdd(&p.ctl->atoms_done, 1ull);
@@ -1155,6 +1163,8 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
     c.tpc_touched[1] = (uint64_t)w[10] | ((uint64_t)w[11] << 32);
     const uint32_t slot = w[12];
     c.dev_first_start_ns = static_cast<int64_t>(t_first) - d->gt_offset;
+    c.dev_ingest_ns = c.dev_first_start_ns - static_cast<int64_t>(w[13]);
+    c.dev_armed_ns = c.dev_first_start_ns - static_cast<int64_t>(w[14]);
     c.dev_last_end_ns = static_cast<int64_t>(t_last) - d->gt_offset;
     c.host_complete_ns = gpuos_dev_now_ns(d);
     if (slot >= d->slots.size() || !d->slots[slot].live || d->slots[slot].atom_id != c.atom_id)

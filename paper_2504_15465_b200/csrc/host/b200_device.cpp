@@ -430,6 +430,8 @@ void B200Device::pump() {
     tl.host_complete_ns = c.host_complete_ns - origin_;
     tl.dev_first_start_ns = c.dev_first_start_ns - origin_;
     tl.dev_last_end_ns = c.dev_last_end_ns - origin_;
+    tl.dev_ingest_ns = c.dev_ingest_ns - origin_;
+    tl.dev_armed_ns = c.dev_armed_ns - origin_;
     tl.touched[0] = c.tpc_touched[0];
     tl.touched[1] = c.tpc_touched[1];
     executed_[tl.kernel] += c.blocks;
@@ -459,9 +461,10 @@ bool B200Device::step() {
   if (timers_.empty() && in_flight == 0) return false;
   now_ = std::max(now_, t);
   if (in_flight == 0 && !timers_.empty()) {
-    // Nothing on the GPU: sleep towards the next arrival, wake early.
+    // Nothing on the GPU: sleep towards the next arrival, waking a full
+    // millisecond early (OS sleeps overshoot) and spinning the rest.
     const SimTime gap = timers_.top().t - t;
-    if (gap > 200'000) std::this_thread::sleep_for(std::chrono::nanoseconds(gap - 100'000));
+    if (gap > 2'000'000) std::this_thread::sleep_for(std::chrono::nanoseconds(gap - 1'000'000));
   }
   return true;
 }

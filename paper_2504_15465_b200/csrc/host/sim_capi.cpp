@@ -380,7 +380,7 @@ int gpuos_probe_dispatch(const char* opts_json, char** result_json) {
     a.priority = 20;
     a.body = GPUOS_BODY_SPIN;
     must(gpuos_dev_start(d));
-    std::vector<double> rtt, to_start, to_end;
+    std::vector<double> rtt, to_start, to_end, ingest_to_armed, armed_to_start, start_to_host;
     gpuos_completion c{};
     for (int i = 0; i < n + 50; ++i) {
       std::uint32_t id = 0;
@@ -391,6 +391,9 @@ int gpuos_probe_dispatch(const char* opts_json, char** result_json) {
       rtt.push_back(static_cast<double>(c.host_complete_ns - c.host_submit_ns));
       to_start.push_back(static_cast<double>(c.dev_first_start_ns - c.host_submit_ns));
       to_end.push_back(static_cast<double>(c.host_complete_ns - c.dev_last_end_ns));
+      ingest_to_armed.push_back(static_cast<double>(c.dev_armed_ns - c.dev_ingest_ns));
+      armed_to_start.push_back(static_cast<double>(c.dev_first_start_ns - c.dev_armed_ns));
+      start_to_host.push_back(static_cast<double>(c.host_complete_ns - c.dev_first_start_ns));
     }
     // Pipelined: keep `depth` empty atoms in flight.
     gpuos_completion buf[64];
@@ -416,6 +419,11 @@ int gpuos_probe_dispatch(const char* opts_json, char** result_json) {
     out["publish_to_first_block_ns"] = {{"p50", pct(to_start, 50)}, {"p90", pct(to_start, 90)},
                                         {"p99", pct(to_start, 99)}};
     out["last_block_to_host_ns"] = {{"p50", pct(to_end, 50)}, {"p90", pct(to_end, 90)}};
+    // Device-clock-only breakdown (no host/device offset error).
+    out["device_ingest_to_armed_ns_p50"] = pct(ingest_to_armed, 50);
+    out["device_armed_to_first_block_ns_p50"] = pct(armed_to_start, 50);
+    out["host_submit_to_device_ingest_ns_p50_offset_sensitive"] =
+        pct(to_start, 50) - pct(ingest_to_armed, 50) - pct(armed_to_start, 50);
     out["pipelined_atoms_per_s"] = m / secs;
     out["pipelined_ns_per_atom"] = secs * 1e9 / m;
     out["depth"] = depth;
