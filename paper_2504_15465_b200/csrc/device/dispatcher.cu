@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <atomic>
 #include <chrono>
 #include <memory>
@@ -52,35 +53,36 @@ static_assert(kResident == 32, "one resident key per lane");
 enum Op : unsigned { kOpSubmit = 1, kOpPause = 2, kOpResume = 3, kOpFence = 4,
                      kOpDrain = 5, kOpShutdown = 6, kOpFenceMask = 7 };
 
-// Device-resident atom slot. The first 32 bytes are what selecting workers
-// read; the rest is written once by the ingest warp.
+// Device-resident atom slot. The first 128-byte line holds everything a
+// claiming worker reads (claim word, count, pause flag, block range, body and
+// its arguments); the ingest warp writes the rest once.
 struct alignas(128) DevAtom {
-  unsigned long long claim;  // seq << 32 | next block offset (fetch-add)
-  unsigned count;            // blocks in the atom
-  unsigned paused;           // (claim, count, paused): one 16-byte load
-  unsigned seq;
-  int prio;                  // 1..255
-  unsigned done;             // finished slices
-  unsigned parts;            // slices per block (count = blocks x parts)
-  unsigned body;
-  long long lo;
-  unsigned atom_id;
-  unsigned pad;
-  unsigned long long args[5];
-  unsigned long long tag;
-  unsigned* trace;
-  unsigned long long mask[2];
-  unsigned long long t_first, t_last;
+  unsigned long long claim;  // +0  seq << 32 | next slice offset (fetch-add)
+  unsigned count;            // +8  slices = blocks x parts
+  unsigned paused;           // +12 (claim, count, paused): one 16-byte load
+  long long lo;              // +16 first block
+  unsigned body;             // +24
+  unsigned parts;            // +28 slices per block
+  unsigned long long args[5];  // +32 .. +72
+  unsigned seq;              // +72
+  int prio;                  // +76 1..255
+  unsigned done;             // +80 finished slices
+  unsigned atom_id;          // +84
+  unsigned long long tag;    // +88
+  unsigned* trace;           // +96
+  unsigned long long mask[2];  // +104
+  unsigned long long t_first, t_last;   // second line: per-block records
   unsigned long long touched[2];
   unsigned long long t_seen, t_armed;   // ingest instrumentation (globaltimer)
   unsigned char entry[GPUOS_MAX_TPCS];  // resident-list index per TPC
 };
+static_assert(offsetof(DevAtom, mask) + 16 <= 128, "hot fields must share one line");
 
 struct DevCtl {
   unsigned quit;
   unsigned drain;
   int outstanding;      // ingested, not yet completed
-  unsigned comp_tail;   // completion records allocated
+  unsigned pad0;
   unsigned long long deadline;  // globaltimer: hard stop (hang guard)
   unsigned long long blocks, busy_ns, retries, atoms_done;
   unsigned long long stale_claims;  // claims that landed on a recycled slot
@@ -124,13 +126,27 @@ struct Params {
   unsigned smem_bytes;  // dynamic shared memory per worker (STREAM ring)
 };
 
+__device__ __forceinline__ void st_release_gpu64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) {
   return static_cast<unsigned long long>(lo) | (static_cast<unsigned long long>(hi) << 32);
 }
 
 // ------------------------------------------------------------ ingest warp
 __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
+  // Shadow occupancy of every TPC's resident list. Only this warp inserts
+  // keys, so an entry whose shadow bit is clear is certainly empty; workers
+  // clear entries behind its back, which the shadow learns on refresh.
+  __shared__ unsigned shadow[GPUOS_MAX_TPCS];
   const unsigned lane = threadIdx.x;
+  for (int t = lane; t < GPUOS_MAX_TPCS; t += 32) shadow[t] = 0u;  // lists start empty
+  __syncwarp();
   unsigned long long head = 0;
   for (;;) {
     if (ld_relaxed_gpu(&p.ctl->quit)) break;
@@ -168,22 +184,21 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
       const unsigned parts = get(kFAux);
       DevAtom* a = p.atoms + slot;
       if (lane == 0) {
-        // Not claimable until every resident key is in place (arming below).
         // Exhausted (offset == count) until armed: a stale fetch-add from a
         // worker still holding the previous occupant's key cannot carry into
-        // the sequence bits, and the arming exchange overwrites it.
+        // the sequence bits, and the arming store overwrites it.
         a->claim = (static_cast<unsigned long long>(seq) << 32) | count;
         a->count = count;
-        a->seq = seq;
-        a->prio = prio;
         a->paused = 0;
-        a->done = 0;
-        a->parts = parts;
-        a->body = body;
         a->lo = lo;
-        a->atom_id = atom_id;
+        a->body = body;
+        a->parts = parts;
 #pragma unroll
         for (int k = 0; k < 5; ++k) a->args[k] = args[k];
+        a->seq = seq;
+        a->prio = prio;
+        a->done = 0;
+        a->atom_id = atom_id;
         a->tag = tag;
         a->trace = reinterpret_cast<unsigned*>(trace);
         a->mask[0] = mask0;
@@ -193,9 +208,9 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
         a->touched[0] = 0;
         a->touched[1] = 0;
         a->t_seen = t_seen;
+        fence_acq_rel_gpu();
       }
       __syncwarp();
-      __threadfence();
       const unsigned long long key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
                                      (static_cast<unsigned long long>(~seq) << 24) |
                                      (slot & 0xffffffu);
@@ -203,34 +218,30 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
         const unsigned long long m = t < 64 ? mask0 : mask1;
         if (!((m >> (t & 63)) & 1ull)) continue;
         unsigned long long* list = p.resident + static_cast<size_t>(t) * kResident;
-        for (;;) {  // host admission control keeps a free entry available
-          int placed = -1;
-          for (int k = 0; k < kResident; ++k) {
-            if (ld_relaxed_gpu64(list + k) == 0ull && atomicCAS(list + k, 0ull, key) == 0ull) {
-              placed = k;
-              break;
-            }
-          }
-          if (placed >= 0) {
-            a->entry[t] = static_cast<unsigned char>(placed);
-            break;
-          }
-          __nanosleep(128);
+        unsigned occ = shadow[t];
+        while (occ == ~0u) {  // refresh from the list (host admission keeps room)
+          occ = 0u;
+          for (int k = 0; k < kResident; ++k)
+            if (ld_relaxed_gpu64(list + k) != 0ull) occ |= 1u << k;
+          if (occ == ~0u) __nanosleep(128);
         }
+        const int k = __ffs(~occ) - 1;
+        shadow[t] = occ | (1u << k);
+        a->entry[t] = static_cast<unsigned char>(k);
+        st_release_gpu64(list + k, key);  // publishes the slot fields with it
       }
       __syncwarp();
-      __threadfence();
       if (lane == 0) {
         atomicAdd(&p.ctl->outstanding, 1);
         a->t_armed = gtimer();
-        __threadfence();
-        atomicExch(&a->claim, static_cast<unsigned long long>(seq) << 32);  // arm
+        // Arm after every key: a worker finishing the atom then finds all
+        // its entry indices recorded.
+        st_release_gpu64(&a->claim, static_cast<unsigned long long>(seq) << 32);
       }
       __syncwarp();
-      __threadfence();
       for (int t = lane; t < p.logical_tpcs; t += 32) {
         const unsigned long long m = t < 64 ? mask0 : mask1;
-        if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
+        if ((m >> (t & 63)) & 1ull) red_release_gpu_add(p.version + t, 1u);
       }
     } else if (op == kOpPause || op == kOpResume) {
       DevAtom* a = p.atoms + get(kFSlot);
@@ -286,18 +297,13 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
 // ------------------------------------------------------------ worker CTAs
 struct WorkerShared {
   BlockCmd cmd;                 // current block: args, block id, body
+  long long lo;                 // first block of the cached atom
   unsigned long long key;       // resident key of the atom being drained
   unsigned long long t_start;
   unsigned slot;
   int go;
 };
 
-__device__ __forceinline__ unsigned long long atom_add_acquire64(unsigned long long* p,
-                                                                 unsigned long long v) {
-  unsigned long long old;
-  asm volatile("atom.add.acquire.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
-  return old;
-}
 __device__ __forceinline__ unsigned atom_add_acq_rel32(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -308,26 +314,32 @@ __device__ __forceinline__ void ld_relaxed_gpu_v2(const void* p, unsigned long l
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
-// Lane 0: claim one block of the atom behind `key` with a fetch-add on its
-// claim word. Returns the block offset, or -1 if the atom is exhausted.
-// Fetch-add never retries, so 300 workers draining one atom cost one L2
-// atomic each (the CAS loop it replaces spent ~140 failed attempts per
-// claim under that contention: profiles/ncu_k_worker_r01_cas.txt).
-// A worker holding a stale key for a recycled slot (the host quarantines
-// freed slots FIFO over the whole table, so this needs a worker stalled for
-// thousands of atom lifetimes) sees a foreign sequence in the returned word;
-// if that offset is valid it now owns a block of the new occupant and runs
-// it rather than lose it, counting the event in ctl->stale_claims.
+// Lane 0: claim one slice of the atom behind `key` with an acquire fetch-add
+// on its claim word: the ingest warp armed that word with a release store
+// after writing the slot, so the slot fields lane 0 reads next are ordered
+// (lane 0 is not the lane that read the key). Fetch-add never retries, so 300 workers
+// draining one atom cost one L2 atomic each; the CAS loop it replaced spent
+// ~140 failed attempts per claim under that contention
+// (profiles/ncu_k_worker_r01_cas.txt). Returns the slice offset or -1.
+// A worker holding a stale key for a recycled slot (the host recycles slots
+// FIFO over the whole table, so this needs a worker stalled for thousands of
+// atom lifetimes) sees a foreign sequence in the returned word; a valid
+// offset then belongs to the slot's new occupant and is run for it
+// (stale = true: the caller re-reads the slot), never lost.
 __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long key,
                                                  DevCtl* ctl, bool& stale) {
   const unsigned seq = ~static_cast<unsigned>(key >> 24);
-  const unsigned long long old = atom_add_acquire64(&a->claim, 1ull);
+  unsigned long long old;
+  asm volatile("atom.add.acquire.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(&a->claim) : "memory");
   const unsigned off = static_cast<unsigned>(old);
-  const unsigned count = ld_relaxed_gpu(&a->count);
   stale = static_cast<unsigned>(old >> 32) != seq;
-  if (off >= count) return -1;
-  if (stale) atomicAdd(&ctl->stale_claims, 1ull);
-  return static_cast<long long>(off);
+  if (stale) {
+    fence_acq_rel_gpu();
+    if (off >= ld_relaxed_gpu(&a->count)) return -1;
+    atomicAdd(&ctl->stale_claims, 1ull);
+    return static_cast<long long>(off);
+  }
+  return off < ld_relaxed_gpu(&a->count) ? static_cast<long long>(off) : -1;
 }
 
 __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
@@ -412,18 +424,20 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           const unsigned slot = static_cast<unsigned>(key & 0xffffffull);
           if (lane == 0) {
             const DevAtom* a = p.atoms + slot;
-            // The acquire fetch-add ordered the ingest warp's slot writes
-            // before these loads; args are cached per drained atom.
+            // Slot fields are immutable while the atom lives (ordered by the
+            // claim's acquire); cached per drained atom so the fast path reads
+            // nothing but the claim word.
             if (stale || key != sh.key || slot != sh.slot) {
 #pragma unroll
               for (int k2 = 0; k2 < 5; ++k2) sh.cmd.args[k2] = a->args[k2];
               sh.cmd.body = a->body;
               sh.cmd.parts = a->parts;
+              sh.lo = a->lo;
               sh.key = stale ? 0ull : key;
               sh.slot = slot;
             }
             const unsigned parts = sh.cmd.parts;
-            sh.cmd.block = a->lo + off / parts;
+            sh.cmd.block = sh.lo + off / parts;
             sh.cmd.part = static_cast<unsigned>(off % parts);
             sh.t_start = gtimer();
           }
@@ -471,35 +485,39 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        __threadfence();
+        if (lane == 0) {
+          // Completion record first (the host is waiting on it), in the
+          // slot's own record: 15 data words, then the ticket (= seq) with
+          // release semantics, which orders the data before it.
+          CompRec* rec = p.comp + sh.slot;
+          const unsigned long long t0 = ld_relaxed_gpu64(&a->t_first);
+          const unsigned long long t1 = ld_relaxed_gpu64(&a->t_last);
+          const unsigned long long m0 = ld_relaxed_gpu64(&a->touched[0]);
+          const unsigned long long m1 = ld_relaxed_gpu64(&a->touched[1]);
+          const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
+          const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
+          const unsigned long long tag = a->tag;
+          st_relaxed_sys_v4(rec->w + 0, a->atom_id, ld_relaxed_gpu(&a->count) / sh.cmd.parts,
+                            static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32));
+          st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
+                            static_cast<unsigned>(t1), static_cast<unsigned>(t1 >> 32));
+          st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
+                            static_cast<unsigned>(m1), static_cast<unsigned>(m1 >> 32));
+          // t_seen / t_armed as ns before t_first (0 in batch mode).
+          st_relaxed_sys_v2(rec->w + 12, sh.slot, ts ? static_cast<unsigned>(t0 - ts) : 0u);
+          st_relaxed_sys(rec->w + 14, ta ? static_cast<unsigned>(t0 - ta) : 0u);
+          st_release_sys(rec->w + 15, ~static_cast<unsigned>(sh.key >> 24));
+        }
+        __syncwarp();
+        // Device-side bookkeeping after the record; the host recycles this
+        // slot only after thousands of others, long after these land.
         const unsigned long long key = sh.key;
         for (int t = lane; t < p.logical_tpcs; t += 32) {
           const unsigned long long m = a->mask[t >> 6];
           if ((m >> (t & 63)) & 1ull)
             atomicCAS(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], key, 0ull);
         }
-        __syncwarp();
-        __threadfence();
         if (lane == 0) {
-          const unsigned idx = atomicAdd(&p.ctl->comp_tail, 1u);
-          CompRec* rec = p.comp + (idx % p.comp_cap);
-          const unsigned long long t0 = *reinterpret_cast<volatile unsigned long long*>(&a->t_first);
-          const unsigned long long t1 = *reinterpret_cast<volatile unsigned long long*>(&a->t_last);
-          const unsigned long long m0 = *reinterpret_cast<volatile unsigned long long*>(&a->touched[0]);
-          const unsigned long long m1 = *reinterpret_cast<volatile unsigned long long*>(&a->touched[1]);
-          st_relaxed_sys_v4(rec->w + 0, a->atom_id, a->count / a->parts, static_cast<unsigned>(a->tag),
-                            static_cast<unsigned>(a->tag >> 32));
-          st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
-                            static_cast<unsigned>(t1), static_cast<unsigned>(t1 >> 32));
-          st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
-                            static_cast<unsigned>(m1), static_cast<unsigned>(m1 >> 32));
-          const unsigned long long ts = *reinterpret_cast<volatile unsigned long long*>(&a->t_seen);
-          const unsigned long long ta = *reinterpret_cast<volatile unsigned long long*>(&a->t_armed);
-          // t_seen / t_armed as ns before t_first (0 in batch mode).
-          st_relaxed_sys_v4(rec->w + 12, sh.slot, ts ? static_cast<unsigned>(t0 - ts) : 0u,
-                            ta ? static_cast<unsigned>(t0 - ta) : 0u, 0u);
-          __threadfence_system();
-          st_release_sys(rec->w + 15, idx + 1u);
           atomicAdd(&p.ctl->atoms_done, 1ull);
           __threadfence();
           atomicSub(&p.ctl->outstanding, 1);
@@ -546,6 +564,7 @@ int64_t steady_ns() {
 
 struct HostAtom {
   uint32_t atom_id = 0;
+  uint32_t seq = 0;
   int64_t submit_ns = 0;
   uint64_t mask[2] = {0, 0};
   bool live = false;
@@ -579,7 +598,7 @@ struct gpuos_dev {
   int grid = 0;
   // host bookkeeping
   uint64_t ring_head = 0;  // next ring index to publish
-  uint32_t comp_head = 0;  // next completion index to consume
+  std::vector<uint32_t> live;  // slots of atoms in flight (completion scan)
   uint32_t next_seq = 1;
   uint32_t next_atom_id = 0;
   std::deque<uint32_t> free_slots;  // FIFO: a freed slot is reused last
@@ -773,7 +792,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   std::memset(d->alive_h, 0, sizeof(unsigned) * d->grid);
   *d->consumed_h = 0;
   d->ring_head = 0;
-  d->comp_head = 0;
+  d->live.clear();
   std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
 
   // Calibrate device globaltimer against the host origin (+- half an RTT),
@@ -947,6 +966,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   std::vector<unsigned long long> resident(static_cast<size_t>(T) * kResident, 0ull);
   std::vector<int> fill(static_cast<size_t>(T), 0);
   std::vector<uint32_t> ids(static_cast<size_t>(n));
+  std::vector<uint32_t> seqs(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) {
     const gpuos_atom_desc& a = descs[i];
     const uint32_t parts = a.parts == 0 ? 1u : a.parts;
@@ -955,6 +975,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     if (a.body != GPUOS_BODY_STREAM && a.body != GPUOS_BODY_SPIN)
       return fail(GPUOS_E_CONFIG, "unknown body kind");
     const uint32_t seq = d->next_seq++;
+    seqs[static_cast<size_t>(i)] = seq;
     const int prio = map_priority(a.priority);
     DevAtom& x = atoms[static_cast<size_t>(i)];
     std::memset(&x, 0, sizeof x);
@@ -993,6 +1014,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   for (int i = 0; i < n; ++i) {
     HostAtom& h = d->slots[static_cast<size_t>(i)];
     h.atom_id = ids[static_cast<size_t>(i)];
+    h.seq = seqs[static_cast<size_t>(i)];
     h.submit_ns = now;
     h.mask[0] = descs[i].tpc_mask[0];
     h.mask[1] = descs[i].tpc_mask[1];
@@ -1001,7 +1023,8 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
   std::memset(d->comp_h, 0, sizeof(CompRec) * d->cfg.atom_slots);
   std::memset(d->alive_h, 0, sizeof(unsigned) * d->grid);
-  d->comp_head = 0;
+  d->live.clear();
+  for (int i = 0; i < n; ++i) d->live.push_back(static_cast<uint32_t>(i));
   d->in_flight = n;
 
   CUDA_TRY(cudaMemcpy(d->atoms, atoms.data(), sizeof(DevAtom) * n, cudaMemcpyHostToDevice));
@@ -1096,6 +1119,7 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   put64(data, kFTrace, reinterpret_cast<uint64_t>(a->trace));
   HostAtom& h = d->slots[slot];
   h.atom_id = id;
+  h.seq = seq;
   h.submit_ns = gpuos_dev_now_ns(d);
   h.mask[0] = a->tpc_mask[0];
   h.mask[1] = a->tpc_mask[1];
@@ -1108,6 +1132,7 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   }
   for (int t = 0; t < T; ++t)
     if ((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) ++d->tpc_resident[t];
+  d->live.push_back(slot);
   ++d->in_flight;
   if (atom_id) *atom_id = id;
   return GPUOS_OK;
@@ -1148,10 +1173,16 @@ int gpuos_dev_set_fence_mask(gpuos_dev* d, const uint64_t mask[2], int32_t min_p
 int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
   if (!d || (!out && max > 0)) return fail(GPUOS_E_CONFIG, "null argument");
   int n = 0;
-  while (n < max) {
-    CompRec* rec = d->comp_h + (d->comp_head % d->cfg.atom_slots);
-    const uint32_t ticket = __atomic_load_n(&rec->w[15], __ATOMIC_ACQUIRE);
-    if (ticket != d->comp_head + 1u) break;
+  // Each in-flight atom owns the completion record of its slot; its ticket
+  // is the atom's sequence number once the device has published it.
+  for (std::size_t i = 0; i < d->live.size() && n < max;) {
+    const uint32_t slot = d->live[i];
+    HostAtom& h = d->slots[slot];
+    CompRec* rec = d->comp_h + slot;
+    if (__atomic_load_n(&rec->w[15], __ATOMIC_ACQUIRE) != h.seq) {
+      ++i;
+      continue;
+    }
     const volatile uint32_t* w = rec->w;
     gpuos_completion& c = out[n];
     c.atom_id = w[0];
@@ -1161,23 +1192,22 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
     const uint64_t t_last = (uint64_t)w[6] | ((uint64_t)w[7] << 32);
     c.tpc_touched[0] = (uint64_t)w[8] | ((uint64_t)w[9] << 32);
     c.tpc_touched[1] = (uint64_t)w[10] | ((uint64_t)w[11] << 32);
-    const uint32_t slot = w[12];
     c.dev_first_start_ns = static_cast<int64_t>(t_first) - d->gt_offset;
     c.dev_ingest_ns = c.dev_first_start_ns - static_cast<int64_t>(w[13]);
     c.dev_armed_ns = c.dev_first_start_ns - static_cast<int64_t>(w[14]);
     c.dev_last_end_ns = static_cast<int64_t>(t_last) - d->gt_offset;
     c.host_complete_ns = gpuos_dev_now_ns(d);
-    if (slot >= d->slots.size() || !d->slots[slot].live || d->slots[slot].atom_id != c.atom_id)
-      return fail(GPUOS_E_INVARIANT, "completion for an unknown atom");
-    HostAtom& h = d->slots[slot];
     c.host_submit_ns = h.submit_ns;
+    if (w[12] != slot || c.atom_id != h.atom_id)
+      return fail(GPUOS_E_INVARIANT, "completion record does not match its atom");
     for (int t = 0; t < d->cfg.logical_tpcs; ++t)
       if ((h.mask[t >> 6] >> (t & 63)) & 1ull) --d->tpc_resident[t];
     h.live = false;
     d->free_slots.push_back(slot);
+    d->live[i] = d->live.back();  // O(1) removal; order is irrelevant
+    d->live.pop_back();
     --d->in_flight;
     ++d->stats.atoms_completed;
-    ++d->comp_head;
     ++n;
   }
   return n;

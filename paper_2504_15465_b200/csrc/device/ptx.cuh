@@ -30,6 +30,12 @@ __device__ __forceinline__ void st_release_sys64(unsigned long long* p,
                                                  unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_v2(unsigned* p, unsigned a, unsigned b) {
+  asm volatile("st.relaxed.sys.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
 __device__ __forceinline__ void st_relaxed_sys_v4(unsigned* p, unsigned a,
                                                   unsigned b, unsigned c,
                                                   unsigned d) {
