@@ -42,7 +42,7 @@ namespace gpuos {
 struct B200Options {
   int device = 0;
   int workers_per_sm = 2;
-  int idle_sleep_ns = 256;
+  int idle_sleep_ns = 128;
   bool trace_blocks = false;        // per-block execution trace (verification)
   enum class Synth { Stream, Spin } synth = Synth::Stream;
   double stream_words_per_us = 2750.0;  // None -> Stream sizing (per worker)

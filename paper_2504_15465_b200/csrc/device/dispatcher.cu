@@ -314,10 +314,9 @@ __device__ __forceinline__ void ld_relaxed_gpu_v2(const void* p, unsigned long l
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
-// Lane 0: claim one slice of the atom behind `key` with an acquire fetch-add
-// on its claim word: the ingest warp armed that word with a release store
-// after writing the slot, so the slot fields lane 0 reads next are ordered
-// (lane 0 is not the lane that read the key). Fetch-add never retries, so 300 workers
+// Lane 0: claim one slice of the atom behind `key` with a relaxed fetch-add
+// on its claim word; the slot fields were read by the lane that acquired the
+// key and are handed over by shuffle. Fetch-add never retries, so 300 workers
 // draining one atom cost one L2 atomic each; the CAS loop it replaced spent
 // ~140 failed attempts per claim under that contention
 // (profiles/ncu_k_worker_r01_cas.txt). Returns the slice offset or -1.
@@ -329,8 +328,7 @@ __device__ __forceinline__ void ld_relaxed_gpu_v2(const void* p, unsigned long l
 __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long key,
                                                  DevCtl* ctl, bool& stale) {
   const unsigned seq = ~static_cast<unsigned>(key >> 24);
-  unsigned long long old;
-  asm volatile("atom.add.acquire.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(&a->claim) : "memory");
+  const unsigned long long old = atomicAdd(&a->claim, 1ull);
   const unsigned off = static_cast<unsigned>(old);
   stale = static_cast<unsigned>(old >> 32) != seq;
   if (stale) {
@@ -383,28 +381,39 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
     if (warp == 0) {
       int go = 0;
+      unsigned ver = ld_relaxed_gpu(p.version + tpc);  // latest observed
       for (;;) {
-        const unsigned ver = ld_relaxed_gpu(p.version + tpc);
         long long off = -1;
         unsigned long long key = 0ull;
         bool stale = false;
         if (cur_key != 0ull && ver == cur_ver) {
+          // Fast path: next slice of the atom being drained. The version is
+          // re-read alongside the claim; a change noticed only after it
+          // costs at most one slice of priority inversion.
           if (lane == 0) off = claim_block(p.atoms + cur_slot, cur_key, p.ctl, stale);
+          ver = ld_relaxed_gpu(p.version + tpc);
           off = __shfl_sync(0xffffffffu, off, 0);
           if (off >= 0) key = cur_key;
+          if (stale && lane == 0) sh.key = 0ull;  // slot recycled: reload its fields
         }
         if (off < 0) {
           cur_key = 0ull;
-          if (ld_relaxed_gpu(&p.ctl->quit)) break;
-          // Full arbitration: eligible = waiting blocks, not paused, not
-          // fenced off this TPC; highest priority then oldest wins.
+          // Full arbitration: eligible = waiting slices, not paused, not
+          // fenced off this TPC; highest priority then oldest wins. Each
+          // lane reads one key (acquire) and then that atom's hot line, so
+          // the winner's fields arrive with the arbitration itself.
           const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
           const unsigned long long k = ld_acquire_gpu64(list + lane);
           bool eligible = false;
+          unsigned long long f_lo = 0, f_bp = 0, f_a[5] = {0, 0, 0, 0, 0};
           if (k != 0ull) {
             const DevAtom* a = p.atoms + (k & 0xffffffull);
             unsigned long long cw, cp;
             ld_relaxed_gpu_v2(a, cw, cp);  // claim | count, paused
+            ld_relaxed_gpu_v2(&a->lo, f_lo, f_bp);  // lo | body, parts
+            ld_relaxed_gpu_v2(&a->args[0], f_a[0], f_a[1]);
+            ld_relaxed_gpu_v2(&a->args[2], f_a[2], f_a[3]);
+            f_a[4] = ld_relaxed_gpu64(&a->args[4]);
             eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
                        static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
                        static_cast<unsigned>(cp >> 32) == 0u &&
@@ -415,25 +424,43 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
             if (lane == 0) off = claim_block(p.atoms + (key & 0xffffffull), key, p.ctl, stale);
             off = __shfl_sync(0xffffffffu, off, 0);
             if (off < 0) {
-              ++retries;  // lost that atom's last blocks to other workers
+              ++retries;  // lost that atom's last slices to other workers
+              ver = ld_relaxed_gpu(p.version + tpc);
               continue;
+            }
+            // Hand the winner's fields to lane 0 (no second round trip).
+            const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
+            f_lo = __shfl_sync(0xffffffffu, f_lo, win);
+            f_bp = __shfl_sync(0xffffffffu, f_bp, win);
+#pragma unroll
+            for (int k2 = 0; k2 < 5; ++k2) f_a[k2] = __shfl_sync(0xffffffffu, f_a[k2], win);
+            if (lane == 0) {
+              if (stale) {
+                sh.key = 0ull;  // recycled slot: fields reloaded below
+              } else {
+#pragma unroll
+                for (int k2 = 0; k2 < 5; ++k2) sh.cmd.args[k2] = f_a[k2];
+                sh.cmd.body = static_cast<unsigned>(f_bp);
+                sh.cmd.parts = static_cast<unsigned>(f_bp >> 32);
+                sh.lo = static_cast<long long>(f_lo);
+                sh.key = key;
+                sh.slot = static_cast<unsigned>(key & 0xffffffull);
+              }
             }
           }
         }
         if (off >= 0) {
           const unsigned slot = static_cast<unsigned>(key & 0xffffffull);
           if (lane == 0) {
-            const DevAtom* a = p.atoms + slot;
-            // Slot fields are immutable while the atom lives (ordered by the
-            // claim's acquire); cached per drained atom so the fast path reads
-            // nothing but the claim word.
-            if (stale || key != sh.key || slot != sh.slot) {
+            if (sh.key == 0ull || sh.slot != slot) {
+              // Recycled slot adopted by claim_block (which fenced): read the
+              // new occupant's fields.
+              const DevAtom* a = p.atoms + slot;
 #pragma unroll
               for (int k2 = 0; k2 < 5; ++k2) sh.cmd.args[k2] = a->args[k2];
               sh.cmd.body = a->body;
               sh.cmd.parts = a->parts;
               sh.lo = a->lo;
-              sh.key = stale ? 0ull : key;
               sh.slot = slot;
             }
             const unsigned parts = sh.cmd.parts;
@@ -441,18 +468,23 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
             sh.cmd.part = static_cast<unsigned>(off % parts);
             sh.t_start = gtimer();
           }
-          cur_key = key;
+          cur_key = stale ? 0ull : key;
           cur_slot = slot;
           cur_ver = ver;
           go = 1;
           break;
         }
+        if (ld_relaxed_gpu(&p.ctl->quit)) break;
         if (ld_relaxed_gpu(&p.ctl->drain) && ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0) break;
         if (gtimer() > p.ctl->deadline) break;
         // Idle: wait for this TPC's candidate set to change.
         for (int k2 = 0; k2 < 64; ++k2) {
           __nanosleep(p.idle_sleep_ns);
-          if (ld_relaxed_gpu(p.version + tpc) != ver) break;
+          const unsigned v = ld_relaxed_gpu(p.version + tpc);
+          if (v != ver) {
+            ver = v;
+            break;
+          }
         }
       }
       if (lane == 0) sh.go = go;
@@ -657,7 +689,7 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   if (cfg.workers_per_sm <= 0) cfg.workers_per_sm = 2;
   if (cfg.atom_slots <= 0) cfg.atom_slots = 4096;
   if (cfg.ring_entries <= 0) cfg.ring_entries = 4096;
-  if (cfg.idle_sleep_ns <= 0) cfg.idle_sleep_ns = 256;
+  if (cfg.idle_sleep_ns <= 0) cfg.idle_sleep_ns = 128;
   if (cfg.workers_per_sm > 8) return fail(GPUOS_E_CONFIG, "workers_per_sm must be <= 8");
   if (cfg.atom_slots > (1 << 24)) return fail(GPUOS_E_CONFIG, "atom_slots must be < 2^24");
 
