@@ -141,9 +141,13 @@ class B200Runtime {
   bool running_ = false;
   std::unordered_map<std::uint32_t, Workspace> ws_;
   std::vector<std::uint32_t*> trace_of_;  // per kernel id
+  // Trace pool: fixed-size chunks kept across runs (allocating during a
+  // live run would stall it), zeroed between runs.
+  static constexpr std::uint64_t kTraceChunkWords = 16ull << 20;
   std::vector<std::uint32_t*> trace_chunks_;
-  std::uint32_t* trace_pool_ = nullptr;
-  std::uint64_t trace_pool_used_ = 0, trace_pool_cap_ = 0;
+  std::vector<std::uint64_t> trace_chunk_words_;
+  std::size_t trace_chunk_ = 0;           // chunk being filled
+  std::uint64_t trace_pool_used_ = 0;     // words used in it
   std::vector<Resolved> resolved_;        // per kernel id
   std::vector<char> has_resolved_;
 };

@@ -102,8 +102,8 @@ enum RingField : int {
   kFArgs = 14 /*10*/, kFTag = 24 /*2*/, kFTrace = 26 /*2*/
 };
 
-// 64-byte completion record written by the device into mapped host memory;
-// word 15 is the ticket, stored after a system-scope fence.
+// 64-byte completion record written by the device into mapped host memory:
+// four 16-byte chunks, word 3 of each is the ticket (the atom's sequence).
 struct CompRec {
   unsigned w[16];
 };
@@ -139,157 +139,241 @@ __device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) 
 }
 
 // ------------------------------------------------------------ ingest warp
+// Ring entries are read kIngestBatch at a time: one 512-byte PCIe read per
+// poll (lane l loads 16 B: entry head + l/8, words 4(l%8)..4(l%8)+3), so a
+// backlog of submissions costs one host round trip per batch, not per atom.
+// Publication uses two GPU-scope fences per batch, not per atom:
+//   A  slot fields (claim exhausted), resident-list entry choice, outstanding
+//      += 1, pause / fence words                              -- MEMBAR --
+//   B  arm claims, insert resident keys                       -- MEMBAR --
+//   C  bump the version of every TPC whose candidates changed (release
+//      pattern: workers read versions with acquire), drain / quit flags.
+// A worker that acquires a key therefore sees the slot fields (A precedes
+// the fence before B), and a worker whose acquire of a TPC version observes
+// phase C sees every key and armed claim of the batch (no lost wake-up).
+constexpr int kIngestBatch = 4;
+
+struct IngestSubmit {
+  unsigned slot, seq;
+  unsigned long long mask[2];
+  unsigned long long key;
+};
+
+__device__ __forceinline__ uint4 ld_relaxed_sys_v4(const unsigned* p) {
+  uint4 r;
+  asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_relaxed_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_relaxed_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
   // Shadow occupancy of every TPC's resident list. Only this warp inserts
   // keys, so an entry whose shadow bit is clear is certainly empty; workers
   // clear entries behind its back, which the shadow learns on refresh.
   __shared__ unsigned shadow[GPUOS_MAX_TPCS];
+  // Entries chosen in the current batch whose keys are not stored yet (a
+  // refresh from the list must not hand them out twice). TPC t is only ever
+  // touched by lane t % 32, so neither array needs synchronisation.
+  __shared__ unsigned pend[GPUOS_MAX_TPCS];
+  __shared__ IngestSubmit subs[kIngestBatch];
   const unsigned lane = threadIdx.x;
-  for (int t = lane; t < GPUOS_MAX_TPCS; t += 32) shadow[t] = 0u;  // lists start empty
+  for (int t = lane; t < GPUOS_MAX_TPCS; t += 32) shadow[t] = pend[t] = 0u;  // lists start empty
   __syncwarp();
   unsigned long long head = 0;
+  unsigned polls = 0;
   for (;;) {
-    if (ld_relaxed_gpu(&p.ctl->quit)) break;
-    if (gtimer() > p.ctl->deadline) {
-      atomicExch(&p.ctl->quit, 1u);
-      break;
+    if ((++polls & 15u) == 1u) {
+      if (ld_relaxed_gpu(&p.ctl->quit)) break;
+      if (gtimer() > p.ctl->deadline) {
+        atomicExch(&p.ctl->quit, 1u);
+        break;
+      }
     }
-    const RingEntry* e = p.ring + (head % p.ring_cap);
-    const unsigned w = ld_relaxed_sys(&e->w[lane]);
-    const unsigned want = static_cast<unsigned>(head + 1);
-    const bool ok = __all_sync(0xffffffffu, (lane & 7) != 7 || w == want);
-    if (!ok) {
-      __nanosleep(64);
+    const unsigned el = lane >> 3;  // entry of this lane's 16 bytes
+    const uint4 v = ld_relaxed_sys_v4(p.ring[(head + el) % p.ring_cap].w + 4 * (lane & 7));
+    // Sector s of entry e ends with its ticket: word 8s+7 = lane 8e+2s+1, .w
+    const bool tk = (lane & 1u) == 0u || v.w == static_cast<unsigned>(head + el + 1);
+    const unsigned okm = __ballot_sync(0xffffffffu, tk);
+    int n = 0;
+    while (n < kIngestBatch && ((okm >> (8 * n)) & 0xffu) == 0xffu) ++n;
+    if (n == 0) {
+      __nanosleep(32);
       continue;
     }
-    auto get = [&](int d) { return __shfl_sync(0xffffffffu, w, ring_word(d)); };
     const unsigned long long t_seen = gtimer();
-    const unsigned op = get(kFOp);
-    bool stop = false;
-    if (op == kOpSubmit) {
-      const unsigned slot = get(kFSlot);
-      const unsigned seq = get(kFSeq);
-      const int prio = static_cast<int>(get(kFPrio));
-      const unsigned long long mask0 = field64(get(kFMask0), get(kFMask0 + 1));
-      const unsigned long long mask1 = field64(get(kFMask1), get(kFMask1 + 1));
-      unsigned long long args[5];
+    int n_sub = 0;
+    unsigned long long bump0 = 0, bump1 = 0;  // TPCs whose candidate set changed
+    bool stop = false, set_drain = false, set_quit = false;
+    for (int j = 0; j < n && !stop; ++j) {
+      // Transpose: lane l gets word l of entry j.
+      const int src = 8 * j + static_cast<int>(lane >> 2);
+      const unsigned x0 = __shfl_sync(0xffffffffu, v.x, src);
+      const unsigned x1 = __shfl_sync(0xffffffffu, v.y, src);
+      const unsigned x2 = __shfl_sync(0xffffffffu, v.z, src);
+      const unsigned x3 = __shfl_sync(0xffffffffu, v.w, src);
+      const unsigned c = lane & 3u;
+      const unsigned w = c == 0 ? x0 : c == 1 ? x1 : c == 2 ? x2 : x3;
+      auto get = [&](int d) { return __shfl_sync(0xffffffffu, w, ring_word(d)); };
+      const unsigned op = get(kFOp);
+      if (op == kOpSubmit) {
+        const unsigned slot = get(kFSlot);
+        const unsigned seq = get(kFSeq);
+        const int prio = static_cast<int>(get(kFPrio));
+        const unsigned long long mask0 = field64(get(kFMask0), get(kFMask0 + 1));
+        const unsigned long long mask1 = field64(get(kFMask1), get(kFMask1 + 1));
+        unsigned long long args[5];
 #pragma unroll
-      for (int k = 0; k < 5; ++k) args[k] = field64(get(kFArgs + 2 * k), get(kFArgs + 2 * k + 1));
-      const unsigned long long tag = field64(get(kFTag), get(kFTag + 1));
-      const unsigned long long trace = field64(get(kFTrace), get(kFTrace + 1));
-      const long long lo = static_cast<long long>(field64(get(kFLo), get(kFLo + 1)));
-      const unsigned count = get(kFCount);  // slices = blocks x parts
-      const unsigned body = get(kFBody);
-      const unsigned atom_id = get(kFAtomId);
-      const unsigned parts = get(kFAux);
-      DevAtom* a = p.atoms + slot;
-      if (lane == 0) {
-        // Exhausted (offset == count) until armed: a stale fetch-add from a
-        // worker still holding the previous occupant's key cannot carry into
-        // the sequence bits, and the arming store overwrites it.
-        a->claim = (static_cast<unsigned long long>(seq) << 32) | count;
-        a->count = count;
-        a->paused = 0;
-        a->lo = lo;
-        a->body = body;
-        a->parts = parts;
+        for (int k = 0; k < 5; ++k) args[k] = field64(get(kFArgs + 2 * k), get(kFArgs + 2 * k + 1));
+        const unsigned long long tag = field64(get(kFTag), get(kFTag + 1));
+        const unsigned long long trace = field64(get(kFTrace), get(kFTrace + 1));
+        const long long lo = static_cast<long long>(field64(get(kFLo), get(kFLo + 1)));
+        const unsigned count = get(kFCount);  // slices = blocks x parts
+        const unsigned body = get(kFBody);
+        const unsigned atom_id = get(kFAtomId);
+        const unsigned parts = get(kFAux);
+        DevAtom* a = p.atoms + slot;
+        if (lane == 0) {
+          // Exhausted (offset == count) until armed in phase B: a stale
+          // fetch-add from a worker still holding the previous occupant's
+          // key cannot carry into the sequence bits, and arming overwrites it.
+          a->claim = (static_cast<unsigned long long>(seq) << 32) | count;
+          a->count = count;
+          a->paused = 0;
+          a->lo = lo;
+          a->body = body;
+          a->parts = parts;
 #pragma unroll
-        for (int k = 0; k < 5; ++k) a->args[k] = args[k];
-        a->seq = seq;
-        a->prio = prio;
-        a->done = 0;
-        a->atom_id = atom_id;
-        a->tag = tag;
-        a->trace = reinterpret_cast<unsigned*>(trace);
-        a->mask[0] = mask0;
-        a->mask[1] = mask1;
-        a->t_first = ~0ull;
-        a->t_last = 0;
-        a->touched[0] = 0;
-        a->touched[1] = 0;
-        a->t_seen = t_seen;
-        fence_acq_rel_gpu();
-      }
-      __syncwarp();
-      const unsigned long long key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
-                                     (static_cast<unsigned long long>(~seq) << 24) |
-                                     (slot & 0xffffffu);
-      for (int t = lane; t < p.logical_tpcs; t += 32) {
-        const unsigned long long m = t < 64 ? mask0 : mask1;
-        if (!((m >> (t & 63)) & 1ull)) continue;
-        unsigned long long* list = p.resident + static_cast<size_t>(t) * kResident;
-        unsigned occ = shadow[t];
-        while (occ == ~0u) {  // refresh from the list (host admission keeps room)
-          occ = 0u;
-          for (int k = 0; k < kResident; ++k)
-            if (ld_relaxed_gpu64(list + k) != 0ull) occ |= 1u << k;
-          if (occ == ~0u) __nanosleep(128);
+          for (int k = 0; k < 5; ++k) a->args[k] = args[k];
+          a->seq = seq;
+          a->prio = prio;
+          a->done = 0;
+          a->atom_id = atom_id;
+          a->tag = tag;
+          a->trace = reinterpret_cast<unsigned*>(trace);
+          a->mask[0] = mask0;
+          a->mask[1] = mask1;
+          a->t_first = ~0ull;
+          a->t_last = 0;
+          a->touched[0] = 0;
+          a->touched[1] = 0;
+          a->t_seen = t_seen;
+          a->t_armed = 0;
+          atomicAdd(&p.ctl->outstanding, 1);  // before any worker can claim
+          IngestSubmit& s = subs[n_sub];
+          s.slot = slot;
+          s.seq = seq;
+          s.mask[0] = mask0;
+          s.mask[1] = mask1;
+          s.key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
+                  (static_cast<unsigned long long>(~seq) << 24) | (slot & 0xffffffu);
         }
-        const int k = __ffs(~occ) - 1;
-        shadow[t] = occ | (1u << k);
-        a->entry[t] = static_cast<unsigned char>(k);
-        st_release_gpu64(list + k, key);  // publishes the slot fields with it
-      }
-      __syncwarp();
-      if (lane == 0) {
-        atomicAdd(&p.ctl->outstanding, 1);
-        a->t_armed = gtimer();
-        // Arm after every key: a worker finishing the atom then finds all
-        // its entry indices recorded.
-        st_release_gpu64(&a->claim, static_cast<unsigned long long>(seq) << 32);
-      }
-      __syncwarp();
-      for (int t = lane; t < p.logical_tpcs; t += 32) {
-        const unsigned long long m = t < 64 ? mask0 : mask1;
-        if ((m >> (t & 63)) & 1ull) red_release_gpu_add(p.version + t, 1u);
-      }
-    } else if (op == kOpPause || op == kOpResume) {
-      DevAtom* a = p.atoms + get(kFSlot);
-      if (lane == 0) {
-        atomicExch(&a->paused, op == kOpPause ? 1u : 0u);
-        __threadfence();
-      }
-      __syncwarp();
-      // Workers drain one atom on a fast path while their TPC's version is
-      // unchanged, so pause and resume both bump it.
-      for (int t = lane; t < p.logical_tpcs; t += 32) {
-          const unsigned long long m = a->mask[t >> 6];
-          if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
+        // Choose each TPC's resident-list entry now (the finishing worker
+        // needs a->entry[] for every TPC), insert the key in phase B.
+        for (int t = lane; t < p.logical_tpcs; t += 32) {
+          const unsigned long long m = t < 64 ? mask0 : mask1;
+          if (!((m >> (t & 63)) & 1ull)) continue;
+          const unsigned long long* list = p.resident + static_cast<size_t>(t) * kResident;
+          unsigned occ = shadow[t];
+          while (occ == ~0u) {  // refresh from the list (host admission keeps room)
+            occ = pend[t];
+            for (int k = 0; k < kResident; ++k)
+              if (ld_relaxed_gpu64(list + k) != 0ull) occ |= 1u << k;
+            if (occ == ~0u) __nanosleep(128);
+          }
+          const int k = __ffs(~occ) - 1;
+          shadow[t] = occ | (1u << k);
+          pend[t] |= 1u << k;
+          a->entry[t] = static_cast<unsigned char>(k);
         }
-    } else if (op == kOpFence) {
-      // Shuffles are warp-collective: read every field before lane-0 work.
-      const int t = static_cast<int>(get(kFAux));
-      const int floor_prio = static_cast<int>(get(kFPrio));
-      if (lane == 0 && t >= 0 && t < p.logical_tpcs) {
-        atomicExch(p.fence + t, floor_prio);
-        __threadfence();
-        atomicAdd(p.version + t, 1u);
+        bump0 |= mask0;
+        bump1 |= mask1;
+        ++n_sub;
+      } else if (op == kOpPause || op == kOpResume) {
+        // Shuffles are warp-collective: read every field before lane-0 work.
+        const unsigned slot = get(kFSlot);
+        DevAtom* a = p.atoms + slot;
+        if (lane == 0) atomicExch(&a->paused, op == kOpPause ? 1u : 0u);
+        // Workers drain one atom on a fast path while their TPC's version is
+        // unchanged, so pause and resume both bump it.
+        // Lane 0 wrote the mask if the atom arrived in this batch: read it
+        // there (program order) and broadcast.
+        unsigned long long m0 = 0, m1 = 0;
+        if (lane == 0) {
+          m0 = ld_relaxed_gpu64(&a->mask[0]);
+          m1 = ld_relaxed_gpu64(&a->mask[1]);
+        }
+        bump0 |= __shfl_sync(0xffffffffu, m0, 0);
+        bump1 |= __shfl_sync(0xffffffffu, m1, 0);
+      } else if (op == kOpFence) {
+        const int t = static_cast<int>(get(kFAux));
+        const int floor_prio = static_cast<int>(get(kFPrio));
+        if (t >= 0 && t < p.logical_tpcs) {
+          if (lane == 0) atomicExch(p.fence + t, floor_prio);
+          if (t < 64) bump0 |= 1ull << t; else bump1 |= 1ull << (t - 64);
+        }
+      } else if (op == kOpFenceMask) {
+        const unsigned long long m0 = field64(get(kFMask0), get(kFMask0 + 1));
+        const unsigned long long m1 = field64(get(kFMask1), get(kFMask1 + 1));
+        const int floor_prio = static_cast<int>(get(kFPrio));
+        for (int t = lane; t < p.logical_tpcs; t += 32) {
+          const unsigned long long m = t < 64 ? m0 : m1;
+          if ((m >> (t & 63)) & 1ull) atomicExch(p.fence + t, floor_prio);
+        }
+        bump0 |= m0;
+        bump1 |= m1;
+      } else if (op == kOpDrain) {
+        set_drain = true;
+        stop = true;
+      } else if (op == kOpShutdown) {
+        set_quit = true;
+        stop = true;
       }
-    } else if (op == kOpFenceMask) {
-      const unsigned long long m0 = field64(get(kFMask0), get(kFMask0 + 1));
-      const unsigned long long m1 = field64(get(kFMask1), get(kFMask1 + 1));
-      const int floor_prio = static_cast<int>(get(kFPrio));
-      for (int t = lane; t < p.logical_tpcs; t += 32) {
-        const unsigned long long m = t < 64 ? m0 : m1;
-        if (!((m >> (t & 63)) & 1ull)) continue;
-        atomicExch(p.fence + t, floor_prio);
-      }
-      __syncwarp();
-      __threadfence();
-      for (int t = lane; t < p.logical_tpcs; t += 32) {
-        const unsigned long long m = t < 64 ? m0 : m1;
-        if ((m >> (t & 63)) & 1ull) atomicAdd(p.version + t, 1u);
-      }
-    } else if (op == kOpDrain) {
-      if (lane == 0) atomicExch(&p.ctl->drain, 1u);
-      stop = true;
-    } else if (op == kOpShutdown) {
-      if (lane == 0) atomicExch(&p.ctl->quit, 1u);
-      stop = true;
+      ++head;
     }
-    ++head;
     __syncwarp();
-    if (lane == 0) st_release_sys64(p.consumed, head);
+    if (n_sub > 0) {
+      fence_acq_rel_gpu();  // every lane: phase A before its phase-B stores
+      __syncwarp();
+      const unsigned long long t_armed = gtimer();
+      for (int i = 0; i < n_sub; ++i) {
+        const IngestSubmit s = subs[i];
+        DevAtom* a = p.atoms + s.slot;
+        if (lane == 0) {
+          st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
+          a->t_armed = t_armed;
+        }
+        for (int t = lane; t < p.logical_tpcs; t += 32) {
+          const unsigned long long m = s.mask[t >> 6];
+          if ((m >> (t & 63)) & 1ull)
+            st_relaxed_gpu64(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], s.key);
+        }
+      }
+      for (int t = lane; t < p.logical_tpcs; t += 32) pend[t] = 0u;
+    }
+    __syncwarp();
+    fence_acq_rel_gpu();  // phase B (and pause / fence words) before the bumps
+    for (int t = lane; t < p.logical_tpcs; t += 32) {
+      const unsigned long long m = t < 64 ? bump0 : bump1;
+      if ((m >> (t & 63)) & 1ull) red_relaxed_gpu_add(p.version + t, 1u);
+    }
+    if (lane == 0) {
+      if (set_drain) atomicExch(&p.ctl->drain, 1u);
+      if (set_quit) atomicExch(&p.ctl->quit, 1u);
+      // The entries' words are in registers: the host may overwrite them.
+      st_relaxed_sys64(p.consumed, head);
+    }
+    __syncwarp();
     if (stop) break;
   }
 }
@@ -326,7 +410,7 @@ __device__ __forceinline__ void ld_relaxed_gpu_v2(const void* p, unsigned long l
 // offset then belongs to the slot's new occupant and is run for it
 // (stale = true: the caller re-reads the slot), never lost.
 __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long key,
-                                                 DevCtl* ctl, bool& stale) {
+                                                 unsigned count, DevCtl* ctl, bool& stale) {
   const unsigned seq = ~static_cast<unsigned>(key >> 24);
   const unsigned long long old = atomicAdd(&a->claim, 1ull);
   const unsigned off = static_cast<unsigned>(old);
@@ -337,7 +421,9 @@ __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long 
     atomicAdd(&ctl->stale_claims, 1ull);
     return static_cast<long long>(off);
   }
-  return off < ld_relaxed_gpu(&a->count) ? static_cast<long long>(off) : -1;
+  // `count` was read with the key's hot line; it never changes while the
+  // sequence matches.
+  return off < count ? static_cast<long long>(off) : -1;
 }
 
 __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
@@ -366,6 +452,7 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   unsigned long long cur_key = 0ull;
   unsigned cur_ver = 0u;
   unsigned cur_slot = 0u;
+  unsigned cur_count = 0u;
   int cur_tpc = -1;
 
   for (;;) {
@@ -381,7 +468,7 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
     if (warp == 0) {
       int go = 0;
-      unsigned ver = ld_relaxed_gpu(p.version + tpc);  // latest observed
+      unsigned ver = ld_acquire_gpu(p.version + tpc);  // latest observed
       for (;;) {
         long long off = -1;
         unsigned long long key = 0ull;
@@ -390,8 +477,8 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           // Fast path: next slice of the atom being drained. The version is
           // re-read alongside the claim; a change noticed only after it
           // costs at most one slice of priority inversion.
-          if (lane == 0) off = claim_block(p.atoms + cur_slot, cur_key, p.ctl, stale);
-          ver = ld_relaxed_gpu(p.version + tpc);
+          if (lane == 0) off = claim_block(p.atoms + cur_slot, cur_key, cur_count, p.ctl, stale);
+          ver = ld_acquire_gpu(p.version + tpc);
           off = __shfl_sync(0xffffffffu, off, 0);
           if (off >= 0) key = cur_key;
           if (stale && lane == 0) sh.key = 0ull;  // slot recycled: reload its fields
@@ -405,11 +492,12 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
           const unsigned long long k = ld_acquire_gpu64(list + lane);
           bool eligible = false;
-          unsigned long long f_lo = 0, f_bp = 0, f_a[5] = {0, 0, 0, 0, 0};
+          unsigned long long f_lo = 0, f_bp = 0, f_cp = 0, f_a[5] = {0, 0, 0, 0, 0};
           if (k != 0ull) {
             const DevAtom* a = p.atoms + (k & 0xffffffull);
             unsigned long long cw, cp;
             ld_relaxed_gpu_v2(a, cw, cp);  // claim | count, paused
+            f_cp = cp;
             ld_relaxed_gpu_v2(&a->lo, f_lo, f_bp);  // lo | body, parts
             ld_relaxed_gpu_v2(&a->args[0], f_a[0], f_a[1]);
             ld_relaxed_gpu_v2(&a->args[2], f_a[2], f_a[3]);
@@ -421,15 +509,18 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           }
           key = warp_max_u64(eligible ? k : 0ull);
           if (key != 0ull) {
-            if (lane == 0) off = claim_block(p.atoms + (key & 0xffffffull), key, p.ctl, stale);
+            // The winner's count travels with the arbitration.
+            const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
+            const unsigned wcount = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp), win);
+            if (lane == 0) off = claim_block(p.atoms + (key & 0xffffffull), key, wcount, p.ctl, stale);
             off = __shfl_sync(0xffffffffu, off, 0);
             if (off < 0) {
               ++retries;  // lost that atom's last slices to other workers
-              ver = ld_relaxed_gpu(p.version + tpc);
+              ver = ld_acquire_gpu(p.version + tpc);
               continue;
             }
             // Hand the winner's fields to lane 0 (no second round trip).
-            const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
+            cur_count = wcount;
             f_lo = __shfl_sync(0xffffffffu, f_lo, win);
             f_bp = __shfl_sync(0xffffffffu, f_bp, win);
 #pragma unroll
@@ -474,18 +565,24 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           go = 1;
           break;
         }
+        // Idle: wait for this TPC's candidate set to change (acquire: a
+        // bump observed here makes the batch's keys and claims visible).
+        // The control block is only consulted when nothing changed, so a
+        // wake-up costs one version load, not four.
+        bool changed = false;
+        for (int k2 = 0; k2 < 64; ++k2) {
+          const unsigned v = ld_acquire_gpu(p.version + tpc);
+          if (v != ver) {
+            ver = v;
+            changed = true;
+            break;
+          }
+          __nanosleep(p.idle_sleep_ns);
+        }
+        if (changed) continue;
         if (ld_relaxed_gpu(&p.ctl->quit)) break;
         if (ld_relaxed_gpu(&p.ctl->drain) && ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0) break;
         if (gtimer() > p.ctl->deadline) break;
-        // Idle: wait for this TPC's candidate set to change.
-        for (int k2 = 0; k2 < 64; ++k2) {
-          __nanosleep(p.idle_sleep_ns);
-          const unsigned v = ld_relaxed_gpu(p.version + tpc);
-          if (v != ver) {
-            ver = v;
-            break;
-          }
-        }
       }
       if (lane == 0) sh.go = go;
     }
@@ -519,8 +616,10 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
       if (last) {
         if (lane == 0) {
           // Completion record first (the host is waiting on it), in the
-          // slot's own record: 15 data words, then the ticket (= seq) with
-          // release semantics, which orders the data before it.
+          // slot's own record: four 16-byte chunks, each three data words and
+          // the ticket (= seq). Each chunk is one PCIe write, so a chunk whose
+          // ticket matches is complete; no system-scope fence (~1 us) sits on
+          // the completion path.
           CompRec* rec = p.comp + sh.slot;
           const unsigned long long t0 = ld_relaxed_gpu64(&a->t_first);
           const unsigned long long t1 = ld_relaxed_gpu64(&a->t_last);
@@ -529,16 +628,18 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
           const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
           const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
           const unsigned long long tag = a->tag;
-          st_relaxed_sys_v4(rec->w + 0, a->atom_id, ld_relaxed_gpu(&a->count) / sh.cmd.parts,
-                            static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32));
+          const unsigned tk = ~static_cast<unsigned>(sh.key >> 24);
+          const unsigned long long span = t1 - t0;
+          st_relaxed_sys_v4(rec->w + 0, ld_relaxed_gpu(&a->count) / sh.cmd.parts,
+                            static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32), tk);
           st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
-                            static_cast<unsigned>(t1), static_cast<unsigned>(t1 >> 32));
+                            span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
           st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
-                            static_cast<unsigned>(m1), static_cast<unsigned>(m1 >> 32));
+                            static_cast<unsigned>(m1), tk);
           // t_seen / t_armed as ns before t_first (0 in batch mode).
-          st_relaxed_sys_v2(rec->w + 12, sh.slot, ts ? static_cast<unsigned>(t0 - ts) : 0u);
-          st_relaxed_sys(rec->w + 14, ta ? static_cast<unsigned>(t0 - ta) : 0u);
-          st_release_sys(rec->w + 15, ~static_cast<unsigned>(sh.key >> 24));
+          st_relaxed_sys_v4(rec->w + 12, static_cast<unsigned>(m1 >> 32),
+                            ts ? static_cast<unsigned>(t0 - ts) : 0u,
+                            ta ? static_cast<unsigned>(t0 - ta) : 0u, tk);
         }
         __syncwarp();
         // Device-side bookkeeping after the record; the host recycles this
@@ -596,6 +697,7 @@ int64_t steady_ns() {
 
 struct HostAtom {
   uint32_t atom_id = 0;
+  uint32_t blocks = 0;
   uint32_t seq = 0;
   int64_t submit_ns = 0;
   uint64_t mask[2] = {0, 0};
@@ -711,8 +813,11 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   const int smem_sm = static_cast<int>(prop.sharedMemPerMultiprocessor);
   // Headroom for the per-CTA reserved shared memory of the workers and of
   // the co-resident ingest CTA.
+  // (the ingest CTA holds ~1.2 KB of static shared memory plus its 1 KB
+  // reserve; a lone worker must leave room for it on the SM it shares).
   int smem_worker = std::min<int>(static_cast<int>(prop.sharedMemPerBlockOptin) - 2048,
-                                  smem_sm / cfg.workers_per_sm - 4096);
+                                  smem_sm / cfg.workers_per_sm -
+                                      (cfg.workers_per_sm == 1 ? 8192 : 4096));
   smem_worker = std::max(smem_worker - smem_worker % 1024, 0);
   if (cfg.workers_per_sm > 1) {
     // W+1 workers must not fit.
@@ -1046,6 +1151,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   for (int i = 0; i < n; ++i) {
     HostAtom& h = d->slots[static_cast<size_t>(i)];
     h.atom_id = ids[static_cast<size_t>(i)];
+    h.blocks = static_cast<uint32_t>(descs[i].hi - descs[i].lo);
     h.seq = seqs[static_cast<size_t>(i)];
     h.submit_ns = now;
     h.mask[0] = descs[i].tpc_mask[0];
@@ -1151,6 +1257,7 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   put64(data, kFTrace, reinterpret_cast<uint64_t>(a->trace));
   HostAtom& h = d->slots[slot];
   h.atom_id = id;
+  h.blocks = static_cast<uint32_t>(a->hi - a->lo);
   h.seq = seq;
   h.submit_ns = gpuos_dev_now_ns(d);
   h.mask[0] = a->tpc_mask[0];
@@ -1211,26 +1318,29 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
     const uint32_t slot = d->live[i];
     HostAtom& h = d->slots[slot];
     CompRec* rec = d->comp_h + slot;
-    if (__atomic_load_n(&rec->w[15], __ATOMIC_ACQUIRE) != h.seq) {
+    if (__atomic_load_n(&rec->w[15], __ATOMIC_ACQUIRE) != h.seq ||
+        __atomic_load_n(&rec->w[11], __ATOMIC_ACQUIRE) != h.seq ||
+        __atomic_load_n(&rec->w[7], __ATOMIC_ACQUIRE) != h.seq ||
+        __atomic_load_n(&rec->w[3], __ATOMIC_ACQUIRE) != h.seq) {
       ++i;
       continue;
     }
     const volatile uint32_t* w = rec->w;
     gpuos_completion& c = out[n];
-    c.atom_id = w[0];
-    c.blocks = w[1];
-    c.tag = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+    c.atom_id = h.atom_id;
+    c.blocks = w[0];
+    c.tag = (uint64_t)w[1] | ((uint64_t)w[2] << 32);
     const uint64_t t_first = (uint64_t)w[4] | ((uint64_t)w[5] << 32);
-    const uint64_t t_last = (uint64_t)w[6] | ((uint64_t)w[7] << 32);
+    const uint64_t t_last = t_first + w[6];
     c.tpc_touched[0] = (uint64_t)w[8] | ((uint64_t)w[9] << 32);
-    c.tpc_touched[1] = (uint64_t)w[10] | ((uint64_t)w[11] << 32);
+    c.tpc_touched[1] = (uint64_t)w[10] | ((uint64_t)w[12] << 32);
     c.dev_first_start_ns = static_cast<int64_t>(t_first) - d->gt_offset;
     c.dev_ingest_ns = c.dev_first_start_ns - static_cast<int64_t>(w[13]);
     c.dev_armed_ns = c.dev_first_start_ns - static_cast<int64_t>(w[14]);
     c.dev_last_end_ns = static_cast<int64_t>(t_last) - d->gt_offset;
     c.host_complete_ns = gpuos_dev_now_ns(d);
     c.host_submit_ns = h.submit_ns;
-    if (w[12] != slot || c.atom_id != h.atom_id)
+    if (c.blocks != h.blocks)
       return fail(GPUOS_E_INVARIANT, "completion record does not match its atom");
     for (int t = 0; t < d->cfg.logical_tpcs; ++t)
       if ((h.mask[t >> 6] >> (t & 63)) & 1ull) --d->tpc_resident[t];

@@ -57,6 +57,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu64(
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
   return r;
 }
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned r;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned r;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");

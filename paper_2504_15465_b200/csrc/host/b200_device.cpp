@@ -110,17 +110,21 @@ void B200Runtime::ensure_trace(KernelId kid, long blocks) {
   if (trace_of_.size() <= kid) trace_of_.resize(kid + 1, nullptr);
   if (trace_of_[kid]) return;
   const std::uint64_t need = static_cast<std::uint64_t>(blocks);
-  if (trace_pool_used_ + need > trace_pool_cap_) {
-    const std::uint64_t cap = std::max<std::uint64_t>(need, 16ull << 20);
+  while (trace_chunk_ < trace_chunks_.size() &&
+         trace_pool_used_ + need > trace_chunk_words_[trace_chunk_]) {
+    ++trace_chunk_;
+    trace_pool_used_ = 0;
+  }
+  if (trace_chunk_ == trace_chunks_.size()) {
+    const std::uint64_t cap = std::max<std::uint64_t>(need, kTraceChunkWords);
     void* p = nullptr;
     check(gpuos_dev_alloc(dev_, cap * 4, &p), "trace alloc");
     check(gpuos_dev_memset(dev_, p, 0, cap * 4), "trace clear");
-    trace_pool_ = static_cast<std::uint32_t*>(p);
-    trace_chunks_.push_back(trace_pool_);
+    trace_chunks_.push_back(static_cast<std::uint32_t*>(p));
+    trace_chunk_words_.push_back(cap);
     trace_pool_used_ = 0;
-    trace_pool_cap_ = cap;
   }
-  trace_of_[kid] = trace_pool_ + trace_pool_used_;
+  trace_of_[kid] = trace_chunks_[trace_chunk_] + trace_pool_used_;
   trace_pool_used_ += need;
 }
 
@@ -200,10 +204,20 @@ void B200Runtime::reset_kernels() {
   resolved_.clear();
   has_resolved_.clear();
   trace_of_.clear();
-  for (auto* p : trace_chunks_) gpuos_dev_free(dev_, p);
-  trace_chunks_.clear();
-  trace_pool_ = nullptr;
-  trace_pool_used_ = trace_pool_cap_ = 0;
+  // Keep the chunks; zero what the last run used.
+  for (std::size_t c = 0; c < trace_chunks_.size() && c <= trace_chunk_; ++c) {
+    const std::uint64_t used = c < trace_chunk_ ? trace_chunk_words_[c] : trace_pool_used_;
+    if (used) check(gpuos_dev_memset(dev_, trace_chunks_[c], 0, used * 4), "trace clear");
+  }
+  trace_chunk_ = 0;
+  trace_pool_used_ = 0;
+  if (opt_.trace_blocks && trace_chunks_.empty()) {
+    void* p = nullptr;  // first chunk up front, outside any run
+    check(gpuos_dev_alloc(dev_, kTraceChunkWords * 4, &p), "trace alloc");
+    check(gpuos_dev_memset(dev_, p, 0, kTraceChunkWords * 4), "trace clear");
+    trace_chunks_.push_back(static_cast<std::uint32_t*>(p));
+    trace_chunk_words_.push_back(kTraceChunkWords);
+  }
 }
 
 void B200Runtime::start() {
