@@ -58,14 +58,17 @@ extern "C" {
                                  block b covers chunk c = chunks ? b % chunks : b:
                                  dst[i] = (src[i] ^ salt) * 0x9E3779B1 + i
                                  for i in [c * words, (c + 1) * words)       */
-#define GPUOS_BODY_GEMM_BF16 2u /* args: A bf16 [M,K], B bf16 [N,K], C bf16
-                                   [M,N] row-major, M|N|K packed (see b200.hpp) */
+#define GPUOS_BODY_GEMM_BF16 2u /* args: [0] = descriptor from
+                                   gpuos_dev_gemm_desc(); block b = output
+                                   tile (b % m_tiles, b / m_tiles) of
+                                   C = A . B^T on the tensor cores       */
 #define GPUOS_BODY_SPIN 3u    /* args: ns to spin per block (globaltimer)    */
 
 /* Launch-time configuration. Zero fields take the defaults in brackets.   */
 typedef struct gpuos_dev_config {
   int32_t device_ordinal;   /* [0] */
-  int32_t workers_per_sm;   /* resident worker CTAs per SM [2]            */
+  int32_t workers_per_sm;   /* resident worker CTAs per SM, 1 or 2 [2]
+                               (each owns 512/W TMEM columns)             */
   int32_t logical_tpcs;     /* TPCs exposed, mapped onto physical TPCs
                                0..n-1 (smid>>1) [all = 74 on B200]        */
   int32_t atom_slots;       /* in-flight atom table size [4096]           */
@@ -163,6 +166,20 @@ int gpuos_dev_poll(struct gpuos_dev* dev, gpuos_completion* out, int32_t max);
 int64_t gpuos_dev_now_ns(struct gpuos_dev* dev);
 int32_t gpuos_dev_in_flight(struct gpuos_dev* dev);
 int gpuos_dev_get_stats(struct gpuos_dev* dev, gpuos_dev_stats* out);
+
+/* GEMM body descriptor (GPUOS_BODY_GEMM_BF16): C[M,N] = A[M,K] . B[N,K]^T
+ * with bf16 operands (both K-major, rows 16-byte aligned: K % 8 == 0), fp32
+ * accumulation on tcgen05 tensor cores, fp32 output (flags 0) or bf16
+ * (GPUOS_GEMM_OUT_BF16), row-major C with leading dimension ldc elements.
+ * Builds the TMA tensor maps, writes the descriptor to device memory and
+ * returns it in *desc (pass as args[0]; release with gpuos_dev_free), the
+ * tenant kernel's grid in *blocks and the tile shape in *tile_m / *tile_n
+ * (128 x min(256, 512 / workers_per_sm)). No reference counterpart: the
+ * reference's "block" is a duration (device.hpp:39-47).                  */
+#define GPUOS_GEMM_OUT_BF16 1u
+int gpuos_dev_gemm_desc(struct gpuos_dev* dev, const void* a, const void* b, void* c,
+                        int64_t m, int64_t n, int64_t k, int64_t ldc, uint32_t flags,
+                        void** desc, int64_t* blocks, int32_t* tile_m, int32_t* tile_n);
 
 /* Device memory helpers (stream-ordered on a side stream: safe while the
  * persistent dispatcher runs; never synchronise the whole device).        */

@@ -31,6 +31,7 @@ LIB_PATH = os.path.join(PKG, "lib", "libgpuos_b200.so")
 GPUOS_BODY_STREAM = 1
 GPUOS_BODY_GEMM_BF16 = 2
 GPUOS_BODY_SPIN = 3
+GPUOS_GEMM_OUT_BF16 = 1
 GPUOS_E_FULL = -5
 GPUOS_DEV_DEFER_WORKERS = 1
 
@@ -42,6 +43,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask",
+    "gpuos_dev_gemm_desc",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -130,6 +132,9 @@ def library() -> C.CDLL:
         "gpuos_dev_host_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
         "gpuos_dev_host_free": (C.c_int, [P, P]),
         "gpuos_dev_consumed": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                          C.c_uint32, C.POINTER(P), C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "gpuos_session_open": (C.c_int, [C.c_char_p, C.POINTER(P)]),
         "gpuos_session_run": (C.c_int, [P, C.c_char_p, C.POINTER(C.c_void_p)]),
         "gpuos_session_close": (C.c_int, [P]),
@@ -300,6 +305,21 @@ class Device:
             if e.code == GPUOS_E_FULL:
                 return None
             raise
+
+    def gemm_desc(self, a: int, b: int, c: int, m: int, n: int, k: int, ldc: int | None = None,
+                  bf16_out: bool = False) -> tuple[int, int, int, int]:
+        """Descriptor for GPUOS_BODY_GEMM_BF16 (C = A . B^T on tcgen05):
+        returns (device pointer for args[0], grid blocks, tile_m, tile_n)."""
+        desc, blocks = C.c_void_p(), C.c_int64()
+        tm, tn = C.c_int32(), C.c_int32()
+        self._check(self._lib.gpuos_dev_gemm_desc(
+            self._h, a, b, c, m, n, k, n if ldc is None else ldc,
+            GPUOS_GEMM_OUT_BF16 if bf16_out else 0, C.byref(desc), C.byref(blocks),
+            C.byref(tm), C.byref(tn)))
+        return desc.value, blocks.value, tm.value, tn.value
+
+    def free(self, ptr: int) -> None:
+        self._check(self._lib.gpuos_dev_free(self._h, ptr))
 
     def pause(self, atom: int, paused: bool) -> None:
         self._check(self._lib.gpuos_dev_set_atom_paused(self._h, atom, 1 if paused else 0))

@@ -42,6 +42,7 @@
 #include <vector>
 
 #include "bodies.cuh"
+#include "gemm_body.cuh"
 #include "gpuos_dev.h"
 #include "ptx.cuh"
 
@@ -123,7 +124,8 @@ struct Params {
   unsigned comp_cap;
   int logical_tpcs;
   int idle_sleep_ns;
-  unsigned smem_bytes;  // dynamic shared memory per worker (STREAM ring)
+  unsigned smem_bytes;  // dynamic shared memory per worker (STREAM / GEMM rings)
+  unsigned tmem_cols;   // TMEM columns each worker owns (GEMM accumulator)
 };
 
 __device__ __forceinline__ void st_release_gpu64(unsigned long long* p, unsigned long long v) {
@@ -386,6 +388,7 @@ struct WorkerShared {
   unsigned long long t_start;
   unsigned slot;
   int go;
+  unsigned tmem_base;           // this worker's TMEM columns (tcgen05.alloc)
 };
 
 __device__ __forceinline__ unsigned atom_add_acq_rel32(unsigned* p, unsigned v) {
@@ -426,6 +429,9 @@ __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long 
   return off < count ? static_cast<long long>(off) : -1;
 }
 
+// Workers own TMEM (GEMM accumulators); the hardware co-schedules at most
+// two TMEM-using CTAs of this kernel per SM (measured: a W=4 launch leaves
+// half the CTAs unlaunched), so W is 1 or 2.
 __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   __shared__ WorkerShared sh;
   extern __shared__ __align__(1024) unsigned char dsmem[];
@@ -443,7 +449,15 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   }
   StreamPipe pipe;
   stream_pipe_init(pipe, dsmem, p.smem_bytes, tid);
+  // TMEM for GEMM accumulators: allocated once for the CTA's lifetime by
+  // warp 1 (512 / W columns, so the W workers of an SM never contend).
+  if (warp == 1) tmem_alloc(&sh.tmem_base, p.tmem_cols);
+  GemmPipe gemm;
+  gemm_pipe_init(gemm, dsmem, p.smem_bytes, p.tmem_cols, tid);
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  gemm.tmem = sh.tmem_base;
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
   // Warp 0's draining state: the atom it last claimed from and the TPC's
   // candidate-set version at that time. While the version is unchanged no
@@ -592,6 +606,7 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     switch (sh.cmd.body) {
       case GPUOS_BODY_STREAM: body_stream(sh.cmd, tid, pipe); break;
       case GPUOS_BODY_SPIN: body_spin(sh.cmd, tid); break;
+      case GPUOS_BODY_GEMM_BF16: body_gemm(sh.cmd, tid, gemm); break;
       default: break;
     }
     __syncthreads();
@@ -664,6 +679,9 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     atomicAdd(&p.ctl->busy_ns, busy);
     atomicAdd(&p.ctl->retries, retries);
   }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free(gemm.tmem, p.tmem_cols);
 }
 
 __global__ void k_gtimer(unsigned long long* out) { *out = gtimer(); }
@@ -777,6 +795,17 @@ void put64(uint32_t* data, int field, uint64_t v) {
 
 int map_priority(int32_t p) { return std::clamp(p, 0, 254) + 1; }
 
+// TMEM columns per worker: the largest power of two <= 512 / W (>= 32).
+unsigned tmem_cols_for(int workers_per_sm) {
+  unsigned c = 512;
+  while (c > 32 && c * static_cast<unsigned>(workers_per_sm) > 512) c >>= 1;
+  return c;
+}
+
+bool known_body(uint32_t b) {
+  return b == GPUOS_BODY_STREAM || b == GPUOS_BODY_SPIN || b == GPUOS_BODY_GEMM_BF16;
+}
+
 }  // namespace
 
 extern "C" {
@@ -792,7 +821,8 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   if (cfg.atom_slots <= 0) cfg.atom_slots = 4096;
   if (cfg.ring_entries <= 0) cfg.ring_entries = 4096;
   if (cfg.idle_sleep_ns <= 0) cfg.idle_sleep_ns = 128;
-  if (cfg.workers_per_sm > 8) return fail(GPUOS_E_CONFIG, "workers_per_sm must be <= 8");
+  if (cfg.workers_per_sm > 2)
+    return fail(GPUOS_E_CONFIG, "workers_per_sm must be 1 or 2 (TMEM-owning workers per SM)");
   if (cfg.atom_slots > (1 << 24)) return fail(GPUOS_E_CONFIG, "atom_slots must be < 2^24");
 
   auto d = std::make_unique<gpuos_dev>();
@@ -813,11 +843,11 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   const int smem_sm = static_cast<int>(prop.sharedMemPerMultiprocessor);
   // Headroom for the per-CTA reserved shared memory of the workers and of
   // the co-resident ingest CTA.
-  // (the ingest CTA holds ~1.2 KB of static shared memory plus its 1 KB
-  // reserve; a lone worker must leave room for it on the SM it shares).
+  // (the ingest CTA holds ~3 KB of static shared memory including its 1 KB
+  // reserve; the workers of the SM it shares must leave room for it).
   int smem_worker = std::min<int>(static_cast<int>(prop.sharedMemPerBlockOptin) - 2048,
                                   smem_sm / cfg.workers_per_sm -
-                                      (cfg.workers_per_sm == 1 ? 8192 : 4096));
+                                      (cfg.workers_per_sm == 1 ? 8192 : 6144));
   smem_worker = std::max(smem_worker - smem_worker % 1024, 0);
   if (cfg.workers_per_sm > 1) {
     // W+1 workers must not fit.
@@ -840,7 +870,11 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   CUDA_TRY(cudaFuncSetAttribute(k_ingest, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_worker, kWorkerThreads, smem_worker));
-  if (per_sm != cfg.workers_per_sm)
+  // The occupancy calculator reports 1 CTA/SM for any kernel that uses
+  // tcgen05.alloc (it cannot see how many TMEM columns a CTA takes); two
+  // workers with 256 columns each do co-reside (measured), and
+  // launch_workers() verifies the real placement: exactly W per SM.
+  if (per_sm > cfg.workers_per_sm)
     return fail(GPUOS_E_CONFIG, "worker occupancy is " + std::to_string(per_sm) +
                                     " CTAs/SM, expected " + std::to_string(cfg.workers_per_sm));
 
@@ -973,6 +1007,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   p.logical_tpcs = d->cfg.logical_tpcs;
   p.idle_sleep_ns = d->cfg.idle_sleep_ns;
   p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
+  p.tmem_cols = tmem_cols_for(d->cfg.workers_per_sm);
 
   d->params = p;
   k_ingest<<<1, 32, 0, d->s_ingest>>>(p);
@@ -1109,8 +1144,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     const uint32_t parts = a.parts == 0 ? 1u : a.parts;
     if (a.lo < 0 || a.hi <= a.lo || (a.hi - a.lo) * static_cast<int64_t>(parts) > 0xfffffffeLL)
       return fail(GPUOS_E_CONFIG, "atom block range out of bounds");
-    if (a.body != GPUOS_BODY_STREAM && a.body != GPUOS_BODY_SPIN)
-      return fail(GPUOS_E_CONFIG, "unknown body kind");
+    if (!known_body(a.body)) return fail(GPUOS_E_CONFIG, "unknown body kind");
     const uint32_t seq = d->next_seq++;
     seqs[static_cast<size_t>(i)] = seq;
     const int prio = map_priority(a.priority);
@@ -1192,6 +1226,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   p.logical_tpcs = T;
   p.idle_sleep_ns = d->cfg.idle_sleep_ns;
   p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
+  p.tmem_cols = tmem_cols_for(d->cfg.workers_per_sm);
   CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
   k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);
   CUDA_TRY(cudaGetLastError());
@@ -1219,8 +1254,7 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   if (parts > 4096) return fail(GPUOS_E_CONFIG, "parts must be <= 4096");
   if ((a->hi - a->lo) * static_cast<int64_t>(parts) > 0xfffffffeLL)
     return fail(GPUOS_E_CONFIG, "atom too large");
-  if (a->body != GPUOS_BODY_STREAM && a->body != GPUOS_BODY_SPIN)
-    return fail(GPUOS_E_CONFIG, "unknown body kind");
+  if (!known_body(a->body)) return fail(GPUOS_E_CONFIG, "unknown body kind");
   const int T = d->cfg.logical_tpcs;
   bool any = false;
   for (int w = 0; w < 2; ++w) {
@@ -1399,6 +1433,68 @@ int gpuos_dev_memset(gpuos_dev* d, void* dst, int value, uint64_t bytes) {
 int gpuos_dev_host_alloc(gpuos_dev* d, uint64_t bytes, void** ptr) {
   if (!d || !ptr) return fail(GPUOS_E_CONFIG, "null argument");
   CUDA_TRY(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault));
+  return GPUOS_OK;
+}
+
+int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int64_t m,
+                        int64_t n, int64_t k, int64_t ldc, uint32_t flags, void** desc,
+                        int64_t* blocks, int32_t* tile_m, int32_t* tile_n) {
+  if (!d || !a || !b || !c || !desc) return fail(GPUOS_E_CONFIG, "null argument");
+  if (m <= 0 || n <= 0 || k <= 0 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
+    return fail(GPUOS_E_CONFIG, "GEMM shape out of range");
+  if (k % 8 != 0) return fail(GPUOS_E_CONFIG, "GEMM K must be a multiple of 8 (16-byte rows)");
+  if (ldc < n) return fail(GPUOS_E_CONFIG, "GEMM ldc < N");
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16 != 0)
+    return fail(GPUOS_E_CONFIG, "GEMM operands must be 16-byte aligned");
+  const unsigned cols = tmem_cols_for(d->cfg.workers_per_sm);
+  const unsigned n_tile = cols < 256u ? cols : 256u;
+  const unsigned stage = kGemmABytes + n_tile * 128u;
+  if (d->topo.smem_per_worker < static_cast<int>(1024 + stage))
+    return fail(GPUOS_E_CONFIG, "worker shared memory too small for a GEMM stage");
+
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      return fail(GPUOS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  GemmDesc h{};
+  auto make = [&](CUtensorMap* map, const void* ptr, int64_t rows, unsigned box_rows) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
+    const cuuint32_t box[2] = {kGemmBK, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  if (make(&h.a, a, m, kGemmBM) != CUDA_SUCCESS || make(&h.b, b, n, n_tile) != CUDA_SUCCESS)
+    return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the GEMM operands");
+  h.c = reinterpret_cast<unsigned long long>(c);
+  h.m = static_cast<unsigned>(m);
+  h.n = static_cast<unsigned>(n);
+  h.k = static_cast<unsigned>(k);
+  h.ldc = static_cast<unsigned>(ldc);
+  h.m_tiles = static_cast<unsigned>((m + kGemmBM - 1) / kGemmBM);
+  h.n_tiles = static_cast<unsigned>((n + n_tile - 1) / n_tile);
+  h.n_tile = n_tile;
+  h.flags = flags & kGemmOutBf16;
+  void* p = nullptr;
+  CUDA_TRY(cudaSetDevice(d->device));
+  CUDA_TRY(cudaMallocAsync(&p, sizeof(GemmDesc), d->s_side));
+  CUDA_TRY(cudaMemcpyAsync(p, &h, sizeof(GemmDesc), cudaMemcpyHostToDevice, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  *desc = p;
+  if (blocks) *blocks = static_cast<int64_t>(h.m_tiles) * h.n_tiles;
+  if (tile_m) *tile_m = static_cast<int32_t>(kGemmBM);
+  if (tile_n) *tile_n = static_cast<int32_t>(n_tile);
   return GPUOS_OK;
 }
 

@@ -1,0 +1,281 @@
+// GEMM atom body on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// A tenant GEMM C[M,N] = A[M,K] . B[N,K]^T (bf16 in, fp32 accumulate, fp32
+// or bf16 out; both operands K-major, i.e. a row-major activation times a
+// row-major nn.Linear weight) is a grid of ceil(M/128) x ceil(N/n_tile)
+// blocks; block b computes output tile (b % m_tiles, b / m_tiles). The
+// reference models such a block only as a duration with sensitivity s ~ 1
+// (device.hpp:39-47); here one resident dispatcher worker executes it:
+//
+//   thread 0   TMA producer: per 64-wide K slice, one 2-D tensor-map load of
+//              A (128 x 64) and of B (n_tile x 64) into a stage of the
+//              shared-memory ring (128-byte swizzle), completing on the
+//              stage's `full` mbarrier.
+//   thread 32  MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16
+//              (M=128, N=n_tile, K=16) per stage into the worker's TMEM
+//              accumulator; tcgen05.commit frees the stage (`empty`) and,
+//              after the last slice, signals `accum`.
+//   all warps  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
+//              32(w%4).., column half w/4) -> registers -> global.
+//
+// Each worker CTA owns 512/W TMEM columns for its lifetime (allocated once
+// at dispatcher start, W = workers per SM), so n_tile = min(256, 512/W) and
+// no per-atom TMEM allocation sits on the path. Pipeline phases persist in
+// GemmPipe across blocks, like the STREAM ring.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "bodies.cuh"
+#include "ptx.cuh"
+
+namespace gpuos_dev_impl {
+
+constexpr unsigned kGemmBM = 128;     // tile rows (UMMA M)
+constexpr unsigned kGemmBK = 64;      // K per stage: 64 bf16 = one 128-byte swizzle row
+constexpr unsigned kGemmMaxStages = 4;
+constexpr unsigned kGemmABytes = kGemmBM * kGemmBK * 2;  // 16 KiB
+
+struct alignas(128) GemmDesc {
+  CUtensorMap a;                 // A [M, K] bf16: box {64, 128}, SWIZZLE_128B
+  CUtensorMap b;                 // B [N, K] bf16: box {64, n_tile}, SWIZZLE_128B
+  unsigned long long c;          // C [M, N] row-major (ldc elements)
+  unsigned m, n, k, ldc;
+  unsigned m_tiles, n_tiles, n_tile, flags;  // flags bit 0: bf16 output
+};
+constexpr unsigned kGemmOutBf16 = 1u;
+
+struct GemmPipe {
+  unsigned char* tiles;          // stages x (16 KiB + n_tile x 128 B), 1024-aligned
+  unsigned long long* full;      // [kGemmMaxStages]
+  unsigned long long* empty;     // [kGemmMaxStages]
+  unsigned long long* accum;     // accumulator ready
+  unsigned stages;
+  unsigned n_tile;
+  unsigned tmem;                 // TMEM base address of this worker's columns
+  unsigned accum_used;           // tiles completed by this CTA (accum parity)
+  unsigned long long kb_used;    // K slices streamed by this CTA so far
+};
+
+// mbarrier wait that traps after 2 s instead of hanging the persistent
+// kernel (a trap aborts the context; the host sees a CUDA error).
+__device__ __forceinline__ void mbar_wait_bounded(unsigned long long* b, unsigned parity) {
+  const unsigned a = smem_u32(b);
+  unsigned ok = 0;
+  unsigned long long t0 = 0;
+  for (unsigned spins = 0;; ++spins) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if ((spins & 1023u) == 0) {
+      const unsigned long long t = gtimer();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 2000000000ull) asm volatile("trap;");
+    }
+  }
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// K-major operand tile with 128-byte swizzle: rows of 128 B, 8-row core
+// groups 1024 B apart (SBO), version 1 (sm_100), layout type 2.
+__device__ __forceinline__ unsigned long long umma_desc_sw128(unsigned saddr) {
+  return static_cast<unsigned long long>((saddr >> 4) & 0x3FFFu) |
+         (1ull << 16) |                 // LBO (unused for swizzled K-major)
+         (64ull << 32) |                // SBO = 1024 B >> 4
+         (1ull << 46) |                 // descriptor version (Blackwell)
+         (2ull << 61);                  // SWIZZLE_128B
+}
+
+// kind::f16 instruction descriptor: bf16 A/B, f32 D, both K-major.
+__device__ __forceinline__ unsigned umma_idesc_bf16(unsigned m, unsigned n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(unsigned tmem_d, unsigned long long a,
+                                          unsigned long long b, unsigned idesc,
+                                          unsigned accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(map), "r"(c0), "r"(c1),
+      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+// 32 lanes x 32 columns of fp32 from TMEM into 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, unsigned (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Whole warp: allocate / free this worker's TMEM columns (once per CTA).
+__device__ __forceinline__ void tmem_alloc(unsigned* holder, unsigned cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(holder))),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_free(unsigned base, unsigned cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
+               : "memory");
+}
+
+// Called once per CTA by all threads (barrier memory at smem + 128 .. 256;
+// the STREAM ring's barriers occupy smem + 0 .. 128, tiles start at 1024).
+__device__ __forceinline__ void gemm_pipe_init(GemmPipe& G, unsigned char* smem,
+                                               unsigned smem_bytes, unsigned tmem_cols, int tid) {
+  G.full = reinterpret_cast<unsigned long long*>(smem + 128);
+  G.empty = G.full + kGemmMaxStages;
+  G.accum = G.empty + kGemmMaxStages;
+  G.tiles = smem + 1024;
+  G.n_tile = tmem_cols < 256u ? tmem_cols : 256u;
+  const unsigned stage = kGemmABytes + G.n_tile * 128u;
+  G.stages = smem_bytes > 1024 ? (smem_bytes - 1024) / stage : 0;
+  if (G.stages > kGemmMaxStages) G.stages = kGemmMaxStages;
+  G.accum_used = 0;
+  G.kb_used = 0;
+  if (tid == 0) {
+    for (unsigned s = 0; s < kGemmMaxStages; ++s) {
+      mbar_init(G.full + s, 1);
+      mbar_init(G.empty + s, 1);
+    }
+    mbar_init(G.accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
+__device__ __forceinline__ void body_gemm(const BlockCmd& c, int tid, GemmPipe& G) {
+  const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
+  const unsigned m_tiles = D->m_tiles;
+  const unsigned n_tile = G.n_tile;
+  const unsigned blk = static_cast<unsigned>(c.block);
+  const unsigned mt = blk % m_tiles, nt = blk / m_tiles;
+  const unsigned nk = (D->k + kGemmBK - 1) / kGemmBK;
+  const unsigned S = G.stages;
+  const unsigned long long g0 = G.kb_used;
+  const unsigned stage_bytes = kGemmABytes + n_tile * 128u;
+  if (S == 0 || D->n_tile != n_tile) return;  // host validated; never on the path
+
+  if (tid == 0) {
+    // TMA producer. The descriptor was written by a host copy while this
+    // persistent kernel runs: acquire it into the tensor-map proxy.
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->a) : "memory");
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->b) : "memory");
+    for (unsigned j = 0; j < nk; ++j) {
+      const unsigned long long k = g0 + j;
+      const unsigned s = static_cast<unsigned>(k % S);
+      const unsigned long long r = k / S;
+      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
+      unsigned char* st = G.tiles + s * stage_bytes;
+      mbar_expect_tx(G.full + s, stage_bytes);
+      tma_load_2d(st, &D->a, static_cast<int>(j * kGemmBK), static_cast<int>(mt * kGemmBM), G.full + s);
+      tma_load_2d(st + kGemmABytes, &D->b, static_cast<int>(j * kGemmBK),
+                  static_cast<int>(nt * n_tile), G.full + s);
+    }
+  } else if (tid == 32) {
+    // MMA issuer: one thread drives the tensor core for the whole CTA.
+    const unsigned idesc = umma_idesc_bf16(kGemmBM, n_tile);
+    for (unsigned j = 0; j < nk; ++j) {
+      const unsigned long long k = g0 + j;
+      const unsigned s = static_cast<unsigned>(k % S);
+      mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1));
+      tc_fence_after();
+      const unsigned a0 = smem_u32(G.tiles + s * stage_bytes);
+      const unsigned b0 = a0 + kGemmABytes;
+#pragma unroll
+      for (unsigned kk = 0; kk < kGemmBK / 16; ++kk)
+        umma_bf16(G.tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
+                  (j | kk) != 0u);
+      umma_commit(G.empty + s);  // stage free once these MMAs have read it
+    }
+    umma_commit(G.accum);        // every MMA of the tile has completed
+  }
+
+  // Epilogue: all 8 warps. Warp w reads TMEM lanes 32(w%4)..+31 (tile rows)
+  // and column half w/4.
+  mbar_wait_bounded(G.accum, G.accum_used & 1u);
+  tc_fence_after();
+  const int warp = tid >> 5, lane = tid & 31;
+  const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
+  const unsigned half = n_tile / 2;
+  const unsigned row = mt * kGemmBM + q * 32 + static_cast<unsigned>(lane);
+  const unsigned M = D->m, N = D->n, ldc = D->ldc;
+  const bool bf16_out = (D->flags & kGemmOutBf16) != 0;
+  for (unsigned ch = 0; ch < half / 32; ++ch) {
+    unsigned v[32];
+    tmem_ld32(G.tmem + ((q * 32u) << 16) + h * half + ch * 32u, v);
+    const unsigned col0 = nt * n_tile + h * half + ch * 32u;
+    if (row >= M || col0 >= N) continue;
+    const bool full_row = col0 + 32 <= N;
+    if (!bf16_out) {
+      float* out = reinterpret_cast<float*>(D->c) + static_cast<size_t>(row) * ldc + col0;
+      if (full_row && (ldc % 4) == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          st_stream(reinterpret_cast<uint4*>(out) + i,
+                    make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+      } else {
+        for (unsigned i = 0; i < 32 && col0 + i < N; ++i) out[i] = __uint_as_float(v[i]);
+      }
+    } else {
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(D->c) + static_cast<size_t>(row) * ldc + col0;
+      if (full_row && (ldc % 8) == 0) {
+        unsigned p[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const __nv_bfloat162 t = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+          p[i] = *reinterpret_cast<const unsigned*>(&t);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          st_stream(reinterpret_cast<uint4*>(out) + i, make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]));
+      } else {
+        for (unsigned i = 0; i < 32 && col0 + i < N; ++i) out[i] = __float2bfloat16_rn(__uint_as_float(v[i]));
+      }
+    }
+  }
+  tc_fence_before();  // the next tile's MMAs overwrite this accumulator
+  G.kb_used = g0 + nk;
+  G.accum_used += 1;
+}
+
+}  // namespace gpuos_dev_impl
