@@ -174,8 +174,9 @@ int gpuos_dev_get_stats(struct gpuos_dev* dev, gpuos_dev_stats* out);
  * Builds the TMA tensor maps, writes the descriptor to device memory and
  * returns it in *desc (pass as args[0]; release with gpuos_dev_free), the
  * tenant kernel's grid in *blocks and the tile shape in *tile_m / *tile_n
- * (128 x min(256, 512 / workers_per_sm)). No reference counterpart: the
- * reference's "block" is a duration (device.hpp:39-47).                  */
+ * (256 x 256: one tile per block, computed by a TPC's two SMs together with
+ * tcgen05.mma.cta_group::2). No reference counterpart: the reference's
+ * "block" is a duration (device.hpp:39-47).                              */
 #define GPUOS_GEMM_OUT_BF16 1u
 int gpuos_dev_gemm_desc(struct gpuos_dev* dev, const void* a, const void* b, void* c,
                         int64_t m, int64_t n, int64_t k, int64_t ldc, uint32_t flags,

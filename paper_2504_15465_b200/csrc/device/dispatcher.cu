@@ -87,6 +87,7 @@ struct DevCtl {
   unsigned long long deadline;  // globaltimer: hard stop (hang guard)
   unsigned long long blocks, busy_ns, retries, atoms_done;
   unsigned long long stale_claims;  // claims that landed on a recycled slot
+  unsigned arrived;                 // worker CTAs that have started
 };
 
 // 128-byte submit-ring entry: four 32-byte sectors, each = 7 data words +
@@ -179,7 +180,8 @@ __device__ __forceinline__ void st_relaxed_gpu64(unsigned long long* p, unsigned
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
+// 64 registers: it shares an SM sub-partition with four worker warps.
+__global__ void __maxnreg__(64) k_ingest(Params p) {
   // Shadow occupancy of every TPC's resident list. Only this warp inserts
   // keys, so an entry whose shadow bit is clear is certainly empty; workers
   // clear entries behind its back, which the shadow learns on refresh.
@@ -381,13 +383,36 @@ __global__ void __launch_bounds__(32, 1) k_ingest(Params p) {
 }
 
 // ------------------------------------------------------------ worker CTAs
-struct WorkerShared {
-  BlockCmd cmd;                 // current block: args, block id, body
-  long long lo;                 // first block of the cached atom
-  unsigned long long key;       // resident key of the atom being drained
-  unsigned long long t_start;
+// Workers run as 2-CTA clusters, one CTA on each SM of a TPC (a 2-CTA
+// cluster always lands on SMs {2k, 2k+1}: profiles/topology_probe_r01.json).
+// Each CTA arbitrates its TPC's resident atoms and claims blocks on its own,
+// so 1-SM bodies (STREAM, SPIN) see 2W independent workers per TPC. A 2-SM
+// body (GEMM: one 256 x 256 tile per block on tcgen05.mma.cta_group::2) is
+// claimed only by the pair's leader (rank 0), which hands the tile to its
+// peer through distributed shared memory (join_rc + join_full mbarrier);
+// the peer takes the request at its next decision point (after its current
+// block, or at once while idle) and confirms on the leader's `joined`
+// mbarrier. A peer whose arbitration winner is a 2-SM atom does not bypass
+// it with a lower-priority block: it waits for the leader's request.
+struct RoundCmd {
+  BlockCmd cmd;                 // block to run: args, block id, body, slice
+  long long lo;                 // first block of the atom
+  unsigned long long key;       // resident key of the atom
   unsigned slot;
-  int go;
+  int pad;
+};
+constexpr int kRoundCmdWords64 = sizeof(RoundCmd) / 8;
+static_assert(sizeof(RoundCmd) % 8 == 0, "RoundCmd copied as 64-bit words");
+
+enum WorkerGo : int { kGoExit = 0, kGoOwn = 1, kGoPair = 2, kGoJoin = 3 };
+
+struct WorkerShared {
+  RoundCmd rc;                  // this CTA's block for the round
+  RoundCmd join_rc;             // peer: pair tile posted by the leader
+  unsigned long long t_start;
+  unsigned long long join_full; // mbarrier (peer): leader posted join_rc
+  unsigned long long joined;    // mbarrier (leader): peer took the request
+  int go;                       // WorkerGo
   unsigned tmem_base;           // this worker's TMEM columns (tcgen05.alloc)
 };
 
@@ -400,65 +425,216 @@ __device__ __forceinline__ void ld_relaxed_gpu_v2(const void* p, unsigned long l
                                                   unsigned long long& b) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// Address of this CTA's shared variable `p` in cluster CTA `rank`.
+__device__ __forceinline__ unsigned map_rank(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_u64(unsigned addr, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity) {
+  const unsigned a = smem_u32(b);
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
 
-// Lane 0: claim one slice of the atom behind `key` with a relaxed fetch-add
-// on its claim word; the slot fields were read by the lane that acquired the
-// key and are handed over by shuffle. Fetch-add never retries, so 300 workers
-// draining one atom cost one L2 atomic each; the CAS loop it replaced spent
-// ~140 failed attempts per claim under that contention
-// (profiles/ncu_k_worker_r01_cas.txt). Returns the slice offset or -1.
+__device__ __forceinline__ bool mbar_test_cluster(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+      "selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Lane 0: claim `n` consecutive slices of the atom behind `key` with one
+// relaxed fetch-add on its claim word; the slot fields were read by the lane
+// that acquired the key and are handed over by shuffle. Fetch-add never
+// retries, so 300 workers draining one atom cost one L2 atomic each; the
+// CAS loop it replaced spent ~140 failed attempts per claim under that
+// contention (profiles/ncu_k_worker_r01_cas.txt). Returns the first slice
+// offset (or -1) and in *got how many of the n are valid.
 // A worker holding a stale key for a recycled slot (the host recycles slots
 // FIFO over the whole table, so this needs a worker stalled for thousands of
-// atom lifetimes) sees a foreign sequence in the returned word; a valid
-// offset then belongs to the slot's new occupant and is run for it
+// atom lifetimes) sees a foreign sequence in the returned word; valid
+// offsets then belong to the slot's new occupant and are run for it
 // (stale = true: the caller re-reads the slot), never lost.
 __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long key,
-                                                 unsigned count, DevCtl* ctl, bool& stale) {
+                                                 unsigned count, unsigned n, DevCtl* ctl,
+                                                 bool& stale, unsigned& got) {
   const unsigned seq = ~static_cast<unsigned>(key >> 24);
-  const unsigned long long old = atomicAdd(&a->claim, 1ull);
+  const unsigned long long old = atomicAdd(&a->claim, static_cast<unsigned long long>(n));
   const unsigned off = static_cast<unsigned>(old);
   stale = static_cast<unsigned>(old >> 32) != seq;
   if (stale) {
     fence_acq_rel_gpu();
-    if (off >= ld_relaxed_gpu(&a->count)) return -1;
-    atomicAdd(&ctl->stale_claims, 1ull);
-    return static_cast<long long>(off);
+    count = ld_relaxed_gpu(&a->count);
+    if (off < count) atomicAdd(&ctl->stale_claims, 1ull);
   }
   // `count` was read with the key's hot line; it never changes while the
   // sequence matches.
-  return off < count ? static_cast<long long>(off) : -1;
+  got = off < count ? (count - off < n ? count - off : n) : 0u;
+  return got ? static_cast<long long>(off) : -1;
 }
+
+// Warp 0 of the CTA that ran `rc`: record the block on its atom and, for the
+// atom's last block, publish the completion and retire its resident keys.
+__device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& rc,
+                                              unsigned long long t_start, int tpc, unsigned sm,
+                                              unsigned lane, unsigned long long& n_blocks,
+                                              unsigned long long& busy) {
+  DevAtom* a = p.atoms + rc.slot;
+  int last = 0;
+  if (lane == 0) {
+    const unsigned long long t_end = gtimer();
+    atomicMin(&a->t_first, t_start);
+    atomicMax(&a->t_last, t_end);
+    atomicOr(&a->touched[tpc >> 6], 1ull << (tpc & 63));
+    if (a->trace != nullptr)
+      atomicAdd(a->trace + rc.cmd.block * rc.cmd.parts + rc.cmd.part, 0x10000u + sm + 1u);
+    busy += t_end - t_start;
+    ++n_blocks;
+    // acq_rel: this block's records (and the body's output stores, ordered
+    // by the CTA barrier before this) precede the count; the last finisher
+    // observes every other block's records.
+    last = atom_add_acq_rel32(&a->done, 1u) + 1u == ld_relaxed_gpu(&a->count);
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  if (lane == 0) {
+    // Completion record first (the host is waiting on it), in the slot's
+    // own record: four 16-byte chunks, each three data words and the ticket
+    // (= seq). Each chunk is one PCIe write, so a chunk whose ticket matches
+    // is complete; no system-scope fence (~1 us) sits on the completion path.
+    CompRec* rec = p.comp + rc.slot;
+    const unsigned long long t0 = ld_relaxed_gpu64(&a->t_first);
+    const unsigned long long t1 = ld_relaxed_gpu64(&a->t_last);
+    const unsigned long long m0 = ld_relaxed_gpu64(&a->touched[0]);
+    const unsigned long long m1 = ld_relaxed_gpu64(&a->touched[1]);
+    const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
+    const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
+    const unsigned long long tag = a->tag;
+    const unsigned tk = ~static_cast<unsigned>(rc.key >> 24);
+    const unsigned long long span = t1 - t0;
+    st_relaxed_sys_v4(rec->w + 0, ld_relaxed_gpu(&a->count) / rc.cmd.parts,
+                      static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32), tk);
+    st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
+                      span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
+    st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
+                      static_cast<unsigned>(m1), tk);
+    // t_seen / t_armed as ns before t_first (0 in batch mode).
+    st_relaxed_sys_v4(rec->w + 12, static_cast<unsigned>(m1 >> 32),
+                      ts ? static_cast<unsigned>(t0 - ts) : 0u,
+                      ta ? static_cast<unsigned>(t0 - ta) : 0u, tk);
+  }
+  __syncwarp();
+  // Device-side bookkeeping after the record; the host recycles this slot
+  // only after thousands of others, long after these land.
+  for (int t = lane; t < p.logical_tpcs; t += 32) {
+    const unsigned long long m = a->mask[t >> 6];
+    if ((m >> (t & 63)) & 1ull)
+      atomicCAS(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], rc.key, 0ull);
+  }
+  if (lane == 0) {
+    // Plain reductions: atoms_done is read after the kernel ends, and the
+    // drain check only needs outstanding to reach zero eventually.
+    atomicAdd(&p.ctl->atoms_done, 1ull);
+    atomicSub(&p.ctl->outstanding, 1);
+  }
+  return true;
+}
+
+__device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned rank,
+                                         StreamPipe& pipe, GemmPipe& gemm) {
+  switch (rc.cmd.body) {
+    case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
+    case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
+    case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ bool body_is_pair(unsigned body) { return body == GPUOS_BODY_GEMM_BF16; }
 
 // Workers own TMEM (GEMM accumulators); the hardware co-schedules at most
 // two TMEM-using CTAs of this kernel per SM (measured: a W=4 launch leaves
 // half the CTAs unlaunched), so W is 1 or 2.
-__global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
+// Register budget: an SM sub-partition holds 16 K registers; with W = 2 it
+// hosts two warps of each worker (4 x 32 x R) plus, on one SM, the ingest
+// warp (32 x 64). R = 104 keeps that SM able to host both workers: a pair
+// that cannot be co-placed there is never launched (measured at R = 103
+// with a 122-register ingest warp).
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   __shared__ WorkerShared sh;
   extern __shared__ __align__(1024) unsigned char dsmem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const unsigned lane = tid & 31;
+  const unsigned rank = cluster_rank();
   unsigned sm = smid();
   int tpc = p.phys2log[sm >> 1];
-  if (tid == 0) st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 ? 0x80000000u : 0u));
-  if (tpc < 0) return;  // TPC not exposed to the scheduler
-
   if (tid == 0) {
-    sh.key = 0ull;
-    sh.slot = ~0u;
+    st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 ? 0x80000000u : 0u));
+    atomicAdd(&p.ctl->arrived, 1u);
   }
+  if (tpc < 0) {
+    // TPC not exposed to the scheduler (both CTAs of the pair). Give up the
+    // TMEM allocation permit at once (an SM does not start a second CTA of a
+    // TMEM-using kernel while the first still holds it: measured, every
+    // unexposed SM then hosted one worker), then stay until every worker
+    // CTA has started: leaving at once would free this SM for a cluster
+    // meant for an exposed TPC, leaving that TPC short.
+    if (warp == 1) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    if (tid == 0)
+      while (ld_relaxed_gpu(&p.ctl->arrived) < gridDim.x && !ld_relaxed_gpu(&p.ctl->quit) &&
+             gtimer() < p.ctl->deadline)
+        __nanosleep(1000);
+    __syncthreads();
+    return;
+  }
+
   StreamPipe pipe;
   stream_pipe_init(pipe, dsmem, p.smem_bytes, tid);
-  // TMEM for GEMM accumulators: allocated once for the CTA's lifetime by
-  // warp 1 (512 / W columns, so the W workers of an SM never contend).
-  if (warp == 1) tmem_alloc(&sh.tmem_base, p.tmem_cols);
   GemmPipe gemm;
   gemm_pipe_init(gemm, dsmem, p.smem_bytes, p.tmem_cols, tid);
+  if (tid == 0) {
+    mbar_init(&sh.join_full, 1);
+    mbar_init(&sh.joined, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // TMEM for the pair's GEMM accumulators: allocated once for the CTA's
+  // lifetime by warp 1 of both CTAs (cta_group::2: same columns in both),
+  // 512 / W columns so the W workers of an SM never contend.
+  if (warp == 1) tmem_alloc2(&sh.tmem_base, p.tmem_cols);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   gemm.tmem = sh.tmem_base;
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
+  // Remote addresses inside the pair.
+  const unsigned peer_join_rc = map_rank(&sh.join_rc, 1);
+  const unsigned peer_join_full = map_rank(&sh.join_full, 1);
+  const unsigned leader_joined = map_rank(&sh.joined, 0);
+  unsigned joins = 0;  // pair tiles this CTA has run (join_full / joined parity)
   // Warp 0's draining state: the atom it last claimed from and the TPC's
   // candidate-set version at that time. While the version is unchanged no
   // higher-priority atom arrived, nothing was paused or fenced, so the next
@@ -467,6 +643,7 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
   unsigned cur_ver = 0u;
   unsigned cur_slot = 0u;
   unsigned cur_count = 0u;
+  unsigned cur_body = 0u;
   int cur_tpc = -1;
 
   for (;;) {
@@ -474,205 +651,190 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     // re-derive the TPC each round so placement stays exact.
     sm = smid();
     tpc = p.phys2log[sm >> 1];
-    if (tpc < 0) break;
     if (tpc != cur_tpc) {
       cur_key = 0ull;
       cur_tpc = tpc;
     }
-    unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
     if (warp == 0) {
-      int go = 0;
-      unsigned ver = ld_acquire_gpu(p.version + tpc);  // latest observed
-      for (;;) {
-        long long off = -1;
-        unsigned long long key = 0ull;
-        bool stale = false;
-        if (cur_key != 0ull && ver == cur_ver) {
-          // Fast path: next slice of the atom being drained. The version is
-          // re-read alongside the claim; a change noticed only after it
-          // costs at most one slice of priority inversion.
-          if (lane == 0) off = claim_block(p.atoms + cur_slot, cur_key, cur_count, p.ctl, stale);
-          ver = ld_acquire_gpu(p.version + tpc);
-          off = __shfl_sync(0xffffffffu, off, 0);
-          if (off >= 0) key = cur_key;
-          if (stale && lane == 0) sh.key = 0ull;  // slot recycled: reload its fields
-        }
-        if (off < 0) {
-          cur_key = 0ull;
-          // Full arbitration: eligible = waiting slices, not paused, not
-          // fenced off this TPC; highest priority then oldest wins. Each
-          // lane reads one key (acquire) and then that atom's hot line, so
-          // the winner's fields arrive with the arbitration itself.
-          const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
-          const unsigned long long k = ld_acquire_gpu64(list + lane);
-          bool eligible = false;
-          unsigned long long f_lo = 0, f_bp = 0, f_cp = 0, f_a[5] = {0, 0, 0, 0, 0};
-          if (k != 0ull) {
-            const DevAtom* a = p.atoms + (k & 0xffffffull);
-            unsigned long long cw, cp;
-            ld_relaxed_gpu_v2(a, cw, cp);  // claim | count, paused
-            f_cp = cp;
-            ld_relaxed_gpu_v2(&a->lo, f_lo, f_bp);  // lo | body, parts
-            ld_relaxed_gpu_v2(&a->args[0], f_a[0], f_a[1]);
-            ld_relaxed_gpu_v2(&a->args[2], f_a[2], f_a[3]);
-            f_a[4] = ld_relaxed_gpu64(&a->args[4]);
-            eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
-                       static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
-                       static_cast<unsigned>(cp >> 32) == 0u &&
-                       static_cast<int>(k >> 56) >= floor_prio;
+      int go = kGoExit;
+      if (tpc >= 0) {
+        unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
+        unsigned ver = ld_acquire_gpu(p.version + tpc);  // latest observed
+        for (;;) {
+          // The peer serves a posted pair tile before anything else.
+          if (rank != 0 && mbar_test_cluster(&sh.join_full, joins & 1u)) {
+            go = kGoJoin;
+            break;
           }
-          key = warp_max_u64(eligible ? k : 0ull);
-          if (key != 0ull) {
-            // The winner's count travels with the arbitration.
-            const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
-            const unsigned wcount = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp), win);
-            if (lane == 0) off = claim_block(p.atoms + (key & 0xffffffull), key, wcount, p.ctl, stale);
+          long long off = -1;
+          unsigned got = 0;
+          unsigned long long key = 0ull;
+          bool stale = false;
+          if (cur_key != 0ull && ver == cur_ver) {
+            // Fast path: next slice of the atom being drained. The version is
+            // re-read alongside the claim; a change noticed only after it
+            // costs at most one slice of priority inversion.
+            if (lane == 0)
+              off = claim_block(p.atoms + cur_slot, cur_key, cur_count, 1u, p.ctl, stale, got);
+            ver = ld_acquire_gpu(p.version + tpc);
             off = __shfl_sync(0xffffffffu, off, 0);
-            if (off < 0) {
-              ++retries;  // lost that atom's last slices to other workers
-              ver = ld_acquire_gpu(p.version + tpc);
-              continue;
+            if (off >= 0) key = cur_key;
+            if (stale && lane == 0) sh.rc.key = 0ull;  // slot recycled: reload its fields
+          }
+          bool defer = false;  // peer: the winner is a 2-SM atom for the leader
+          if (off < 0) {
+            cur_key = 0ull;
+            // Full arbitration: eligible = waiting slices, not paused, not
+            // fenced off this TPC; highest priority then oldest wins. Each
+            // lane reads one key (acquire) and then that atom's hot line, so
+            // the winner's fields arrive with the arbitration itself.
+            const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
+            const unsigned long long k = ld_acquire_gpu64(list + lane);
+            bool eligible = false;
+            unsigned long long f_lo = 0, f_bp = 0, f_cp = 0, f_a[5] = {0, 0, 0, 0, 0};
+            if (k != 0ull) {
+              const DevAtom* a = p.atoms + (k & 0xffffffull);
+              unsigned long long cw, cp;
+              ld_relaxed_gpu_v2(a, cw, cp);  // claim | count, paused
+              f_cp = cp;
+              ld_relaxed_gpu_v2(&a->lo, f_lo, f_bp);  // lo | body, parts
+              ld_relaxed_gpu_v2(&a->args[0], f_a[0], f_a[1]);
+              ld_relaxed_gpu_v2(&a->args[2], f_a[2], f_a[3]);
+              f_a[4] = ld_relaxed_gpu64(&a->args[4]);
+              eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
+                         static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
+                         static_cast<unsigned>(cp >> 32) == 0u &&
+                         static_cast<int>(k >> 56) >= floor_prio;
             }
-            // Hand the winner's fields to lane 0 (no second round trip).
-            cur_count = wcount;
-            f_lo = __shfl_sync(0xffffffffu, f_lo, win);
-            f_bp = __shfl_sync(0xffffffffu, f_bp, win);
-#pragma unroll
-            for (int k2 = 0; k2 < 5; ++k2) f_a[k2] = __shfl_sync(0xffffffffu, f_a[k2], win);
-            if (lane == 0) {
-              if (stale) {
-                sh.key = 0ull;  // recycled slot: fields reloaded below
+            key = warp_max_u64(eligible ? k : 0ull);
+            if (key != 0ull) {
+              // The winner's count and body travel with the arbitration.
+              const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
+              const unsigned wcount = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp), win);
+              f_bp = __shfl_sync(0xffffffffu, f_bp, win);
+              if (rank != 0 && body_is_pair(static_cast<unsigned>(f_bp))) {
+                defer = true;  // no lower-priority bypass: wait for the leader
               } else {
+                if (lane == 0)
+                  off = claim_block(p.atoms + (key & 0xffffffull), key, wcount, 1u, p.ctl, stale, got);
+                off = __shfl_sync(0xffffffffu, off, 0);
+                if (off < 0) {
+                  ++retries;  // lost that atom's last slices to other workers
+                  ver = ld_acquire_gpu(p.version + tpc);
+                  continue;
+                }
+                // Hand the winner's fields to lane 0 (no second round trip).
+                cur_count = wcount;
+                f_lo = __shfl_sync(0xffffffffu, f_lo, win);
 #pragma unroll
-                for (int k2 = 0; k2 < 5; ++k2) sh.cmd.args[k2] = f_a[k2];
-                sh.cmd.body = static_cast<unsigned>(f_bp);
-                sh.cmd.parts = static_cast<unsigned>(f_bp >> 32);
-                sh.lo = static_cast<long long>(f_lo);
-                sh.key = key;
-                sh.slot = static_cast<unsigned>(key & 0xffffffull);
+                for (int k2 = 0; k2 < 5; ++k2) f_a[k2] = __shfl_sync(0xffffffffu, f_a[k2], win);
+                if (lane == 0) {
+                  if (stale) {
+                    sh.rc.key = 0ull;  // recycled slot: fields reloaded below
+                  } else {
+#pragma unroll
+                    for (int k2 = 0; k2 < 5; ++k2) sh.rc.cmd.args[k2] = f_a[k2];
+                    sh.rc.cmd.body = static_cast<unsigned>(f_bp);
+                    sh.rc.cmd.parts = static_cast<unsigned>(f_bp >> 32);
+                    sh.rc.lo = static_cast<long long>(f_lo);
+                    sh.rc.key = key;
+                    sh.rc.slot = static_cast<unsigned>(key & 0xffffffull);
+                  }
+                }
               }
             }
           }
-        }
-        if (off >= 0) {
-          const unsigned slot = static_cast<unsigned>(key & 0xffffffull);
-          if (lane == 0) {
-            if (sh.key == 0ull || sh.slot != slot) {
-              // Recycled slot adopted by claim_block (which fenced): read the
-              // new occupant's fields.
-              const DevAtom* a = p.atoms + slot;
+          if (off >= 0) {
+            const unsigned slot = static_cast<unsigned>(key & 0xffffffull);
+            if (lane == 0) {
+              if (sh.rc.key == 0ull || sh.rc.slot != slot) {
+                // Recycled slot adopted by claim_block (which fenced): read the
+                // new occupant's fields.
+                const DevAtom* a = p.atoms + slot;
 #pragma unroll
-              for (int k2 = 0; k2 < 5; ++k2) sh.cmd.args[k2] = a->args[k2];
-              sh.cmd.body = a->body;
-              sh.cmd.parts = a->parts;
-              sh.lo = a->lo;
-              sh.slot = slot;
+                for (int k2 = 0; k2 < 5; ++k2) sh.rc.cmd.args[k2] = a->args[k2];
+                sh.rc.cmd.body = a->body;
+                sh.rc.cmd.parts = a->parts;
+                sh.rc.lo = a->lo;
+                sh.rc.slot = slot;
+                sh.rc.key = key;
+              }
+              const unsigned parts = sh.rc.cmd.parts;
+              sh.rc.cmd.block = sh.rc.lo + off / parts;
+              sh.rc.cmd.part = static_cast<unsigned>(off % parts);
             }
-            const unsigned parts = sh.cmd.parts;
-            sh.cmd.block = sh.lo + off / parts;
-            sh.cmd.part = static_cast<unsigned>(off % parts);
-            sh.t_start = gtimer();
-          }
-          cur_key = stale ? 0ull : key;
-          cur_slot = slot;
-          cur_ver = ver;
-          go = 1;
-          break;
-        }
-        // Idle: wait for this TPC's candidate set to change (acquire: a
-        // bump observed here makes the batch's keys and claims visible).
-        // The control block is only consulted when nothing changed, so a
-        // wake-up costs one version load, not four.
-        bool changed = false;
-        for (int k2 = 0; k2 < 64; ++k2) {
-          const unsigned v = ld_acquire_gpu(p.version + tpc);
-          if (v != ver) {
-            ver = v;
-            changed = true;
+            cur_key = stale ? 0ull : key;
+            cur_slot = slot;
+            cur_ver = ver;
+            cur_body = __shfl_sync(0xffffffffu, sh.rc.cmd.body, 0);
+            go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
+            // A peer reaches a 2-SM block only by adopting a recycled slot
+            // (stale claim, see claim_block): it cannot run it alone.
+            if (go == kGoPair && rank != 0) asm volatile("trap;");
             break;
           }
-          __nanosleep(p.idle_sleep_ns);
+          // Idle: wait for this TPC's candidate set to change (acquire: a
+          // bump observed here makes the batch's keys and claims visible) or,
+          // on the peer, for a pair tile. The control block is only consulted
+          // when nothing changed, so a wake-up costs one version load.
+          bool changed = false;
+          for (int k2 = 0; k2 < 64; ++k2) {
+            if (rank != 0 && mbar_test_cluster(&sh.join_full, joins & 1u)) {
+              changed = true;
+              break;
+            }
+            const unsigned v = ld_acquire_gpu(p.version + tpc);
+            if (v != ver) {
+              ver = v;
+              changed = true;
+              break;
+            }
+            __nanosleep(p.idle_sleep_ns);
+          }
+          if (changed) continue;
+          if (ld_relaxed_gpu(&p.ctl->quit)) break;
+          if (!defer && ld_relaxed_gpu(&p.ctl->drain) &&
+              ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0)
+            break;
+          if (gtimer() > p.ctl->deadline) break;
         }
-        if (changed) continue;
-        if (ld_relaxed_gpu(&p.ctl->quit)) break;
-        if (ld_relaxed_gpu(&p.ctl->drain) && ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0) break;
-        if (gtimer() > p.ctl->deadline) break;
       }
-      if (lane == 0) sh.go = go;
-    }
-    __syncthreads();
-    if (!sh.go) break;
-
-    switch (sh.cmd.body) {
-      case GPUOS_BODY_STREAM: body_stream(sh.cmd, tid, pipe); break;
-      case GPUOS_BODY_SPIN: body_spin(sh.cmd, tid); break;
-      case GPUOS_BODY_GEMM_BF16: body_gemm(sh.cmd, tid, gemm); break;
-      default: break;
-    }
-    __syncthreads();
-
-    if (warp == 0) {
-      DevAtom* a = p.atoms + sh.slot;
-      int last = 0;
       if (lane == 0) {
-        const unsigned long long t_end = gtimer();
-        atomicMin(&a->t_first, sh.t_start);
-        atomicMax(&a->t_last, t_end);
-        atomicOr(&a->touched[tpc >> 6], 1ull << (tpc & 63));
-        if (a->trace != nullptr)
-          atomicAdd(a->trace + sh.cmd.block * sh.cmd.parts + sh.cmd.part, 0x10000u + sm + 1u);
-        busy += t_end - sh.t_start;
-        ++n_blocks;
-        // acq_rel: this block's records precede the count; the last finisher
-        // observes every other block's records.
-        last = atom_add_acq_rel32(&a->done, 1u) + 1u == ld_relaxed_gpu(&a->count);
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        if (lane == 0) {
-          // Completion record first (the host is waiting on it), in the
-          // slot's own record: four 16-byte chunks, each three data words and
-          // the ticket (= seq). Each chunk is one PCIe write, so a chunk whose
-          // ticket matches is complete; no system-scope fence (~1 us) sits on
-          // the completion path.
-          CompRec* rec = p.comp + sh.slot;
-          const unsigned long long t0 = ld_relaxed_gpu64(&a->t_first);
-          const unsigned long long t1 = ld_relaxed_gpu64(&a->t_last);
-          const unsigned long long m0 = ld_relaxed_gpu64(&a->touched[0]);
-          const unsigned long long m1 = ld_relaxed_gpu64(&a->touched[1]);
-          const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
-          const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
-          const unsigned long long tag = a->tag;
-          const unsigned tk = ~static_cast<unsigned>(sh.key >> 24);
-          const unsigned long long span = t1 - t0;
-          st_relaxed_sys_v4(rec->w + 0, ld_relaxed_gpu(&a->count) / sh.cmd.parts,
-                            static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32), tk);
-          st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
-                            span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
-          st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
-                            static_cast<unsigned>(m1), tk);
-          // t_seen / t_armed as ns before t_first (0 in batch mode).
-          st_relaxed_sys_v4(rec->w + 12, static_cast<unsigned>(m1 >> 32),
-                            ts ? static_cast<unsigned>(t0 - ts) : 0u,
-                            ta ? static_cast<unsigned>(t0 - ta) : 0u, tk);
+        if (go == kGoPair) {
+          // Post the tile to the peer (release: the command precedes the
+          // arrival), then wait until it has taken it.
+          const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&sh.rc);
+#pragma unroll
+          for (int w = 0; w < kRoundCmdWords64; ++w) st_cluster_u64(peer_join_rc + 8 * w, src[w]);
+          mbar_arrive_remote(peer_join_full);
+          // The peer takes it at its next decision point; only an abort
+          // (quit, hang guard) can leave it untaken.
+          for (unsigned polls = 0; !mbar_test_cluster(&sh.joined, joins & 1u); ++polls) {
+            if ((polls & 255u) == 255u &&
+                (ld_relaxed_gpu(&p.ctl->quit) || gtimer() > p.ctl->deadline)) {
+              go = kGoExit;
+              break;
+            }
+          }
+        } else if (go == kGoJoin) {
+          sh.rc = sh.join_rc;
+          mbar_arrive_remote(leader_joined);
         }
-        __syncwarp();
-        // Device-side bookkeeping after the record; the host recycles this
-        // slot only after thousands of others, long after these land.
-        const unsigned long long key = sh.key;
-        for (int t = lane; t < p.logical_tpcs; t += 32) {
-          const unsigned long long m = a->mask[t >> 6];
-          if ((m >> (t & 63)) & 1ull)
-            atomicCAS(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], key, 0ull);
-        }
-        if (lane == 0) {
-          atomicAdd(&p.ctl->atoms_done, 1ull);
-          __threadfence();
-          atomicSub(&p.ctl->outstanding, 1);
-        }
-        cur_key = 0ull;
+        sh.go = go;
+        sh.t_start = gtimer();
       }
     }
+    __syncthreads();
+    const int go = sh.go;
+    if (go == kGoExit) break;
+    run_body(sh.rc, tid, rank, pipe, gemm);  // pair tiles end with a cluster barrier
+    if (go == kGoPair || go == kGoJoin) ++joins;
+    __syncthreads();
+    // The leader records pair tiles (the peer's half is complete: cluster
+    // barrier at the end of the body).
+    if (warp == 0 && go != kGoJoin &&
+        account_block(p, sh.rc, sh.t_start, tpc, sm, lane, n_blocks, busy))
+      cur_key = 0ull;  // the atom is done: rescan rather than claim from it
   }
   if (tid == 0) {
     atomicAdd(&p.ctl->blocks, n_blocks);
@@ -680,8 +842,8 @@ __global__ void __launch_bounds__(kWorkerThreads, 1) k_worker(Params p) {
     atomicAdd(&p.ctl->retries, retries);
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_free(gemm.tmem, p.tmem_cols);
+  cluster_sync_all();  // neither CTA frees TMEM or leaves while the other may still use it
+  if (warp == 1) tmem_free2(gemm.tmem, p.tmem_cols);
 }
 
 __global__ void k_gtimer(unsigned long long* out) { *out = gtimer(); }
@@ -844,10 +1006,12 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   // Headroom for the per-CTA reserved shared memory of the workers and of
   // the co-resident ingest CTA.
   // (the ingest CTA holds ~3 KB of static shared memory including its 1 KB
-  // reserve; the workers of the SM it shares must leave room for it).
+  // reserve; the workers of the SM it shares must leave room for it. A
+  // cluster-launched pair needs more slack than the arithmetic suggests:
+  // with 6 KB per worker the pair that must share the ingest's TPC is never
+  // placed, measured; 8 KB places all.)
   int smem_worker = std::min<int>(static_cast<int>(prop.sharedMemPerBlockOptin) - 2048,
-                                  smem_sm / cfg.workers_per_sm -
-                                      (cfg.workers_per_sm == 1 ? 8192 : 6144));
+                                  smem_sm / cfg.workers_per_sm - 8192);
   smem_worker = std::max(smem_worker - smem_worker % 1024, 0);
   if (cfg.workers_per_sm > 1) {
     // W+1 workers must not fit.
@@ -1035,9 +1199,22 @@ int gpuos_dev_launch_workers(gpuos_dev* d) {
       ready += __atomic_load_n(d->alive_h + i, __ATOMIC_ACQUIRE) != 0u;
     if (ready == d->grid) break;
     if (steady_ns() > deadline) {
+      std::vector<int> per_sm(d->topo.sm_count, 0);
+      std::string missing;
+      for (int i = 0; i < d->grid; ++i) {
+        const unsigned v = __atomic_load_n(d->alive_h + i, __ATOMIC_ACQUIRE);
+        if (v == 0u) missing += " cta" + std::to_string(i);
+        else if ((v & 0x7fffffffu) - 1u < per_sm.size()) ++per_sm[(v & 0x7fffffffu) - 1u];
+      }
+      std::string sms;
+      for (int s = 0; s < d->topo.sm_count; ++s)
+        if (per_sm[s] != d->cfg.workers_per_sm)
+          sms += " sm" + std::to_string(s) + "=" + std::to_string(per_sm[s]);
       gpuos_dev_stop(d, 0, nullptr);
       return fail(GPUOS_E_TIMEOUT, "only " + std::to_string(ready) + " of " +
-                                       std::to_string(d->grid) + " worker CTAs became resident");
+                                       std::to_string(d->grid) +
+                                       " worker CTAs became resident; missing:" + missing +
+                                       "; short SMs:" + sms);
     }
   }
   std::vector<int> per_sm(d->topo.sm_count, 0);
@@ -1047,9 +1224,16 @@ int gpuos_dev_launch_workers(gpuos_dev* d) {
   }
   for (int s = 0; s < d->topo.sm_count; ++s)
     if (per_sm[s] != d->cfg.workers_per_sm) {
+      std::string detail;
+      for (int i = 0; i < d->grid; ++i) {
+        const unsigned smi = (d->alive_h[i] & 0x7fffffffu) - 1u;
+        if (static_cast<int>(smi) == s || per_sm[smi] != d->cfg.workers_per_sm)
+          detail += " cta" + std::to_string(i) + "@sm" + std::to_string(smi);
+      }
       gpuos_dev_stop(d, 0, nullptr);
       return fail(GPUOS_E_INVARIANT, "SM " + std::to_string(s) + " hosts " +
-                                         std::to_string(per_sm[s]) + " workers");
+                                         std::to_string(per_sm[s]) + " workers (W=" +
+                                         std::to_string(d->cfg.workers_per_sm) + "):" + detail);
     }
   return GPUOS_OK;
 }
@@ -1447,10 +1631,9 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
   if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16 != 0)
     return fail(GPUOS_E_CONFIG, "GEMM operands must be 16-byte aligned");
   const unsigned cols = tmem_cols_for(d->cfg.workers_per_sm);
-  const unsigned n_tile = cols < 256u ? cols : 256u;
-  const unsigned stage = kGemmABytes + n_tile * 128u;
-  if (d->topo.smem_per_worker < static_cast<int>(1024 + stage))
-    return fail(GPUOS_E_CONFIG, "worker shared memory too small for a GEMM stage");
+  if (cols < kGemmTile || d->topo.smem_per_worker < static_cast<int>(1024 + kGemmStageBytes))
+    return fail(GPUOS_E_CONFIG, "workers cannot host a GEMM stage");
+  const unsigned n_tile = kGemmTile;
 
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1475,14 +1658,14 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   };
-  if (make(&h.a, a, m, kGemmBM) != CUDA_SUCCESS || make(&h.b, b, n, n_tile) != CUDA_SUCCESS)
+  if (make(&h.a, a, m, kGemmHalf) != CUDA_SUCCESS || make(&h.b, b, n, kGemmHalf) != CUDA_SUCCESS)
     return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the GEMM operands");
   h.c = reinterpret_cast<unsigned long long>(c);
   h.m = static_cast<unsigned>(m);
   h.n = static_cast<unsigned>(n);
   h.k = static_cast<unsigned>(k);
   h.ldc = static_cast<unsigned>(ldc);
-  h.m_tiles = static_cast<unsigned>((m + kGemmBM - 1) / kGemmBM);
+  h.m_tiles = static_cast<unsigned>((m + kGemmTile - 1) / kGemmTile);
   h.n_tiles = static_cast<unsigned>((n + n_tile - 1) / n_tile);
   h.n_tile = n_tile;
   h.flags = flags & kGemmOutBf16;
@@ -1493,7 +1676,7 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
   CUDA_TRY(cudaStreamSynchronize(d->s_side));
   *desc = p;
   if (blocks) *blocks = static_cast<int64_t>(h.m_tiles) * h.n_tiles;
-  if (tile_m) *tile_m = static_cast<int32_t>(kGemmBM);
+  if (tile_m) *tile_m = static_cast<int32_t>(kGemmTile);
   if (tile_n) *tile_n = static_cast<int32_t>(n_tile);
   return GPUOS_OK;
 }

@@ -1,26 +1,31 @@
-// GEMM atom body on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+// GEMM atom body on the 5th-generation tensor cores (tcgen05 + TMEM + TMA),
+// run by a TPC's worker pair (the 2-CTA cluster on SMs 2k, 2k+1).
 //
 // A tenant GEMM C[M,N] = A[M,K] . B[N,K]^T (bf16 in, fp32 accumulate, fp32
 // or bf16 out; both operands K-major, i.e. a row-major activation times a
-// row-major nn.Linear weight) is a grid of ceil(M/128) x ceil(N/n_tile)
-// blocks; block b computes output tile (b % m_tiles, b / m_tiles). The
-// reference models such a block only as a duration with sensitivity s ~ 1
-// (device.hpp:39-47); here one resident dispatcher worker executes it:
+// row-major nn.Linear weight) is a grid of ceil(M/256) x ceil(N/256) blocks;
+// block b computes the 256 x 256 output tile (b % m_tiles, b / m_tiles).
+// The reference models such a block only as a duration with sensitivity
+// s ~ 1 (device.hpp:39-47); here the pair executes it:
 //
-//   thread 0   TMA producer: per 64-wide K slice, one 2-D tensor-map load of
-//              A (128 x 64) and of B (n_tile x 64) into a stage of the
-//              shared-memory ring (128-byte swizzle), completing on the
-//              stage's `full` mbarrier.
-//   thread 32  MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16
-//              (M=128, N=n_tile, K=16) per stage into the worker's TMEM
-//              accumulator; tcgen05.commit frees the stage (`empty`) and,
-//              after the last slice, signals `accum`.
-//   all warps  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
-//              32(w%4).., column half w/4) -> registers -> global.
+//   thread 0 of each CTA   TMA producer: per 64-wide K slice, a 2-SM
+//              tensor-map load of its 128 rows of A and its 128 rows of B
+//              (128-byte swizzle) into its own stage, completing on the
+//              LEADER's `full` mbarrier (the leader expects both halves).
+//   thread 32 of the leader  MMA issuer: 4 x tcgen05.mma.cta_group::2
+//              (M=256, N=256, K=16) per stage, reading A and B from both
+//              CTAs' shared memory, accumulating into both CTAs' TMEM
+//              (rows 0-127 in the leader, 128-255 in the peer);
+//              tcgen05.commit multicasts `empty` (stage free) to both CTAs
+//              and, after the last slice, `accum`.
+//   all warps of both CTAs  epilogue: tcgen05.ld 32x32b.x32 (warp w reads
+//              TMEM lanes 32(w%4).., column half w/4) -> registers -> global.
 //
+// Per SM and K step the pair moves 128 + 128 operand rows for 128 x 256
+// MACs, two thirds of a 1-SM 128 x 256 tile's 128 + 256: the L2 -> SM
+// traffic that bounds a 1-SM tile (profiles/ncu_gemm_1sm_r01.txt).
 // Each worker CTA owns 512/W TMEM columns for its lifetime (allocated once
-// at dispatcher start, W = workers per SM), so n_tile = min(256, 512/W) and
-// no per-atom TMEM allocation sits on the path. Pipeline phases persist in
+// at dispatcher start, W = workers per SM). Pipeline phases persist in
 // GemmPipe across blocks, like the STREAM ring.
 #pragma once
 
@@ -32,22 +37,24 @@
 
 namespace gpuos_dev_impl {
 
-constexpr unsigned kGemmBM = 128;     // tile rows (UMMA M)
+constexpr unsigned kGemmTile = 256;   // pair tile: 256 x 256 (UMMA M = N = 256)
+constexpr unsigned kGemmHalf = 128;   // rows of A and of B each CTA loads
 constexpr unsigned kGemmBK = 64;      // K per stage: 64 bf16 = one 128-byte swizzle row
 constexpr unsigned kGemmMaxStages = 4;
-constexpr unsigned kGemmABytes = kGemmBM * kGemmBK * 2;  // 16 KiB
+constexpr unsigned kGemmABytes = kGemmHalf * kGemmBK * 2;  // 16 KiB
+constexpr unsigned kGemmStageBytes = 2 * kGemmABytes;      // A half + B half
 
 struct alignas(128) GemmDesc {
   CUtensorMap a;                 // A [M, K] bf16: box {64, 128}, SWIZZLE_128B
-  CUtensorMap b;                 // B [N, K] bf16: box {64, n_tile}, SWIZZLE_128B
+  CUtensorMap b;                 // B [N, K] bf16: box {64, 128}, SWIZZLE_128B
   unsigned long long c;          // C [M, N] row-major (ldc elements)
   unsigned m, n, k, ldc;
-  unsigned m_tiles, n_tiles, n_tile, flags;  // flags bit 0: bf16 output
+  unsigned m_tiles, n_tiles, n_tile, flags;  // 256-wide tiles; flags bit 0: bf16 output
 };
 constexpr unsigned kGemmOutBf16 = 1u;
 
 struct GemmPipe {
-  unsigned char* tiles;          // stages x (16 KiB + n_tile x 128 B), 1024-aligned
+  unsigned char* tiles;          // stages x 32 KiB (A half, B half), 1024-aligned
   unsigned long long* full;      // [kGemmMaxStages]
   unsigned long long* empty;     // [kGemmMaxStages]
   unsigned long long* accum;     // accumulator ready
@@ -101,34 +108,6 @@ __device__ __forceinline__ unsigned umma_idesc_bf16(unsigned m, unsigned n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
-__device__ __forceinline__ void umma_bf16(unsigned tmem_d, unsigned long long a,
-                                          unsigned long long b, unsigned idesc,
-                                          unsigned accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          static_cast<unsigned>(__cvta_generic_to_shared(bar)))
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-      "l"(map), "r"(c0), "r"(c1),
-      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
-      : "memory");
-}
-
 // 32 lanes x 32 columns of fp32 from TMEM into 32 registers per thread.
 __device__ __forceinline__ void tmem_ld32(unsigned taddr, unsigned (&v)[32]) {
   asm volatile(
@@ -146,17 +125,52 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, unsigned (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Whole warp: allocate / free this worker's TMEM columns (once per CTA).
-__device__ __forceinline__ void tmem_alloc(unsigned* holder, unsigned cols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+// The pair's variants: cta_group::2 allocation (same columns in both CTAs,
+// issued by the same warp of each), MMA, multicast commit, 2-SM TMA load.
+__device__ __forceinline__ void tmem_alloc2(unsigned* holder, unsigned cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    static_cast<unsigned>(__cvta_generic_to_shared(holder))),
                "r"(cols)
                : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_free(unsigned base, unsigned cols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
+__device__ __forceinline__ void tmem_free2(unsigned base, unsigned cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
                : "memory");
+}
+__device__ __forceinline__ void umma2_bf16(unsigned tmem_d, unsigned long long a,
+                                           unsigned long long b, unsigned idesc,
+                                           unsigned accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on the mbarrier at the same offset in both CTAs of the pair once
+// every prior tcgen05 operation of this thread has completed.
+__device__ __forceinline__ void umma2_commit_both(unsigned long long* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+      "h"(static_cast<unsigned short>(3))
+      : "memory");
+}
+// 2-SM tensor-map load into this CTA's shared memory, completing on the
+// leader's mbarrier (the peer bit of the shared::cluster address cleared).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(map), "r"(c0), "r"(c1),
+      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 
 // Called once per CTA by all threads (barrier memory at smem + 128 .. 256;
@@ -167,9 +181,8 @@ __device__ __forceinline__ void gemm_pipe_init(GemmPipe& G, unsigned char* smem,
   G.empty = G.full + kGemmMaxStages;
   G.accum = G.empty + kGemmMaxStages;
   G.tiles = smem + 1024;
-  G.n_tile = tmem_cols < 256u ? tmem_cols : 256u;
-  const unsigned stage = kGemmABytes + G.n_tile * 128u;
-  G.stages = smem_bytes > 1024 ? (smem_bytes - 1024) / stage : 0;
+  G.n_tile = kGemmTile;
+  G.stages = tmem_cols >= kGemmTile && smem_bytes > 1024 ? (smem_bytes - 1024) / kGemmStageBytes : 0;
   if (G.stages > kGemmMaxStages) G.stages = kGemmMaxStages;
   G.accum_used = 0;
   G.kb_used = 0;
@@ -183,67 +196,73 @@ __device__ __forceinline__ void gemm_pipe_init(GemmPipe& G, unsigned char* smem,
   }
 }
 
-__device__ __forceinline__ void body_gemm(const BlockCmd& c, int tid, GemmPipe& G) {
+// Both CTAs of the pair, all threads; rank 0 is the leader.
+__device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G) {
   const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
   const unsigned m_tiles = D->m_tiles;
-  const unsigned n_tile = G.n_tile;
   const unsigned blk = static_cast<unsigned>(c.block);
   const unsigned mt = blk % m_tiles, nt = blk / m_tiles;
   const unsigned nk = (D->k + kGemmBK - 1) / kGemmBK;
   const unsigned S = G.stages;
   const unsigned long long g0 = G.kb_used;
-  const unsigned stage_bytes = kGemmABytes + n_tile * 128u;
-  if (S == 0 || D->n_tile != n_tile) return;  // host validated; never on the path
+  if (S == 0) {  // host validated; never on the path
+    cluster_sync_all();
+    return;
+  }
 
   if (tid == 0) {
-    // TMA producer. The descriptor was written by a host copy while this
-    // persistent kernel runs: acquire it into the tensor-map proxy.
+    // TMA producer (both CTAs). The descriptor was written by a host copy
+    // while this persistent kernel runs: acquire it into the tensor-map proxy.
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->a) : "memory");
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->b) : "memory");
+    const int a_row = static_cast<int>(mt * kGemmTile + rank * kGemmHalf);
+    const int b_row = static_cast<int>(nt * kGemmTile + rank * kGemmHalf);
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;
       if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
-      unsigned char* st = G.tiles + s * stage_bytes;
-      mbar_expect_tx(G.full + s, stage_bytes);
-      tma_load_2d(st, &D->a, static_cast<int>(j * kGemmBK), static_cast<int>(mt * kGemmBM), G.full + s);
-      tma_load_2d(st + kGemmABytes, &D->b, static_cast<int>(j * kGemmBK),
-                  static_cast<int>(nt * n_tile), G.full + s);
+      unsigned char* st = G.tiles + s * kGemmStageBytes;
+      if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemmStageBytes);  // both halves
+      const int kc = static_cast<int>(j * kGemmBK);
+      tma_load_2d_pair(st, &D->a, kc, a_row, G.full + s);
+      tma_load_2d_pair(st + kGemmABytes, &D->b, kc, b_row, G.full + s);
     }
-  } else if (tid == 32) {
-    // MMA issuer: one thread drives the tensor core for the whole CTA.
-    const unsigned idesc = umma_idesc_bf16(kGemmBM, n_tile);
+  } else if (tid == 32 && rank == 0) {
+    // MMA issuer: one thread of the leader drives both SMs' tensor cores.
+    tc_fence_after();
+    const unsigned idesc = umma_idesc_bf16(kGemmTile, kGemmTile);
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1));
       tc_fence_after();
-      const unsigned a0 = smem_u32(G.tiles + s * stage_bytes);
+      const unsigned a0 = smem_u32(G.tiles + s * kGemmStageBytes);
       const unsigned b0 = a0 + kGemmABytes;
 #pragma unroll
       for (unsigned kk = 0; kk < kGemmBK / 16; ++kk)
-        umma_bf16(G.tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
-                  (j | kk) != 0u);
-      umma_commit(G.empty + s);  // stage free once these MMAs have read it
+        umma2_bf16(G.tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
+                   (j | kk) != 0u);
+      umma2_commit_both(G.empty + s);  // stage free in both CTAs once read
     }
-    umma_commit(G.accum);        // every MMA of the tile has completed
+    umma2_commit_both(G.accum);        // every MMA of the tile has completed
   }
 
-  // Epilogue: all 8 warps. Warp w reads TMEM lanes 32(w%4)..+31 (tile rows)
-  // and column half w/4.
+  // Epilogue: all 8 warps of both CTAs. Warp w reads TMEM lanes 32(w%4)..+31
+  // (this CTA's 128 tile rows) and column half w/4.
   mbar_wait_bounded(G.accum, G.accum_used & 1u);
   tc_fence_after();
   const int warp = tid >> 5, lane = tid & 31;
   const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
-  const unsigned half = n_tile / 2;
-  const unsigned row = mt * kGemmBM + q * 32 + static_cast<unsigned>(lane);
+  constexpr unsigned half = kGemmTile / 2;
+  const unsigned row = mt * kGemmTile + rank * kGemmHalf + q * 32 + static_cast<unsigned>(lane);
   const unsigned M = D->m, N = D->n, ldc = D->ldc;
   const bool bf16_out = (D->flags & kGemmOutBf16) != 0;
+#pragma unroll 1
   for (unsigned ch = 0; ch < half / 32; ++ch) {
     unsigned v[32];
     tmem_ld32(G.tmem + ((q * 32u) << 16) + h * half + ch * 32u, v);
-    const unsigned col0 = nt * n_tile + h * half + ch * 32u;
+    const unsigned col0 = nt * kGemmTile + h * half + ch * 32u;
     if (row >= M || col0 >= N) continue;
     const bool full_row = col0 + 32 <= N;
     if (!bf16_out) {
@@ -254,28 +273,35 @@ __device__ __forceinline__ void body_gemm(const BlockCmd& c, int tid, GemmPipe& 
           st_stream(reinterpret_cast<uint4*>(out) + i,
                     make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
       } else {
-        for (unsigned i = 0; i < 32 && col0 + i < N; ++i) out[i] = __uint_as_float(v[i]);
+#pragma unroll
+        for (unsigned i = 0; i < 32; ++i)
+          if (col0 + i < N) out[i] = __uint_as_float(v[i]);
       }
     } else {
       __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(D->c) + static_cast<size_t>(row) * ldc + col0;
       if (full_row && (ldc % 8) == 0) {
-        unsigned p[16];
+        unsigned pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const __nv_bfloat162 t = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          p[i] = *reinterpret_cast<const unsigned*>(&t);
+          pk[i] = *reinterpret_cast<const unsigned*>(&t);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          st_stream(reinterpret_cast<uint4*>(out) + i, make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]));
+          st_stream(reinterpret_cast<uint4*>(out) + i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
       } else {
-        for (unsigned i = 0; i < 32 && col0 + i < N; ++i) out[i] = __float2bfloat16_rn(__uint_as_float(v[i]));
+#pragma unroll
+        for (unsigned i = 0; i < 32; ++i)
+          if (col0 + i < N) out[i] = __float2bfloat16_rn(__uint_as_float(v[i]));
       }
     }
   }
   tc_fence_before();  // the next tile's MMAs overwrite this accumulator
   G.kb_used = g0 + nk;
   G.accum_used += 1;
+  // Both halves of the tile are written (and both TMEMs read) before the
+  // leader records the tile or issues the next tile's MMAs.
+  cluster_sync_all();
 }
 
 }  // namespace gpuos_dev_impl

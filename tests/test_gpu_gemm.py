@@ -77,7 +77,7 @@ def test_gemm_atoms_match_reference(api, cuda_device, m, n, k, bf16_out, workers
     with api.Device(workers_per_sm=workers) as dev:
         desc, blocks, tm, tn = dev.gemm_desc(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k,
                                              bf16_out=bf16_out)
-        assert tm == 128 and tn == min(256, 512 // workers)
+        assert tm == 256 and tn == 256
         assert blocks == -(-m // tm) * -(-n // tn)
         trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
         atoms = random_atoms(rng, blocks, min(blocks, 7))
