@@ -129,6 +129,11 @@ typedef struct gpuos_dev_stats {
   uint64_t claim_retries;    /* lost CAS races on block claims              */
   int64_t kernel_elapsed_ns; /* CUDA-event time of the last start..stop     */
   int64_t ingest_entries;    /* ring entries consumed by the device         */
+  int64_t worker_span_ns;    /* last run: first worker CTA entry .. last
+                                exit on the device clock (the CUDA-event
+                                time minus this is launch + teardown)      */
+  int64_t first_block_ns;    /* last run: first worker entry .. first block
+                                start (per-CTA setup: TMEM, barriers)      */
 } gpuos_dev_stats;
 
 int gpuos_dev_open(const gpuos_dev_config* cfg, struct gpuos_dev** out);

@@ -92,7 +92,8 @@ class Completion(C.Structure):
 class DevStats(C.Structure):
     _fields_ = [("blocks_executed", C.c_uint64), ("atoms_completed", C.c_uint64),
                 ("worker_busy_ns", C.c_uint64), ("claim_retries", C.c_uint64),
-                ("kernel_elapsed_ns", C.c_int64), ("ingest_entries", C.c_int64)]
+                ("kernel_elapsed_ns", C.c_int64), ("ingest_entries", C.c_int64),
+                ("worker_span_ns", C.c_int64), ("first_block_ns", C.c_int64)]
 
 
 _lib: C.CDLL | None = None

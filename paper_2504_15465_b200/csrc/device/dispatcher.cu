@@ -88,6 +88,9 @@ struct DevCtl {
   unsigned long long blocks, busy_ns, retries, atoms_done;
   unsigned long long stale_claims;  // claims that landed on a recycled slot
   unsigned arrived;                 // worker CTAs that have started
+  unsigned pad1;
+  unsigned long long t_enter, t_exit;  // first worker entry / last exit (globaltimer)
+  unsigned long long t_first_block;    // earliest block start
 };
 
 // 128-byte submit-ring entry: four 32-byte sectors, each = 7 data words +
@@ -593,6 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   unsigned sm = smid();
   int tpc = p.phys2log[sm >> 1];
   if (tid == 0) {
+    atomicMin(&p.ctl->t_enter, gtimer());
     st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 ? 0x80000000u : 0u));
     atomicAdd(&p.ctl->arrived, 1u);
   }
@@ -630,6 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   tc_fence_after();
   gemm.tmem = sh.tmem_base;
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
+  unsigned long long first_start = ~0ull;
   // Remote addresses inside the pair.
   const unsigned peer_join_rc = map_rank(&sh.join_rc, 1);
   const unsigned peer_join_full = map_rank(&sh.join_full, 1);
@@ -777,7 +782,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
           // bump observed here makes the batch's keys and claims visible) or,
           // on the peer, for a pair tile. The control block is only consulted
           // when nothing changed, so a wake-up costs one version load.
-          bool changed = false;
+          // Exit conditions are checked every 8 polls (a drained batch ends
+          // within a few microseconds of its last atom).
+          bool changed = false, leave = false;
           for (int k2 = 0; k2 < 64; ++k2) {
             if (rank != 0 && mbar_test_cluster(&sh.join_full, joins & 1u)) {
               changed = true;
@@ -789,14 +796,17 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               changed = true;
               break;
             }
+            if ((k2 & 7) == 7) {
+              leave = ld_relaxed_gpu(&p.ctl->quit) ||
+                      (!defer && ld_relaxed_gpu(&p.ctl->drain) &&
+                       ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0) ||
+                      gtimer() > p.ctl->deadline;
+              if (leave) break;
+            }
             __nanosleep(p.idle_sleep_ns);
           }
           if (changed) continue;
-          if (ld_relaxed_gpu(&p.ctl->quit)) break;
-          if (!defer && ld_relaxed_gpu(&p.ctl->drain) &&
-              ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0)
-            break;
-          if (gtimer() > p.ctl->deadline) break;
+          if (leave) break;
         }
       }
       if (lane == 0) {
@@ -822,6 +832,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
         }
         sh.go = go;
         sh.t_start = gtimer();
+        if (go != kGoExit && first_start == ~0ull) first_start = sh.t_start;
       }
     }
     __syncthreads();
@@ -840,10 +851,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     atomicAdd(&p.ctl->blocks, n_blocks);
     atomicAdd(&p.ctl->busy_ns, busy);
     atomicAdd(&p.ctl->retries, retries);
+    if (first_start != ~0ull) atomicMin(&p.ctl->t_first_block, first_start);
   }
   tc_fence_before();
   cluster_sync_all();  // neither CTA frees TMEM or leaves while the other may still use it
   if (warp == 1) tmem_free2(gemm.tmem, p.tmem_cols);
+  if (tid == 0) atomicMax(&p.ctl->t_exit, gtimer());
 }
 
 __global__ void k_gtimer(unsigned long long* out) { *out = gtimer(); }
@@ -956,6 +969,13 @@ void put64(uint32_t* data, int field, uint64_t v) {
 }
 
 int map_priority(int32_t p) { return std::clamp(p, 0, 254) + 1; }
+
+void record_spans(gpuos_dev* d, const DevCtl& c) {
+  const bool ok = c.t_enter != ~0ull && c.t_exit >= c.t_enter;
+  d->stats.worker_span_ns = ok ? static_cast<int64_t>(c.t_exit - c.t_enter) : 0;
+  d->stats.first_block_ns =
+      ok && c.t_first_block != ~0ull ? static_cast<int64_t>(c.t_first_block - c.t_enter) : 0;
+}
 
 // TMEM columns per worker: the largest power of two <= 512 / W (>= 32).
 unsigned tmem_cols_for(int workers_per_sm) {
@@ -1149,6 +1169,7 @@ int gpuos_dev_start(gpuos_dev* d) {
     d->calibrated = true;
   }
   DevCtl ctl{};
+  ctl.t_enter = ctl.t_first_block = ~0ull;
   // Hang guard: every dispatcher kernel exits 30 min after start regardless.
   ctl.deadline = static_cast<unsigned long long>(d->gt_offset + gpuos_dev_now_ns(d)) +
                  1800ull * 1000000000ull;
@@ -1301,6 +1322,7 @@ int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
   d->stats.claim_retries += ctl.retries;
   d->stats.kernel_elapsed_ns = static_cast<int64_t>(ms * 1e6);
   d->stats.ingest_entries += static_cast<int64_t>(*d->consumed_h);
+  record_spans(d, ctl);
   if (drain && ctl.outstanding != 0)
     return fail(GPUOS_E_INVARIANT, "drained with atoms outstanding");
   return GPUOS_OK;
@@ -1389,6 +1411,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
   DevCtl ctl{};
+  ctl.t_enter = ctl.t_first_block = ~0ull;
   ctl.drain = 1;
   ctl.outstanding = n;
   ctl.deadline = ~0ull >> 1;
@@ -1426,6 +1449,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   d->stats.worker_busy_ns += after.busy_ns;
   d->stats.claim_retries += after.retries;
   d->stats.kernel_elapsed_ns = static_cast<int64_t>(ms * 1e6);
+  record_spans(d, after);
   if (after.outstanding != 0) return fail(GPUOS_E_INVARIANT, "batch finished with atoms outstanding");
   return GPUOS_OK;
 }
@@ -1669,6 +1693,7 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
   h.n_tiles = static_cast<unsigned>((n + n_tile - 1) / n_tile);
   h.n_tile = n_tile;
   h.flags = flags & kGemmOutBf16;
+  h.timing = nullptr;
   void* p = nullptr;
   CUDA_TRY(cudaSetDevice(d->device));
   CUDA_TRY(cudaMallocAsync(&p, sizeof(GemmDesc), d->s_side));

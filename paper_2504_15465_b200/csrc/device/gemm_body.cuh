@@ -50,6 +50,7 @@ struct alignas(128) GemmDesc {
   unsigned long long c;          // C [M, N] row-major (ldc elements)
   unsigned m, n, k, ldc;
   unsigned m_tiles, n_tiles, n_tile, flags;  // 256-wide tiles; flags bit 0: bf16 output
+  unsigned long long* timing;    // optional: 4 globaltimer stamps per tile (profiling)
 };
 constexpr unsigned kGemmOutBf16 = 1u;
 
@@ -210,6 +211,8 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
     return;
   }
 
+  unsigned long long* tm = D->timing != nullptr && rank == 0 ? D->timing + 4ull * blk : nullptr;
+  if (tm && tid == 0) tm[0] = gtimer();
   if (tid == 0) {
     // TMA producer (both CTAs). The descriptor was written by a host copy
     // while this persistent kernel runs: acquire it into the tensor-map proxy.
@@ -237,6 +240,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
       const unsigned s = static_cast<unsigned>(k % S);
       mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1));
       tc_fence_after();
+      if (tm && j == 0) tm[1] = gtimer();
       const unsigned a0 = smem_u32(G.tiles + s * kGemmStageBytes);
       const unsigned b0 = a0 + kGemmABytes;
 #pragma unroll
@@ -252,6 +256,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   // (this CTA's 128 tile rows) and column half w/4.
   mbar_wait_bounded(G.accum, G.accum_used & 1u);
   tc_fence_after();
+  if (tm && tid == 0) tm[2] = gtimer();
   const int warp = tid >> 5, lane = tid & 31;
   const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
   constexpr unsigned half = kGemmTile / 2;
@@ -297,6 +302,10 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
     }
   }
   tc_fence_before();  // the next tile's MMAs overwrite this accumulator
+  if (tm) {
+    __syncthreads();
+    if (tid == 0) tm[3] = gtimer();
+  }
   G.kb_used = g0 + nk;
   G.accum_used += 1;
   // Both halves of the tile are written (and both TMEMs read) before the

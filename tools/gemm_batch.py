@@ -32,6 +32,9 @@ with api.Device(workers_per_sm=workers) as dev:
         ms = dev.run_batch(descs)
         while dev.in_flight():
             dev.poll()
+        st = dev.stats()
         print(f"gemm {m}x{n}x{k} W={workers} tiles {tm}x{tn} ({blocks}) atoms {n_atoms}: "
-              f"{ms:.3f} ms, {2 * m * n * k / ms / 1e9:.0f} TFLOP/s", flush=True)
+              f"{ms:.3f} ms, {2 * m * n * k / ms / 1e9:.0f} TFLOP/s "
+              f"(device span {st.worker_span_ns / 1e3:.1f} us, first block after "
+              f"{st.first_block_ns / 1e3:.1f} us)", flush=True)
     dev.free(desc)
