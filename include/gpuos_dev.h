@@ -63,6 +63,10 @@ extern "C" {
                                    tile (b % m_tiles, b / m_tiles) of
                                    C = A . B^T on the tensor cores       */
 #define GPUOS_BODY_SPIN 3u    /* args: ns to spin per block (globaltimer)    */
+#define GPUOS_BODY_GEMV_BF16 4u /* args: [0] = descriptor from
+                                   gpuos_dev_gemv_desc(); block b = rows
+                                   [256 b, 256 b + 256) of y = W . x (decode
+                                   GEMV, HBM-bound, tensor-core MACs)      */
 
 /* Launch-time configuration. Zero fields take the defaults in brackets.   */
 typedef struct gpuos_dev_config {
@@ -186,6 +190,21 @@ int gpuos_dev_get_stats(struct gpuos_dev* dev, gpuos_dev_stats* out);
 int gpuos_dev_gemm_desc(struct gpuos_dev* dev, const void* a, const void* b, void* c,
                         int64_t m, int64_t n, int64_t k, int64_t ldc, uint32_t flags,
                         void** desc, int64_t* blocks, int32_t* tile_m, int32_t* tile_n);
+
+/* GEMV body descriptor (GPUOS_BODY_GEMV_BF16): y[N] = W[N,K] . x[K] with
+ * bf16 W and x (16-byte aligned, K % 8 == 0), fp32 accumulation, fp32 y
+ * (flags 0) or bf16 (GPUOS_GEMV_OUT_BF16). Blocks are 256-row tiles of W
+ * computed by a TPC's two SMs (tcgen05.mma.cta_group::2, M = 256, N = 32
+ * with x as the only non-zero column). k_splits > 1 also splits K (decode
+ * shapes have few row tiles): block b = (row tile b % row_tiles, K split
+ * b / row_tiles), each adding its partial sums into y, which must then be
+ * fp32 and zeroed by the caller before the kernel. The content of x (and W)
+ * may change between atoms; the descriptor holds addresses only. Release
+ * with gpuos_dev_free. No reference counterpart (device.hpp:39-47).      */
+#define GPUOS_GEMV_OUT_BF16 1u
+int gpuos_dev_gemv_desc(struct gpuos_dev* dev, const void* w, const void* x, void* y,
+                        int64_t n, int64_t k, uint32_t flags, int32_t k_splits, void** desc,
+                        int64_t* blocks);
 
 /* Device memory helpers (stream-ordered on a side stream: safe while the
  * persistent dispatcher runs; never synchronise the whole device).        */

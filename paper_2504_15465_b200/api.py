@@ -31,6 +31,7 @@ LIB_PATH = os.path.join(PKG, "lib", "libgpuos_b200.so")
 GPUOS_BODY_STREAM = 1
 GPUOS_BODY_GEMM_BF16 = 2
 GPUOS_BODY_SPIN = 3
+GPUOS_BODY_GEMV_BF16 = 4
 GPUOS_GEMM_OUT_BF16 = 1
 GPUOS_E_FULL = -5
 GPUOS_DEV_DEFER_WORKERS = 1
@@ -43,7 +44,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask",
-    "gpuos_dev_gemm_desc",
+    "gpuos_dev_gemm_desc", "gpuos_dev_gemv_desc",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -133,6 +134,8 @@ def library() -> C.CDLL:
         "gpuos_dev_host_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
         "gpuos_dev_host_free": (C.c_int, [P, P]),
         "gpuos_dev_consumed": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "gpuos_dev_gemv_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_uint32, C.c_int32,
+                                          C.POINTER(P), C.POINTER(C.c_int64)]),
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                           C.c_uint32, C.POINTER(P), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
@@ -318,6 +321,16 @@ class Device:
             GPUOS_GEMM_OUT_BF16 if bf16_out else 0, C.byref(desc), C.byref(blocks),
             C.byref(tm), C.byref(tn)))
         return desc.value, blocks.value, tm.value, tn.value
+
+    def gemv_desc(self, w: int, x: int, y: int, n: int, k: int, bf16_out: bool = False,
+                  k_splits: int = 1) -> tuple[int, int]:
+        """Descriptor for GPUOS_BODY_GEMV_BF16 (y = W . x, decode GEMV):
+        returns (device pointer for args[0], grid blocks). k_splits > 1:
+        y (fp32) must be zeroed first; blocks add partial sums."""
+        desc, blocks = C.c_void_p(), C.c_int64()
+        self._check(self._lib.gpuos_dev_gemv_desc(self._h, w, x, y, n, k, 1 if bf16_out else 0,
+                                                  k_splits, C.byref(desc), C.byref(blocks)))
+        return desc.value, blocks.value
 
     def free(self, ptr: int) -> None:
         self._check(self._lib.gpuos_dev_free(self._h, ptr))

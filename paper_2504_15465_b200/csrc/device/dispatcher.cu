@@ -43,6 +43,7 @@
 
 #include "bodies.cuh"
 #include "gemm_body.cuh"
+#include "gemv_body.cuh"
 #include "gpuos_dev.h"
 #include "ptx.cuh"
 
@@ -567,16 +568,19 @@ __device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& r
 }
 
 __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned rank,
-                                         StreamPipe& pipe, GemmPipe& gemm) {
+                                         StreamPipe& pipe, GemmPipe& gemm, GemvPipe& gemv) {
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
+    case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
     case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm); break;
     default: break;
   }
 }
 
-__device__ __forceinline__ bool body_is_pair(unsigned body) { return body == GPUOS_BODY_GEMM_BF16; }
+__device__ __forceinline__ bool body_is_pair(unsigned body) {
+  return body == GPUOS_BODY_GEMM_BF16 || body == GPUOS_BODY_GEMV_BF16;
+}
 
 // Workers own TMEM (GEMM accumulators); the hardware co-schedules at most
 // two TMEM-using CTAs of this kernel per SM (measured: a W=4 launch leaves
@@ -620,6 +624,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   stream_pipe_init(pipe, dsmem, p.smem_bytes, tid);
   GemmPipe gemm;
   gemm_pipe_init(gemm, dsmem, p.smem_bytes, p.tmem_cols, tid);
+  GemvPipe gemv;
+  gemv_pipe_init(gemv, dsmem, p.smem_bytes, p.tmem_cols, tid);
   if (tid == 0) {
     mbar_init(&sh.join_full, 1);
     mbar_init(&sh.joined, 1);
@@ -632,7 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   tc_fence_before();
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
-  gemm.tmem = sh.tmem_base;
+  gemm.tmem = gemv.tmem = sh.tmem_base;
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
   unsigned long long first_start = ~0ull;
   // Remote addresses inside the pair.
@@ -838,7 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     __syncthreads();
     const int go = sh.go;
     if (go == kGoExit) break;
-    run_body(sh.rc, tid, rank, pipe, gemm);  // pair tiles end with a cluster barrier
+    run_body(sh.rc, tid, rank, pipe, gemm, gemv);  // pair tiles end with a cluster barrier
     if (go == kGoPair || go == kGoJoin) ++joins;
     __syncthreads();
     // The leader records pair tiles (the peer's half is complete: cluster
@@ -970,6 +976,24 @@ void put64(uint32_t* data, int field, uint64_t v) {
 
 int map_priority(int32_t p) { return std::clamp(p, 0, 254) + 1; }
 
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// The driver's tensor-map encoder, through the runtime (no libcuda link).
+EncodeTiledFn tensor_map_encoder() {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  return encode;
+}
+
 void record_spans(gpuos_dev* d, const DevCtl& c) {
   const bool ok = c.t_enter != ~0ull && c.t_exit >= c.t_enter;
   d->stats.worker_span_ns = ok ? static_cast<int64_t>(c.t_exit - c.t_enter) : 0;
@@ -985,7 +1009,17 @@ unsigned tmem_cols_for(int workers_per_sm) {
 }
 
 bool known_body(uint32_t b) {
-  return b == GPUOS_BODY_STREAM || b == GPUOS_BODY_SPIN || b == GPUOS_BODY_GEMM_BF16;
+  return b == GPUOS_BODY_STREAM || b == GPUOS_BODY_SPIN || b == GPUOS_BODY_GEMM_BF16 ||
+         b == GPUOS_BODY_GEMV_BF16;
+}
+
+// Argument checks the device bodies rely on (empty string: valid).
+std::string body_args_error(const gpuos_atom_desc& a) {
+  if (a.body == GPUOS_BODY_GEMV_BF16 || a.body == GPUOS_BODY_GEMM_BF16) {
+    if (a.args[0] == 0 || a.args[0] % 128 != 0) return "tensor-core bodies take a descriptor in args[0]";
+    if ((a.parts == 0 ? 1u : a.parts) != 1u) return "tensor-core tiles cannot be sliced";
+  }
+  return {};
 }
 
 }  // namespace
@@ -1351,6 +1385,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     if (a.lo < 0 || a.hi <= a.lo || (a.hi - a.lo) * static_cast<int64_t>(parts) > 0xfffffffeLL)
       return fail(GPUOS_E_CONFIG, "atom block range out of bounds");
     if (!known_body(a.body)) return fail(GPUOS_E_CONFIG, "unknown body kind");
+    if (const std::string e = body_args_error(a); !e.empty()) return fail(GPUOS_E_CONFIG, e);
     const uint32_t seq = d->next_seq++;
     seqs[static_cast<size_t>(i)] = seq;
     const int prio = map_priority(a.priority);
@@ -1463,6 +1498,7 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   if ((a->hi - a->lo) * static_cast<int64_t>(parts) > 0xfffffffeLL)
     return fail(GPUOS_E_CONFIG, "atom too large");
   if (!known_body(a->body)) return fail(GPUOS_E_CONFIG, "unknown body kind");
+  if (const std::string e = body_args_error(*a); !e.empty()) return fail(GPUOS_E_CONFIG, e);
   const int T = d->cfg.logical_tpcs;
   bool any = false;
   for (int w = 0; w < 2; ++w) {
@@ -1659,19 +1695,8 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
     return fail(GPUOS_E_CONFIG, "workers cannot host a GEMM stage");
   const unsigned n_tile = kGemmTile;
 
-  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static EncodeFn encode = nullptr;
-  if (!encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess)
-      return fail(GPUOS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-    encode = reinterpret_cast<EncodeFn>(fn);
-  }
+  EncodeTiledFn encode = tensor_map_encoder();
+  if (!encode) return fail(GPUOS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   GemmDesc h{};
   auto make = [&](CUtensorMap* map, const void* ptr, int64_t rows, unsigned box_rows) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
@@ -1703,6 +1728,54 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
   if (blocks) *blocks = static_cast<int64_t>(h.m_tiles) * h.n_tiles;
   if (tile_m) *tile_m = static_cast<int32_t>(kGemmTile);
   if (tile_n) *tile_n = static_cast<int32_t>(n_tile);
+  return GPUOS_OK;
+}
+
+int gpuos_dev_gemv_desc(gpuos_dev* d, const void* w, const void* x, void* y, int64_t n, int64_t k,
+                        uint32_t flags, int32_t k_splits, void** desc, int64_t* blocks) {
+  if (!d || !w || !x || !y || !desc) return fail(GPUOS_E_CONFIG, "null argument");
+  if (n <= 0 || k <= 0 || n > 0x7fffffff || k > 0x7fffffff)
+    return fail(GPUOS_E_CONFIG, "GEMV shape out of range");
+  if (k % 8 != 0) return fail(GPUOS_E_CONFIG, "GEMV K must be a multiple of 8 (16-byte rows)");
+  if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(x)) % 16 != 0)
+    return fail(GPUOS_E_CONFIG, "GEMV W and x must be 16-byte aligned");
+  if (tmem_cols_for(d->cfg.workers_per_sm) < kGemvN ||
+      d->topo.smem_per_worker < static_cast<int>(1024 + kGemvStageBytes))
+    return fail(GPUOS_E_CONFIG, "workers cannot host a GEMV stage");
+  EncodeTiledFn encode = tensor_map_encoder();
+  if (!encode) return fail(GPUOS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  GemvDesc h{};
+  auto make = [&](CUtensorMap* map, const void* ptr, int64_t rows, unsigned box_rows) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
+    const cuuint32_t box[2] = {kGemmBK, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  // x is a one-row tensor read with a 16-row box: rows >= 1 are zero fill.
+  if (make(&h.w, w, n, kGemmHalf) != CUDA_SUCCESS || make(&h.x, x, 1, kGemvXRows) != CUDA_SUCCESS)
+    return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the GEMV operands");
+  h.y = reinterpret_cast<unsigned long long>(y);
+  h.n = static_cast<unsigned>(n);
+  h.k = static_cast<unsigned>(k);
+  const unsigned nk = static_cast<unsigned>((k + kGemmBK - 1) / kGemmBK);
+  const unsigned splits = std::clamp<unsigned>(k_splits <= 0 ? 1u : static_cast<unsigned>(k_splits), 1u, nk);
+  if (splits > 1 && (flags & GPUOS_GEMV_OUT_BF16))
+    return fail(GPUOS_E_CONFIG, "split-K GEMV accumulates into fp32 y");
+  h.row_tiles = static_cast<unsigned>((n + kGemvTile - 1) / kGemvTile);
+  h.k_slices_per_block = (nk + splits - 1) / splits;
+  const unsigned used_splits = (nk + h.k_slices_per_block - 1) / h.k_slices_per_block;
+  h.blocks = h.row_tiles * used_splits;
+  h.flags = (flags & kGemvOutBf16) | (splits > 1 ? kGemvAccumulate : 0u);
+  void* p = nullptr;
+  CUDA_TRY(cudaSetDevice(d->device));
+  CUDA_TRY(cudaMallocAsync(&p, sizeof(GemvDesc), d->s_side));
+  CUDA_TRY(cudaMemcpyAsync(p, &h, sizeof(GemvDesc), cudaMemcpyHostToDevice, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  *desc = p;
+  if (blocks) *blocks = h.blocks;
   return GPUOS_OK;
 }
 
