@@ -119,6 +119,7 @@ struct Params {
   unsigned long long* resident;  // [tpcs][32]
   unsigned* version;             // [tpcs] bumped when a TPC's candidates change
   int* fence;                    // [tpcs] minimum priority allowed to start
+  unsigned* tc_busy;             // [tpcs] pair tiles running on the TPC's tensor cores
   DevCtl* ctl;
   const int* phys2log;           // [physical tpcs]
   RingEntry* ring;               // mapped host memory
@@ -410,6 +411,14 @@ static_assert(sizeof(RoundCmd) % 8 == 0, "RoundCmd copied as 64-bit words");
 
 enum WorkerGo : int { kGoExit = 0, kGoOwn = 1, kGoPair = 2, kGoJoin = 3 };
 
+// Spreading pair tiles: a leader whose TPC's tensor cores already run a
+// pair tile (the other pair of the TPC) waits up to this long before
+// claiming another, so a wave with fewer tiles than TPCs lands one tile per
+// TPC instead of two sharing one TPC while others idle (measured: a 16-tile
+// GEMM on 16 TPCs ran 26 % slower than on 32 without it). In a full wave the
+// second pair just starts a little later and overlaps its partner's epilogue.
+constexpr unsigned long long kSpreadNs = 4000;
+
 struct WorkerShared {
   RoundCmd rc;                  // this CTA's block for the round
   RoundCmd join_rc;             // peer: pair tile posted by the leader
@@ -656,6 +665,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   unsigned cur_count = 0u;
   unsigned cur_body = 0u;
   int cur_tpc = -1;
+  unsigned long long spread_since = 0;  // leader: deferring a pair tile since
+  bool tc_hold = false;                 // leader thread 0: holds the TPC's tensor reservation
 
   for (;;) {
     // %smid can change if the CTA is ever preempted and restored elsewhere;
@@ -681,7 +692,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
           unsigned got = 0;
           unsigned long long key = 0ull;
           bool stale = false;
-          if (cur_key != 0ull && ver == cur_ver) {
+          // (Pair tiles always go through the full arbitration: it holds
+          // the TPC's tensor-core reservation, below.)
+          if (cur_key != 0ull && ver == cur_ver && !body_is_pair(cur_body)) {
             // Fast path: next slice of the atom being drained. The version is
             // re-read alongside the claim; a change noticed only after it
             // costs at most one slice of priority inversion.
@@ -702,12 +715,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
             const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
             const unsigned long long k = ld_acquire_gpu64(list + lane);
             bool eligible = false;
-            unsigned long long f_lo = 0, f_bp = 0, f_cp = 0, f_a[5] = {0, 0, 0, 0, 0};
+            unsigned long long f_lo = 0, f_bp = 0, f_cp = 0, f_cw = 0, f_a[5] = {0, 0, 0, 0, 0};
             if (k != 0ull) {
               const DevAtom* a = p.atoms + (k & 0xffffffull);
               unsigned long long cw, cp;
               ld_relaxed_gpu_v2(a, cw, cp);  // claim | count, paused
               f_cp = cp;
+              f_cw = cw;
               ld_relaxed_gpu_v2(&a->lo, f_lo, f_bp);  // lo | body, parts
               ld_relaxed_gpu_v2(&a->args[0], f_a[0], f_a[1]);
               ld_relaxed_gpu_v2(&a->args[2], f_a[2], f_a[3]);
@@ -718,23 +732,53 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                          static_cast<int>(k >> 56) >= floor_prio;
             }
             key = warp_max_u64(eligible ? k : 0ull);
+            if (key == 0ull) spread_since = 0;  // nothing to defer any more
             if (key != 0ull) {
               // The winner's count and body travel with the arbitration.
               const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
               const unsigned wcount = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp), win);
               f_bp = __shfl_sync(0xffffffffu, f_bp, win);
-              if (rank != 0 && body_is_pair(static_cast<unsigned>(f_bp))) {
+              const bool pair = body_is_pair(static_cast<unsigned>(f_bp));
+              // Leader and a pair tile: reserve the TPC's tensor cores. If
+              // the other pair holds them, defer up to kSpreadNs so an idle
+              // TPC takes the tile first; after that, claim anyway.
+              // Deferring only helps while the atom runs fewer tiles than it
+              // has TPCs (some TPC of its set may be tensor-idle); in a full
+              // wave the second pair claims at once.
+              int reserved = 0;
+              const unsigned long long wcw = __shfl_sync(0xffffffffu, f_cw, win);
+              if (rank == 0 && pair && lane == 0) {
+                const bool expired = spread_since != 0 && gtimer() - spread_since >= kSpreadNs;
+                const unsigned before = atomicAdd(p.tc_busy + tpc, 1u);
+                reserved = before == 0u || expired ? 1 : 0;
+                if (!reserved) {
+                  const DevAtom* wa = p.atoms + (key & 0xffffffull);
+                  const unsigned in_flight = static_cast<unsigned>(wcw) - ld_relaxed_gpu(&wa->done);
+                  const unsigned width = __popcll(ld_relaxed_gpu64(&wa->mask[0])) +
+                                         __popcll(ld_relaxed_gpu64(&wa->mask[1]));
+                  if (in_flight >= width) reserved = 1;
+                }
+                if (!reserved) atomicSub(p.tc_busy + tpc, 1u);
+              }
+              reserved = __shfl_sync(0xffffffffu, reserved, 0);
+              if (rank != 0 && pair) {
                 defer = true;  // no lower-priority bypass: wait for the leader
+              } else if (rank == 0 && pair && !reserved) {
+                defer = true;  // let an idle TPC take it first (kSpreadNs)
+                if (spread_since == 0) spread_since = gtimer();
               } else {
+                spread_since = 0;
                 if (lane == 0)
                   off = claim_block(p.atoms + (key & 0xffffffull), key, wcount, 1u, p.ctl, stale, got);
                 off = __shfl_sync(0xffffffffu, off, 0);
                 if (off < 0) {
+                  if (reserved && lane == 0) atomicSub(p.tc_busy + tpc, 1u);
                   ++retries;  // lost that atom's last slices to other workers
                   ver = ld_acquire_gpu(p.version + tpc);
                   continue;
                 }
                 // Hand the winner's fields to lane 0 (no second round trip).
+                if (lane == 0 && reserved) tc_hold = true;
                 cur_count = wcount;
                 f_lo = __shfl_sync(0xffffffffu, f_lo, win);
 #pragma unroll
@@ -778,6 +822,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
             cur_slot = slot;
             cur_ver = ver;
             cur_body = __shfl_sync(0xffffffffu, sh.rc.cmd.body, 0);
+            spread_since = 0;
             go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
             // A peer reaches a 2-SM block only by adopting a recycled slot
             // (stale claim, see claim_block): it cannot run it alone.
@@ -803,6 +848,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               break;
             }
             if ((k2 & 7) == 7) {
+              if (spread_since != 0 && gtimer() - spread_since >= kSpreadNs) {
+                changed = true;  // spreading wait over: claim now
+                break;
+              }
               leave = ld_relaxed_gpu(&p.ctl->quit) ||
                       (!defer && ld_relaxed_gpu(&p.ctl->drain) &&
                        ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0) ||
@@ -817,6 +866,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
       }
       if (lane == 0) {
         if (go == kGoPair) {
+          // (the TPC's tensor-core reservation was taken at the claim)
           // Post the tile to the peer (release: the command precedes the
           // arrival), then wait until it has taken it.
           const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&sh.rc);
@@ -846,6 +896,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     if (go == kGoExit) break;
     run_body(sh.rc, tid, rank, pipe, gemm, gemv);  // pair tiles end with a cluster barrier
     if (go == kGoPair || go == kGoJoin) ++joins;
+    if (tc_hold && tid == 0) {
+      atomicSub(p.tc_busy + tpc, 1u);
+      tc_hold = false;
+    }
     __syncthreads();
     // The leader records pair tiles (the peer's half is complete: cluster
     // barrier at the end of the body).
@@ -916,6 +970,7 @@ struct gpuos_dev {
   unsigned long long* resident = nullptr;
   unsigned* version = nullptr;
   int* fence = nullptr;
+  unsigned* tc_busy = nullptr;
   DevCtl* ctl = nullptr;
   int* phys2log = nullptr;
   unsigned long long* gt_scratch = nullptr;
@@ -1108,6 +1163,7 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   CUDA_TRY(cudaMalloc(&d->resident, sizeof(unsigned long long) * T * kResident));
   CUDA_TRY(cudaMalloc(&d->version, sizeof(unsigned) * T));
   CUDA_TRY(cudaMalloc(&d->fence, sizeof(int) * T));
+  CUDA_TRY(cudaMalloc(&d->tc_busy, sizeof(unsigned) * T));
   CUDA_TRY(cudaMalloc(&d->ctl, sizeof(DevCtl)));
   CUDA_TRY(cudaMalloc(&d->phys2log, sizeof(int) * phys_tpcs));
   CUDA_TRY(cudaMalloc(&d->gt_scratch, sizeof(unsigned long long)));
@@ -1142,6 +1198,7 @@ int gpuos_dev_close(gpuos_dev* d) {
   cudaFree(d->resident);
   cudaFree(d->version);
   cudaFree(d->fence);
+  cudaFree(d->tc_busy);
   cudaFree(d->ctl);
   cudaFree(d->phys2log);
   cudaFree(d->gt_scratch);
@@ -1176,6 +1233,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   CUDA_TRY(cudaMemset(d->resident, 0, sizeof(unsigned long long) * T * kResident));
   CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
+  CUDA_TRY(cudaMemset(d->tc_busy, 0, sizeof(unsigned) * T));
   std::memset(d->ring_h, 0, sizeof(RingEntry) * d->cfg.ring_entries);
   std::memset(d->comp_h, 0, sizeof(CompRec) * d->cfg.atom_slots);
   std::memset(d->alive_h, 0, sizeof(unsigned) * d->grid);
@@ -1215,6 +1273,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   p.resident = d->resident;
   p.version = d->version;
   p.fence = d->fence;
+  p.tc_busy = d->tc_busy;
   p.ctl = d->ctl;
   p.phys2log = d->phys2log;
   p.ring = d->ring_d;
@@ -1445,6 +1504,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
                       cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
+  CUDA_TRY(cudaMemset(d->tc_busy, 0, sizeof(unsigned) * T));
   DevCtl ctl{};
   ctl.t_enter = ctl.t_first_block = ~0ull;
   ctl.drain = 1;
@@ -1457,6 +1517,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   p.resident = d->resident;
   p.version = d->version;
   p.fence = d->fence;
+  p.tc_busy = d->tc_busy;
   p.ctl = d->ctl;
   p.phys2log = d->phys2log;
   p.ring = d->ring_d;

@@ -175,3 +175,21 @@ def test_library_rejects_bad_inputs(api):
     assert api.filter_cap(0, 1, 54) == -2
     with pytest.raises(api.GpuosError):
         api.fit_scaling(1, 1, 1)
+
+
+def test_rightsize_r_squared_matches_reference_semantics():
+    """paper_2504_15465_b200.rightsize.r_squared restates rightsizer.cpp:105-119:
+    exact fit -> 1, constant data with a perfect fit -> 1, constant data
+    with residual -> -ss_res, and the ordinary 1 - ss_res / ss_tot."""
+    from paper_2504_15465_b200.rightsize import r_squared
+
+    m, b = 36e6, 2e6
+    pts = [(t, m / t + b) for t in (1, 2, 4, 8, 36)]
+    assert r_squared(m, b, pts) == 1.0
+    assert r_squared(0.0, 5.0, [(1, 5.0), (2, 5.0)]) == 1.0
+    assert r_squared(0.0, 4.0, [(1, 5.0), (2, 5.0)]) == -2.0
+    pts = [(1, 10.0), (2, 7.0), (4, 4.0)]
+    mean = 7.0
+    ss_res = sum((l - (8.0 / t + 2.0)) ** 2 for t, l in pts)
+    ss_tot = sum((l - mean) ** 2 for _, l in pts)
+    assert abs(r_squared(8.0, 2.0, pts) - (1 - ss_res / ss_tot)) < 1e-12
