@@ -68,6 +68,11 @@ extern "C" {
                                    [256 b, 256 b + 256) of y = W . x (decode
                                    GEMV, HBM-bound, tensor-core MACs)      */
 
+#define GPUOS_BODY_CONV_BF16 5u /* args: [0] = descriptor from
+                                   gpuos_dev_conv_desc(); block b = 256
+                                   output pixels x 256 output channels of an
+                                   implicit-GEMM convolution on tcgen05    */
+
 /* Launch-time configuration. Zero fields take the defaults in brackets.   */
 typedef struct gpuos_dev_config {
   int32_t device_ordinal;   /* [0] */
@@ -205,6 +210,21 @@ int gpuos_dev_gemm_desc(struct gpuos_dev* dev, const void* a, const void* b, voi
 int gpuos_dev_gemv_desc(struct gpuos_dev* dev, const void* w, const void* x, void* y,
                         int64_t n, int64_t k, uint32_t flags, int32_t k_splits, void** desc,
                         int64_t* blocks);
+
+/* Convolution body descriptor (GPUOS_BODY_CONV_BF16): y = conv2d(x, w),
+ * x NHWC bf16 [n, h, wd, c] (c % 8 == 0), w bf16 [k][r][s][cb] with cb = c
+ * rounded up to 64 (zero-padded channels), padding `pad`, stride 1 or 2,
+ * y NHWC [n, p, q, k] fp32 (flags 0) or bf16 (GPUOS_CONV_OUT_BF16) with
+ * p = (h + 2 pad - r) / stride + 1 (q likewise). Implicit GEMM on a TPC's
+ * two SMs: each K-step is one 4-D TMA box of x (an output patch's input
+ * pixels for one filter tap and 64 channels; padding is the TMA's zero
+ * fill) and one 2-D box of w. Returns the descriptor (args[0]; release with
+ * gpuos_dev_free), the grid and the output size.                        */
+#define GPUOS_CONV_OUT_BF16 1u
+int gpuos_dev_conv_desc(struct gpuos_dev* dev, const void* x, const void* w, void* y, int32_t n,
+                        int32_t h, int32_t wd, int32_t c, int32_t k, int32_t r, int32_t s,
+                        int32_t pad, int32_t stride, uint32_t flags, void** desc, int64_t* blocks,
+                        int32_t* p, int32_t* q);
 
 /* Device memory helpers (stream-ordered on a side stream: safe while the
  * persistent dispatcher runs; never synchronise the whole device).        */

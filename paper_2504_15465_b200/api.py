@@ -32,6 +32,7 @@ GPUOS_BODY_STREAM = 1
 GPUOS_BODY_GEMM_BF16 = 2
 GPUOS_BODY_SPIN = 3
 GPUOS_BODY_GEMV_BF16 = 4
+GPUOS_BODY_CONV_BF16 = 5
 GPUOS_GEMM_OUT_BF16 = 1
 GPUOS_E_FULL = -5
 GPUOS_DEV_DEFER_WORKERS = 1
@@ -44,7 +45,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask",
-    "gpuos_dev_gemm_desc", "gpuos_dev_gemv_desc",
+    "gpuos_dev_gemm_desc", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -134,6 +135,9 @@ def library() -> C.CDLL:
         "gpuos_dev_host_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
         "gpuos_dev_host_free": (C.c_int, [P, P]),
         "gpuos_dev_consumed": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "gpuos_dev_conv_desc": (C.c_int, [P, P, P, P] + [C.c_int32] * 9 + [C.c_uint32, C.POINTER(P),
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_int32)]),
         "gpuos_dev_gemv_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_uint32, C.c_int32,
                                           C.POINTER(P), C.POINTER(C.c_int64)]),
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
@@ -331,6 +335,16 @@ class Device:
         self._check(self._lib.gpuos_dev_gemv_desc(self._h, w, x, y, n, k, 1 if bf16_out else 0,
                                                   k_splits, C.byref(desc), C.byref(blocks)))
         return desc.value, blocks.value
+
+    def conv_desc(self, x: int, w: int, y: int, n: int, h: int, wd: int, c: int, k: int, r: int,
+                  s: int, pad: int, stride: int, bf16_out: bool = False) -> tuple[int, int, int, int]:
+        """Descriptor for GPUOS_BODY_CONV_BF16 (NHWC implicit-GEMM conv on
+        tcgen05): returns (device pointer for args[0], grid blocks, P, Q)."""
+        desc, blocks, p, q = C.c_void_p(), C.c_int64(), C.c_int32(), C.c_int32()
+        self._check(self._lib.gpuos_dev_conv_desc(self._h, x, w, y, n, h, wd, c, k, r, s, pad, stride,
+                                                  1 if bf16_out else 0, C.byref(desc),
+                                                  C.byref(blocks), C.byref(p), C.byref(q)))
+        return desc.value, blocks.value, p.value, q.value
 
     def free(self, ptr: int) -> None:
         self._check(self._lib.gpuos_dev_free(self._h, ptr))

@@ -44,6 +44,7 @@
 #include "bodies.cuh"
 #include "gemm_body.cuh"
 #include "gemv_body.cuh"
+#include "conv_body.cuh"
 #include "gpuos_dev.h"
 #include "ptx.cuh"
 
@@ -581,6 +582,7 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
     case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv); break;
+    case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
     case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm); break;
     default: break;
@@ -588,7 +590,8 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
 }
 
 __device__ __forceinline__ bool body_is_pair(unsigned body) {
-  return body == GPUOS_BODY_GEMM_BF16 || body == GPUOS_BODY_GEMV_BF16;
+  return body == GPUOS_BODY_GEMM_BF16 || body == GPUOS_BODY_GEMV_BF16 ||
+         body == GPUOS_BODY_CONV_BF16;
 }
 
 // Workers own TMEM (GEMM accumulators); the hardware co-schedules at most
@@ -1065,12 +1068,13 @@ unsigned tmem_cols_for(int workers_per_sm) {
 
 bool known_body(uint32_t b) {
   return b == GPUOS_BODY_STREAM || b == GPUOS_BODY_SPIN || b == GPUOS_BODY_GEMM_BF16 ||
-         b == GPUOS_BODY_GEMV_BF16;
+         b == GPUOS_BODY_GEMV_BF16 || b == GPUOS_BODY_CONV_BF16;
 }
 
 // Argument checks the device bodies rely on (empty string: valid).
 std::string body_args_error(const gpuos_atom_desc& a) {
-  if (a.body == GPUOS_BODY_GEMV_BF16 || a.body == GPUOS_BODY_GEMM_BF16) {
+  if (a.body == GPUOS_BODY_GEMV_BF16 || a.body == GPUOS_BODY_GEMM_BF16 ||
+      a.body == GPUOS_BODY_CONV_BF16) {
     if (a.args[0] == 0 || a.args[0] % 128 != 0) return "tensor-core bodies take a descriptor in args[0]";
     if ((a.parts == 0 ? 1u : a.parts) != 1u) return "tensor-core tiles cannot be sliced";
   }
@@ -1837,6 +1841,81 @@ int gpuos_dev_gemv_desc(gpuos_dev* d, const void* w, const void* x, void* y, int
   CUDA_TRY(cudaStreamSynchronize(d->s_side));
   *desc = p;
   if (blocks) *blocks = h.blocks;
+  return GPUOS_OK;
+}
+
+int gpuos_dev_conv_desc(gpuos_dev* d, const void* x, const void* w, void* y, int32_t n, int32_t h,
+                        int32_t wd, int32_t c, int32_t k, int32_t r, int32_t s, int32_t pad,
+                        int32_t stride, uint32_t flags, void** desc, int64_t* blocks, int32_t* p_out,
+                        int32_t* q_out) {
+  if (!d || !x || !w || !y || !desc) return fail(GPUOS_E_CONFIG, "null argument");
+  if (n <= 0 || h <= 0 || wd <= 0 || c <= 0 || k <= 0 || r <= 0 || s <= 0 || pad < 0 || stride <= 0)
+    return fail(GPUOS_E_CONFIG, "conv shape out of range");
+  if (c % 8 != 0) return fail(GPUOS_E_CONFIG, "conv C must be a multiple of 8 (16-byte pixels)");
+  if (stride > 2) return fail(GPUOS_E_CONFIG, "conv stride must be 1 or 2");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) % 16 != 0)
+    return fail(GPUOS_E_CONFIG, "conv tensors must be 16-byte aligned");
+  const int P = (h + 2 * pad - r) / stride + 1, Q = (wd + 2 * pad - s) / stride + 1;
+  if (P <= 0 || Q <= 0) return fail(GPUOS_E_CONFIG, "conv output is empty");
+  if (tmem_cols_for(d->cfg.workers_per_sm) < kGemmTile ||
+      d->topo.smem_per_worker < static_cast<int>(1024 + kGemmStageBytes))
+    return fail(GPUOS_E_CONFIG, "workers cannot host a conv stage");
+  EncodeTiledFn encode = tensor_map_encoder();
+  if (!encode) return fail(GPUOS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  auto pow2 = [](unsigned v) {
+    unsigned p2 = 1;
+    while (p2 < v) p2 <<= 1;
+    return p2;
+  };
+  ConvDesc hd{};
+  hd.wb = std::min(128u, pow2(static_cast<unsigned>(Q)));
+  hd.hb = std::min(128u / hd.wb, pow2(static_cast<unsigned>(P)));
+  hd.nb = 128u / (hd.wb * hd.hb);
+  const unsigned cb = (static_cast<unsigned>(c) + kGemmBK - 1) / kGemmBK;
+  {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(wd),
+                                static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2,
+                                   static_cast<cuuint64_t>(c) * 2 * wd,
+                                   static_cast<cuuint64_t>(c) * 2 * wd * h};
+    const cuuint32_t box[4] = {kGemmBK, hd.wb * stride, hd.hb * stride, hd.nb};
+    const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
+    if (encode(&hd.act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the conv activations");
+  }
+  {
+    const uint64_t kdim = static_cast<uint64_t>(r) * s * cb * kGemmBK;
+    const cuuint64_t dims[2] = {kdim, static_cast<cuuint64_t>(k)};
+    const cuuint64_t strides[1] = {kdim * 2};
+    const cuuint32_t box[2] = {kGemmBK, kGemmHalf};
+    const cuuint32_t estr[2] = {1, 1};
+    if (encode(&hd.wgt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the conv weights");
+  }
+  hd.y = reinterpret_cast<unsigned long long>(y);
+  hd.n = n; hd.h = h; hd.w = wd; hd.c = c; hd.k = k; hd.r = r; hd.s = s;
+  hd.pad = pad; hd.stride = stride; hd.p = P; hd.q = Q;
+  hd.tiles_q = (Q + hd.wb - 1) / hd.wb;
+  hd.tiles_p = (P + hd.hb - 1) / hd.hb;
+  const unsigned tiles_n = (n + hd.nb - 1) / hd.nb;
+  hd.patches = hd.tiles_q * hd.tiles_p * tiles_n;
+  hd.pair_tiles = (hd.patches + 1) / 2;
+  hd.k_tiles = (static_cast<unsigned>(k) + kGemmTile - 1) / kGemmTile;
+  hd.c_blocks = cb;
+  hd.flags = flags & kConvOutBf16;
+  void* pdev = nullptr;
+  CUDA_TRY(cudaSetDevice(d->device));
+  CUDA_TRY(cudaMallocAsync(&pdev, sizeof(ConvDesc), d->s_side));
+  CUDA_TRY(cudaMemcpyAsync(pdev, &hd, sizeof(ConvDesc), cudaMemcpyHostToDevice, d->s_side));
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  *desc = pdev;
+  if (blocks) *blocks = static_cast<int64_t>(hd.pair_tiles) * hd.k_tiles;
+  if (p_out) *p_out = P;
+  if (q_out) *q_out = Q;
   return GPUOS_OK;
 }
 
