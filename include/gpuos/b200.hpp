@@ -18,6 +18,10 @@
 //           p2 = distinct chunks (0: min(blocks, stream_chunk_cap));
 //           workspace = buffer-pair slot shared by kernels of a tenant.
 //   Spin:   p0 = ns per block.
+//   GemmBf16: p = [M, N, K]; GemvBf16: p = [N, K, k_splits];
+//   ConvBf16: p = [n, h, w, c, k, r, s, pad, stride]. Operands are random
+//           bf16 per (workspace, shape), bf16 outputs; the kernel's grid
+//           must equal the descriptor's (256 x 256 tiles / 256-row tiles).
 //   None:   the reference's cost-only kernels; synthesised per
 //           B200Options::synth (Stream sized from block_us, or Spin).
 #pragma once
@@ -102,6 +106,10 @@ class B200Runtime {
     std::uint32_t parts;    // preemption slices per block
   };
   Resolved resolve(KernelId kid, const SimKernelSpec& spec);
+  // Allocates (and initialises) whatever the body needs without binding it
+  // to a kernel id: called for every kernel of a scenario before the
+  // dispatcher starts, so no allocation or fill kernel runs beside it.
+  void prepare(const SimKernelSpec& spec) { (void)resolve_body(spec); }
 
   void start();
   float stop(bool drain);  // returns the worker kernel's CUDA-event ms
@@ -133,6 +141,14 @@ class B200Runtime {
     std::uint32_t* host_src = nullptr;  // pinned tenant input
   };
   Workspace& workspace(std::uint32_t id, std::uint64_t words);
+  Resolved resolve_body(const SimKernelSpec& spec);
+  struct TensorBody {  // operands + descriptor of a tensor-core kernel shape
+    std::vector<void*> bufs;
+    void* desc = nullptr;
+    std::int64_t blocks = 0;
+  };
+  const TensorBody& tensor_body(const BodyRef& b);
+  std::map<std::string, TensorBody> tensors_;
   void ensure_trace(KernelId kid, long blocks);
 
   gpuos_dev* dev_ = nullptr;
@@ -258,6 +274,7 @@ class MirrorDevice final : public Device {
   VerifyReport verify();
   long gpu_atoms() const { return gpu_atoms_; }
   float gpu_kernel_ms() const { return gpu_ms_; }
+  B200Runtime& runtime() { return *rt_; }
 
  private:
   void drain_some(bool all);

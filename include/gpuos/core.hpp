@@ -80,14 +80,25 @@ struct FrequencyDomain {
 enum class BodyKind : std::uint32_t {
   None = 0,      // no device work (replay-only descriptors)
   Stream = 1,    // HBM-bound streaming transform, bytes_per_block per block
-  GemmBf16 = 2,  // bf16 GEMM, one 128 x n_tile output tile per block
+  GemmBf16 = 2,  // bf16 GEMM on tcgen05, one 256 x 256 output tile per block
   Spin = 3,      // fixed-duration compute spin (calibration / control)
+  GemvBf16 = 4,  // decode GEMV (HBM-bound), 256 rows of W per block
+  ConvBf16 = 5,  // NHWC implicit-GEMM convolution on tcgen05
 };
 
 struct BodyRef {
   BodyKind kind = BodyKind::None;
   std::uint32_t workspace = 0;  // tenant workspace slot (buffers reused)
   std::int64_t p0 = 0, p1 = 0, p2 = 0;  // body parameters (see b200.hpp)
+  std::int64_t px[7] = {0, 0, 0, 0, 0, 0, 0};  // parameters 3..9 (conv shapes)
+  std::int64_t param(int i) const { return i == 0 ? p0 : i == 1 ? p1 : i == 2 ? p2 : px[i - 3]; }
+  void set_param(int i, std::int64_t v) {
+    if (i == 0) p0 = v;
+    else if (i == 1) p1 = v;
+    else if (i == 2) p2 = v;
+    else px[i - 3] = v;
+  }
+  static constexpr int kParams = 10;
 };
 
 // Ground truth for one kernel launch (device.hpp:39-47).

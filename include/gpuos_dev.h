@@ -202,10 +202,11 @@ int gpuos_dev_gemm_desc(struct gpuos_dev* dev, const void* a, const void* b, voi
  * computed by a TPC's two SMs (tcgen05.mma.cta_group::2, M = 256, N = 32
  * with x as the only non-zero column). k_splits > 1 also splits K (decode
  * shapes have few row tiles): block b = (row tile b % row_tiles, K split
- * b / row_tiles), each adding its partial sums into y, which must then be
- * fp32 and zeroed by the caller before the kernel. The content of x (and W)
- * may change between atoms; the descriptor holds addresses only. Release
- * with gpuos_dev_free. No reference counterpart (device.hpp:39-47).      */
+ * b / row_tiles); the row tile's last block sums the partials in split
+ * order (deterministic) and writes y. One run of a descriptor at a time.
+ * The content of x (and W) may change between runs; the descriptor holds
+ * addresses. Release with gpuos_dev_free. No reference counterpart
+ * (device.hpp:39-47).                                                    */
 #define GPUOS_GEMV_OUT_BF16 1u
 int gpuos_dev_gemv_desc(struct gpuos_dev* dev, const void* w, const void* x, void* y,
                         int64_t n, int64_t k, uint32_t flags, int32_t k_splits, void** desc,
@@ -225,6 +226,10 @@ int gpuos_dev_conv_desc(struct gpuos_dev* dev, const void* x, const void* w, voi
                         int32_t h, int32_t wd, int32_t c, int32_t k, int32_t r, int32_t s,
                         int32_t pad, int32_t stride, uint32_t flags, void** desc, int64_t* blocks,
                         int32_t* p, int32_t* q);
+
+/* Uniform [-1, 1) bf16 contents from a counter hash (tenant operand init),
+ * on the side stream.                                                     */
+int gpuos_dev_fill_bf16(struct gpuos_dev* dev, void* ptr, uint64_t count, uint64_t seed);
 
 /* Device memory helpers (stream-ordered on a side stream: safe while the
  * persistent dispatcher runs; never synchronise the whole device).        */

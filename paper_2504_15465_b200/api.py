@@ -45,7 +45,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask",
-    "gpuos_dev_gemm_desc", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc",
+    "gpuos_dev_gemm_desc", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -138,6 +138,7 @@ def library() -> C.CDLL:
         "gpuos_dev_conv_desc": (C.c_int, [P, P, P, P] + [C.c_int32] * 9 + [C.c_uint32, C.POINTER(P),
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                                           C.POINTER(C.c_int32)]),
+        "gpuos_dev_fill_bf16": (C.c_int, [P, P, C.c_uint64, C.c_uint64]),
         "gpuos_dev_gemv_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_uint32, C.c_int32,
                                           C.POINTER(P), C.POINTER(C.c_int64)]),
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
@@ -329,8 +330,8 @@ class Device:
     def gemv_desc(self, w: int, x: int, y: int, n: int, k: int, bf16_out: bool = False,
                   k_splits: int = 1) -> tuple[int, int]:
         """Descriptor for GPUOS_BODY_GEMV_BF16 (y = W . x, decode GEMV):
-        returns (device pointer for args[0], grid blocks). k_splits > 1:
-        y (fp32) must be zeroed first; blocks add partial sums."""
+        returns (device pointer for args[0], grid blocks). k_splits > 1
+        splits K; the last block of each row tile reduces the partials."""
         desc, blocks = C.c_void_p(), C.c_int64()
         self._check(self._lib.gpuos_dev_gemv_desc(self._h, w, x, y, n, k, 1 if bf16_out else 0,
                                                   k_splits, C.byref(desc), C.byref(blocks)))

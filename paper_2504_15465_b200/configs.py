@@ -1,0 +1,96 @@
+"""Live runs of BASELINE.json configs #2 and #3 on the persistent dispatcher
+(model kernel traces from models.py through the gpuos:: scheduler).
+
+For each config: warm-up runs (operand allocation and the predictor learn
+the kernels), then `reps` stacked runs, each tenant alone with the same
+scheduler, and a static partition (stealing and atomizer off). Reported per
+tenant: completed requests, p50 / p99 latency (nearest rank), p99 against
+alone, SLO attainment; for best-effort tenants throughput against static.
+
+    python -m paper_2504_15465_b200.configs [infer4|hybrid] [--horizon-ms 2000]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+from typing import Any
+
+from . import api, workloads
+
+
+def nearest_rank(xs: list[float], p: float) -> float | None:
+    s = sorted(xs)
+    if not s:
+        return None
+    return s[max(1, math.ceil(p / 100.0 * len(s))) - 1]
+
+
+def per_app(results: list[dict]) -> dict[str, dict]:
+    lat: dict[str, list[float]] = {}
+    done: dict[str, int] = {}
+    atoms: dict[str, int] = {}
+    for r in results:
+        for line in r["request_log"].splitlines():
+            j = json.loads(line)
+            if j["completed"]:
+                lat.setdefault(j["app"], []).append(j["latency_us"] / 1e3)
+                done[j["app"]] = done.get(j["app"], 0) + 1
+        for a, n in zip(r["report"]["apps"], r["atoms"]["per_app"]):
+            atoms[a["app_id"]] = atoms.get(a["app_id"], 0) + n
+    secs = sum(r["b200"]["run_wall_ns"] for r in results) * 1e-9
+    out = {}
+    for app in set(lat) | set(done) | set(atoms):
+        xs = lat.get(app, [])
+        out[app] = {"completed": done.get(app, 0), "per_s": done.get(app, 0) / secs if secs else None,
+                    "p50_ms": nearest_rank(xs, 50), "p99_ms": nearest_rank(xs, 99),
+                    "atoms": atoms.get(app, 0)}
+    return out
+
+
+def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0) -> dict[str, Any]:
+    cfg = workloads.infer4(horizon_ms) if name == "infer4" else workloads.hybrid(horizon_ms)
+    req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
+           "b200": {"chunk_cap": 256, "device": device}, "set": {"block_revocation": True}}
+    with api.Session(req) as s:
+        s.run()
+        s.run()  # warm: operands allocated, predictor and right-sizer state learned
+        live = [s.run() for _ in range(reps)]
+        alone = {}
+        for a in cfg["apps"]:
+            others = [b["id"] for b in cfg["apps"] if b["id"] != a["id"]]
+            solo = workloads.without_apps(cfg, *others)
+            alone[a["id"]] = per_app([s.run(scenario={"config": solo}) for _ in range(reps)])[a["id"]]
+        static = per_app([s.run(scenario={"config": workloads.variant(cfg, stealing=False, atomizer=False)})
+                          for _ in range(reps)])
+    stacked = per_app(live)
+    apps = {}
+    for a in cfg["apps"]:
+        i = a["id"]
+        st, al, sp = stacked.get(i, {}), alone.get(i, {}), static.get(i, {})
+        row = {"priority": a["priority"], "stacked": st, "alone": al, "static": sp}
+        if a["priority"] == "hp" and st.get("p99_ms") and al.get("p99_ms"):
+            row["p99_vs_alone"] = st["p99_ms"] / al["p99_ms"]
+            lat = [json.loads(x)["latency_us"] / 1e3 for r in live for x in r["request_log"].splitlines()
+                   if json.loads(x)["app"] == i and json.loads(x)["completed"]]
+            row["slo_attainment"] = sum(v <= a["slo_ms"] for v in lat) / len(lat) if lat else None
+        if a["priority"] == "be" and st.get("per_s") and sp.get("per_s"):
+            row["throughput_vs_static"] = st["per_s"] / sp["per_s"]
+        apps[i] = row
+    return {"config": name, "horizon_ms": horizon_ms, "reps": reps, "apps": apps,
+            "tpc_utilization": sum(r["report"]["tpc_utilization"] for r in live) / len(live)}
+
+
+def main(argv: list[str] | None = None) -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", choices=["infer4", "hybrid"])
+    ap.add_argument("--horizon-ms", type=float, default=2000.0)
+    ap.add_argument("--reps", type=int, default=2)
+    args = ap.parse_args(argv)
+    json.dump(run(args.config, args.horizon_ms, args.reps), sys.stdout, indent=1)
+    print()
+
+
+if __name__ == "__main__":
+    main()

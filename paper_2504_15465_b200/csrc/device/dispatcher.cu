@@ -93,6 +93,8 @@ struct DevCtl {
   unsigned pad1;
   unsigned long long t_enter, t_exit;  // first worker entry / last exit (globaltimer)
   unsigned long long t_first_block;    // earliest block start
+  unsigned tc_active;                  // TPCs whose tensor cores run a pair tile
+  unsigned idle_leaders;               // leaders waiting with nothing eligible
 };
 
 // 128-byte submit-ring entry: four 32-byte sectors, each = 7 data words +
@@ -709,6 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
             if (stale && lane == 0) sh.rc.key = 0ull;  // slot recycled: reload its fields
           }
           bool defer = false;  // peer: the winner is a 2-SM atom for the leader
+          bool nothing = false;  // nothing eligible on this TPC
           if (off < 0) {
             cur_key = 0ull;
             // Full arbitration: eligible = waiting slices, not paused, not
@@ -734,20 +737,29 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                          static_cast<unsigned>(cp >> 32) == 0u &&
                          static_cast<int>(k >> 56) >= floor_prio;
             }
-            key = warp_max_u64(eligible ? k : 0ull);
-            if (key == 0ull) spread_since = 0;  // nothing to defer any more
-            if (key != 0ull) {
+            // Candidates of this snapshot, best first: a claim lost to other
+            // workers (the atom ran out) moves on to the next candidate
+            // without reloading the list (32 small atoms drained by 148
+            // pairs otherwise cost ~12 rescans per block: 1397 vs 36 retries
+            // measured, tools/gemv_batch.py).
+            for (;;) {
+              key = warp_max_u64(eligible ? k : 0ull);
+              if (key == 0ull) {
+                spread_since = 0;  // nothing to defer any more
+                nothing = true;
+                break;
+              }
               // The winner's count and body travel with the arbitration.
               const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
               const unsigned wcount = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp), win);
-              f_bp = __shfl_sync(0xffffffffu, f_bp, win);
-              const bool pair = body_is_pair(static_cast<unsigned>(f_bp));
+              const unsigned long long wbp = __shfl_sync(0xffffffffu, f_bp, win);
+              const bool pair = body_is_pair(static_cast<unsigned>(wbp));
               // Leader and a pair tile: reserve the TPC's tensor cores. If
               // the other pair holds them, defer up to kSpreadNs so an idle
               // TPC takes the tile first; after that, claim anyway.
               // Deferring only helps while the atom runs fewer tiles than it
-              // has TPCs (some TPC of its set may be tensor-idle); in a full
-              // wave the second pair claims at once.
+              // has TPCs and some leader is idle; in a full wave the second
+              // pair claims at once.
               int reserved = 0;
               const unsigned long long wcw = __shfl_sync(0xffffffffu, f_cw, win);
               if (rank == 0 && pair && lane == 0) {
@@ -759,47 +771,54 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                   const unsigned in_flight = static_cast<unsigned>(wcw) - ld_relaxed_gpu(&wa->done);
                   const unsigned width = __popcll(ld_relaxed_gpu64(&wa->mask[0])) +
                                          __popcll(ld_relaxed_gpu64(&wa->mask[1]));
-                  if (in_flight >= width) reserved = 1;
+                  if (in_flight >= width || ld_relaxed_gpu(&p.ctl->idle_leaders) == 0u)
+                    reserved = 1;  // no idle leader would take it sooner
                 }
                 if (!reserved) atomicSub(p.tc_busy + tpc, 1u);
+                else if (before == 0u) atomicAdd(&p.ctl->tc_active, 1u);
               }
               reserved = __shfl_sync(0xffffffffu, reserved, 0);
               if (rank != 0 && pair) {
                 defer = true;  // no lower-priority bypass: wait for the leader
-              } else if (rank == 0 && pair && !reserved) {
+                break;
+              }
+              if (rank == 0 && pair && !reserved) {
                 defer = true;  // let an idle TPC take it first (kSpreadNs)
                 if (spread_since == 0) spread_since = gtimer();
-              } else {
-                spread_since = 0;
-                if (lane == 0)
-                  off = claim_block(p.atoms + (key & 0xffffffull), key, wcount, 1u, p.ctl, stale, got);
-                off = __shfl_sync(0xffffffffu, off, 0);
-                if (off < 0) {
-                  if (reserved && lane == 0) atomicSub(p.tc_busy + tpc, 1u);
-                  ++retries;  // lost that atom's last slices to other workers
-                  ver = ld_acquire_gpu(p.version + tpc);
-                  continue;
-                }
-                // Hand the winner's fields to lane 0 (no second round trip).
-                if (lane == 0 && reserved) tc_hold = true;
-                cur_count = wcount;
-                f_lo = __shfl_sync(0xffffffffu, f_lo, win);
+                break;
+              }
+              spread_since = 0;
+              if (lane == 0)
+                off = claim_block(p.atoms + (key & 0xffffffull), key, wcount, 1u, p.ctl, stale, got);
+              off = __shfl_sync(0xffffffffu, off, 0);
+              if (off < 0) {
+                if (reserved && lane == 0 && atomicSub(p.tc_busy + tpc, 1u) == 1u)
+                  atomicSub(&p.ctl->tc_active, 1u);
+                ++retries;  // lost that atom's last slices to other workers
+                if (eligible && k == key) eligible = false;
+                continue;
+              }
+              // Hand the winner's fields to lane 0 (no second round trip).
+              if (lane == 0 && reserved) tc_hold = true;
+              cur_count = wcount;
+              const unsigned long long wlo = __shfl_sync(0xffffffffu, f_lo, win);
+              unsigned long long wa5[5];
 #pragma unroll
-                for (int k2 = 0; k2 < 5; ++k2) f_a[k2] = __shfl_sync(0xffffffffu, f_a[k2], win);
-                if (lane == 0) {
-                  if (stale) {
-                    sh.rc.key = 0ull;  // recycled slot: fields reloaded below
-                  } else {
+              for (int k2 = 0; k2 < 5; ++k2) wa5[k2] = __shfl_sync(0xffffffffu, f_a[k2], win);
+              if (lane == 0) {
+                if (stale) {
+                  sh.rc.key = 0ull;  // recycled slot: fields reloaded below
+                } else {
 #pragma unroll
-                    for (int k2 = 0; k2 < 5; ++k2) sh.rc.cmd.args[k2] = f_a[k2];
-                    sh.rc.cmd.body = static_cast<unsigned>(f_bp);
-                    sh.rc.cmd.parts = static_cast<unsigned>(f_bp >> 32);
-                    sh.rc.lo = static_cast<long long>(f_lo);
-                    sh.rc.key = key;
-                    sh.rc.slot = static_cast<unsigned>(key & 0xffffffull);
-                  }
+                  for (int k2 = 0; k2 < 5; ++k2) sh.rc.cmd.args[k2] = wa5[k2];
+                  sh.rc.cmd.body = static_cast<unsigned>(wbp);
+                  sh.rc.cmd.parts = static_cast<unsigned>(wbp >> 32);
+                  sh.rc.lo = static_cast<long long>(wlo);
+                  sh.rc.key = key;
+                  sh.rc.slot = static_cast<unsigned>(key & 0xffffffull);
                 }
               }
+              break;
             }
           }
           if (off >= 0) {
@@ -837,7 +856,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
           // on the peer, for a pair tile. The control block is only consulted
           // when nothing changed, so a wake-up costs one version load.
           // Exit conditions are checked every 8 polls (a drained batch ends
-          // within a few microseconds of its last atom).
+          // within a few microseconds of its last atom). A leader with
+          // nothing eligible counts itself idle (pair-tile spreading).
+          const bool count_idle = rank == 0 && nothing && lane == 0;
+          if (count_idle) atomicAdd(&p.ctl->idle_leaders, 1u);
           bool changed = false, leave = false;
           for (int k2 = 0; k2 < 64; ++k2) {
             if (rank != 0 && mbar_test_cluster(&sh.join_full, joins & 1u)) {
@@ -863,6 +885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
             }
             __nanosleep(p.idle_sleep_ns);
           }
+          if (count_idle) atomicSub(&p.ctl->idle_leaders, 1u);
           if (changed) continue;
           if (leave) break;
         }
@@ -900,7 +923,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     run_body(sh.rc, tid, rank, pipe, gemm, gemv);  // pair tiles end with a cluster barrier
     if (go == kGoPair || go == kGoJoin) ++joins;
     if (tc_hold && tid == 0) {
-      atomicSub(p.tc_busy + tpc, 1u);
+      if (atomicSub(p.tc_busy + tpc, 1u) == 1u) atomicSub(&p.ctl->tc_active, 1u);
       tc_hold = false;
     }
     __syncthreads();
@@ -923,6 +946,19 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
 }
 
 __global__ void k_gtimer(unsigned long long* out) { *out = gtimer(); }
+
+// Uniform [-1, 1) bf16 fill from a counter hash (tenant operand init).
+__global__ void k_fill_bf16(unsigned short* p, unsigned long long n, unsigned long long seed) {
+  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
+    unsigned long long x = seed + i * 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    const float u = static_cast<float>(x >> 40) * (2.0f / 16777216.0f) - 1.0f;
+    const __nv_bfloat16 b = __float2bfloat16_rn(u);
+    p[i] = *reinterpret_cast<const unsigned short*>(&b);
+  }
+}
 
 }  // namespace gpuos_dev_impl
 
@@ -1827,16 +1863,22 @@ int gpuos_dev_gemv_desc(gpuos_dev* d, const void* w, const void* x, void* y, int
   h.k = static_cast<unsigned>(k);
   const unsigned nk = static_cast<unsigned>((k + kGemmBK - 1) / kGemmBK);
   const unsigned splits = std::clamp<unsigned>(k_splits <= 0 ? 1u : static_cast<unsigned>(k_splits), 1u, nk);
-  if (splits > 1 && (flags & GPUOS_GEMV_OUT_BF16))
-    return fail(GPUOS_E_CONFIG, "split-K GEMV accumulates into fp32 y");
   h.row_tiles = static_cast<unsigned>((n + kGemvTile - 1) / kGemvTile);
   h.k_slices_per_block = (nk + splits - 1) / splits;
-  const unsigned used_splits = (nk + h.k_slices_per_block - 1) / h.k_slices_per_block;
-  h.blocks = h.row_tiles * used_splits;
-  h.flags = (flags & kGemvOutBf16) | (splits > 1 ? kGemvAccumulate : 0u);
+  h.splits = (nk + h.k_slices_per_block - 1) / h.k_slices_per_block;
+  h.blocks = h.row_tiles * h.splits;
+  h.flags = flags & kGemvOutBf16;
+  // One allocation: descriptor, then the split counters (zeroed), then the
+  // partial sums; gpuos_dev_free(desc) releases all of it.
+  const size_t counters_off = sizeof(GemvDesc);
+  const size_t partial_off = (counters_off + 4ull * h.row_tiles + 255) & ~size_t{255};
+  const size_t total = partial_off + (h.splits > 1 ? 4ull * h.splits * static_cast<size_t>(n) : 0);
   void* p = nullptr;
   CUDA_TRY(cudaSetDevice(d->device));
-  CUDA_TRY(cudaMallocAsync(&p, sizeof(GemvDesc), d->s_side));
+  CUDA_TRY(cudaMallocAsync(&p, total, d->s_side));
+  h.arrivals = reinterpret_cast<unsigned*>(static_cast<char*>(p) + counters_off);
+  h.partial = h.splits > 1 ? reinterpret_cast<float*>(static_cast<char*>(p) + partial_off) : nullptr;
+  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(p) + counters_off, 0, 4ull * h.row_tiles, d->s_side));
   CUDA_TRY(cudaMemcpyAsync(p, &h, sizeof(GemvDesc), cudaMemcpyHostToDevice, d->s_side));
   CUDA_TRY(cudaStreamSynchronize(d->s_side));
   *desc = p;
@@ -1916,6 +1958,26 @@ int gpuos_dev_conv_desc(gpuos_dev* d, const void* x, const void* w, void* y, int
   if (blocks) *blocks = static_cast<int64_t>(hd.pair_tiles) * hd.k_tiles;
   if (p_out) *p_out = P;
   if (q_out) *q_out = Q;
+  return GPUOS_OK;
+}
+
+int gpuos_dev_fill_bf16(gpuos_dev* d, void* ptr, uint64_t count, uint64_t seed) {
+  if (!d || (!ptr && count)) return fail(GPUOS_E_CONFIG, "null argument");
+  if (count == 0) return GPUOS_OK;
+  CUDA_TRY(cudaSetDevice(d->device));
+  // Tenants register kernels (and so initialise operands) while the
+  // persistent dispatcher runs: the fill CTAs must fit beside the workers,
+  // which needs the same shared-memory carveout (csrc/tools/residency_probe.cu).
+  static bool carveout_set = false;
+  if (!carveout_set) {
+    CUDA_TRY(cudaFuncSetAttribute(k_fill_bf16, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    carveout_set = true;
+  }
+  const unsigned long long blocks = std::min<unsigned long long>((count + 255) / 256, 4096);
+  k_fill_bf16<<<static_cast<unsigned>(blocks), 256, 0, d->s_side>>>(static_cast<unsigned short*>(ptr),
+                                                                    count, seed);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
   return GPUOS_OK;
 }
 

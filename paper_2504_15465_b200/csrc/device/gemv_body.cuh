@@ -16,8 +16,9 @@
 // Algorithmic bytes per block: 256 K 2 (W) + K 2 (x) + 256 x 4 or 2 (y).
 //
 // Decode shapes have few 256-row tiles (N = 4096: 16), so the descriptor may
-// split K: block b = (row tile b % row_tiles, K split b / row_tiles), each
-// adding its partial sums into a zeroed fp32 y with RED.ADD.
+// split K: block b = (row tile b % row_tiles, K split b / row_tiles); each
+// block stores its partial sums, and the row tile's last block (a counter
+// that resets itself) adds them in split order and writes y.
 //
 // args: [0] descriptor from gpuos_dev_gemv_desc().
 #pragma once
@@ -38,15 +39,18 @@ constexpr unsigned kGemvXBytes = kGemvXRows * kGemmBK * 2;   // 2 KiB
 constexpr unsigned kGemvStageBytes = kGemvWBytes + kGemvXBytes;
 constexpr unsigned kGemvMaxStages = 8;
 constexpr unsigned kGemvOutBf16 = 1u;
-constexpr unsigned kGemvAccumulate = 2u;  // y += W . x (split-K partial sums)
 
 struct alignas(128) GemvDesc {
   CUtensorMap w;                 // W [N, K] bf16: box {64, 128}, SWIZZLE_128B
   CUtensorMap x;                 // x [1, K] bf16: box {64, 16}, SWIZZLE_128B (rows >= 1 zero)
   unsigned long long y;
-  unsigned n, k, blocks, flags;  // flags: kGemvOutBf16, kGemvAccumulate
+  unsigned n, k, blocks, flags;  // flags: kGemvOutBf16
   unsigned row_tiles;            // ceil(N / 256)
   unsigned k_slices_per_block;   // 64-wide K slices per block (split-K)
+  unsigned splits;               // K splits (1: no split)
+  unsigned pad0;
+  float* partial;                // [splits][N] fp32 partial sums (split-K)
+  unsigned* arrivals;            // [row_tiles] self-resetting split counters
 };
 
 struct GemvPipe {
@@ -147,14 +151,15 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
   mbar_wait_bounded(G.accum, G.accum_used & 1u);
   tc_fence_after();
   const int warp = tid >> 5, lane = tid & 31;
+  const bool bf16_y = (D->flags & kGemvOutBf16) != 0;
   if (warp < 4) {
     const float v = __uint_as_float(tmem_ld1(G.tmem + ((static_cast<unsigned>(warp) * 32u) << 16)));
     const unsigned row = blk * kGemvTile + rank * kGemmHalf + static_cast<unsigned>(warp) * 32u +
                          static_cast<unsigned>(lane);
     if (row < D->n) {
-      if (D->flags & kGemvAccumulate)
-        atomicAdd(reinterpret_cast<float*>(D->y) + row, v);  // RED.ADD.F32
-      else if (D->flags & kGemvOutBf16)
+      if (D->splits > 1)
+        D->partial[static_cast<size_t>(split) * D->n + row] = v;
+      else if (bf16_y)
         reinterpret_cast<__nv_bfloat16*>(D->y)[row] = __float2bfloat16_rn(v);
       else
         reinterpret_cast<float*>(D->y)[row] = v;
@@ -164,6 +169,36 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
   G.kb_used = g0 + nk;
   G.accum_used += 1;
   cluster_sync_all();  // both halves written, both TMEMs read
+  if (D->splits > 1) {
+    // Split-K: the last block of the row tile (self-resetting arrival
+    // counter) sums the partials in split order -- deterministic, no
+    // zeroed output or float atomics -- and writes y.
+    __shared__ int last_split;
+    if (rank == 0) {
+      if (tid == 0) {
+        __threadfence();  // this tile's partials (both CTAs, via the cluster barrier)
+        const unsigned before = atomicAdd(D->arrivals + blk, 1u);
+        last_split = before == D->splits - 1;
+        if (last_split) {
+          __threadfence();
+          D->arrivals[blk] = 0u;  // ready for the kernel's next run
+        }
+      }
+      __syncthreads();
+      if (last_split) {
+        const unsigned row = blk * kGemvTile + static_cast<unsigned>(tid);
+        if (row < D->n) {
+          float acc = 0.f;
+          for (unsigned sp = 0; sp < D->splits; ++sp)
+            acc += __ldcg(D->partial + static_cast<size_t>(sp) * D->n + row);
+          if (bf16_y)
+            reinterpret_cast<__nv_bfloat16*>(D->y)[row] = __float2bfloat16_rn(acc);
+          else
+            reinterpret_cast<float*>(D->y)[row] = acc;
+        }
+      }
+    }
+  }
 }
 
 }  // namespace gpuos_dev_impl

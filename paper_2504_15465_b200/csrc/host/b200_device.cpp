@@ -7,6 +7,7 @@
 #include <thread>
 
 #include "gpuos/b200.hpp"
+#include "gpuos/tenants.hpp"
 #include "gpuos_dev.h"
 
 namespace gpuos {
@@ -72,6 +73,10 @@ B200Runtime::~B200Runtime() {
     gpuos_dev_host_free(dev_, w.host_src);
   }
   for (auto* p : trace_chunks_) gpuos_dev_free(dev_, p);
+  for (auto& [key, t] : tensors_) {
+    gpuos_dev_free(dev_, t.desc);
+    for (void* p : t.bufs) gpuos_dev_free(dev_, p);
+  }
   gpuos_dev_close(dev_);
 }
 
@@ -106,6 +111,62 @@ B200Runtime::Workspace& B200Runtime::workspace(std::uint32_t id, std::uint64_t w
   return w;
 }
 
+// Tensor-core tenant kernels: operands random-initialised on the device
+// (uniform in [-1, 1), bf16) and a descriptor, per (workspace, shape). Each
+// workspace id is a distinct set of weights, so model traces that give
+// every layer its own id stream their real weight bytes from HBM.
+const B200Runtime::TensorBody& B200Runtime::tensor_body(const BodyRef& b) {
+  std::string key = std::to_string(static_cast<int>(b.kind)) + "/" + std::to_string(b.workspace);
+  for (int i = 0; i < BodyRef::kParams; ++i) key += "/" + std::to_string(b.param(i));
+  auto it = tensors_.find(key);
+  if (it != tensors_.end()) return it->second;
+  TensorBody t;
+  const std::uint64_t seed = mix64(std::hash<std::string>{}(key));
+  auto tensor = [&](std::uint64_t elems, bool fill) {
+    void* p = nullptr;
+    check(gpuos_dev_alloc(dev_, std::max<std::uint64_t>(elems, 8) * 2, &p), "tensor alloc");
+    if (fill) check(gpuos_dev_fill_bf16(dev_, p, elems, seed + t.bufs.size()), "tensor init");
+    t.bufs.push_back(p);
+    return p;
+  };
+  if (b.kind == BodyKind::GemmBf16) {
+    const std::int64_t M = b.p0, N = b.p1, K = b.p2;
+    if (M <= 0 || N <= 0 || K <= 0) throw ConfigError("gemm_bf16 needs p = [M, N, K]");
+    void* A = tensor(static_cast<std::uint64_t>(M) * K, true);
+    void* B = tensor(static_cast<std::uint64_t>(N) * K, true);
+    void* C = tensor(static_cast<std::uint64_t>(M) * N, false);
+    int32_t tm = 0, tn = 0;
+    check(gpuos_dev_gemm_desc(dev_, A, B, C, M, N, K, N, GPUOS_GEMM_OUT_BF16, &t.desc, &t.blocks, &tm, &tn),
+          "gemm descriptor");
+  } else if (b.kind == BodyKind::GemvBf16) {
+    const std::int64_t N = b.p0, K = b.p1, splits = std::max<std::int64_t>(1, b.p2);
+    if (N <= 0 || K <= 0) throw ConfigError("gemv_bf16 needs p = [N, K, k_splits]");
+    void* W = tensor(static_cast<std::uint64_t>(N) * K, true);
+    void* X = tensor(static_cast<std::uint64_t>(K), true);
+    void* Y = tensor(static_cast<std::uint64_t>(N), false);
+    check(gpuos_dev_gemv_desc(dev_, W, X, Y, N, K, GPUOS_GEMV_OUT_BF16, static_cast<int32_t>(splits),
+                              &t.desc, &t.blocks),
+          "gemv descriptor");
+  } else {
+    const std::int64_t n = b.p0, h = b.p1, w = b.p2, c = b.param(3), k = b.param(4), r = b.param(5),
+                       sd = b.param(6), pad = b.param(7), st = std::max<std::int64_t>(1, b.param(8));
+    if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || k <= 0 || r <= 0 || sd <= 0)
+      throw ConfigError("conv_bf16 needs p = [n, h, w, c, k, r, s, pad, stride]");
+    const std::int64_t cb = (c + 63) / 64 * 64;
+    const std::int64_t P = (h + 2 * pad - r) / st + 1, Q = (w + 2 * pad - sd) / st + 1;
+    void* X = tensor(static_cast<std::uint64_t>(n) * h * w * c, true);
+    void* Wt = tensor(static_cast<std::uint64_t>(k) * r * sd * cb, true);
+    void* Y = tensor(static_cast<std::uint64_t>(std::max<std::int64_t>(0, n * P * Q * k)), false);
+    int32_t po = 0, qo = 0;
+    check(gpuos_dev_conv_desc(dev_, X, Wt, Y, static_cast<int32_t>(n), static_cast<int32_t>(h),
+                              static_cast<int32_t>(w), static_cast<int32_t>(c), static_cast<int32_t>(k),
+                              static_cast<int32_t>(r), static_cast<int32_t>(sd), static_cast<int32_t>(pad),
+                              static_cast<int32_t>(st), GPUOS_CONV_OUT_BF16, &t.desc, &t.blocks, &po, &qo),
+          "conv descriptor");
+  }
+  return tensors_.emplace(key, t).first->second;
+}
+
 void B200Runtime::ensure_trace(KernelId kid, long blocks) {
   if (trace_of_.size() <= kid) trace_of_.resize(kid + 1, nullptr);
   if (trace_of_[kid]) return;
@@ -130,6 +191,21 @@ void B200Runtime::ensure_trace(KernelId kid, long blocks) {
 
 B200Runtime::Resolved B200Runtime::resolve(KernelId kid, const SimKernelSpec& spec) {
   if (has_resolved_.size() > kid && has_resolved_[kid]) return resolved_[kid];
+  Resolved r = resolve_body(spec);
+  if (opt_.trace_blocks) {
+    ensure_trace(kid, spec.total_blocks * static_cast<long>(r.parts));
+    r.trace = trace_of_[kid];
+  }
+  if (resolved_.size() <= kid) {
+    resolved_.resize(kid + 1);
+    has_resolved_.resize(kid + 1, 0);
+  }
+  resolved_[kid] = r;
+  has_resolved_[kid] = 1;
+  return r;
+}
+
+B200Runtime::Resolved B200Runtime::resolve_body(const SimKernelSpec& spec) {
   Resolved r{};
   BodyRef b = spec.body;
   if (b.kind == BodyKind::None) {
@@ -168,27 +244,28 @@ B200Runtime::Resolved B200Runtime::resolve(KernelId kid, const SimKernelSpec& sp
       r.args[0] = static_cast<std::uint64_t>(b.p0);
       break;
     case BodyKind::GemmBf16:
-      throw ConfigError("gemm_bf16 body is not available in this build");
+    case BodyKind::GemvBf16:
+    case BodyKind::ConvBf16: {
+      const TensorBody& t = tensor_body(b);
+      if (spec.total_blocks != t.blocks)
+        throw ConfigError(std::string(body_kind_name(b.kind)) + " kernel of this shape has " +
+                          std::to_string(t.blocks) + " blocks, the descriptor says " +
+                          std::to_string(spec.total_blocks));
+      r.body = static_cast<std::uint32_t>(b.kind);
+      r.args[0] = reinterpret_cast<std::uint64_t>(t.desc);
+      break;
+    }
     case BodyKind::None:
       break;
   }
   r.parts = 1;
-  if (opt_.quantum_ns > 0) {
+  // Preemption slices apply to CUDA-core bodies; a tensor-core tile runs whole.
+  if (opt_.quantum_ns > 0 && (r.body == GPUOS_BODY_STREAM || r.body == GPUOS_BODY_SPIN)) {
     const std::int64_t block_ns = b.kind == BodyKind::Spin ? b.p0 : spec.block_duration_at_fmax;
     std::int64_t parts = (block_ns + opt_.quantum_ns - 1) / opt_.quantum_ns;
     if (r.body == GPUOS_BODY_STREAM) parts = std::min<std::int64_t>(parts, r.words / 4);
     r.parts = static_cast<std::uint32_t>(std::clamp<std::int64_t>(parts, 1, 4096));
   }
-  if (opt_.trace_blocks) {
-    ensure_trace(kid, spec.total_blocks * static_cast<long>(r.parts));
-    r.trace = trace_of_[kid];
-  }
-  if (resolved_.size() <= kid) {
-    resolved_.resize(kid + 1);
-    has_resolved_.resize(kid + 1, 0);
-  }
-  resolved_[kid] = r;
-  has_resolved_[kid] = 1;
   return r;
 }
 

@@ -19,6 +19,27 @@ using namespace gpuos;
 
 namespace {
 
+// Allocate every tenant kernel's operands before the dispatcher starts (no
+// allocation or initialisation kernel may run beside the resident workers).
+void prepare_bodies(B200Runtime& rt, const ScenarioConfig& cfg) {
+  auto prep = [&](const RequestTemplate& tmpl) {
+    for (const KernelRecord& k : tmpl.kernels) {
+      SimKernelSpec spec;
+      spec.total_blocks = k.total_blocks();
+      spec.block_duration_at_fmax = k.block_duration_at_fmax;
+      spec.sensitivity_s = k.sensitivity_s;
+      spec.occupancy_per_tpc = k.occupancy_per_tpc;
+      spec.body = k.body;
+      rt.prepare(spec);
+    }
+  };
+  for (const AppWorkload& w : resolve_workloads(cfg)) {
+    prep(w.request);
+    for (const RequestTemplate& t : w.per_request) prep(t);
+  }
+}
+
+
 thread_local std::string g_error;
 
 char* dup_text(const std::string& s) {
@@ -186,6 +207,7 @@ std::string run_session(gpuos_session* s, const json& overrides) {
                          .count();
   } else if (s->backend == "mirror") {
     MirrorDevice dev(cfg.topo, cfg.freq, cfg.power, b200_options(merged.value("b200", json::object())));
+    prepare_bodies(dev.runtime(), cfg);
     res = run_scenario_on(dev, cfg, hooks);
     out["verify"] = verify_json(dev.verify());
     out["gpu_atoms"] = dev.gpu_atoms();
@@ -197,6 +219,7 @@ std::string run_session(gpuos_session* s, const json& overrides) {
       s->b200 = std::make_unique<B200Device>(cfg.topo, cfg.freq, opt);
     B200Device& dev = *s->b200;
     dev.reset_run();
+    prepare_bodies(dev.runtime(), cfg);
     std::uint64_t h2d = 0, d2h = 0;
     const auto t0 = std::chrono::steady_clock::now();
     // End-to-end leg: every tenant input is copied from host memory before

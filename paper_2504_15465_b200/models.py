@@ -1,0 +1,220 @@
+"""Random-init kernel traces of the BASELINE.json model configs, as scenario
+kernels (the reference's kernel records -- blocks, block_us, s, occ,
+sim.cpp:86-156 / workload.hpp:38-44 -- plus the B200 "body" extension that
+the reference ignores). Every kernel is one tenant launch; its blocks are
+the body's real grid:
+
+  conv_bf16  NHWC implicit GEMM, 256 pixels x 256 channels per block
+  gemm_bf16  256 x 256 output tile per block
+  gemv_bf16  256 rows of W per block (x split-K)
+  stream     HBM-bound elementwise (norms, activations, residuals, pooling,
+             softmax, attention over the KV cache, optimizer), sized by the
+             tensor bytes it moves
+
+Each layer has its own workspace id, so each layer's weights are distinct
+buffers (decode streams 15 GB of Llama-3-8B weights per token, as the real
+model does). block_us / s are first estimates for the reference's timing
+model (replay); the live scheduler's predictor learns measured latencies.
+
+  resnet50_infer(batch)   ResNet-50 forward at 224 x 224   (configs #2, #3)
+  bert_base_infer(batch)  BERT-base, seq 128               (config #2)
+  llama3_8b_decode(ctx)   Llama-3-8B, one token at batch 1 (config #3)
+  resnet50_train(batch)   ResNet-50 forward + backward + SGD (config #3)
+"""
+from __future__ import annotations
+
+import math
+
+TPC_TFLOPS = 1650.0 / 74      # measured bf16 peak per TPC
+TPC_GBS = 6550.0 / 74         # measured HBM bandwidth per TPC
+STREAM_WORDS = 16384          # u32 words per STREAM block (64 KiB in, 64 KiB out)
+
+
+def _pow2(v: int) -> int:
+    p = 1
+    while p < v:
+        p <<= 1
+    return p
+
+
+def conv_blocks(n, h, w, c, k, r, s, pad, stride) -> tuple[int, int, int]:
+    """Grid of gpuos_dev_conv_desc (conv_body.cuh): (blocks, P, Q)."""
+    P = (h + 2 * pad - r) // stride + 1
+    Q = (w + 2 * pad - s) // stride + 1
+    wb = min(128, _pow2(Q))
+    hb = min(128 // wb, _pow2(P))
+    nb = 128 // (wb * hb)
+    patches = math.ceil(Q / wb) * math.ceil(P / hb) * math.ceil(n / nb)
+    return math.ceil(patches / 2) * math.ceil(k / 256), P, Q
+
+
+def gemm_blocks(m, n, k) -> int:
+    return math.ceil(m / 256) * math.ceil(n / 256)
+
+
+def gemv_blocks(n, k, splits) -> int:
+    nk = math.ceil(k / 64)
+    per = math.ceil(nk / max(1, splits))
+    return math.ceil(n / 256) * math.ceil(nk / per)
+
+
+class Builder:
+    """Accumulates kernels; `ws` hands out a fresh workspace id per layer."""
+
+    def __init__(self, ws_base: int):
+        self.kernels: list[dict] = []
+        self.ws = ws_base
+        self.stream_ws = ws_base + 99_000  # one buffer pair for all elementwise kernels
+
+    def _next(self) -> int:
+        self.ws += 1
+        return self.ws
+
+    def conv(self, n, h, w, c, k, r, s, pad, stride) -> tuple[int, int]:
+        blocks, P, Q = conv_blocks(n, h, w, c, k, r, s, pad, stride)
+        cb = math.ceil(c / 64) * 64
+        tile_flops = 2.0 * 256 * 256 * r * s * cb
+        self.kernels.append({
+            "blocks": blocks, "block_us": round(tile_flops / (TPC_TFLOPS * 1e6), 3), "s": 0.9, "occ": 2,
+            "body": {"kind": "conv_bf16", "ws": self._next(), "p": [n, h, w, c, k, r, s, pad, stride]}})
+        return P, Q
+
+    def gemm(self, m, n, k) -> None:
+        self.kernels.append({
+            "blocks": gemm_blocks(m, n, k),
+            "block_us": round(2.0 * 256 * 256 * k / (TPC_TFLOPS * 1e6), 3), "s": 0.9, "occ": 2,
+            "body": {"kind": "gemm_bf16", "ws": self._next(), "p": [m, n, k]}})
+
+    def gemv(self, n, k, splits=1) -> None:
+        blocks = gemv_blocks(n, k, splits)
+        per_block = n * k * 2 / blocks
+        self.kernels.append({
+            "blocks": blocks, "block_us": round(per_block / (TPC_GBS * 1e3), 3), "s": 0.2, "occ": 2,
+            "body": {"kind": "gemv_bf16", "ws": self._next(), "p": [n, k, splits]}})
+
+    def stream(self, nbytes) -> None:
+        """Elementwise kernel moving `nbytes` (read + written)."""
+        words = STREAM_WORDS
+        blocks = max(1, math.ceil(nbytes / (8 * words)))
+        self.kernels.append({
+            "blocks": blocks, "block_us": round(8 * words / (TPC_GBS / 4 * 1e3), 3), "s": 0.2, "occ": 4,
+            "body": {"kind": "stream", "ws": self.stream_ws, "p": [words, 0, 256]}})
+
+
+RESNET_STAGES = [(3, 64, 256, 1), (4, 128, 512, 2), (6, 256, 1024, 2), (3, 512, 2048, 2)]
+
+
+def _resnet_forward(b: Builder, n: int) -> list[tuple]:
+    """Forward pass; returns the conv shapes (for the backward pass)."""
+    convs = []
+
+    def conv(*a):
+        convs.append(a)
+        return b.conv(*a)
+
+    h = conv(n, 224, 224, 8, 64, 7, 7, 3, 2)[0]         # stem, 3 channels padded to 8
+    b.stream(n * 112 * 112 * 64 * 2 * 2)                # BN + ReLU
+    b.stream(n * (112 * 112 + 56 * 56) * 64 * 2)         # max pool 3x3/2
+    h, c = 56, 64
+    for blocks, mid, out, stride in RESNET_STAGES:
+        for i in range(blocks):
+            st = stride if i == 0 else 1
+            conv(n, h, h, c, mid, 1, 1, 0, 1)
+            ho = conv(n, h, h, mid, mid, 3, 3, 1, st)[0]
+            conv(n, ho, ho, mid, out, 1, 1, 0, 1)
+            if i == 0:
+                conv(n, h, h, c, out, 1, 1, 0, st)       # downsample
+            b.stream(n * ho * ho * out * 2 * 3)          # residual add + ReLU
+            h, c = ho, out
+    b.stream(n * 7 * 7 * 2048 * 2)                       # global average pool
+    return convs
+
+
+def resnet50_infer(batch: int = 1, ws_base: int = 0) -> list[dict]:
+    b = Builder(ws_base)
+    _resnet_forward(b, batch)
+    if batch == 1:
+        b.gemv(1000, 2048)                               # classifier
+    else:
+        b.gemm(batch, 1000, 2048)
+    return b.kernels
+
+
+def resnet50_train(batch: int = 64, ws_base: int = 0) -> list[dict]:
+    """Forward, backward (for every conv: data-gradient conv of the same
+    FLOPs and weight-gradient GEMM [k, r s c] reduced over n p q), ReLU/BN
+    backward elementwise, and an SGD-momentum update over 25.6 M fp32 params."""
+    b = Builder(ws_base)
+    convs = _resnet_forward(b, batch)
+    b.gemm(batch, 1000, 2048)
+    b.gemm(1000, 2048, batch if batch % 8 == 0 else 8)   # classifier weight gradient
+    for (n, h, w, c, k, r, s, pad, stride) in reversed(convs):
+        P = (h + 2 * pad - r) // stride + 1
+        if c >= 64:                                      # no data gradient for the stem input
+            b.conv(n, P, P, k, c, r, s, (r - 1) // 2, 1)  # dgrad (same FLOPs as forward)
+        b.gemm(k, r * s * math.ceil(c / 64) * 64, n * P * P)  # wgrad
+        b.stream(n * P * P * k * 2 * 3)                  # BN / ReLU backward
+    b.stream(25_600_000 * 4 * 5)                         # SGD with momentum: w, g, m read; w, m written
+    return b.kernels
+
+
+def bert_base_infer(batch: int = 8, seq: int = 128, ws_base: int = 0) -> list[dict]:
+    b = Builder(ws_base)
+    t = batch * seq
+    d, heads, ffn = 768, 12, 3072
+    b.stream(t * d * 2 * 3)                              # embeddings + LayerNorm
+    for _ in range(12):
+        b.gemm(t, 3 * d, d)                              # QKV projection
+        b.gemm(batch * heads * seq, seq, d // heads)     # scores (per-head GEMMs as one of equal FLOPs)
+        b.stream(batch * heads * seq * seq * 2 * 2)      # softmax
+        b.gemm(batch * heads * seq, d // heads, seq)     # context
+        b.gemm(t, d, d)                                  # output projection
+        b.stream(t * d * 2 * 3)                          # residual + LayerNorm
+        b.gemm(t, ffn, d)                                # FFN up
+        b.stream(t * ffn * 2 * 2)                        # GELU
+        b.gemm(t, d, ffn)                                # FFN down
+        b.stream(t * d * 2 * 3)                          # residual + LayerNorm
+    return b.kernels
+
+
+def llama3_8b_decode(context: int = 1024, ws_base: int = 0) -> list[dict]:
+    """One token: 32 layers of RMSNorm, QKV / O / gate-up / down GEMVs (split-K
+    so every TPC streams weights), attention over a `context`-long KV cache
+    (8 KV heads x 128), SiLU-mul; then the final norm and the LM head."""
+    b = Builder(ws_base)
+    d, kv, ffn, vocab = 4096, 1024, 14336, 128256
+    for _ in range(32):
+        b.stream(d * 2 * 2)                              # RMSNorm
+        b.gemv(d + 2 * kv, d, 8)                         # QKV
+        b.stream(context * kv * 2 * 2 + d * 2 * 2)       # RoPE + attention over K and V
+        b.gemv(d, d, 8)                                  # output projection
+        b.stream(d * 2 * 3)                              # residual + RMSNorm
+        b.gemv(2 * ffn, d, 2)                            # gate + up
+        b.stream(2 * ffn * 2 + ffn * 2)                  # SiLU(gate) * up
+        b.gemv(d, ffn, 16)                               # down projection
+    b.stream(d * 2 * 2)                                  # final norm
+    b.gemv(vocab, d, 1)                                  # LM head
+    return b.kernels
+
+
+def summary(kernels: list[dict]) -> dict:
+    """Kernel count, blocks and algorithmic work of a trace."""
+    flops = nbytes = 0.0
+    for k in kernels:
+        body, p = k["body"], k["body"]["p"]
+        if body["kind"] == "gemm_bf16":
+            flops += 2.0 * p[0] * p[1] * p[2]
+            nbytes += 2.0 * (p[0] * p[2] + p[1] * p[2] + p[0] * p[1])
+        elif body["kind"] == "conv_bf16":
+            n, h, w, c, kk, r, s, pad, st = p
+            P = (h + 2 * pad - r) // st + 1
+            Q = (w + 2 * pad - s) // st + 1
+            flops += 2.0 * n * P * Q * kk * r * s * c
+            nbytes += 2.0 * (n * h * w * c + kk * r * s * c + n * P * Q * kk)
+        elif body["kind"] == "gemv_bf16":
+            flops += 2.0 * p[0] * p[1]
+            nbytes += 2.0 * (p[0] * p[1] + p[1] + p[0])
+        else:
+            nbytes += 8.0 * p[0] * k["blocks"]
+    return {"kernels": len(kernels), "blocks": sum(k["blocks"] for k in kernels),
+            "gflop": flops / 1e9, "gbytes": nbytes / 1e9}

@@ -98,7 +98,7 @@ def default_bodies(dev: api.Device, torch, keep: list) -> list[Body]:
     desc, blocks = dev.gemv_desc(w.data_ptr(), x.data_ptr(), y.data_ptr(), n, k, k_splits=4)
     keep.append(("desc", desc))
     out.append(Body(f"gemv_bf16 {n}x{k} (split-K 4)", api.GPUOS_BODY_GEMV_BF16, [desc], blocks, 1,
-                    f"{n * k * 2 / 1e6:.0f} MB of W", reset=lambda: y.zero_()))
+                    f"{n * k * 2 / 1e6:.0f} MB of W"))
     words = 256 * 1024  # 1 MiB per block in, 1 MiB out
     nblocks = 512
     src = torch.randint(-2**31, 2**31 - 1, (nblocks * words,), dtype=torch.int32, device="cuda")

@@ -95,3 +95,51 @@ def tenant_set(rank: int, time_scale: float = 10.0, horizon_ms: float = 2000.0,
                       "default_unknown_us": 10_000.0 / s, "time_slice_window_us": 2000.0 / s},
         "apps": apps,
     }
+
+
+def infer4(horizon_ms: float = 2000.0, rps: tuple = (120.0, 120.0, 40.0, 40.0),
+           slo_ms: tuple = (10.0, 10.0, 25.0, 25.0), tpcs: int = 74) -> dict:
+    """BASELINE config #2, inference stacking: four latency-critical tenants
+    on one B200 -- two ResNet-50 at batch 1 and two BERT-base at batch 8
+    (random-init kernel traces, models.py) -- with Poisson arrivals, equal
+    quotas and TPC stealing (atomizer on, right-sizer off)."""
+    from . import models
+
+    traces = [models.resnet50_infer(1, ws_base=0), models.resnet50_infer(1, ws_base=10_000),
+              models.bert_base_infer(8, ws_base=20_000), models.bert_base_infer(8, ws_base=30_000)]
+    names = ["rn50_a", "rn50_b", "bert_a", "bert_b"]
+    quota = tpcs // 4
+    apps = [{"id": nm, "priority": "hp", "quota": quota, "slo_ms": slo_ms[i],
+             "arrival": {"poisson_rps": rps[i], "seed_offset": i}, "kernels": traces[i]}
+            for i, nm in enumerate(names)]
+    return {
+        "name": "infer4-b200", "device": {"gpc_count": 2, "tpcs_per_gpc": tpcs // 2},
+        "policy": "full_system", "horizon_ms": horizon_ms, "seed": 2,
+        "scheduler": {"rightsizer": False, "dvfs": False, "stealing": True, "atomizer": True,
+                      "atom_duration_us": 1000.0, "steal_horizon_us": 0.0},
+        "apps": apps,
+    }
+
+
+def hybrid(horizon_ms: float = 2000.0, tokens_per_s: float = 60.0, slo_ms: float = 25.0,
+           train_batch: int = 64, tpcs: int = 74) -> dict:
+    """BASELINE config #3, hybrid stacking: Llama-3-8B bf16 decode at batch 1
+    (latency-critical, Poisson token requests, one request = one token's 258
+    kernels over 15 GB of weights) with ResNet-50 training (best-effort,
+    closed loop, forward + backward + SGD) on one B200; mid-kernel
+    reallocation through TPC stealing, atomization and block revocation."""
+    from . import models
+
+    return {
+        "name": "hybrid-b200", "device": {"gpc_count": 2, "tpcs_per_gpc": tpcs // 2},
+        "policy": "full_system", "horizon_ms": horizon_ms, "seed": 3,
+        "scheduler": {"rightsizer": False, "dvfs": False, "stealing": True, "atomizer": True,
+                      "atom_duration_us": 1000.0, "steal_horizon_us": 0.0},
+        "apps": [
+            {"id": "llama_decode", "priority": "hp", "quota": tpcs // 2, "slo_ms": slo_ms,
+             "arrival": {"poisson_rps": tokens_per_s, "seed_offset": 0},
+             "kernels": models.llama3_8b_decode(1024, ws_base=0)},
+            {"id": "rn50_train", "priority": "be", "quota": tpcs - tpcs // 2,
+             "arrival": "closed_loop", "kernels": models.resnet50_train(train_batch, ws_base=100_000)},
+        ],
+    }

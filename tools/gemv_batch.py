@@ -24,8 +24,6 @@ with api.Device() as dev:
     descs = [api.Device.desc(i * blocks // n_atoms, (i + 1) * blocks // n_atoms, range(74), 20,
                              api.GPUOS_BODY_GEMV_BF16, [desc]) for i in range(n_atoms)]
     for _ in range(reps):
-        y.zero_()
-        torch.cuda.synchronize()
         ms = dev.run_batch(descs)
         while dev.in_flight():
             dev.poll()
@@ -33,7 +31,7 @@ with api.Device() as dev:
         st = dev.stats()
         print(f"gemv {n}x{k} ({blocks} blocks of 256 rows, {n_atoms} atoms): {ms:.3f} ms, "
               f"{nbytes / ms / 1e6:.0f} GB/s (device span {st.worker_span_ns / 1e3:.1f} us: "
-              f"{nbytes / st.worker_span_ns:.0f} GB/s)", flush=True)
+              f"{nbytes / st.worker_span_ns:.0f} GB/s, claim retries {st.claim_retries})", flush=True)
     dev.free(desc)
 ref = (w.float() @ x.float())
 print("max rel err", ((y - ref).abs().max() / ref.abs().max()).item())
