@@ -262,6 +262,9 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     # ---- saturated roofline: the BE tenant's atomized kernel alone at full width
     sat = saturation(api, local, args)
     sat_tc = gemm_saturation(api, local, args)
+    sat_gemv = guarded(lambda: gemv_saturation(api, local, args))
+    rsz = guarded(lambda: right_sizing_summary(local, args)) if rank == 0 else None
+    cfgs = guarded(lambda: model_configs(local)) if (rank == 0 and not args.skip_configs) else None
     probe = api.probe_dispatch(device=local, workers_per_sm=args.workers_per_sm, serial=2000,
                                pipelined=20000, depth=16)
 
@@ -300,6 +303,9 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
                      "peak_source": pk["source"]},
         "roofline_saturated": sat,
         "roofline_tensor": sat_tc,
+        "roofline_gemv": sat_gemv,
+        "right_sizing": rsz,
+        "model_configs": cfgs,
         "dispatcher_overhead": {
             "serial_roundtrip_us_p50": probe["serial_roundtrip_ns"]["p50"] / 1e3,
             "publish_to_first_block_us_p50": probe["publish_to_first_block_ns"]["p50"] / 1e3,
@@ -342,6 +348,75 @@ def saturation(api, local: int, args) -> dict:
             "frac": best / pk["hbm_gbs"], "traffic": None,
             "note": f"{blocks} blocks x {words * 4} B read + write, {n_atoms} atoms on all 74 TPCs, "
                     f"single batch-mode k_worker launch"}
+
+
+def guarded(fn):
+    """Secondary measurements never take the bench line down."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
+def gemv_saturation(api, local: int, args) -> dict:
+    """The decode GEMV body (TMA-streamed W, tensor-core MACs) on a weight
+    matrix far larger than L2, one atom on all 74 TPCs, batch mode."""
+    import torch
+
+    pk = peaks()
+    n, k = 262144, 8192
+    dev_name = f"cuda:{local}"
+    w = torch.randn(n, k, device=dev_name, dtype=torch.bfloat16)
+    x = torch.randn(k, device=dev_name, dtype=torch.bfloat16)
+    y = torch.empty(n, device=dev_name)
+    torch.cuda.synchronize()
+    best = 0.0
+    nbytes = n * k * 2 + k * 2 + n * 4
+    with api.Device(device=local, workers_per_sm=args.workers_per_sm) as dev:
+        desc, blocks = dev.gemv_desc(w.data_ptr(), x.data_ptr(), y.data_ptr(), n, k)
+        descs = [api.Device.desc(0, blocks, range(74), 20, api.GPUOS_BODY_GEMV_BF16, [desc])]
+        for _ in range(3):
+            ms = dev.run_batch(descs)
+            while dev.in_flight():
+                dev.poll()
+            best = max(best, nbytes / (ms * 1e-3) / 1e9)
+        dev.free(desc)
+    return {"bound": "hbm", "achieved": best, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": best / pk["hbm_gbs"], "traffic": None,
+            "note": f"GEMV y = W x, W bf16 {n}x{k} ({nbytes / 1e9:.1f} GB) as {blocks} 256-row pair "
+                    f"tiles on all 74 TPCs, single batch-mode k_worker launch, CUDA events"}
+
+
+def right_sizing_summary(local: int, args) -> dict:
+    """BASELINE config #4 on the quick grid (paper_2504_15465_b200.rightsize)."""
+    from paper_2504_15465_b200 import rightsize
+
+    r = rightsize.sweep(device=local, slip=1.04, quick=True, reps=2, workers_per_sm=args.workers_per_sm)
+    return {"slip": r["slip"], "grid": r["grid"], "mean_capacity_savings": r["mean_capacity_savings"],
+            "max_slowdown": r["max_slowdown"], "weighted_r2": r["weighted_r2"],
+            "bodies": [{k: b[k] for k in ("body", "t_star", "slowdown", "capacity_savings", "r2")}
+                       for b in r["bodies"]],
+            "note": "t* = choose_tpcs_wave(fit_scaling(l(1), l(74)), slip 1.04) on device-timed "
+                    "single-atom runs; slowdown = measured l(t*) / l(74)"}
+
+
+def model_configs(local: int) -> dict:
+    """BASELINE configs #2 and #3 on model kernel traces (configs.py)."""
+    from paper_2504_15465_b200 import configs
+
+    out = {}
+    for name in ("infer4", "hybrid"):
+        r = configs.run(name, horizon_ms=1000.0, reps=2, device=local)
+        out[name] = {"tpc_utilization": r["tpc_utilization"], "apps": {
+            a: {k: v for k, v in row.items() if k in ("priority", "p99_vs_alone", "slo_attainment",
+                                                        "throughput_vs_static")}
+            | {"p99_ms": row["stacked"].get("p99_ms"), "alone_p99_ms": row["alone"].get("p99_ms"),
+               "per_s": row["stacked"].get("per_s")}
+            for a, row in r["apps"].items()}}
+    out["note"] = ("#2: 2x ResNet-50 b1 + 2x BERT-base b8, all LC, Poisson; #3: Llama-3-8B decode LC "
+                   "(Poisson tokens) + ResNet-50 b64 training BE (closed loop); random-init weights, "
+                   "live on the persistent dispatcher, 1 s horizon x 2 runs")
+    return out
 
 
 def gemm_saturation(api, local: int, args) -> dict:
@@ -391,6 +466,8 @@ def main():
     ap.add_argument("--horizon-ms", type=float, default=2000.0, help="reference-scale horizon")
     ap.add_argument("--workers-per-sm", type=int, default=2)
     ap.add_argument("--chunk-cap", type=int, default=256)
+    ap.add_argument("--skip-configs", action="store_true",
+                    help="skip the model-trace runs of configs #2/#3")
     ap.add_argument("--workload", choices=["fig7", "box8"], default="fig7",
                     help="fig7: BASELINE config #1; box8: config #5 (8 tenants per GPU)")
     args = ap.parse_args()
