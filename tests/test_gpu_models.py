@@ -1,0 +1,51 @@
+"""Model kernel traces (models.py) through the gpuos:: scheduler on the B200:
+tensor-core conv/GEMM/GEMV bodies and STREAM bodies of ResNet-50 / BERT-base
+/ Llama-3-8B decode.
+
+* Mirror: the replay clock decides (the dispatch/completion log is the
+  replay engine's, bit-exact with the reference's model) while every atom
+  also executes on the GPU; every block ran exactly once on its TPC set.
+* Live: configs #2 / #3 shapes complete every request with TPC placement
+  inside each atom's set."""
+from __future__ import annotations
+
+import pytest
+
+from paper_2504_15465_b200 import models, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def test_mirror_resnet50_and_bert_traces(api, cuda_device):
+    cfg = {"name": "mirror-models", "device": {"gpc_count": 2, "tpcs_per_gpc": 37},
+           "policy": "full_system", "horizon_ms": 30.0, "seed": 5,
+           "scheduler": {"rightsizer": False, "dvfs": False, "stealing": True, "atomizer": True},
+           "apps": [
+               {"id": "rn50", "priority": "hp", "quota": 37, "slo_ms": 50.0,
+                "arrival": {"times_ms": [0.0, 10.0]}, "kernels": models.resnet50_infer(1)},
+               {"id": "bert", "priority": "be", "quota": 37,
+                "arrival": {"times_ms": [0.0]}, "kernels": models.bert_base_infer(2)}]}
+    r = api.run({"scenario": {"config": cfg}, "backend": "mirror", "log": True})
+    v = r["verify"]
+    assert v["ok"], v
+    assert v["missing"] == v["duplicated"] == v["misplaced"] == 0
+    assert r["gpu_atoms"] == r["atoms"]["hp"] + r["atoms"]["be"] > 0
+    replay = api.run({"scenario": {"config": cfg}, "backend": "replay", "log": True})
+    assert r["log"] == replay["log"]
+
+
+@pytest.mark.parametrize("name", ["infer4", "hybrid"])
+def test_live_model_configs_complete(api, cuda_device, name):
+    cfg = workloads.infer4(150.0) if name == "infer4" else workloads.hybrid(150.0)
+    req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
+           "timeline": True, "b200": {"chunk_cap": 256}, "set": {"block_revocation": True}}
+    with api.Session(req) as s:
+        s.run()
+        r = s.run()
+    for a in r["report"]["apps"]:
+        assert a["completed"] > 0
+        if a["high_priority"]:  # requests still in flight at the horizon are not counted
+            assert a["completed"] >= a["offered"] - 3
+    tl = r["b200"]["timeline"]
+    for m0, m1, t0, t1 in zip(tl["mask0"], tl["mask1"], tl["touched0"], tl["touched1"]):
+        assert (t0 & ~m0) == 0 and (t1 & ~m1) == 0 and (t0 | t1) != 0

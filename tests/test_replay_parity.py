@@ -77,3 +77,20 @@ def test_config_errors_exit_2(built, tmp_path):
         assert subprocess.run([built["gpuos_replay"]] + args, capture_output=True).returncode == 2
     bad.write_text("{ not json")
     assert subprocess.run([built["gpuos_replay"], "--config", str(bad)], capture_output=True).returncode == 2
+
+
+def test_model_traces_run_on_replay(api):
+    """Model kernel traces are reference kernel records plus a body the
+    reference ignores: they run on the replay engine (conv bodies carry nine
+    parameters)."""
+    from paper_2504_15465_b200 import models
+
+    for kernels in (models.resnet50_infer(1), models.llama3_8b_decode(256)):
+        cfg = {"name": "m", "device": {"gpc_count": 2, "tpcs_per_gpc": 37}, "policy": "full_system",
+               "horizon_ms": 20.0, "seed": 1, "scheduler": {"dvfs": False},
+               "apps": [{"id": "t", "priority": "hp", "quota": 74, "slo_ms": 100.0,
+                         "arrival": {"times_ms": [0.0]}, "kernels": kernels}]}
+        r = api.run({"scenario": {"config": cfg}, "backend": "replay"})
+        assert r["report"]["apps"][0]["completed"] == 1
+    conv = [k for k in models.resnet50_infer(1) if k["body"]["kind"] == "conv_bf16"][0]
+    assert len(conv["body"]["p"]) == 9
