@@ -150,7 +150,7 @@ __device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) 
 }
 
 // ------------------------------------------------------------ ingest warp
-// Ring entries are read kIngestBatch at a time: one 512-byte PCIe read per
+// Ring entries are read kIngestBatch at a time: two 512-byte PCIe reads per
 // poll (lane l loads 16 B: entry head + l/8, words 4(l%8)..4(l%8)+3), so a
 // backlog of submissions costs one host round trip per batch, not per atom.
 // Publication uses two GPU-scope fences per batch, not per atom:
@@ -162,7 +162,7 @@ __device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) 
 // A worker that acquires a key therefore sees the slot fields (A precedes
 // the fence before B), and a worker whose acquire of a TPC version observes
 // phase C sees every key and armed claim of the batch (no lost wake-up).
-constexpr int kIngestBatch = 4;
+constexpr int kIngestBatch = 8;  // two 512-byte reads per poll
 
 struct IngestSubmit {
   unsigned slot, seq;
@@ -212,13 +212,16 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
         break;
       }
     }
-    const unsigned el = lane >> 3;  // entry of this lane's 16 bytes
-    const uint4 v = ld_relaxed_sys_v4(p.ring[(head + el) % p.ring_cap].w + 4 * (lane & 7));
+    const unsigned el = lane >> 3;  // entry of this lane's 16 bytes (and el + 4)
+    const uint4 va = ld_relaxed_sys_v4(p.ring[(head + el) % p.ring_cap].w + 4 * (lane & 7));
+    const uint4 vb = ld_relaxed_sys_v4(p.ring[(head + 4 + el) % p.ring_cap].w + 4 * (lane & 7));
     // Sector s of entry e ends with its ticket: word 8s+7 = lane 8e+2s+1, .w
-    const bool tk = (lane & 1u) == 0u || v.w == static_cast<unsigned>(head + el + 1);
-    const unsigned okm = __ballot_sync(0xffffffffu, tk);
+    const bool tka = (lane & 1u) == 0u || va.w == static_cast<unsigned>(head + el + 1);
+    const bool tkb = (lane & 1u) == 0u || vb.w == static_cast<unsigned>(head + 4 + el + 1);
+    const unsigned long long okm = static_cast<unsigned long long>(__ballot_sync(0xffffffffu, tka)) |
+                                   (static_cast<unsigned long long>(__ballot_sync(0xffffffffu, tkb)) << 32);
     int n = 0;
-    while (n < kIngestBatch && ((okm >> (8 * n)) & 0xffu) == 0xffu) ++n;
+    while (n < kIngestBatch && ((okm >> (8 * n)) & 0xffull) == 0xffull) ++n;
     if (n == 0) {
       __nanosleep(32);
       continue;
@@ -229,7 +232,8 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
     bool stop = false, set_drain = false, set_quit = false;
     for (int j = 0; j < n && !stop; ++j) {
       // Transpose: lane l gets word l of entry j.
-      const int src = 8 * j + static_cast<int>(lane >> 2);
+      const int src = 8 * (j & 3) + static_cast<int>(lane >> 2);
+      const uint4 v = j < 4 ? va : vb;
       const unsigned x0 = __shfl_sync(0xffffffffu, v.x, src);
       const unsigned x1 = __shfl_sync(0xffffffffu, v.y, src);
       const unsigned x2 = __shfl_sync(0xffffffffu, v.z, src);
@@ -407,7 +411,7 @@ struct RoundCmd {
   long long lo;                 // first block of the atom
   unsigned long long key;       // resident key of the atom
   unsigned slot;
-  int pad;
+  unsigned count;               // slices of the atom (1: single-block fast path)
 };
 constexpr int kRoundCmdWords64 = sizeof(RoundCmd) / 8;
 static_assert(sizeof(RoundCmd) % 8 == 0, "RoundCmd copied as 64-bit words");
@@ -471,6 +475,20 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigne
   } while (!ok);
 }
 
+// Sleeps in hardware on the barrier for up to `hint_ns` (wakes at once on a
+// remote arrive): the peer's idle wait for a pair tile.
+__device__ __forceinline__ bool mbar_try_wait_cluster(unsigned long long* b, unsigned parity,
+                                                      unsigned hint_ns) {
+  unsigned ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3; "
+      "selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ bool mbar_test_cluster(unsigned long long* b, unsigned parity) {
   unsigned ok;
   asm volatile(
@@ -520,19 +538,30 @@ __device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& r
                                               unsigned long long& busy) {
   DevAtom* a = p.atoms + rc.slot;
   int last = 0;
+  // A single-slice atom is complete with its only block: its first / last
+  // times and TPC are this block's, so no atomics on the slot (three L2
+  // round trips less on every small kernel).
+  const bool single = rc.count == 1u;
+  unsigned long long s_t0 = t_start, s_t1 = 0;
   if (lane == 0) {
     const unsigned long long t_end = gtimer();
-    atomicMin(&a->t_first, t_start);
-    atomicMax(&a->t_last, t_end);
-    atomicOr(&a->touched[tpc >> 6], 1ull << (tpc & 63));
+    s_t1 = t_end;
     if (a->trace != nullptr)
       atomicAdd(a->trace + rc.cmd.block * rc.cmd.parts + rc.cmd.part, 0x10000u + sm + 1u);
     busy += t_end - t_start;
     ++n_blocks;
-    // acq_rel: this block's records (and the body's output stores, ordered
-    // by the CTA barrier before this) precede the count; the last finisher
-    // observes every other block's records.
-    last = atom_add_acq_rel32(&a->done, 1u) + 1u == ld_relaxed_gpu(&a->count);
+    if (single) {
+      __threadfence();  // the body's output (and trace) precede the completion record
+      last = 1;
+    } else {
+      atomicMin(&a->t_first, t_start);
+      atomicMax(&a->t_last, t_end);
+      atomicOr(&a->touched[tpc >> 6], 1ull << (tpc & 63));
+      // acq_rel: this block's records (and the body's output stores, ordered
+      // by the CTA barrier before this) precede the count; the last finisher
+      // observes every other block's records.
+      last = atom_add_acq_rel32(&a->done, 1u) + 1u == ld_relaxed_gpu(&a->count);
+    }
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return false;
@@ -542,10 +571,12 @@ __device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& r
     // (= seq). Each chunk is one PCIe write, so a chunk whose ticket matches
     // is complete; no system-scope fence (~1 us) sits on the completion path.
     CompRec* rec = p.comp + rc.slot;
-    const unsigned long long t0 = ld_relaxed_gpu64(&a->t_first);
-    const unsigned long long t1 = ld_relaxed_gpu64(&a->t_last);
-    const unsigned long long m0 = ld_relaxed_gpu64(&a->touched[0]);
-    const unsigned long long m1 = ld_relaxed_gpu64(&a->touched[1]);
+    const unsigned long long t0 = single ? s_t0 : ld_relaxed_gpu64(&a->t_first);
+    const unsigned long long t1 = single ? s_t1 : ld_relaxed_gpu64(&a->t_last);
+    const unsigned long long m0 =
+        single ? (tpc < 64 ? 1ull << tpc : 0ull) : ld_relaxed_gpu64(&a->touched[0]);
+    const unsigned long long m1 =
+        single ? (tpc >= 64 ? 1ull << (tpc - 64) : 0ull) : ld_relaxed_gpu64(&a->touched[1]);
     const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
     const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
     const unsigned long long tag = a->tag;
@@ -816,6 +847,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                   sh.rc.lo = static_cast<long long>(wlo);
                   sh.rc.key = key;
                   sh.rc.slot = static_cast<unsigned>(key & 0xffffffull);
+                  sh.rc.count = wcount;
                 }
               }
               break;
@@ -835,6 +867,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                 sh.rc.lo = a->lo;
                 sh.rc.slot = slot;
                 sh.rc.key = key;
+                sh.rc.count = ld_relaxed_gpu(&a->count);
               }
               const unsigned parts = sh.rc.cmd.parts;
               sh.rc.cmd.block = sh.rc.lo + off / parts;
@@ -862,7 +895,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
           if (count_idle) atomicAdd(&p.ctl->idle_leaders, 1u);
           bool changed = false, leave = false;
           for (int k2 = 0; k2 < 64; ++k2) {
-            if (rank != 0 && mbar_test_cluster(&sh.join_full, joins & 1u)) {
+            // The peer sleeps on its join barrier between version polls, so
+            // a posted pair tile wakes it at once.
+            if (rank != 0 && mbar_try_wait_cluster(&sh.join_full, joins & 1u, 200u)) {
               changed = true;
               break;
             }
@@ -883,7 +918,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                       gtimer() > p.ctl->deadline;
               if (leave) break;
             }
-            __nanosleep(p.idle_sleep_ns);
+            if (rank == 0) __nanosleep(p.idle_sleep_ns);
           }
           if (count_idle) atomicSub(&p.ctl->idle_leaders, 1u);
           if (changed) continue;

@@ -253,13 +253,15 @@ std::string run_session(gpuos_session* s, const json& overrides) {
     b["stream_bytes"] = stream_bytes;
     if (want_timeline) {
       json tl = json::object();
-      std::vector<long long> submit, complete, first, last, lo, hi, tag, prio, kern;
+      std::vector<long long> submit, complete, first, last, lo, hi, tag, prio, kern, ingest, armed;
       std::vector<unsigned long long> m0, m1, t0v, t1v;
       for (const AtomTimeline& a : dev.timeline()) {
         submit.push_back(a.host_submit_ns);
         complete.push_back(a.host_complete_ns);
         first.push_back(a.dev_first_start_ns);
         last.push_back(a.dev_last_end_ns);
+        ingest.push_back(a.dev_ingest_ns);
+        armed.push_back(a.dev_armed_ns);
         lo.push_back(a.lo);
         hi.push_back(a.hi);
         tag.push_back(static_cast<long long>(a.tag));
@@ -274,6 +276,8 @@ std::string run_session(gpuos_session* s, const json& overrides) {
       tl["complete"] = complete;
       tl["dev_first"] = first;
       tl["dev_last"] = last;
+      tl["dev_ingest"] = ingest;
+      tl["dev_armed"] = armed;
       tl["lo"] = lo;
       tl["hi"] = hi;
       tl["tag"] = tag;
