@@ -475,20 +475,6 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigne
   } while (!ok);
 }
 
-// Sleeps in hardware on the barrier for up to `hint_ns` (wakes at once on a
-// remote arrive): the peer's idle wait for a pair tile.
-__device__ __forceinline__ bool mbar_try_wait_cluster(unsigned long long* b, unsigned parity,
-                                                      unsigned hint_ns) {
-  unsigned ok;
-  asm volatile(
-      "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3; "
-      "selp.u32 %0, 1, 0, p; }"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity), "r"(hint_ns)
-      : "memory");
-  return ok != 0;
-}
-
 __device__ __forceinline__ bool mbar_test_cluster(unsigned long long* b, unsigned parity) {
   unsigned ok;
   asm volatile(
@@ -895,9 +881,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
           if (count_idle) atomicAdd(&p.ctl->idle_leaders, 1u);
           bool changed = false, leave = false;
           for (int k2 = 0; k2 < 64; ++k2) {
-            // The peer sleeps on its join barrier between version polls, so
-            // a posted pair tile wakes it at once.
-            if (rank != 0 && mbar_try_wait_cluster(&sh.join_full, joins & 1u, 200u)) {
+            // (A suspend-time hint on this wait stretched the peers' exit at
+            // drain by ~250 us: the hardware sleeps far past the hint.)
+            if (rank != 0 && mbar_test_cluster(&sh.join_full, joins & 1u)) {
               changed = true;
               break;
             }
@@ -918,7 +904,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                       gtimer() > p.ctl->deadline;
               if (leave) break;
             }
-            if (rank == 0) __nanosleep(p.idle_sleep_ns);
+            __nanosleep(p.idle_sleep_ns);
           }
           if (count_idle) atomicSub(&p.ctl->idle_leaders, 1u);
           if (changed) continue;
@@ -1913,6 +1899,7 @@ int gpuos_dev_gemv_desc(gpuos_dev* d, const void* w, const void* x, void* y, int
   CUDA_TRY(cudaMallocAsync(&p, total, d->s_side));
   h.arrivals = reinterpret_cast<unsigned*>(static_cast<char*>(p) + counters_off);
   h.partial = h.splits > 1 ? reinterpret_cast<float*>(static_cast<char*>(p) + partial_off) : nullptr;
+  h.timing = nullptr;
   CUDA_TRY(cudaMemsetAsync(static_cast<char*>(p) + counters_off, 0, 4ull * h.row_tiles, d->s_side));
   CUDA_TRY(cudaMemcpyAsync(p, &h, sizeof(GemvDesc), cudaMemcpyHostToDevice, d->s_side));
   CUDA_TRY(cudaStreamSynchronize(d->s_side));

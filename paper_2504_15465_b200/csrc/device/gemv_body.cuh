@@ -51,6 +51,7 @@ struct alignas(128) GemvDesc {
   unsigned pad0;
   float* partial;                // [splits][N] fp32 partial sums (split-K)
   unsigned* arrivals;            // [row_tiles] self-resetting split counters
+  unsigned long long* timing;    // optional: 4 globaltimer stamps per block (profiling)
 };
 
 struct GemvPipe {
@@ -111,6 +112,8 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
     cluster_sync_all();
     return;
   }
+  unsigned long long* tm = D->timing != nullptr && rank == 0 ? D->timing + 4ull * c.block : nullptr;
+  if (tm && tid == 0) tm[0] = gtimer();
   if (tid == 0) {
     // TMA producer (both CTAs); descriptor written by a host copy while
     // this persistent kernel runs: acquire it into the tensor-map proxy.
@@ -137,6 +140,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       const unsigned s = static_cast<unsigned>(k % S);
       mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1));
       tc_fence_after();
+      if (tm && j == 0) tm[1] = gtimer();
       const unsigned a0 = smem_u32(G.tiles + s * kGemvStageBytes);
       const unsigned b0 = a0 + kGemvWBytes;
 #pragma unroll
@@ -150,6 +154,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
   // Epilogue: warps 0-3 of both CTAs read TMEM column 0 (y) of their lanes.
   mbar_wait_bounded(G.accum, G.accum_used & 1u);
   tc_fence_after();
+  if (tm && tid == 0) tm[2] = gtimer();
   const int warp = tid >> 5, lane = tid & 31;
   const bool bf16_y = (D->flags & kGemvOutBf16) != 0;
   if (warp < 4) {
@@ -199,6 +204,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       }
     }
   }
+  if (tm && tid == 0) tm[3] = gtimer();
 }
 
 }  // namespace gpuos_dev_impl
