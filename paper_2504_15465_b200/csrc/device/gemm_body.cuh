@@ -43,6 +43,7 @@ constexpr unsigned kGemmBK = 64;      // K per stage: 64 bf16 = one 128-byte swi
 constexpr unsigned kGemmMaxStages = 4;
 constexpr unsigned kGemmABytes = kGemmHalf * kGemmBK * 2;  // 16 KiB
 constexpr unsigned kGemmStageBytes = 2 * kGemmABytes;      // A half + B half
+constexpr unsigned kEpiRowBytes = 272;  // epilogue staging row: 256 B + 16 B pad (bank spread)
 
 struct alignas(128) GemmDesc {
   CUtensorMap a;                 // A [M, K] bf16: box {64, 128}, SWIZZLE_128B
@@ -260,31 +261,26 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   const int warp = tid >> 5, lane = tid & 31;
   const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
   constexpr unsigned half = kGemmTile / 2;
-  const unsigned row = mt * kGemmTile + rank * kGemmHalf + q * 32 + static_cast<unsigned>(lane);
+  const unsigned row0 = mt * kGemmTile + rank * kGemmHalf + q * 32;  // warp's first row
   const unsigned M = D->m, N = D->n, ldc = D->ldc;
   const bool bf16_out = (D->flags & kGemmOutBf16) != 0;
+  // Staged through shared memory (the operand stages are free now): each
+  // thread writes its row's values, then the warp stores two 256-byte rows
+  // per instruction -- coalesced, where storing straight from the TMEM
+  // registers wrote 32 scattered 16-byte pieces per instruction (9 us per
+  // tile, tools/gemm_batch.py timing hook).
+  const unsigned esz = bf16_out ? 2u : 4u;
+  const unsigned pass_cols = 256u / esz;                 // 256 bytes of a row per pass
+  unsigned char* stg = G.tiles + static_cast<unsigned>(warp) * (32u * kEpiRowBytes);
+  const bool vec_ok = (static_cast<size_t>(ldc) * esz) % 16 == 0;
 #pragma unroll 1
-  for (unsigned ch = 0; ch < half / 32; ++ch) {
-    unsigned v[32];
-    tmem_ld32(G.tmem + ((q * 32u) << 16) + h * half + ch * 32u, v);
-    const unsigned col0 = nt * kGemmTile + h * half + ch * 32u;
-    if (row >= M || col0 >= N) continue;
-    const bool full_row = col0 + 32 <= N;
-    if (!bf16_out) {
-      float* out = reinterpret_cast<float*>(D->c) + static_cast<size_t>(row) * ldc + col0;
-      if (full_row && (ldc % 4) == 0) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          st_stream(reinterpret_cast<uint4*>(out) + i,
-                    make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
-      } else {
-#pragma unroll
-        for (unsigned i = 0; i < 32; ++i)
-          if (col0 + i < N) out[i] = __uint_as_float(v[i]);
-      }
-    } else {
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(D->c) + static_cast<size_t>(row) * ldc + col0;
-      if (full_row && (ldc % 8) == 0) {
+  for (unsigned pc = 0; pc < half; pc += pass_cols) {
+#pragma unroll 1
+    for (unsigned ch = 0; ch < pass_cols / 32; ++ch) {
+      unsigned v[32];
+      tmem_ld32(G.tmem + ((q * 32u) << 16) + h * half + pc + ch * 32u, v);
+      uint4* dst = reinterpret_cast<uint4*>(stg + static_cast<unsigned>(lane) * kEpiRowBytes + ch * 32u * esz);
+      if (bf16_out) {
         unsigned pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -292,14 +288,32 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
           pk[i] = *reinterpret_cast<const unsigned*>(&t);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          st_stream(reinterpret_cast<uint4*>(out) + i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
       } else {
 #pragma unroll
-        for (unsigned i = 0; i < 32; ++i)
-          if (col0 + i < N) out[i] = __float2bfloat16_rn(__uint_as_float(v[i]));
+        for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       }
     }
+    __syncwarp();
+    // 16 lanes per row, 16 bytes each: rows 2i and 2i + 1 per instruction.
+    const unsigned seg = static_cast<unsigned>(lane) & 15u;
+    const unsigned col = nt * kGemmTile + h * half + pc + seg * (16u / esz);
+#pragma unroll 4
+    for (unsigned i = 0; i < 16; ++i) {
+      const unsigned r = 2 * i + (static_cast<unsigned>(lane) >> 4);
+      const unsigned grow = row0 + r;
+      if (grow >= M || col >= N) continue;
+      const uint4 val = *reinterpret_cast<const uint4*>(stg + r * kEpiRowBytes + seg * 16u);
+      unsigned char* out = reinterpret_cast<unsigned char*>(D->c) + (static_cast<size_t>(grow) * ldc + col) * esz;
+      if (vec_ok && col + 16u / esz <= N) {
+        st_stream(reinterpret_cast<uint4*>(out), val);
+      } else {
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(&val);
+        for (unsigned e = 0; e < 16u / esz && col + e < N; ++e)
+          for (unsigned byte = 0; byte < esz; ++byte) out[e * esz + byte] = src[e * esz + byte];
+      }
+    }
+    __syncwarp();  // staging reused by the next pass
   }
   tc_fence_before();  // the next tile's MMAs overwrite this accumulator
   if (tm) {
