@@ -121,10 +121,11 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
   const bool bf16_out = (D->flags & kConvOutBf16) != 0;
 #pragma unroll 1
   for (unsigned ch = 0; ch < half / 32; ++ch) {
+    const unsigned col0 = kt * kGemmTile + h * half + ch * 32u;
+    if (col0 >= K) break;  // warp-uniform: narrow layers skip the empty columns
     unsigned v[32];
     tmem_ld32(G.tmem + ((qd * 32u) << 16) + h * half + ch * 32u, v);
-    const unsigned col0 = kt * kGemmTile + h * half + ch * 32u;
-    if (!valid || col0 >= K) continue;
+    if (!valid) continue;
     const bool full_row = col0 + 32 <= K;
     if (!bf16_out) {
       float* out = reinterpret_cast<float*>(D->y) + orow * K + col0;

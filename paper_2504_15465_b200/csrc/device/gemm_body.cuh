@@ -275,6 +275,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   const bool vec_ok = (static_cast<size_t>(ldc) * esz) % 16 == 0;
 #pragma unroll 1
   for (unsigned pc = 0; pc < half; pc += pass_cols) {
+    if (nt * kGemmTile + h * half + pc >= N) break;  // warp-uniform: ragged last tile
 #pragma unroll 1
     for (unsigned ch = 0; ch < pass_cols / 32; ++ch) {
       unsigned v[32];
