@@ -345,9 +345,20 @@ def saturation(api, local: int, args) -> dict:
                 dev.poll()
             best = max(best, blocks * words * 8 / (ms * 1e-3) / 1e9)
     return {"bound": "hbm", "achieved": best, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": best / pk["hbm_gbs"], "traffic": None,
+            "frac": best / pk["hbm_gbs"], "traffic": ncu_traffic("stream", f"{blocks} blocks x {words} words"),
+            "algorithmic_bytes": blocks * words * 8,
             "note": f"{blocks} blocks x {words * 4} B read + write, {n_atoms} atoms on all 74 TPCs, "
                     f"single batch-mode k_worker launch"}
+
+
+def ncu_traffic(name: str, config: str):
+    """DRAM bytes (read + write) of one launch of the same shape from the
+    committed ncu capture (profiles/ncu_traffic_r01.json), else None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")))[name]
+    except (OSError, KeyError, ValueError):
+        return None
+    return t["dram_read"] + t["dram_write"] if t.get("config") == config else None
 
 
 def guarded(fn):
@@ -382,7 +393,8 @@ def gemv_saturation(api, local: int, args) -> dict:
             best = max(best, nbytes / (ms * 1e-3) / 1e9)
         dev.free(desc)
     return {"bound": "hbm", "achieved": best, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": best / pk["hbm_gbs"], "traffic": None,
+            "frac": best / pk["hbm_gbs"], "traffic": ncu_traffic("gemv", f"{n}x{k}"),
+            "algorithmic_bytes": nbytes,
             "note": f"GEMV y = W x, W bf16 {n}x{k} ({nbytes / 1e9:.1f} GB) as {blocks} 256-row pair "
                     f"tiles on all 74 TPCs, single batch-mode k_worker launch, CUDA events"}
 
@@ -448,7 +460,8 @@ def gemm_saturation(api, local: int, args) -> dict:
                 best, span = tf, dev.stats().worker_span_ns * 1e-9
         dev.free(desc)
     return {"bound": "tensor", "achieved": best, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": best / pk["bf16_tflops"], "traffic": None,
+            "frac": best / pk["bf16_tflops"], "traffic": ncu_traffic("gemm", f"{m}x{n}x{k} bf16 out"),
+            "algorithmic_bytes": 2 * (m * k + n * k + m * n),
             "note": f"bf16 GEMM {m}x{n}x{k} (bf16 out) as {blocks} 256x256 pair tiles "
                     f"(tcgen05.mma.cta_group::2) in {n_atoms} atoms on all 74 TPCs, single "
                     f"batch-mode k_worker launch, CUDA events; peak = measured cuBLAS burst; "
