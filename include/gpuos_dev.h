@@ -59,8 +59,8 @@ extern "C" {
                                  dst[i] = (src[i] ^ salt) * 0x9E3779B1 + i
                                  for i in [c * words, (c + 1) * words)       */
 #define GPUOS_BODY_GEMM_BF16 2u /* args: [0] = descriptor from
-                                   gpuos_dev_gemm_desc(); block b = output
-                                   tile (b % m_tiles, b / m_tiles) of
+                                   gpuos_dev_gemm_desc(); block b = one
+                                   256 x 256 output tile (grouped raster) of
                                    C = A . B^T on the tensor cores       */
 #define GPUOS_BODY_SPIN 3u    /* args: ns to spin per block (globaltimer)    */
 #define GPUOS_BODY_GEMV_BF16 4u /* args: [0] = descriptor from

@@ -4,7 +4,7 @@
 // A tenant GEMM C[M,N] = A[M,K] . B[N,K]^T (bf16 in, fp32 accumulate, fp32
 // or bf16 out; both operands K-major, i.e. a row-major activation times a
 // row-major nn.Linear weight) is a grid of ceil(M/256) x ceil(N/256) blocks;
-// block b computes the 256 x 256 output tile (b % m_tiles, b / m_tiles).
+// block b computes one 256 x 256 output tile (grouped raster, body_gemm2).
 // The reference models such a block only as a duration with sensitivity
 // s ~ 1 (device.hpp:39-47); here the pair executes it:
 //
@@ -201,9 +201,17 @@ __device__ __forceinline__ void gemm_pipe_init(GemmPipe& G, unsigned char* smem,
 // Both CTAs of the pair, all threads; rank 0 is the leader.
 __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G) {
   const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
-  const unsigned m_tiles = D->m_tiles;
+  const unsigned m_tiles = D->m_tiles, n_tiles = D->n_tiles;
   const unsigned blk = static_cast<unsigned>(c.block);
-  const unsigned mt = blk % m_tiles, nt = blk / m_tiles;
+  // Grouped raster: blocks walk 8 M-tiles down an N column before moving
+  // right, so ~150 concurrent tiles touch 8 A panels and ~18 B panels (fits
+  // L2) instead of every A panel (8192^3: DRAM reads 3x the operands).
+  constexpr unsigned kGroup = 8;
+  const unsigned group = blk / (kGroup * n_tiles);
+  const unsigned first_m = group * kGroup;
+  const unsigned gm = m_tiles - first_m < kGroup ? m_tiles - first_m : kGroup;
+  const unsigned in_group = blk - group * kGroup * n_tiles;
+  const unsigned mt = first_m + in_group % gm, nt = in_group / gm;
   const unsigned nk = (D->k + kGemmBK - 1) / kGemmBK;
   const unsigned S = G.stages;
   const unsigned long long g0 = G.kb_used;
