@@ -265,6 +265,7 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     sat_gemv = guarded(lambda: gemv_saturation(api, local, args))
     rsz = guarded(lambda: right_sizing_summary(local, args)) if rank == 0 else None
     cfgs = guarded(lambda: model_configs(local)) if (rank == 0 and not args.skip_configs) else None
+    pols = guarded(lambda: policy_rows(local)) if (rank == 0 and not args.skip_configs) else None
     probe = api.probe_dispatch(device=local, workers_per_sm=args.workers_per_sm, serial=2000,
                                pipelined=20000, depth=16)
 
@@ -306,6 +307,7 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
         "roofline_gemv": sat_gemv,
         "right_sizing": rsz,
         "model_configs": cfgs,
+        "policy_comparison": pols,
         "dispatcher_overhead": {
             "serial_roundtrip_us_p50": probe["serial_roundtrip_ns"]["p50"] / 1e3,
             "publish_to_first_block_us_p50": probe["publish_to_first_block_ns"]["p50"] / 1e3,
@@ -410,6 +412,17 @@ def right_sizing_summary(local: int, args) -> dict:
                        for b in r["bodies"]],
             "note": "t* = choose_tpcs_wave(fit_scaling(l(1), l(74)), slip 1.04) on device-timed "
                     "single-atom runs; slowdown = measured l(t*) / l(74)"}
+
+
+def policy_rows(local: int) -> dict:
+    """The reference's baseline policies on the live dispatcher, config #1
+    workload."""
+    from paper_2504_15465_b200 import configs
+
+    r = configs.policy_comparison(horizon_ms=500.0, reps=2, device=local)
+    r["note"] = ("fig7-b200 (time-scaled /10) under each scheduling policy, live; "
+                 "be_blocks_per_s over device time")
+    return r
 
 
 def model_configs(local: int) -> dict:

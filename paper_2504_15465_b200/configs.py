@@ -82,13 +82,47 @@ def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0) -
             "tpc_utilization": sum(r["report"]["tpc_utilization"] for r in live) / len(live)}
 
 
+POLICIES = ["full_system", "mps_like", "mig_like", "time_slice", "priority_only", "reef_like"]
+
+
+def policy_comparison(horizon_ms: float = 1000.0, reps: int = 2, device: int = 0,
+                      time_scale: float = 10.0) -> dict[str, Any]:
+    """the reference's baseline policies
+    (scheduler.cpp:111-121, 199-226, 494-521) on the live dispatcher, on the
+    config #1 workload: LC p99 and BE throughput per policy (Fig. 9-style).
+    mig_like gets one GPC (die half) per tenant."""
+    base = workloads.fig7_b200(time_scale, horizon_ms * time_scale)
+    out: dict[str, Any] = {}
+    req = {"scenario": {"config": base}, "backend": "b200", "device": "b200", "requests": True,
+           "b200": {"chunk_cap": 256, "device": device, "quantum_us": 25.0},
+           "set": {"block_revocation": True}}
+    with api.Session(req) as s:
+        s.run()
+        for pol in POLICIES:
+            cfg = dict(base, policy=pol)
+            if pol == "mig_like":
+                cfg["mig_gpcs"] = {"hp": [0], "be": [1]}
+            runs = [s.run(scenario={"config": cfg}) for _ in range(reps)]
+            lat = [json.loads(x)["latency_us"] / 1e3 for r in runs for x in r["request_log"].splitlines()
+                   if json.loads(x)["app"] == "hp" and json.loads(x)["completed"]]
+            ms = sum(r["b200"]["kernel_ms"] for r in runs)
+            be_blocks = sum(r["blocks_per_app"][1] for r in runs)
+            out[pol] = {"lc_p99_ms": nearest_rank(lat, 99), "lc_p50_ms": nearest_rank(lat, 50),
+                        "lc_completed": len(lat), "be_blocks_per_s": be_blocks / (ms * 1e-3) if ms else None,
+                        "be_atoms": sum(r["atoms"]["be"] for r in runs)}
+    return out
+
+
 def main(argv: list[str] | None = None) -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("config", choices=["infer4", "hybrid"])
+    ap.add_argument("config", choices=["infer4", "hybrid", "policies"])
     ap.add_argument("--horizon-ms", type=float, default=2000.0)
     ap.add_argument("--reps", type=int, default=2)
     args = ap.parse_args(argv)
-    json.dump(run(args.config, args.horizon_ms, args.reps), sys.stdout, indent=1)
+    if args.config == "policies":
+        json.dump(policy_comparison(args.horizon_ms, args.reps), sys.stdout, indent=1)
+    else:
+        json.dump(run(args.config, args.horizon_ms, args.reps), sys.stdout, indent=1)
     print()
 
 

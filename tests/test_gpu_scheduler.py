@@ -110,3 +110,16 @@ def test_live_mechanisms_lc_tail_and_be_throughput(api, cuda_device):
     for r in live:
         hp = r["report"]["apps"][0]
         assert hp["completed"] == hp["offered"]
+
+
+def test_baseline_policies_run_live(api, cuda_device):
+    """Every reference policy (scheduler.cpp:111-121, 199-226, 494-521) drives
+    the live dispatcher: all LC requests complete; full_system has the lowest
+    LC tail and mps_like the highest (the paper's ordering)."""
+    from paper_2504_15465_b200 import configs
+
+    r = configs.policy_comparison(horizon_ms=200.0, reps=1)
+    assert set(r) == set(configs.POLICIES)
+    for row in r.values():
+        assert row["lc_completed"] > 0 and row["be_atoms"] > 0
+    assert r["full_system"]["lc_p99_ms"] < r["mps_like"]["lc_p99_ms"]
