@@ -97,8 +97,10 @@ def test_live_mechanisms_lc_tail_and_be_throughput(api, cuda_device):
     with api.Session(req) as s:
         s.run()
         s.run()
-        live = [s.run() for _ in range(2)]
-        alone = [s.run(scenario={"config": workloads.without_apps(cfg, "be")}) for _ in range(2)]
+        # 4 runs (400 LC requests): p99 is the 4th-worst request, so one
+        # burst caught by a host-side stall does not decide the test.
+        live = [s.run() for _ in range(4)]
+        alone = [s.run(scenario={"config": workloads.without_apps(cfg, "be")}) for _ in range(4)]
         static = [s.run(scenario={"config": workloads.variant(cfg, stealing=False, atomizer=False)})
                   for _ in range(2)]
     p_live = percentile(sum((hp_latencies(r) for r in live), []), 99)
