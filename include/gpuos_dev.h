@@ -116,7 +116,21 @@ typedef struct gpuos_atom_desc {
                                 claimed independently, so a higher-priority
                                 atom waits at most one slice for a slot.
                                 trace is then indexed block * parts + part. */
+  uint32_t after;            /* kernel chaining: 1 + atom id of the
+                                predecessor this atom runs behind (0: none).
+                                The atom becomes claimable on the device the
+                                moment the predecessor's last block ends --
+                                no host round trip between the two. The
+                                predecessor must carry GPUOS_ATOM_CHAIN_HEAD;
+                                if it already completed (was polled) the atom
+                                runs at once. poll() never reports an atom
+                                before its predecessor.                     */
+  uint32_t flags;            /* GPUOS_ATOM_*                                */
 } gpuos_atom_desc;
+
+#define GPUOS_ATOM_CHAIN_HEAD 1u /* a successor may be chained behind this
+                                    atom (its completion then arms it: one
+                                    extra L2 atomic on the last block)    */
 
 typedef struct gpuos_completion {
   uint32_t atom_id;          /* id returned by gpuos_dev_submit_atom        */

@@ -80,7 +80,10 @@ class AtomDesc(C.Structure):
     _fields_ = [("lo", C.c_int64), ("hi", C.c_int64), ("tpc_mask", C.c_uint64 * 2),
                 ("priority", C.c_int32), ("body", C.c_uint32), ("args", C.c_uint64 * 5),
                 ("tag", C.c_uint64), ("trace", C.c_void_p), ("atomized", C.c_int32),
-                ("parts", C.c_uint32)]
+                ("parts", C.c_uint32), ("after", C.c_uint32), ("flags", C.c_uint32)]
+
+
+GPUOS_ATOM_CHAIN_HEAD = 1
 
 
 class Completion(C.Structure):
@@ -271,7 +274,11 @@ class Device:
 
     @staticmethod
     def desc(lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
-             trace: int | None = None, parts: int = 1) -> AtomDesc:
+             trace: int | None = None, parts: int = 1, after: int | None = None,
+             chain_head: bool = False) -> AtomDesc:
+        """One atom. `after`: atom id of a predecessor this atom is chained
+        behind (armed on the device when the predecessor's last block ends);
+        the predecessor must have been submitted with chain_head=True."""
         d = AtomDesc()
         d.parts = parts
         d.lo, d.hi, d.priority, d.body, d.tag = lo, hi, priority, body, tag
@@ -282,6 +289,8 @@ class Device:
         for i, a in enumerate(args):
             d.args[i] = int(a)
         d.trace = trace
+        d.after = 0 if after is None else after + 1
+        d.flags = GPUOS_ATOM_CHAIN_HEAD if chain_head else 0
         return d
 
     def run_batch(self, descs: list[AtomDesc]) -> float:
@@ -292,17 +301,9 @@ class Device:
         return ms.value
 
     def submit(self, lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
-               trace: int | None = None, parts: int = 1) -> int:
-        d = AtomDesc()
-        d.parts = parts
-        d.lo, d.hi, d.priority, d.body, d.tag = lo, hi, priority, body, tag
-        m = [0, 0]
-        for t in tpcs:
-            m[t >> 6] |= 1 << (t & 63)
-        d.tpc_mask[0], d.tpc_mask[1] = m
-        for i, a in enumerate(args):
-            d.args[i] = int(a)
-        d.trace = trace
+               trace: int | None = None, parts: int = 1, after: int | None = None,
+               chain_head: bool = False) -> int:
+        d = self.desc(lo, hi, tpcs, priority, body, args, tag, trace, parts, after, chain_head)
         aid = C.c_uint32()
         self._check(self._lib.gpuos_dev_submit_atom(self._h, C.byref(d), C.byref(aid)))
         return aid.value

@@ -39,6 +39,7 @@
 #include <deque>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "bodies.cuh"
@@ -70,16 +71,30 @@ struct alignas(128) DevAtom {
   unsigned seq;              // +72
   int prio;                  // +76 1..255
   unsigned done;             // +80 finished slices
-  unsigned atom_id;          // +84
+  unsigned pad0;             // +84
   unsigned long long tag;    // +88
   unsigned* trace;           // +96
   unsigned long long mask[2];  // +104
+  unsigned chain;            // +120 kChainHead: completion arms a successor
+  unsigned succ;             // +124 chained successor: slot + 1, kSuccDone once finished
   unsigned long long t_first, t_last;   // second line: per-block records
   unsigned long long touched[2];
   unsigned long long t_seen, t_armed;   // ingest instrumentation (globaltimer)
   unsigned char entry[GPUOS_MAX_TPCS];  // resident-list index per TPC
 };
-static_assert(offsetof(DevAtom, mask) + 16 <= 128, "hot fields must share one line");
+static_assert(offsetof(DevAtom, succ) + 4 <= 128, "hot fields must share one line");
+static_assert(offsetof(DevAtom, chain) % 8 == 0 && offsetof(DevAtom, succ) == offsetof(DevAtom, chain) + 4,
+              "chain | succ: one 64-bit load");
+
+// Kernel chaining (gpuos_atom_desc::after). A successor is ingested
+// unarmed (claim exhausted, keys resident); the ingest warp then registers
+// it on the predecessor with a CAS on `succ`, and the predecessor's
+// finishing worker swaps in kSuccDone. Whichever comes second arms the
+// successor: exactly one does, and a successor registered after the
+// predecessor finished is armed by the ingest warp itself.
+constexpr unsigned kSuccDone = 0xffffffffu;
+constexpr unsigned kChainHead = 1u;
+constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head
 
 struct DevCtl {
   unsigned quit;
@@ -107,7 +122,7 @@ struct RingEntry {
 __host__ __device__ constexpr int ring_word(int d) { return (d / 7) * 8 + d % 7; }
 enum RingField : int {
   kFOp = 0, kFSlot = 1, kFSeq = 2, kFPrio = 3, kFLo = 4 /*2*/, kFCount = 6,
-  kFBody = 7, kFMask0 = 8 /*2*/, kFMask1 = 10 /*2*/, kFAtomId = 12, kFAux = 13,
+  kFBody = 7, kFMask0 = 8 /*2*/, kFMask1 = 10 /*2*/, kFPred = 12, kFAux = 13,
   kFArgs = 14 /*10*/, kFTag = 24 /*2*/, kFTrace = 26 /*2*/
 };
 
@@ -166,6 +181,7 @@ constexpr int kIngestBatch = 8;  // two 512-byte reads per poll
 
 struct IngestSubmit {
   unsigned slot, seq;
+  unsigned pred;  // chained: predecessor slot + 1 (0: none)
   unsigned long long mask[2];
   unsigned long long key;
 };
@@ -256,8 +272,9 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
         const long long lo = static_cast<long long>(field64(get(kFLo), get(kFLo + 1)));
         const unsigned count = get(kFCount);  // slices = blocks x parts
         const unsigned body = get(kFBody);
-        const unsigned atom_id = get(kFAtomId);
-        const unsigned parts = get(kFAux);
+        const unsigned pred = get(kFPred);
+        const unsigned aux = get(kFAux);
+        const unsigned parts = aux & ~kAuxChainHead;
         DevAtom* a = p.atoms + slot;
         if (lane == 0) {
           // Exhausted (offset == count) until armed in phase B: a stale
@@ -274,7 +291,8 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           a->seq = seq;
           a->prio = prio;
           a->done = 0;
-          a->atom_id = atom_id;
+          a->succ = 0;
+          a->chain = (aux & kAuxChainHead) ? kChainHead : 0u;
           a->tag = tag;
           a->trace = reinterpret_cast<unsigned*>(trace);
           a->mask[0] = mask0;
@@ -289,6 +307,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           IngestSubmit& s = subs[n_sub];
           s.slot = slot;
           s.seq = seq;
+          s.pred = pred;
           s.mask[0] = mask0;
           s.mask[1] = mask1;
           s.key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
@@ -362,13 +381,15 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
       fence_acq_rel_gpu();  // every lane: phase A before its phase-B stores
       __syncwarp();
       const unsigned long long t_armed = gtimer();
+      bool chained = false;
       for (int i = 0; i < n_sub; ++i) {
         const IngestSubmit s = subs[i];
         DevAtom* a = p.atoms + s.slot;
-        if (lane == 0) {
+        if (lane == 0 && s.pred == 0u) {
           st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
           a->t_armed = t_armed;
         }
+        chained = chained || s.pred != 0u;
         for (int t = lane; t < p.logical_tpcs; t += 32) {
           const unsigned long long m = s.mask[t >> 6];
           if ((m >> (t & 63)) & 1ull)
@@ -376,6 +397,24 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
         }
       }
       for (int t = lane; t < p.logical_tpcs; t += 32) pend[t] = 0u;
+      if (chained) {
+        // Keys (and slot fields) before the registration: the finisher that
+        // reads it arms the successor and wakes its TPCs.
+        __syncwarp();
+        fence_acq_rel_gpu();
+        if (lane == 0) {
+          for (int i = 0; i < n_sub; ++i) {
+            const IngestSubmit s = subs[i];
+            if (s.pred == 0u) continue;
+            DevAtom* a = p.atoms + s.slot;
+            if (atomicCAS(&p.atoms[s.pred - 1u].succ, 0u, s.slot + 1u) == kSuccDone) {
+              // Predecessor already finished: arm here (woken below).
+              st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
+              a->t_armed = gtimer();
+            }
+          }
+        }
+      }
     }
     __syncwarp();
     fence_acq_rel_gpu();  // phase B (and pause / fence words) before the bumps
@@ -516,12 +555,41 @@ __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long 
   return got ? static_cast<long long>(off) : -1;
 }
 
+__device__ __forceinline__ bool body_is_pair(unsigned body) {
+  return body == GPUOS_BODY_GEMM_BF16 || body == GPUOS_BODY_GEMV_BF16 ||
+         body == GPUOS_BODY_CONV_BF16;
+}
+
 // Warp 0 of the CTA that ran `rc`: record the block on its atom and, for the
 // atom's last block, publish the completion and retire its resident keys.
-__device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& rc,
-                                              unsigned long long t_start, int tpc, unsigned sm,
-                                              unsigned lane, unsigned long long& n_blocks,
-                                              unsigned long long& busy) {
+// Returns 0 (more blocks to go), 1 (atom done) or 2 (atom done, and `rc`
+// now holds block 0 of its chained successor, claimed for this worker).
+// A chained successor's hot-line fields (account_block).
+struct SuccFields {
+  unsigned long long count_paused, lo, body_parts, args[5], seq_prio, mask[2];
+  __device__ __forceinline__ void load(const DevAtom* b) {
+    unsigned long long claim;
+    ld_relaxed_gpu_v2(b, claim, count_paused);
+    ld_relaxed_gpu_v2(&b->lo, lo, body_parts);
+    ld_relaxed_gpu_v2(&b->args[0], args[0], args[1]);
+    ld_relaxed_gpu_v2(&b->args[2], args[2], args[3]);
+    ld_relaxed_gpu_v2(&b->args[4], args[4], seq_prio);
+    mask[0] = ld_relaxed_gpu64(&b->mask[0]);  // (+104: 8-byte aligned)
+    mask[1] = ld_relaxed_gpu64(&b->mask[1]);
+  }
+};
+
+__device__ __forceinline__ unsigned atom_exch_acq_rel32(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
+                                             unsigned long long t_start, int tpc, unsigned sm,
+                                             unsigned rank, unsigned lane,
+                                             unsigned long long& n_blocks,
+                                             unsigned long long& busy) {
   DevAtom* a = p.atoms + rc.slot;
   int last = 0;
   // A single-slice atom is complete with its only block: its first / last
@@ -529,15 +597,33 @@ __device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& r
   // round trips less on every small kernel).
   const bool single = rc.count == 1u;
   unsigned long long s_t0 = t_start, s_t1 = 0;
+  // Fields fixed for the atom's lifetime, read by its finisher (for a
+  // single-slice atom up front, overlapping the accounting). For a chain
+  // head, a successor already registered (set once) is read with them,
+  // with acquire: the finisher then arms it without the swap.
+  unsigned long long tag = 0, ts = 0, ta = 0;
+  unsigned chain = 0, pre = 0;
+  SuccFields bf;
+  auto finisher_fields = [&] {
+    tag = a->tag;
+    ts = ld_relaxed_gpu64(&a->t_seen);
+    ta = ld_relaxed_gpu64(&a->t_armed);
+    const unsigned long long cs = ld_acquire_gpu64(reinterpret_cast<unsigned long long*>(&a->chain));
+    chain = static_cast<unsigned>(cs);
+    pre = (chain & kChainHead) ? static_cast<unsigned>(cs >> 32) : 0u;
+  };
   if (lane == 0) {
     const unsigned long long t_end = gtimer();
     s_t1 = t_end;
+    if (single) finisher_fields();
     if (a->trace != nullptr)
       atomicAdd(a->trace + rc.cmd.block * rc.cmd.parts + rc.cmd.part, 0x10000u + sm + 1u);
     busy += t_end - t_start;
     ++n_blocks;
     if (single) {
-      __threadfence();  // the body's output (and trace) precede the completion record
+      // The body's output (and trace) precede the completion record; a
+      // chain head fences after arming its successor (off its path).
+      if (!(chain & kChainHead)) __threadfence();
       last = 1;
     } else {
       atomicMin(&a->t_first, t_start);
@@ -546,14 +632,76 @@ __device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& r
       // acq_rel: this block's records (and the body's output stores, ordered
       // by the CTA barrier before this) precede the count; the last finisher
       // observes every other block's records.
-      last = atom_add_acq_rel32(&a->done, 1u) + 1u == ld_relaxed_gpu(&a->count);
+      last = atom_add_acq_rel32(&a->done, 1u) + 1u == rc.count;
+      if (last) finisher_fields();
     }
   }
   last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return false;
+  if (!last) return 0;
+  // Chain head: arm the registered successor (or mark this atom finished so
+  // the ingest warp arms it) before anything else -- the successor's start
+  // is the chain's critical path. The swap is acq_rel: our outputs (ordered
+  // by the fence / acq_rel count above) precede it, and it acquires the
+  // successor's fields and keys (the ingest warp fenced them before
+  // registering). When this worker may run the successor here (its TPC is
+  // in the set, the fence admits it, and a 2-SM body has this CTA as the
+  // pair's leader) the arming store claims block 0 for it: no version
+  // wake-up, list scan or claim atomic before the successor's first block
+  // (the other workers are woken for the rest).
+  RoundCmd ho;
+  int handoff = 0;
+  chain = __shfl_sync(0xffffffffu, chain, 0);
+  if (chain & kChainHead) {
+    unsigned next = 0;
+    if (lane == 0) {
+      // Registered before we looked: nothing to race with (registration
+      // happens once), and the acquire above ordered its fields.
+      next = pre != 0u ? pre : atom_exch_acq_rel32(&a->succ, kSuccDone);
+      if (next != 0u) {
+        bf.load(p.atoms + (next - 1u));
+        DevAtom* b = p.atoms + (next - 1u);
+        const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
+        const unsigned bseq = static_cast<unsigned>(bf.seq_prio);
+        const int bprio = static_cast<int>(bf.seq_prio >> 32);
+        const unsigned bcount = static_cast<unsigned>(bf.count_paused);
+        const unsigned bbody = static_cast<unsigned>(bf.body_parts);
+        const bool here = (((tpc < 64 ? bf.mask[0] : bf.mask[1]) >> (tpc & 63)) & 1ull) && (bf.count_paused >> 32) == 0u &&
+                          bprio >= floor_prio && (!body_is_pair(bbody) || rank == 0u);
+        st_relaxed_gpu64(&b->claim, (static_cast<unsigned long long>(bseq) << 32) | (here ? 1u : 0u));
+        b->t_armed = gtimer();
+        if (here) {
+          handoff = 1;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) ho.cmd.args[k] = bf.args[k];
+          ho.cmd.body = bbody;
+          ho.cmd.parts = static_cast<unsigned>(bf.body_parts >> 32);
+          ho.cmd.part = 0;
+          ho.lo = static_cast<long long>(bf.lo);
+          ho.cmd.block = ho.lo;
+          ho.key = (static_cast<unsigned long long>(bprio & 0xff) << 56) |
+                   (static_cast<unsigned long long>(~bseq) << 24) | (next - 1u);
+          ho.slot = next - 1u;
+          ho.count = bcount;
+          if (bcount == 1u) next = 0;  // nothing left for other workers: no wake-up
+        }
+      }
+    }
+    next = __shfl_sync(0xffffffffu, next, 0);
+    handoff = __shfl_sync(0xffffffffu, handoff, 0);
+    if (next != 0u) {
+      __syncwarp();
+      fence_acq_rel_gpu();  // every lane: the armed claim before its version bumps
+      const DevAtom* b = p.atoms + (next - 1u);
+      for (int t = lane; t < p.logical_tpcs; t += 32) {
+        const unsigned long long m = b->mask[t >> 6];
+        if ((m >> (t & 63)) & 1ull) red_relaxed_gpu_add(p.version + t, 1u);
+      }
+    }
+  }
   if (lane == 0) {
-    // Completion record first (the host is waiting on it), in the slot's
-    // own record: four 16-byte chunks, each three data words and the ticket
+    if (single && (chain & kChainHead)) __threadfence();
+    // Completion record (the host is waiting on it), in the slot's own
+    // record: four 16-byte chunks, each three data words and the ticket
     // (= seq). Each chunk is one PCIe write, so a chunk whose ticket matches
     // is complete; no system-scope fence (~1 us) sits on the completion path.
     CompRec* rec = p.comp + rc.slot;
@@ -563,12 +711,9 @@ __device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& r
         single ? (tpc < 64 ? 1ull << tpc : 0ull) : ld_relaxed_gpu64(&a->touched[0]);
     const unsigned long long m1 =
         single ? (tpc >= 64 ? 1ull << (tpc - 64) : 0ull) : ld_relaxed_gpu64(&a->touched[1]);
-    const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
-    const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
-    const unsigned long long tag = a->tag;
     const unsigned tk = ~static_cast<unsigned>(rc.key >> 24);
     const unsigned long long span = t1 - t0;
-    st_relaxed_sys_v4(rec->w + 0, ld_relaxed_gpu(&a->count) / rc.cmd.parts,
+    st_relaxed_sys_v4(rec->w + 0, rc.count / rc.cmd.parts,
                       static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32), tk);
     st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
                       span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
@@ -581,19 +726,23 @@ __device__ __forceinline__ bool account_block(const Params& p, const RoundCmd& r
   }
   __syncwarp();
   // Device-side bookkeeping after the record; the host recycles this slot
-  // only after thousands of others, long after these land.
+  // only after thousands of others, long after these land. Our key still
+  // occupies its list entries (only this finisher clears them, and the
+  // ingest warp fills only cleared entries): plain stores, no round trip.
   for (int t = lane; t < p.logical_tpcs; t += 32) {
     const unsigned long long m = a->mask[t >> 6];
     if ((m >> (t & 63)) & 1ull)
-      atomicCAS(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], rc.key, 0ull);
+      st_relaxed_gpu64(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], 0ull);
   }
   if (lane == 0) {
     // Plain reductions: atoms_done is read after the kernel ends, and the
     // drain check only needs outstanding to reach zero eventually.
     atomicAdd(&p.ctl->atoms_done, 1ull);
     atomicSub(&p.ctl->outstanding, 1);
+    if (handoff) rc = ho;  // (rc's old contents are no longer needed)
   }
-  return true;
+  __syncwarp();
+  return 1 + handoff;
 }
 
 __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned rank,
@@ -606,11 +755,6 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
     case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm); break;
     default: break;
   }
-}
-
-__device__ __forceinline__ bool body_is_pair(unsigned body) {
-  return body == GPUOS_BODY_GEMM_BF16 || body == GPUOS_BODY_GEMV_BF16 ||
-         body == GPUOS_BODY_CONV_BF16;
 }
 
 // Workers own TMEM (GEMM accumulators); the hardware co-schedules at most
@@ -689,19 +833,34 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   int cur_tpc = -1;
   unsigned long long spread_since = 0;  // leader: deferring a pair tile since
   bool tc_hold = false;                 // leader thread 0: holds the TPC's tensor reservation
+  bool handoff = false;                 // warp 0: sh.rc holds a chained successor's block 0
 
   for (;;) {
     // %smid can change if the CTA is ever preempted and restored elsewhere;
-    // re-derive the TPC each round so placement stays exact.
-    sm = smid();
-    tpc = p.phys2log[sm >> 1];
+    // re-derive the TPC whenever it does so placement stays exact (the
+    // table load stays off the common path: one L2 round trip per block).
+    if (const unsigned now_sm = smid(); now_sm != sm) {
+      sm = now_sm;
+      tpc = p.phys2log[sm >> 1];
+    }
     if (tpc != cur_tpc) {
       cur_key = 0ull;
       cur_tpc = tpc;
     }
     if (warp == 0) {
       int go = kGoExit;
-      if (tpc >= 0) {
+      if (handoff) {
+        // Block 0 of a chained successor, claimed when its predecessor ended
+        // here (account_block); a pair tile takes the tensor reservation.
+        handoff = false;
+        cur_key = 0ull;
+        cur_body = __shfl_sync(0xffffffffu, sh.rc.cmd.body, 0);
+        go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
+        if (go == kGoPair && lane == 0) {
+          if (atomicAdd(p.tc_busy + tpc, 1u) == 0u) atomicAdd(&p.ctl->tc_active, 1u);
+          tc_hold = true;
+        }
+      } else if (tpc >= 0) {
         unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
         unsigned ver = ld_acquire_gpu(p.version + tpc);  // latest observed
         for (;;) {
@@ -950,9 +1109,11 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     __syncthreads();
     // The leader records pair tiles (the peer's half is complete: cluster
     // barrier at the end of the body).
-    if (warp == 0 && go != kGoJoin &&
-        account_block(p, sh.rc, sh.t_start, tpc, sm, lane, n_blocks, busy))
-      cur_key = 0ull;  // the atom is done: rescan rather than claim from it
+    if (warp == 0 && go != kGoJoin) {
+      const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, n_blocks, busy);
+      if (done) cur_key = 0ull;  // the atom is done: rescan rather than claim from it
+      handoff = done == 2;
+    }
   }
   if (tid == 0) {
     atomicAdd(&p.ctl->blocks, n_blocks);
@@ -1015,6 +1176,10 @@ struct HostAtom {
   int64_t submit_ns = 0;
   uint64_t mask[2] = {0, 0};
   bool live = false;
+  bool chain_head = false;   // submitted with GPUOS_ATOM_CHAIN_HEAD
+  bool has_succ = false;     // a successor is chained behind it
+  uint32_t pred_slot = 0;    // chained: predecessor's slot and sequence
+  uint32_t pred_seq = 0;     // (0: not chained)
 };
 
 }  // namespace
@@ -1051,6 +1216,7 @@ struct gpuos_dev {
   uint32_t next_atom_id = 0;
   std::deque<uint32_t> free_slots;  // FIFO: a freed slot is reused last
   std::vector<HostAtom> slots;
+  std::unordered_map<uint32_t, uint32_t> slot_of;  // live atom id -> slot
   std::vector<int> tpc_resident;  // keys currently resident per logical TPC
   int32_t in_flight = 0;
   bool running = false;
@@ -1301,6 +1467,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   *d->consumed_h = 0;
   d->ring_head = 0;
   d->live.clear();
+  d->slot_of.clear();
   std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
 
   // Calibrate device globaltimer against the host origin (+- half an RTT),
@@ -1499,8 +1666,21 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   std::vector<int> fill(static_cast<size_t>(T), 0);
   std::vector<uint32_t> ids(static_cast<size_t>(n));
   std::vector<uint32_t> seqs(static_cast<size_t>(n));
+  std::vector<int> pred(static_cast<size_t>(n), -1);  // chained: predecessor index
+  const uint32_t id_base = d->next_atom_id;
   for (int i = 0; i < n; ++i) {
     const gpuos_atom_desc& a = descs[i];
+    if (a.flags & ~GPUOS_ATOM_CHAIN_HEAD) return fail(GPUOS_E_CONFIG, "unknown atom flags");
+    if (a.after != 0) {
+      // Only atoms of this batch exist: the predecessor is an earlier entry.
+      const int64_t j = static_cast<int64_t>(a.after - 1u) - static_cast<int64_t>(id_base);
+      if (j < 0 || j >= i) return fail(GPUOS_E_CONFIG, "predecessor must be an earlier atom of the batch");
+      if (!(descs[j].flags & GPUOS_ATOM_CHAIN_HEAD))
+        return fail(GPUOS_E_CONFIG, "predecessor was not submitted as a chain head");
+      if (atoms[static_cast<size_t>(j)].succ != 0u)
+        return fail(GPUOS_E_CONFIG, "predecessor already has a successor");
+      pred[static_cast<size_t>(i)] = static_cast<int>(j);
+    }
     const uint32_t parts = a.parts == 0 ? 1u : a.parts;
     if (a.lo < 0 || a.hi <= a.lo || (a.hi - a.lo) * static_cast<int64_t>(parts) > 0xfffffffeLL)
       return fail(GPUOS_E_CONFIG, "atom block range out of bounds");
@@ -1518,7 +1698,12 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     x.prio = prio;
     x.body = a.body;
     x.lo = a.lo;
-    x.atom_id = ids[static_cast<size_t>(i)] = d->next_atom_id++;
+    ids[static_cast<size_t>(i)] = d->next_atom_id++;
+    x.chain = (a.flags & GPUOS_ATOM_CHAIN_HEAD) ? kChainHead : 0u;
+    if (pred[static_cast<size_t>(i)] >= 0) {
+      x.claim |= x.count;  // unarmed until the predecessor's last block
+      atoms[static_cast<size_t>(pred[static_cast<size_t>(i)])].succ = static_cast<unsigned>(i) + 1u;
+    }
     std::memcpy(x.args, a.args, sizeof x.args);
     x.tag = a.tag;
     x.trace = a.trace;
@@ -1543,6 +1728,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   d->free_slots.clear();
   for (int s = d->cfg.atom_slots - 1; s >= n; --s) d->free_slots.push_back(static_cast<uint32_t>(s));
   const int64_t now = gpuos_dev_now_ns(d);
+  d->slot_of.clear();
   for (int i = 0; i < n; ++i) {
     HostAtom& h = d->slots[static_cast<size_t>(i)];
     h.atom_id = ids[static_cast<size_t>(i)];
@@ -1552,6 +1738,12 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     h.mask[0] = descs[i].tpc_mask[0];
     h.mask[1] = descs[i].tpc_mask[1];
     h.live = true;
+    h.chain_head = (descs[i].flags & GPUOS_ATOM_CHAIN_HEAD) != 0;
+    h.has_succ = atoms[static_cast<size_t>(i)].succ != 0u;
+    const int j = pred[static_cast<size_t>(i)];
+    h.pred_slot = j >= 0 ? static_cast<uint32_t>(j) : 0u;
+    h.pred_seq = j >= 0 ? seqs[static_cast<size_t>(j)] : 0u;
+    d->slot_of[h.atom_id] = static_cast<uint32_t>(i);
   }
   std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
   std::memset(d->comp_h, 0, sizeof(CompRec) * d->cfg.atom_slots);
@@ -1635,6 +1827,24 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
     if (((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) && d->tpc_resident[t] >= kResident)
       return fail(GPUOS_E_FULL, "TPC " + std::to_string(t) + " already holds 32 resident atoms");
   if (d->free_slots.empty()) return fail(GPUOS_E_FULL, "atom table full");
+  if (a->flags & ~GPUOS_ATOM_CHAIN_HEAD) return fail(GPUOS_E_CONFIG, "unknown atom flags");
+  // Chaining: a live predecessor (not yet polled) arms this atom on the
+  // device; one that already completed leaves nothing to wait for.
+  uint32_t pred_slot = 0, pred_seq = 0;
+  bool chained = false;
+  if (a->after != 0) {
+    const auto it = d->slot_of.find(a->after - 1u);
+    if (it != d->slot_of.end()) {
+      HostAtom& p = d->slots[it->second];
+      if (!p.chain_head) return fail(GPUOS_E_CONFIG, "predecessor was not submitted as a chain head");
+      if (p.has_succ) return fail(GPUOS_E_CONFIG, "predecessor already has a successor");
+      pred_slot = it->second;
+      pred_seq = p.seq;
+      chained = true;
+    } else if (a->after - 1u >= d->next_atom_id) {
+      return fail(GPUOS_E_CONFIG, "predecessor atom id was never issued");
+    }
+  }
 
   const uint32_t slot = d->free_slots.front();
   d->free_slots.pop_front();
@@ -1647,11 +1857,11 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   data[kFPrio] = static_cast<uint32_t>(map_priority(a->priority));
   put64(data, kFLo, static_cast<uint64_t>(a->lo));
   data[kFCount] = static_cast<uint32_t>((a->hi - a->lo) * parts);
-  data[kFAux] = parts;
+  data[kFAux] = parts | ((a->flags & GPUOS_ATOM_CHAIN_HEAD) ? kAuxChainHead : 0u);
   data[kFBody] = a->body;
   put64(data, kFMask0, a->tpc_mask[0]);
   put64(data, kFMask1, a->tpc_mask[1]);
-  data[kFAtomId] = id;
+  data[kFPred] = chained ? pred_slot + 1u : 0u;
   for (int k = 0; k < 5; ++k) put64(data, kFArgs + 2 * k, a->args[k]);
   put64(data, kFTag, a->tag);
   put64(data, kFTrace, reinterpret_cast<uint64_t>(a->trace));
@@ -1663,12 +1873,18 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   h.mask[0] = a->tpc_mask[0];
   h.mask[1] = a->tpc_mask[1];
   h.live = true;
+  h.chain_head = (a->flags & GPUOS_ATOM_CHAIN_HEAD) != 0;
+  h.has_succ = false;
+  h.pred_slot = pred_slot;
+  h.pred_seq = pred_seq;
   const int rc = publish(d, data);
   if (rc != GPUOS_OK) {
     h.live = false;
     d->free_slots.push_front(slot);
     return rc;
   }
+  if (chained) d->slots[pred_slot].has_succ = true;
+  d->slot_of[id] = slot;
   for (int t = 0; t < T; ++t)
     if ((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) ++d->tpc_resident[t];
   d->live.push_back(slot);
@@ -1679,14 +1895,12 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
 
 int gpuos_dev_set_atom_paused(gpuos_dev* d, uint32_t atom_id, int paused) {
   if (!d) return fail(GPUOS_E_CONFIG, "null device");
-  for (uint32_t s = 0; s < d->slots.size(); ++s) {
-    if (!d->slots[s].live || d->slots[s].atom_id != atom_id) continue;
-    uint32_t data[28] = {};
-    data[kFOp] = paused ? kOpPause : kOpResume;
-    data[kFSlot] = s;
-    return publish(d, data);
-  }
-  return GPUOS_OK;  // already finished: nothing to pause (device.cpp:167)
+  const auto it = d->slot_of.find(atom_id);
+  if (it == d->slot_of.end()) return GPUOS_OK;  // already finished: nothing to pause (device.cpp:167)
+  uint32_t data[28] = {};
+  data[kFOp] = paused ? kOpPause : kOpResume;
+  data[kFSlot] = it->second;
+  return publish(d, data);  // already finished: nothing to pause (device.cpp:167)
 }
 
 int gpuos_dev_set_tpc_fence(gpuos_dev* d, int32_t tpc, int32_t min_priority) {
@@ -1718,6 +1932,10 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
     const uint32_t slot = d->live[i];
     HostAtom& h = d->slots[slot];
     CompRec* rec = d->comp_h + slot;
+    if (h.pred_seq != 0 && d->slots[h.pred_slot].live && d->slots[h.pred_slot].seq == h.pred_seq) {
+      ++i;  // chained: reported after its predecessor (next poll)
+      continue;
+    }
     if (__atomic_load_n(&rec->w[15], __ATOMIC_ACQUIRE) != h.seq ||
         __atomic_load_n(&rec->w[11], __ATOMIC_ACQUIRE) != h.seq ||
         __atomic_load_n(&rec->w[7], __ATOMIC_ACQUIRE) != h.seq ||
@@ -1745,6 +1963,7 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
     for (int t = 0; t < d->cfg.logical_tpcs; ++t)
       if ((h.mask[t >> 6] >> (t & 63)) & 1ull) --d->tpc_resident[t];
     h.live = false;
+    d->slot_of.erase(h.atom_id);
     d->free_slots.push_back(slot);
     d->live[i] = d->live.back();  // O(1) removal; order is irrelevant
     d->live.pop_back();

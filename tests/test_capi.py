@@ -76,3 +76,28 @@ def test_time_scaled_scenario_scales_latencies(api):
     assert fast["horizon_ns"] == base["horizon_ns"] // 10
     assert hp1["completed"] == hp0["completed"]
     assert abs(hp1["p99_ns"] * 10 - hp0["p99_ns"]) <= 0.02 * hp0["p99_ns"]
+
+
+def test_ctypes_structs_match_the_header(api, tmp_path):
+    """The Python mirror of every gpuos_dev.h struct has the C layout."""
+    import subprocess
+
+    structs = {"gpuos_dev_config": api.DevConfig, "gpuos_dev_topology": api.DevTopology,
+               "gpuos_atom_desc": api.AtomDesc, "gpuos_completion": api.Completion,
+               "gpuos_dev_stats": api.DevStats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gpuos_dev.h"', "int main(void) {"]
+    for c_name, py in structs.items():
+        lines.append(f'printf("{c_name} size %zu\\n", sizeof({c_name}));')
+        for f in py._fields_:
+            lines.append(f'printf("{c_name} {f[0]} %zu\\n", offsetof({c_name}, {f[0]}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    for line in filter(None, got):
+        c_name, field, value = line.split()
+        py = structs[c_name]
+        want = ctypes.sizeof(py) if field == "size" else getattr(py, field).offset
+        assert int(value) == want, (c_name, field, value, want)
