@@ -199,6 +199,10 @@ class B200Device final : public Device {
 
   void set_tpc_fence(const std::vector<int>& tpcs, int min_priority) override;
   bool preempts_stolen() const override { return true; }
+  bool supports_chaining() const override { return true; }
+  AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,
+                        const std::vector<int>& tpcs, int priority, bool atomized,
+                        std::uint64_t tag, bool chain_head) override;
 
   B200Runtime& runtime() { return *rt_; }
   // Clears per-run state so one device (and its workspaces) serves many runs.

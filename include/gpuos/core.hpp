@@ -130,6 +130,7 @@ Duration reference_kernel_latency(const SimKernelSpec& spec, int t, FreqMhz f,
 
 using KernelId = std::uint32_t;
 using AtomId = std::uint32_t;
+constexpr AtomId kNoAtom = 0xffffffffu;
 
 struct AtomCompletion {
   AtomId atom;
@@ -179,6 +180,14 @@ class Device {
   // be handed back to their owner immediately (device priority arbitration
   // preempts at the next block boundary).
   virtual bool preempts_stolen() const { return false; }
+  // Live-backend hook: kernel chaining. submit_chained() posts an atom that
+  // the device arms itself when atom `after` completes (kNoAtom: at once);
+  // `chain_head` lets a later atom be chained behind this one. Completions
+  // still arrive in chain order. Backends without it never see the call.
+  virtual bool supports_chaining() const { return false; }
+  virtual AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,
+                                const std::vector<int>& tpcs, int priority,
+                                bool atomized, std::uint64_t tag, bool chain_head);
 };
 
 }  // namespace gpuos

@@ -31,6 +31,13 @@ class DeviceEngine final : public Device {
                      const std::vector<int>& tpcs, int priority, bool atomized,
                      std::uint64_t tag) override;
   void set_atom_paused(AtomId atom, bool paused) override;
+  // Chaining (off the reference's path: only SchedulerConfig::chain_launches
+  // uses it): the atom is resident at once but starts no block until its
+  // predecessor retires, at that same instant.
+  bool supports_chaining() const override { return true; }
+  AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,
+                        const std::vector<int>& tpcs, int priority, bool atomized,
+                        std::uint64_t tag, bool chain_head) override;
   SimTime request_frequency(FreqMhz f) override;
   void schedule_call(SimTime t, std::function<void()> fn) override;
   void set_atom_complete_handler(
@@ -79,6 +86,8 @@ class DeviceEngine final : public Device {
     bool atomized;
     bool paused = false;
     bool finished = false;
+    bool held = false;         // chained: waiting for its predecessor
+    AtomId succ = kNoAtom;     // chained successor
   };
   enum class Kind : std::uint8_t { BlockDone, Clock, Call };
   struct Event {
@@ -113,6 +122,7 @@ class DeviceEngine final : public Device {
   std::vector<SimKernelSpec> kernels_;
   std::vector<long> executed_;
   std::vector<Atom> atoms_;
+  bool held_next_ = false;  // submit_chained: the next atom starts held
   std::function<void(const AtomCompletion&)> on_complete_;
 
   SimTime accounted_ = 0;

@@ -49,10 +49,14 @@ def per_app(results: list[dict]) -> dict[str, dict]:
     return out
 
 
-def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0) -> dict[str, Any]:
+def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0,
+        chain: bool = True) -> dict[str, Any]:
+    """chain: HP tenants' dependent kernels chained on the device
+    (SchedulerConfig::chain_launches) instead of host-paced launches."""
     cfg = workloads.infer4(horizon_ms) if name == "infer4" else workloads.hybrid(horizon_ms)
     req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
-           "b200": {"chunk_cap": 256, "device": device}, "set": {"block_revocation": True}}
+           "b200": {"chunk_cap": 256, "device": device},
+           "set": {"block_revocation": True, "chain_launches": chain}}
     with api.Session(req) as s:
         s.run()
         s.run()  # warm: operands allocated, predictor and right-sizer state learned
@@ -78,7 +82,7 @@ def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0) -
         if a["priority"] == "be" and st.get("per_s") and sp.get("per_s"):
             row["throughput_vs_static"] = st["per_s"] / sp["per_s"]
         apps[i] = row
-    return {"config": name, "horizon_ms": horizon_ms, "reps": reps, "apps": apps,
+    return {"config": name, "horizon_ms": horizon_ms, "reps": reps, "chain_launches": chain, "apps": apps,
             "tpc_utilization": sum(r["report"]["tpc_utilization"] for r in live) / len(live)}
 
 
@@ -118,11 +122,13 @@ def main(argv: list[str] | None = None) -> None:
     ap.add_argument("config", choices=["infer4", "hybrid", "policies"])
     ap.add_argument("--horizon-ms", type=float, default=2000.0)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--no-chain", action="store_true")
     args = ap.parse_args(argv)
     if args.config == "policies":
         json.dump(policy_comparison(args.horizon_ms, args.reps), sys.stdout, indent=1)
     else:
-        json.dump(run(args.config, args.horizon_ms, args.reps), sys.stdout, indent=1)
+        json.dump(run(args.config, args.horizon_ms, args.reps, chain=not args.no_chain), sys.stdout,
+                  indent=1)
     print()
 
 

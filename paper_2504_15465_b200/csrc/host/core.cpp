@@ -82,4 +82,9 @@ Duration reference_kernel_latency(const SimKernelSpec& spec, int t, FreqMhz f,
   return waves * block_latency(spec, f, fd);
 }
 
+AtomId Device::submit_chained(AtomId, KernelId, long, long, const std::vector<int>&, int, bool,
+                              std::uint64_t, bool) {
+  throw InvariantError("this backend does not chain kernels");
+}
+
 }  // namespace gpuos

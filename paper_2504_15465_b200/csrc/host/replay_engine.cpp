@@ -94,6 +94,7 @@ AtomId DeviceEngine::submit_atom(KernelId kernel, long lo, long hi,
     a.tag = tag;
     a.dispatched = clock_;
     a.atomized = atomized;
+    a.held = held_next_;
     atoms_.push_back(std::move(a));
   }
   const Atom& me = atoms_[id];
@@ -111,6 +112,22 @@ AtomId DeviceEngine::submit_atom(KernelId kernel, long lo, long hi,
   for (int t : me.tpcs) refill(t);  // refill never appends to atoms_
   if (atoms_[id].cursor == atoms_[id].end && atoms_[id].running == 0)
     throw InvariantError("atom completed at submit");
+  return id;
+}
+
+AtomId DeviceEngine::submit_chained(AtomId after, KernelId kernel, long lo, long hi,
+                                    const std::vector<int>& tpcs, int priority,
+                                    bool atomized, std::uint64_t tag, bool /*chain_head*/) {
+  if (after == kNoAtom || atoms_.at(after).finished)
+    return submit_atom(kernel, lo, hi, tpcs, priority, atomized, tag);
+  if (atoms_[after].succ != kNoAtom) throw InvariantError("atom already has a successor");
+  // Resident but held: refill() skips it until the predecessor retires.
+  const AtomId id = static_cast<AtomId>(atoms_.size());
+  atoms_[after].succ = id;
+  held_next_ = true;
+  const AtomId got = submit_atom(kernel, lo, hi, tpcs, priority, atomized, tag);
+  held_next_ = false;
+  if (got != id) throw InvariantError("chained atom id mismatch");
   return id;
 }
 
@@ -145,7 +162,7 @@ void DeviceEngine::refill(int tpc) {
     AtomId pick_id = 0;
     for (AtomId id : ts.queue) {
       const Atom& a = atoms_[id];
-      if (!a.paused && a.cursor < a.end) {
+      if (!a.paused && !a.held && a.cursor < a.end) {
         pick = &a;
         pick_id = id;
         break;
@@ -165,8 +182,14 @@ void DeviceEngine::retire(AtomId id) {
     auto& q = tpc_[t].queue;
     q.erase(std::remove(q.begin(), q.end(), id), q.end());
   }
+  if (a.succ != kNoAtom) {  // its chained successor starts now
+    Atom& s = atoms_[a.succ];
+    s.held = false;
+    const std::vector<int> order = s.tpcs;
+    for (int t : order) refill(t);
+  }
   if (on_complete_) {
-    const AtomCompletion c{id, a.tag, a.dispatched, clock_};
+    const AtomCompletion c{id, atoms_[id].tag, atoms_[id].dispatched, clock_};
     on_complete_(c);
   }
 }
