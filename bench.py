@@ -208,12 +208,13 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     torch.cuda.set_device(local)
     pk = peaks()
     # B200-native live mechanisms: block-granular revocation (fences + HP
-    # preemption of best-effort TPCs) and a preemption quantum of a quarter
-    # atom (blocks run as independently claimed slices).
+    # preemption of best-effort TPCs), a preemption quantum of a quarter
+    # atom (blocks run as independently claimed slices) and LC kernels
+    # chained on the device (no host round trip between dependent kernels).
     quantum_us = 250.0 / args.time_scale
     b200 = {"device": local, "workers_per_sm": args.workers_per_sm, "chunk_cap": args.chunk_cap,
             "quantum_us": quantum_us}
-    live_set = {"block_revocation": True}
+    live_set = {"block_revocation": True, "chain_launches": True}
     sess = api.Session({"scenario": {"config": cfg}, "backend": "b200", "b200": b200,
                         "requests": True, "set": live_set})
     for _ in range(max(args.warmup, 1)):  # the first run creates the tenant workspaces
@@ -242,7 +243,8 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     static = [sess.run(scenario={"config": static_cfg}) for _ in range(args.steps)]
     # Ablation: the reference's semantics on the same dispatcher (atom-
     # boundary revocation, whole blocks).
-    ref_sem = [sess.run(set={"block_revocation": False}, b200=dict(b200, quantum_us=0.0))
+    ref_sem = [sess.run(set={"block_revocation": False, "chain_launches": False},
+                        b200=dict(b200, quantum_us=0.0))
                for _ in range(args.steps)]
     lat_alone = replicas.gather_samples(sum((hp_latencies_us(s) for s in alone), []))
     lat_ref_sem = replicas.gather_samples(sum((hp_latencies_us(s) for s in ref_sem), []))
@@ -292,7 +294,7 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
         "be_blocks_per_s_static": static_blocks / (static_ms * 1e-3),
         "be_vs_static": (be_blocks / dev_ms) / (static_blocks / static_ms),
         "tpc_utilization": sum(s["report"]["tpc_utilization"] for s in steps) / len(steps),
-        "live_mechanisms": {"block_revocation": True, "quantum_us": quantum_us},
+        "live_mechanisms": {"block_revocation": True, "chain_launches": True, "quantum_us": quantum_us},
         "ablation_reference_semantics": {
             "lc_p99_ms": nearest_rank(lat_ref_sem, 99) / 1e3,
             "lc_p99_vs_alone": nearest_rank(lat_ref_sem, 99) / nearest_rank(lat_alone, 99),

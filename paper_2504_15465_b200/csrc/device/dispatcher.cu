@@ -856,7 +856,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
         cur_key = 0ull;
         cur_body = __shfl_sync(0xffffffffu, sh.rc.cmd.body, 0);
         go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
-        if (go == kGoPair && lane == 0) {
+        if (go == kGoPair && cur_body != GPUOS_BODY_GEMV_BF16 && lane == 0) {
           if (atomicAdd(p.tc_busy + tpc, 1u) == 0u) atomicAdd(&p.ctl->tc_active, 1u);
           tc_hold = true;
         }
@@ -930,6 +930,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               const unsigned wcount = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp), win);
               const unsigned long long wbp = __shfl_sync(0xffffffffu, f_bp, win);
               const bool pair = body_is_pair(static_cast<unsigned>(wbp));
+              // GEMV tiles are HBM-bound (their MMAs are a few percent of
+              // the tensor cores): both pairs of a TPC stream at once, no
+              // reservation or spreading.
+              const bool tensor = pair && static_cast<unsigned>(wbp) != GPUOS_BODY_GEMV_BF16;
               // Leader and a pair tile: reserve the TPC's tensor cores. If
               // the other pair holds them, defer up to kSpreadNs so an idle
               // TPC takes the tile first; after that, claim anyway.
@@ -938,7 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               // pair claims at once.
               int reserved = 0;
               const unsigned long long wcw = __shfl_sync(0xffffffffu, f_cw, win);
-              if (rank == 0 && pair && lane == 0) {
+              if (rank == 0 && tensor && lane == 0) {
                 const bool expired = spread_since != 0 && gtimer() - spread_since >= kSpreadNs;
                 const unsigned before = atomicAdd(p.tc_busy + tpc, 1u);
                 reserved = before == 0u || expired ? 1 : 0;
@@ -958,7 +962,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                 defer = true;  // no lower-priority bypass: wait for the leader
                 break;
               }
-              if (rank == 0 && pair && !reserved) {
+              if (rank == 0 && tensor && !reserved) {
                 defer = true;  // let an idle TPC take it first (kSpreadNs)
                 if (spread_since == 0) spread_since = gtimer();
                 break;
