@@ -4,18 +4,24 @@
 // bf16 or fp32 output. The reference models a conv block only as a duration
 // (device.hpp:39-47); ResNet traces need the real thing.
 //
-// GEMM view: M = output pixels, N = K output channels, reduction = (r, s, c).
-// A CTA's 128 rows of a pair tile are one output patch of Wb x Hb x Nb
-// pixels (Wb Hb Nb = 128; Wb, Hb powers of two covering Q, P). For tap
-// (r, s) and a 64-channel slice the patch's input pixels are ONE 4-D TMA
-// box of the NHWC tensor: start (c, q0 st - pad + s, p0 st - pad + r, n0),
-// traversal strides (1, st, st, 1), box (64, Wb st, Hb st, Nb). Rows land
-// in (w, h, n) order with 128-byte swizzle -- exactly the K-major A tile the
-// GEMM body uses; padding and patch overhang are the TMA's zero fill (no
-// im2col buffer). Weights are a 2-D [K, R S Cb] tensor read like GEMM B.
-// Pair tile t covers patches 2t (leader) and 2t + 1 (peer) by 256 output
-// channels; block b = (pair tile b % pair_tiles, channel tile b / pair_tiles).
-// Algorithmic flops per block: 2 x 256 x 256 x R S C (less the overhang).
+// GEMM view: M = output pixels (n, p, q) in NPQ order, N = K output
+// channels, reduction = (r, s, c). A CTA's 128 rows of a pair tile are 128
+// consecutive output pixels -- across row and image boundaries -- loaded by
+// the TMA's im2col mode: the activation map is encoded with the filter's
+// bounding box (lower corner -pad, upper corner pad - (R - 1) per spatial
+// dim, traversal stride = conv stride), so one cp.async.bulk.tensor ...
+// .im2col per (tap, 64-channel slice) gathers the 128 pixels' input
+// channels at offset (s, r) from each pixel's window origin, padding and
+// the tail past the last image as zero fill (no im2col buffer, no padded
+// patches: every MMA row is a real output pixel except the final tile's
+// tail). Semantics pinned on the hardware by scratch/im2col_probe.cu:
+// pixel i of a load is the i-th window origin after (w0, h0, n0) in
+// (w, h, n) order over the bounding box. Rows land with 128-byte swizzle
+// -- the K-major A tile the GEMM body uses. Weights are a 2-D [K, R S Cb]
+// tensor read like GEMM B. Pair tile t covers pixels [256 t, 256 t + 256)
+// (leader the first 128) by 256 output channels; block b = (pair tile
+// b % pair_tiles, channel tile b / pair_tiles).
+// Algorithmic flops per block: 2 x 256 x 256 x R S C (less the tail).
 //
 // args: [0] descriptor from gpuos_dev_conv_desc().
 #pragma once
@@ -31,21 +37,22 @@ namespace gpuos_dev_impl {
 constexpr unsigned kConvOutBf16 = 1u;
 
 struct alignas(128) ConvDesc {
-  CUtensorMap act;               // x [N, H, W, C]: dims {C, W, H, N}, box {64, Wb st, Hb st, Nb}
+  CUtensorMap act;               // x [N, H, W, C]: im2col map, 64 channels x 128 pixels per load
   CUtensorMap wgt;               // w [K, R S Cb]: box {64, 128}
   unsigned long long y;          // [N, P, Q, K]
   unsigned n, h, w, c, k, r, s, pad, stride, p, q;
-  unsigned wb, hb, nb;           // patch (wb hb nb = 128)
-  unsigned tiles_q, tiles_p, patches, pair_tiles, k_tiles, c_blocks, flags;
+  unsigned pixels;               // N P Q
+  unsigned pair_tiles, k_tiles, c_blocks, flags;
 };
 
-__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
-                                                 int c2, int c3, unsigned long long* bar) {
+__device__ __forceinline__ void tma_load_im2col_pair(void* dst, const CUtensorMap* map, int c0, int w0,
+                                                     int h0, int n0, unsigned short off_w,
+                                                     unsigned short off_h, unsigned long long* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)) & 0xFEFFFFFFu)
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(map), "r"(c0), "r"(w0), "r"(h0), "r"(n0),
+      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)) & 0xFEFFFFFFu), "h"(off_w), "h"(off_h)
       : "memory");
 }
 
@@ -55,11 +62,10 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
   const ConvDesc* D = reinterpret_cast<const ConvDesc*>(c.args[0]);
   const unsigned pt = static_cast<unsigned>(c.block) % D->pair_tiles;
   const unsigned kt = static_cast<unsigned>(c.block) / D->pair_tiles;
-  const unsigned patch = 2 * pt + rank;
-  const unsigned pq = patch % D->tiles_q, pp = (patch / D->tiles_q) % D->tiles_p;
-  const unsigned pn = patch / (D->tiles_q * D->tiles_p);
-  const int q0 = static_cast<int>(pq * D->wb), p0 = static_cast<int>(pp * D->hb);
-  const int n0 = static_cast<int>(pn * D->nb);
+  const unsigned m0 = pt * kGemmTile + rank * kGemmHalf;  // this CTA's first output pixel
+  const unsigned pq = D->p * D->q;
+  const unsigned n0 = m0 / pq, rem = m0 - n0 * pq;
+  const unsigned p0 = rem / D->q, q0 = rem - p0 * D->q;
   const unsigned taps = D->r * D->s;
   const unsigned nk = taps * D->c_blocks;
   const unsigned S = G.stages;
@@ -72,19 +78,20 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->act) : "memory");
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->wgt) : "memory");
     const int st = static_cast<int>(D->stride), pad = static_cast<int>(D->pad);
+    const int w0 = static_cast<int>(q0) * st - pad, h0 = static_cast<int>(p0) * st - pad;
     const int k_row = static_cast<int>(kt * kGemmTile + rank * kGemmHalf);
     const unsigned cb_count = D->c_blocks;
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned tap = j / cb_count, cb = j - tap * cb_count;
-      const int rr = static_cast<int>(tap / D->s), ss = static_cast<int>(tap % D->s);
+      const unsigned rr = tap / D->s, ss = tap - rr * D->s;
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;
       if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
       unsigned char* stg = G.tiles + s * kGemmStageBytes;
       if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemmStageBytes);
-      tma_load_4d_pair(stg, &D->act, static_cast<int>(cb * kGemmBK), q0 * st - pad + ss,
-                       p0 * st - pad + rr, n0, G.full + s);
+      tma_load_im2col_pair(stg, &D->act, static_cast<int>(cb * kGemmBK), w0, h0, static_cast<int>(n0),
+                           static_cast<unsigned short>(ss), static_cast<unsigned short>(rr), G.full + s);
       tma_load_2d_pair(stg + kGemmABytes, &D->wgt, static_cast<int>(j * kGemmBK), k_row, G.full + s);
     }
   } else if (tid == 32 && rank == 0) {
@@ -105,63 +112,17 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
     }
     umma2_commit_both(G.accum);
   }
-  // Epilogue: TMEM lane i of this CTA = patch pixel i in (w, h, n) order.
+  // Epilogue: TMEM lane i of this CTA = output pixel m0 + i (NPQ order).
   mbar_wait_bounded(G.accum, G.accum_used & 1u);
   tc_fence_after();
-  const int warp = tid >> 5, lane = tid & 31;
-  const unsigned qd = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
-  constexpr unsigned half = kGemmTile / 2;
-  const unsigned i = qd * 32 + static_cast<unsigned>(lane);
-  const unsigned oq = static_cast<unsigned>(q0) + i % D->wb;
-  const unsigned op = static_cast<unsigned>(p0) + (i / D->wb) % D->hb;
-  const unsigned on = static_cast<unsigned>(n0) + i / (D->wb * D->hb);
-  const bool valid = oq < D->q && op < D->p && on < D->n;
-  const size_t orow = (static_cast<size_t>(on) * D->p + op) * D->q + oq;
-  const unsigned K = D->k;
-  const bool bf16_out = (D->flags & kConvOutBf16) != 0;
-#pragma unroll 1
-  for (unsigned ch = 0; ch < half / 32; ++ch) {
-    const unsigned col0 = kt * kGemmTile + h * half + ch * 32u;
-    if (col0 >= K) break;  // warp-uniform: narrow layers skip the empty columns
-    unsigned v[32];
-    tmem_ld32(G.tmem + ((qd * 32u) << 16) + h * half + ch * 32u, v);
-    if (!valid) continue;
-    const bool full_row = col0 + 32 <= K;
-    if (!bf16_out) {
-      float* out = reinterpret_cast<float*>(D->y) + orow * K + col0;
-      if (full_row && (K % 4) == 0) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          st_stream(reinterpret_cast<uint4*>(out) + e,
-                    make_uint4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]));
-      } else {
-#pragma unroll
-        for (unsigned e = 0; e < 32; ++e)
-          if (col0 + e < K) out[e] = __uint_as_float(v[e]);
-      }
-    } else {
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(D->y) + orow * K + col0;
-      if (full_row && (K % 8) == 0) {
-        unsigned pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-          pk[e] = *reinterpret_cast<const unsigned*>(&t2);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          st_stream(reinterpret_cast<uint4*>(out) + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]));
-      } else {
-#pragma unroll
-        for (unsigned e = 0; e < 32; ++e)
-          if (col0 + e < K) out[e] = __float2bfloat16_rn(__uint_as_float(v[e]));
-      }
-    }
-  }
+  // The tile's rows are consecutive rows of the [N P Q, K] output: the
+  // GEMM body's staged, coalesced epilogue applies as is.
+  epilogue_staged(G, tid, m0, kt * kGemmTile, D->pixels, D->k, D->k, (D->flags & kConvOutBf16) != 0,
+                  reinterpret_cast<void*>(D->y));
   tc_fence_before();
   G.kb_used = g0 + nk;
   G.accum_used += 1;
-  cluster_sync_all();  // both patches written, both TMEMs read
+  cluster_sync_all();  // both halves written, both TMEMs read
 }
 
 }  // namespace gpuos_dev_impl

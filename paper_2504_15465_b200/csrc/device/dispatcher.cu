@@ -1279,6 +1279,24 @@ EncodeTiledFn tensor_map_encoder() {
   return encode;
 }
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                    cuuint32_t, cuuint32_t, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn im2col_map_encoder() {
+  static EncodeIm2colFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<EncodeIm2colFn>(fn);
+  }
+  return encode;
+}
+
 void record_spans(gpuos_dev* d, const DevCtl& c) {
   const bool ok = c.t_enter != ~0ull && c.t_exit >= c.t_enter;
   d->stats.worker_span_ns = ok ? static_cast<int64_t>(c.t_exit - c.t_enter) : 0;
@@ -2147,30 +2165,28 @@ int gpuos_dev_conv_desc(gpuos_dev* d, const void* x, const void* w, void* y, int
   if (tmem_cols_for(d->cfg.workers_per_sm) < kGemmTile ||
       d->topo.smem_per_worker < static_cast<int>(1024 + kGemmStageBytes))
     return fail(GPUOS_E_CONFIG, "workers cannot host a conv stage");
+  if (r > 128 || s > 128 || pad > 127) return fail(GPUOS_E_CONFIG, "conv filter or padding too large");
   EncodeTiledFn encode = tensor_map_encoder();
-  if (!encode) return fail(GPUOS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  auto pow2 = [](unsigned v) {
-    unsigned p2 = 1;
-    while (p2 < v) p2 <<= 1;
-    return p2;
-  };
+  EncodeIm2colFn encode_im2col = im2col_map_encoder();
+  if (!encode || !encode_im2col) return fail(GPUOS_E_CUDA, "cuTensorMapEncode* unavailable");
   ConvDesc hd{};
-  hd.wb = std::min(128u, pow2(static_cast<unsigned>(Q)));
-  hd.hb = std::min(128u / hd.wb, pow2(static_cast<unsigned>(P)));
-  hd.nb = 128u / (hd.wb * hd.hb);
   const unsigned cb = (static_cast<unsigned>(c) + kGemmBK - 1) / kGemmBK;
   {
+    // im2col: the bounding box of window origins is [-pad, dim + pad - (F - 1))
+    // per spatial dim ({W, H} order), walked with the conv stride.
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(wd),
                                 static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2,
                                    static_cast<cuuint64_t>(c) * 2 * wd,
                                    static_cast<cuuint64_t>(c) * 2 * wd * h};
-    const cuuint32_t box[4] = {kGemmBK, hd.wb * stride, hd.hb * stride, hd.nb};
+    const int lower[2] = {-pad, -pad};
+    const int upper[2] = {pad - (s - 1), pad - (r - 1)};
     const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
-    if (encode(&hd.act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
-               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the conv activations");
+    if (encode_im2col(&hd.act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
+                      lower, upper, kGemmBK, kGemmHalf, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeIm2col rejected the conv activations");
   }
   {
     const uint64_t kdim = static_cast<uint64_t>(r) * s * cb * kGemmBK;
@@ -2186,11 +2202,10 @@ int gpuos_dev_conv_desc(gpuos_dev* d, const void* x, const void* w, void* y, int
   hd.y = reinterpret_cast<unsigned long long>(y);
   hd.n = n; hd.h = h; hd.w = wd; hd.c = c; hd.k = k; hd.r = r; hd.s = s;
   hd.pad = pad; hd.stride = stride; hd.p = P; hd.q = Q;
-  hd.tiles_q = (Q + hd.wb - 1) / hd.wb;
-  hd.tiles_p = (P + hd.hb - 1) / hd.hb;
-  const unsigned tiles_n = (n + hd.nb - 1) / hd.nb;
-  hd.patches = hd.tiles_q * hd.tiles_p * tiles_n;
-  hd.pair_tiles = (hd.patches + 1) / 2;
+  const uint64_t pixels = static_cast<uint64_t>(n) * P * Q;
+  if (pixels > 0x7fffffffull) return fail(GPUOS_E_CONFIG, "conv output too large");
+  hd.pixels = static_cast<unsigned>(pixels);
+  hd.pair_tiles = static_cast<unsigned>((pixels + kGemmTile - 1) / kGemmTile);
   hd.k_tiles = (static_cast<unsigned>(k) + kGemmTile - 1) / kGemmTile;
   hd.c_blocks = cb;
   hd.flags = flags & kConvOutBf16;

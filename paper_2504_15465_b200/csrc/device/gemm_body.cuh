@@ -198,6 +198,72 @@ __device__ __forceinline__ void gemm_pipe_init(GemmPipe& G, unsigned char* smem,
   }
 }
 
+// Accumulator -> global for one CTA's 128 rows of a pair tile (all 8
+// warps; the operand stages must be free). Warp w reads TMEM lanes
+// 32(w%4)..+31 and column half w/4. Rows cta_row0.. of a row-major [M, N]
+// matrix (ldc elements), columns col_base..col_base+255, ragged edges
+// masked.
+__device__ __forceinline__ void epilogue_staged(const GemmPipe& G, int tid, unsigned cta_row0,
+                                                unsigned col_base, unsigned M, unsigned N,
+                                                unsigned ldc, bool bf16_out, void* C) {
+  const int warp = tid >> 5, lane = tid & 31;
+  const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
+  constexpr unsigned half = kGemmTile / 2;
+  const unsigned row0 = cta_row0 + q * 32;  // warp's first row
+  // Staged through shared memory (the operand stages are free now): each
+  // thread writes its row's values, then the warp stores two 256-byte rows
+  // per instruction -- coalesced, where storing straight from the TMEM
+  // registers wrote 32 scattered 16-byte pieces per instruction (9 us per
+  // tile, tools/gemm_batch.py timing hook).
+  const unsigned esz = bf16_out ? 2u : 4u;
+  const unsigned pass_cols = 256u / esz;                 // 256 bytes of a row per pass
+  unsigned char* stg = G.tiles + static_cast<unsigned>(warp) * (32u * kEpiRowBytes);
+  const bool vec_ok = (static_cast<size_t>(ldc) * esz) % 16 == 0;
+#pragma unroll 1
+  for (unsigned pc = 0; pc < half; pc += pass_cols) {
+    if (col_base + h * half + pc >= N) break;  // warp-uniform: ragged last tile
+#pragma unroll 1
+    for (unsigned ch = 0; ch < pass_cols / 32; ++ch) {
+      unsigned v[32];
+      tmem_ld32(G.tmem + ((q * 32u) << 16) + h * half + pc + ch * 32u, v);
+      uint4* dst = reinterpret_cast<uint4*>(stg + static_cast<unsigned>(lane) * kEpiRowBytes + ch * 32u * esz);
+      if (bf16_out) {
+        unsigned pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const __nv_bfloat162 t = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+          pk[i] = *reinterpret_cast<const unsigned*>(&t);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
+    }
+    __syncwarp();
+    // 16 lanes per row, 16 bytes each: rows 2i and 2i + 1 per instruction.
+    const unsigned seg = static_cast<unsigned>(lane) & 15u;
+    const unsigned col = col_base + h * half + pc + seg * (16u / esz);
+#pragma unroll 4
+    for (unsigned i = 0; i < 16; ++i) {
+      const unsigned r = 2 * i + (static_cast<unsigned>(lane) >> 4);
+      const unsigned grow = row0 + r;
+      if (grow >= M || col >= N) continue;
+      const uint4 val = *reinterpret_cast<const uint4*>(stg + r * kEpiRowBytes + seg * 16u);
+      unsigned char* out = reinterpret_cast<unsigned char*>(C) + (static_cast<size_t>(grow) * ldc + col) * esz;
+      if (vec_ok && col + 16u / esz <= N) {
+        st_stream(reinterpret_cast<uint4*>(out), val);
+      } else {
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(&val);
+        for (unsigned e = 0; e < 16u / esz && col + e < N; ++e)
+          for (unsigned byte = 0; byte < esz; ++byte) out[e * esz + byte] = src[e * esz + byte];
+      }
+    }
+    __syncwarp();  // staging reused by the next pass
+  }
+}
+
 // Both CTAs of the pair, all threads; rank 0 is the leader.
 __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G) {
   const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
@@ -266,64 +332,8 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   mbar_wait_bounded(G.accum, G.accum_used & 1u);
   tc_fence_after();
   if (tm && tid == 0) tm[2] = gtimer();
-  const int warp = tid >> 5, lane = tid & 31;
-  const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
-  constexpr unsigned half = kGemmTile / 2;
-  const unsigned row0 = mt * kGemmTile + rank * kGemmHalf + q * 32;  // warp's first row
-  const unsigned M = D->m, N = D->n, ldc = D->ldc;
-  const bool bf16_out = (D->flags & kGemmOutBf16) != 0;
-  // Staged through shared memory (the operand stages are free now): each
-  // thread writes its row's values, then the warp stores two 256-byte rows
-  // per instruction -- coalesced, where storing straight from the TMEM
-  // registers wrote 32 scattered 16-byte pieces per instruction (9 us per
-  // tile, tools/gemm_batch.py timing hook).
-  const unsigned esz = bf16_out ? 2u : 4u;
-  const unsigned pass_cols = 256u / esz;                 // 256 bytes of a row per pass
-  unsigned char* stg = G.tiles + static_cast<unsigned>(warp) * (32u * kEpiRowBytes);
-  const bool vec_ok = (static_cast<size_t>(ldc) * esz) % 16 == 0;
-#pragma unroll 1
-  for (unsigned pc = 0; pc < half; pc += pass_cols) {
-    if (nt * kGemmTile + h * half + pc >= N) break;  // warp-uniform: ragged last tile
-#pragma unroll 1
-    for (unsigned ch = 0; ch < pass_cols / 32; ++ch) {
-      unsigned v[32];
-      tmem_ld32(G.tmem + ((q * 32u) << 16) + h * half + pc + ch * 32u, v);
-      uint4* dst = reinterpret_cast<uint4*>(stg + static_cast<unsigned>(lane) * kEpiRowBytes + ch * 32u * esz);
-      if (bf16_out) {
-        unsigned pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const __nv_bfloat162 t = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          pk[i] = *reinterpret_cast<const unsigned*>(&t);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-      }
-    }
-    __syncwarp();
-    // 16 lanes per row, 16 bytes each: rows 2i and 2i + 1 per instruction.
-    const unsigned seg = static_cast<unsigned>(lane) & 15u;
-    const unsigned col = nt * kGemmTile + h * half + pc + seg * (16u / esz);
-#pragma unroll 4
-    for (unsigned i = 0; i < 16; ++i) {
-      const unsigned r = 2 * i + (static_cast<unsigned>(lane) >> 4);
-      const unsigned grow = row0 + r;
-      if (grow >= M || col >= N) continue;
-      const uint4 val = *reinterpret_cast<const uint4*>(stg + r * kEpiRowBytes + seg * 16u);
-      unsigned char* out = reinterpret_cast<unsigned char*>(D->c) + (static_cast<size_t>(grow) * ldc + col) * esz;
-      if (vec_ok && col + 16u / esz <= N) {
-        st_stream(reinterpret_cast<uint4*>(out), val);
-      } else {
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(&val);
-        for (unsigned e = 0; e < 16u / esz && col + e < N; ++e)
-          for (unsigned byte = 0; byte < esz; ++byte) out[e * esz + byte] = src[e * esz + byte];
-      }
-    }
-    __syncwarp();  // staging reused by the next pass
-  }
+  epilogue_staged(G, tid, mt * kGemmTile + rank * kGemmHalf, nt * kGemmTile, D->m, D->n, D->ldc,
+                  (D->flags & kGemmOutBf16) != 0, reinterpret_cast<void*>(D->c));
   tc_fence_before();  // the next tile's MMAs overwrite this accumulator
   if (tm) {
     __syncthreads();

@@ -4,7 +4,7 @@ sim.cpp:86-156 / workload.hpp:38-44 -- plus the B200 "body" extension that
 the reference ignores). Every kernel is one tenant launch; its blocks are
 the body's real grid:
 
-  conv_bf16  NHWC implicit GEMM, 256 pixels x 256 channels per block
+  conv_bf16  NHWC implicit GEMM (TMA im2col), 256 pixels x 256 channels per block
   gemm_bf16  256 x 256 output tile per block
   gemv_bf16  256 rows of W per block (x split-K)
   stream     HBM-bound elementwise (norms, activations, residuals, pooling,
@@ -30,22 +30,12 @@ TPC_GBS = 6550.0 / 74         # measured HBM bandwidth per TPC
 STREAM_WORDS = 16384          # u32 words per STREAM block (64 KiB in, 64 KiB out)
 
 
-def _pow2(v: int) -> int:
-    p = 1
-    while p < v:
-        p <<= 1
-    return p
-
-
 def conv_blocks(n, h, w, c, k, r, s, pad, stride) -> tuple[int, int, int]:
-    """Grid of gpuos_dev_conv_desc (conv_body.cuh): (blocks, P, Q)."""
+    """Grid of gpuos_dev_conv_desc (conv_body.cuh): (blocks, P, Q) -- pair
+    tiles of 256 consecutive output pixels (TMA im2col) x 256 channels."""
     P = (h + 2 * pad - r) // stride + 1
     Q = (w + 2 * pad - s) // stride + 1
-    wb = min(128, _pow2(Q))
-    hb = min(128 // wb, _pow2(P))
-    nb = 128 // (wb * hb)
-    patches = math.ceil(Q / wb) * math.ceil(P / hb) * math.ceil(n / nb)
-    return math.ceil(patches / 2) * math.ceil(k / 256), P, Q
+    return math.ceil(n * P * Q / 256) * math.ceil(k / 256), P, Q
 
 
 def gemm_blocks(m, n, k) -> int:

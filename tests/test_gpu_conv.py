@@ -1,5 +1,5 @@
 """Convolution atom body (NHWC implicit GEMM on the TPC pair's tensor cores,
-4-D TMA boxes per filter tap, padding = TMA zero fill) checked against
+TMA im2col loads per filter tap, padding = TMA zero fill) checked against
 torch's float64 conv2d of the same bf16 inputs. Tolerance: fp32 output
 max |y - ref| <= 1e-3 max |ref|, relative Frobenius <= 1e-5; bf16 output
 within one rounding. Shapes cover ResNet-50 stages (3x3 and 1x1, stride 1
@@ -30,9 +30,11 @@ CASES = [
     (1, 56, 56, 64, 64, 3, 3, 1, 1, True),
     (2, 28, 28, 128, 256, 1, 1, 0, 1, False),
     (2, 28, 28, 128, 128, 3, 3, 1, 2, False),     # stride 2: 28 -> 14
-    (4, 7, 7, 512, 512, 3, 3, 1, 1, True),        # 7x7 maps: patches span images
+    (4, 7, 7, 512, 512, 3, 3, 1, 1, True),        # 7x7 maps: tiles span images
     (1, 32, 32, 8, 64, 7, 7, 3, 2, False),        # stem-like: C = 3 padded to 8, 7x7 s2
     (3, 10, 12, 72, 300, 3, 3, 1, 1, False),      # ragged everything
+    (1, 7, 7, 256, 256, 3, 3, 1, 1, False),       # 49 pixels: the peer's rows are all past the end
+    (2, 28, 28, 256, 512, 1, 1, 0, 2, True),      # 1x1 stride-2 downsample
 ]
 
 

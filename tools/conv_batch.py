@@ -1,5 +1,5 @@
 """Batch-mode launches of the worker kernel executing an NHWC implicit-GEMM
-convolution (tcgen05 pair tiles, 4-D TMA boxes per filter tap) atomized over
+convolution (tcgen05 pair tiles, TMA im2col loads per filter tap) atomized over
 all 74 TPCs; prints ms and TFLOP/s (algorithmic: 2 N P Q K R S C).
 
 usage: conv_batch.py N H W C K R S pad stride [launches]"""
