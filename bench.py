@@ -516,7 +516,8 @@ def conv_saturation(api, local: int, args) -> dict:
                 best, span = tf, dev.stats().worker_span_ns * 1e-9
         dev.free(desc)
     return {"bound": "tensor", "achieved": best, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": best / pk["bf16_tflops"], "traffic": None,
+            "frac": best / pk["bf16_tflops"],
+            "traffic": ncu_traffic("conv", f"n{n} {h}x{w}x{c} k{k} {r}x{s_}/{st}"),
             "algorithmic_bytes": 2 * (n * h * w * c + k * r * s_ * c + n * P * Q * k),
             "note": f"conv n{n} {h}x{w}x{c} -> {P}x{Q}x{k} {r}x{s_}/{st} (bf16 out) as {blocks} pair tiles "
                     f"of 256 pixels x 256 channels (TMA im2col, tcgen05.mma.cta_group::2) in {n_atoms} atoms "
