@@ -43,6 +43,7 @@ struct alignas(128) ConvDesc {
   unsigned n, h, w, c, k, r, s, pad, stride, p, q;
   unsigned pixels;               // N P Q
   unsigned pair_tiles, k_tiles, c_blocks, flags;
+  unsigned n_tile;               // output channels per block: 64, 128 or 256
 };
 
 __device__ __forceinline__ void tma_load_im2col_pair(void* dst, const CUtensorMap* map, int c0, int w0,
@@ -79,7 +80,9 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->wgt) : "memory");
     const int st = static_cast<int>(D->stride), pad = static_cast<int>(D->pad);
     const int w0 = static_cast<int>(q0) * st - pad, h0 = static_cast<int>(p0) * st - pad;
-    const int k_row = static_cast<int>(kt * kGemmTile + rank * kGemmHalf);
+    const unsigned n_tile = D->n_tile;
+    const int k_row = static_cast<int>(kt * n_tile + rank * (n_tile / 2));
+    const unsigned tx = 2 * (kGemmABytes + n_tile / 2 * kGemmBK * 2);  // both CTAs' A and B halves
     const unsigned cb_count = D->c_blocks;
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned tap = j / cb_count, cb = j - tap * cb_count;
@@ -89,14 +92,14 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
       const unsigned long long r = k / S;
       if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
       unsigned char* stg = G.tiles + s * kGemmStageBytes;
-      if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemmStageBytes);
+      if (rank == 0) mbar_expect_tx(G.full + s, tx);
       tma_load_im2col_pair(stg, &D->act, static_cast<int>(cb * kGemmBK), w0, h0, static_cast<int>(n0),
                            static_cast<unsigned short>(ss), static_cast<unsigned short>(rr), G.full + s);
       tma_load_2d_pair(stg + kGemmABytes, &D->wgt, static_cast<int>(j * kGemmBK), k_row, G.full + s);
     }
   } else if (tid == 32 && rank == 0) {
     tc_fence_after();
-    const unsigned idesc = umma_idesc_bf16(kGemmTile, kGemmTile);
+    const unsigned idesc = umma_idesc_bf16(kGemmTile, D->n_tile);
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
@@ -117,8 +120,9 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
   tc_fence_after();
   // The tile's rows are consecutive rows of the [N P Q, K] output: the
   // GEMM body's staged, coalesced epilogue applies as is.
-  epilogue_staged(G, tid, m0, kt * kGemmTile, D->pixels, D->k, D->k, (D->flags & kConvOutBf16) != 0,
-                  reinterpret_cast<void*>(D->y));
+  const unsigned col0 = kt * D->n_tile;
+  epilogue_staged(G, tid, m0, col0, D->pixels, D->k - col0 < D->n_tile ? D->k : col0 + D->n_tile, D->k,
+                  (D->flags & kConvOutBf16) != 0, reinterpret_cast<void*>(D->y));
   tc_fence_before();
   G.kb_used = g0 + nk;
   G.accum_used += 1;

@@ -1304,6 +1304,9 @@ void record_spans(gpuos_dev* d, const DevCtl& c) {
       ok && c.t_first_block != ~0ull ? static_cast<int64_t>(c.t_first_block - c.t_enter) : 0;
 }
 
+// UMMA N for a pair tile over `cols` output columns: 64, 128 or 256.
+unsigned narrow_tile(int64_t cols) { return cols <= 64 ? 64u : cols <= 128 ? 128u : kGemmTile; }
+
 // TMEM columns per worker: the largest power of two <= 512 / W (>= 32).
 unsigned tmem_cols_for(int workers_per_sm) {
   unsigned c = 512;
@@ -2056,7 +2059,9 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
   const unsigned cols = tmem_cols_for(d->cfg.workers_per_sm);
   if (cols < kGemmTile || d->topo.smem_per_worker < static_cast<int>(1024 + kGemmStageBytes))
     return fail(GPUOS_E_CONFIG, "workers cannot host a GEMM stage");
-  const unsigned n_tile = kGemmTile;
+  // Narrow outputs (attention heads, narrow layers) take a 64- or 128-wide
+  // UMMA N so the tensor cores do not compute padding columns.
+  const unsigned n_tile = narrow_tile(n);
 
   EncodeTiledFn encode = tensor_map_encoder();
   if (!encode) return fail(GPUOS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -2070,7 +2075,7 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   };
-  if (make(&h.a, a, m, kGemmHalf) != CUDA_SUCCESS || make(&h.b, b, n, kGemmHalf) != CUDA_SUCCESS)
+  if (make(&h.a, a, m, kGemmHalf) != CUDA_SUCCESS || make(&h.b, b, n, n_tile / 2) != CUDA_SUCCESS)
     return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the GEMM operands");
   h.c = reinterpret_cast<unsigned long long>(c);
   h.m = static_cast<unsigned>(m);
@@ -2170,6 +2175,7 @@ int gpuos_dev_conv_desc(gpuos_dev* d, const void* x, const void* w, void* y, int
   EncodeIm2colFn encode_im2col = im2col_map_encoder();
   if (!encode || !encode_im2col) return fail(GPUOS_E_CUDA, "cuTensorMapEncode* unavailable");
   ConvDesc hd{};
+  hd.n_tile = narrow_tile(k);
   const unsigned cb = (static_cast<unsigned>(c) + kGemmBK - 1) / kGemmBK;
   {
     // im2col: the bounding box of window origins is [-pad, dim + pad - (F - 1))
@@ -2192,7 +2198,7 @@ int gpuos_dev_conv_desc(gpuos_dev* d, const void* x, const void* w, void* y, int
     const uint64_t kdim = static_cast<uint64_t>(r) * s * cb * kGemmBK;
     const cuuint64_t dims[2] = {kdim, static_cast<cuuint64_t>(k)};
     const cuuint64_t strides[1] = {kdim * 2};
-    const cuuint32_t box[2] = {kGemmBK, kGemmHalf};
+    const cuuint32_t box[2] = {kGemmBK, hd.n_tile / 2};
     const cuuint32_t estr[2] = {1, 1};
     if (encode(&hd.wgt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box,
                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -2206,7 +2212,7 @@ int gpuos_dev_conv_desc(gpuos_dev* d, const void* x, const void* w, void* y, int
   if (pixels > 0x7fffffffull) return fail(GPUOS_E_CONFIG, "conv output too large");
   hd.pixels = static_cast<unsigned>(pixels);
   hd.pair_tiles = static_cast<unsigned>((pixels + kGemmTile - 1) / kGemmTile);
-  hd.k_tiles = (static_cast<unsigned>(k) + kGemmTile - 1) / kGemmTile;
+  hd.k_tiles = (static_cast<unsigned>(k) + hd.n_tile - 1) / hd.n_tile;
   hd.c_blocks = cb;
   hd.flags = flags & kConvOutBf16;
   void* pdev = nullptr;

@@ -50,7 +50,7 @@ struct alignas(128) GemmDesc {
   CUtensorMap b;                 // B [N, K] bf16: box {64, 128}, SWIZZLE_128B
   unsigned long long c;          // C [M, N] row-major (ldc elements)
   unsigned m, n, k, ldc;
-  unsigned m_tiles, n_tiles, n_tile, flags;  // 256-wide tiles; flags bit 0: bf16 output
+  unsigned m_tiles, n_tiles, n_tile, flags;  // n_tile: 64, 128 or 256 columns; flags bit 0: bf16 output
   unsigned long long* timing;    // optional: 4 globaltimer stamps per tile (profiling)
 };
 constexpr unsigned kGemmOutBf16 = 1u;
@@ -206,6 +206,7 @@ __device__ __forceinline__ void gemm_pipe_init(GemmPipe& G, unsigned char* smem,
 __device__ __forceinline__ void epilogue_staged(const GemmPipe& G, int tid, unsigned cta_row0,
                                                 unsigned col_base, unsigned M, unsigned N,
                                                 unsigned ldc, bool bf16_out, void* C) {
+  // (N here is the tile's column limit: min(matrix N, col_base + tile width).)
   const int warp = tid >> 5, lane = tid & 31;
   const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
   constexpr unsigned half = kGemmTile / 2;
@@ -267,7 +268,7 @@ __device__ __forceinline__ void epilogue_staged(const GemmPipe& G, int tid, unsi
 // Both CTAs of the pair, all threads; rank 0 is the leader.
 __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G) {
   const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
-  const unsigned m_tiles = D->m_tiles, n_tiles = D->n_tiles;
+  const unsigned m_tiles = D->m_tiles, n_tiles = D->n_tiles, n_tile = D->n_tile;
   const unsigned blk = static_cast<unsigned>(c.block);
   // Grouped raster: blocks walk 8 M-tiles down an N column before moving
   // right, so ~150 concurrent tiles touch 8 A panels and ~18 B panels (fits
@@ -294,14 +295,15 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->a) : "memory");
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->b) : "memory");
     const int a_row = static_cast<int>(mt * kGemmTile + rank * kGemmHalf);
-    const int b_row = static_cast<int>(nt * kGemmTile + rank * kGemmHalf);
+    const int b_row = static_cast<int>(nt * n_tile + rank * (n_tile / 2));
+    const unsigned tx = 2 * (kGemmABytes + n_tile / 2 * kGemmBK * 2);  // both CTAs' A and B halves
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;
       if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
       unsigned char* st = G.tiles + s * kGemmStageBytes;
-      if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemmStageBytes);  // both halves
+      if (rank == 0) mbar_expect_tx(G.full + s, tx);
       const int kc = static_cast<int>(j * kGemmBK);
       tma_load_2d_pair(st, &D->a, kc, a_row, G.full + s);
       tma_load_2d_pair(st + kGemmABytes, &D->b, kc, b_row, G.full + s);
@@ -309,7 +311,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   } else if (tid == 32 && rank == 0) {
     // MMA issuer: one thread of the leader drives both SMs' tensor cores.
     tc_fence_after();
-    const unsigned idesc = umma_idesc_bf16(kGemmTile, kGemmTile);
+    const unsigned idesc = umma_idesc_bf16(kGemmTile, n_tile);
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
@@ -332,7 +334,9 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   mbar_wait_bounded(G.accum, G.accum_used & 1u);
   tc_fence_after();
   if (tm && tid == 0) tm[2] = gtimer();
-  epilogue_staged(G, tid, mt * kGemmTile + rank * kGemmHalf, nt * kGemmTile, D->m, D->n, D->ldc,
+  const unsigned col0 = nt * n_tile;
+  epilogue_staged(G, tid, mt * kGemmTile + rank * kGemmHalf, col0, D->m,
+                  D->n - col0 < n_tile ? D->n : col0 + n_tile, D->ldc,
                   (D->flags & kGemmOutBf16) != 0, reinterpret_cast<void*>(D->c));
   tc_fence_before();  // the next tile's MMAs overwrite this accumulator
   if (tm) {

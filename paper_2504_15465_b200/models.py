@@ -30,16 +30,22 @@ TPC_GBS = 6550.0 / 74         # measured HBM bandwidth per TPC
 STREAM_WORDS = 16384          # u32 words per STREAM block (64 KiB in, 64 KiB out)
 
 
+def n_tile(cols: int) -> int:
+    """UMMA N of a pair tile over `cols` output columns (dispatcher.cu
+    narrow_tile): narrow outputs do not compute padding columns."""
+    return 64 if cols <= 64 else 128 if cols <= 128 else 256
+
+
 def conv_blocks(n, h, w, c, k, r, s, pad, stride) -> tuple[int, int, int]:
     """Grid of gpuos_dev_conv_desc (conv_body.cuh): (blocks, P, Q) -- pair
-    tiles of 256 consecutive output pixels (TMA im2col) x 256 channels."""
+    tiles of 256 consecutive output pixels (TMA im2col) x n_tile(k) channels."""
     P = (h + 2 * pad - r) // stride + 1
     Q = (w + 2 * pad - s) // stride + 1
-    return math.ceil(n * P * Q / 256) * math.ceil(k / 256), P, Q
+    return math.ceil(n * P * Q / 256) * math.ceil(k / n_tile(k)), P, Q
 
 
 def gemm_blocks(m, n, k) -> int:
-    return math.ceil(m / 256) * math.ceil(n / 256)
+    return math.ceil(m / 256) * math.ceil(n / n_tile(n))
 
 
 def gemv_blocks(n, k, splits) -> int:
@@ -63,7 +69,7 @@ class Builder:
     def conv(self, n, h, w, c, k, r, s, pad, stride) -> tuple[int, int]:
         blocks, P, Q = conv_blocks(n, h, w, c, k, r, s, pad, stride)
         cb = math.ceil(c / 64) * 64
-        tile_flops = 2.0 * 256 * 256 * r * s * cb
+        tile_flops = 2.0 * 256 * n_tile(k) * r * s * cb
         self.kernels.append({
             "blocks": blocks, "block_us": round(tile_flops / (TPC_TFLOPS * 1e6), 3), "s": 0.9, "occ": 2,
             "body": {"kind": "conv_bf16", "ws": self._next(), "p": [n, h, w, c, k, r, s, pad, stride]}})
@@ -72,7 +78,7 @@ class Builder:
     def gemm(self, m, n, k) -> None:
         self.kernels.append({
             "blocks": gemm_blocks(m, n, k),
-            "block_us": round(2.0 * 256 * 256 * k / (TPC_TFLOPS * 1e6), 3), "s": 0.9, "occ": 2,
+            "block_us": round(2.0 * 256 * n_tile(n) * k / (TPC_TFLOPS * 1e6), 3), "s": 0.9, "occ": 2,
             "body": {"kind": "gemm_bf16", "ws": self._next(), "p": [m, n, k]}})
 
     def gemv(self, n, k, splits=1) -> None:

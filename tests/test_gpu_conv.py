@@ -35,6 +35,8 @@ CASES = [
     (3, 10, 12, 72, 300, 3, 3, 1, 1, False),      # ragged everything
     (1, 7, 7, 256, 256, 3, 3, 1, 1, False),       # 49 pixels: the peer's rows are all past the end
     (2, 28, 28, 256, 512, 1, 1, 0, 2, True),      # 1x1 stride-2 downsample
+    (2, 56, 56, 64, 64, 3, 3, 1, 1, False),       # 64-wide channel tiles
+    (2, 28, 28, 128, 96, 3, 3, 1, 1, True),       # 128-wide tiles, ragged K
 ]
 
 

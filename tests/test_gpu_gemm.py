@@ -66,6 +66,8 @@ def random_atoms(rng, blocks, n_atoms):
     (300, 200, 72, True, 2),      # ragged M / N tiles, K not a multiple of 64
     (1024, 768, 1024, False, 1),  # 1 worker per SM: deeper ring
     (640, 384, 520, True, 1),
+    (1000, 64, 384, False, 2),    # 64-wide tiles (attention-head output)
+    (520, 100, 128, True, 2),     # 128-wide tiles, ragged N
 ])
 def test_gemm_atoms_match_reference(api, cuda_device, m, n, k, bf16_out, workers):
     import torch
@@ -77,7 +79,7 @@ def test_gemm_atoms_match_reference(api, cuda_device, m, n, k, bf16_out, workers
     with api.Device(workers_per_sm=workers) as dev:
         desc, blocks, tm, tn = dev.gemm_desc(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k,
                                              bf16_out=bf16_out)
-        assert tm == 256 and tn == 256
+        assert tm == 256 and tn == (64 if n <= 64 else 128 if n <= 128 else 256)
         assert blocks == -(-m // tm) * -(-n // tn)
         trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
         atoms = random_atoms(rng, blocks, min(blocks, 7))
