@@ -26,7 +26,8 @@ import os
 from typing import Any
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libgpuos_b200.so")
+# GPUOS_LIB overrides the in-tree library (A/B builds of the same tree).
+LIB_PATH = os.environ.get("GPUOS_LIB") or os.path.join(PKG, "lib", "libgpuos_b200.so")
 
 GPUOS_BODY_STREAM = 1
 GPUOS_BODY_GEMM_BF16 = 2

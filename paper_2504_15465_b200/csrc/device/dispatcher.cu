@@ -150,7 +150,6 @@ struct Params {
   int idle_sleep_ns;
   unsigned smem_bytes;  // dynamic shared memory per worker (STREAM / GEMM rings)
   unsigned tmem_cols;   // TMEM columns each worker owns (GEMM accumulator)
-  unsigned long long* dbg;  // profiling: 5 words per block (gpuos_dev_debug_stamps), or null
 };
 
 __device__ __forceinline__ void st_release_gpu64(unsigned long long* p, unsigned long long v) {
@@ -160,13 +159,6 @@ __device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-
-// %globaltimer read that waits for `dep` (profiling stamps).
-__device__ __forceinline__ unsigned long long gtimer_after(unsigned dep) {
-  unsigned long long t;
-  asm volatile("{ .reg .u32 d; mov.u32 d, %1; mov.u64 %0, %%globaltimer; }" : "=l"(t) : "r"(dep) : "memory");
-  return t;
-}
 
 __device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) {
   return static_cast<unsigned long long>(lo) | (static_cast<unsigned long long>(hi) << 32);
@@ -480,6 +472,7 @@ struct WorkerShared {
   unsigned long long join_full; // mbarrier (peer): leader posted join_rc
   unsigned long long joined;    // mbarrier (leader): peer took the request
   int go;                       // WorkerGo
+  unsigned long long touched_key;  // warp 0: atom whose `touched` word has this TPC
   unsigned tmem_base;           // this worker's TMEM columns (tcgen05.alloc)
 };
 
@@ -855,7 +848,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   unsigned long long spread_since = 0;  // leader: deferring a pair tile since
   bool tc_hold = false;                 // leader thread 0: holds the TPC's tensor reservation
   bool handoff = false;                 // warp 0: sh.rc holds a chained successor's block 0
-  unsigned long long touched_key = 0ull;  // warp 0 lane 0: atom whose `touched` has our TPC
 
   for (;;) {
     // %smid can change if the CTA is ever preempted and restored elsewhere;
@@ -867,7 +859,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     }
     if (tpc != cur_tpc) {
       cur_key = 0ull;
-      touched_key = 0ull;
+      if (tid == 0) sh.touched_key = 0ull;
       cur_tpc = tpc;
     }
     if (warp == 0) {
@@ -879,20 +871,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
         cur_key = 0ull;
         cur_body = __shfl_sync(0xffffffffu, sh.rc.cmd.body, 0);
         go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
-        const bool want = go == kGoPair && cur_body != GPUOS_BODY_GEMV_BF16;
-        if (lane == 0 && want != tc_hold) {  // (a tensor predecessor's reservation carries over)
-          if (want) {
-            if (atomicAdd(p.tc_busy + tpc, 1u) == 0u) atomicAdd(&p.ctl->tc_active, 1u);
-          } else if (atomicSub(p.tc_busy + tpc, 1u) == 1u) {
-            atomicSub(&p.ctl->tc_active, 1u);
-          }
-          tc_hold = want;
+        if (go == kGoPair && cur_body != GPUOS_BODY_GEMV_BF16 && lane == 0) {
+          if (atomicAdd(p.tc_busy + tpc, 1u) == 0u) atomicAdd(&p.ctl->tc_active, 1u);
+          tc_hold = true;
         }
       } else if (tpc >= 0) {
         unsigned long long* list = p.resident + static_cast<size_t>(tpc) * kResident;
-        const unsigned long long dbg_top = p.dbg ? gtimer() : 0;
         unsigned ver = ld_acquire_gpu(p.version + tpc);  // latest observed
-        const unsigned long long dbg_ver = p.dbg ? gtimer_after(ver) : 0;
         for (;;) {
           // The peer serves a posted pair tile before anything else.
           if (rank != 0 && mbar_test_cluster(&sh.join_full, joins & 1u)) {
@@ -903,13 +888,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
           unsigned got = 0;
           unsigned long long key = 0ull;
           bool stale = false;
-          // Fast path: next slice of the atom being drained -- for a 2-SM
-          // body only on the leader, which then keeps the TPC's tensor-core
-          // reservation from the previous tile (a pair tile otherwise pays a
-          // list scan, a reservation and a claim round trip each). The
+          // Fast path: next slice of the atom being drained (a GEMV tile
+          // only on the leader; GEMM / conv tiles go through the full
+          // arbitration, which takes the TPC's tensor-core reservation --
+          // keeping it across tiles measured 3 % slower on conv). The
           // version is re-read alongside the claim; a change noticed only
           // after it costs at most one slice of priority inversion.
-          const bool fast = cur_key != 0ull && ver == cur_ver && (rank == 0 || !body_is_pair(cur_body));
+          const bool fast = cur_key != 0ull && ver == cur_ver &&
+                            (!body_is_pair(cur_body) || (rank == 0 && cur_body == GPUOS_BODY_GEMV_BF16));
           if (fast) {
             if (lane == 0)
               off = claim_block(p.atoms + cur_slot, cur_key, cur_count, 1u, p.ctl, stale, got);
@@ -917,10 +903,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
             off = __shfl_sync(0xffffffffu, off, 0);
             if (off >= 0) key = cur_key;
             if (stale && lane == 0) sh.rc.key = 0ull;  // slot recycled: reload its fields
-          }
-          if (off < 0 && tc_hold && lane == 0) {  // not continuing a tensor atom here
-            if (atomicSub(p.tc_busy + tpc, 1u) == 1u) atomicSub(&p.ctl->tc_active, 1u);
-            tc_hold = false;
           }
           bool defer = false;  // peer: the winner is a 2-SM atom for the leader
           bool nothing = false;  // nothing eligible on this TPC
@@ -1057,13 +1039,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               const unsigned parts = sh.rc.cmd.parts;
               sh.rc.cmd.block = sh.rc.lo + off / parts;
               sh.rc.cmd.part = static_cast<unsigned>(off % parts);
-              if (p.dbg) {
-                p.dbg[8ull * static_cast<unsigned long long>(sh.rc.cmd.block) + 2] = gtimer();
-                p.dbg[8ull * static_cast<unsigned long long>(sh.rc.cmd.block) + 4] = blockIdx.x;
-                p.dbg[8ull * static_cast<unsigned long long>(sh.rc.cmd.block) + 5] = dbg_ver;
-                p.dbg[8ull * static_cast<unsigned long long>(sh.rc.cmd.block) + 6] = dbg_top;
-                p.dbg[8ull * static_cast<unsigned long long>(sh.rc.cmd.block) + 7] = fast ? 1 : 0;
-              }
             }
             cur_key = stale ? 0ull : key;
             cur_slot = slot;
@@ -1141,8 +1116,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
         }
         sh.go = go;
         sh.t_start = gtimer();
-        if (p.dbg && go != kGoExit && go != kGoJoin)
-          p.dbg[8ull * static_cast<unsigned long long>(sh.rc.cmd.block) + 3] = sh.t_start;
         if (go != kGoExit && first_start == ~0ull) first_start = sh.t_start;
       }
     }
@@ -1151,16 +1124,15 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     if (go == kGoExit) break;
     run_body(sh.rc, tid, rank, pipe, gemm, gemv);  // pair tiles end with a cluster barrier
     if (go == kGoPair || go == kGoJoin) ++joins;
-    // (A tensor tile's reservation is kept into the next decision: the
-    // leader releases it there unless it continues the same atom.)
+    if (tc_hold && tid == 0) {
+      if (atomicSub(p.tc_busy + tpc, 1u) == 1u) atomicSub(&p.ctl->tc_active, 1u);
+      tc_hold = false;
+    }
     __syncthreads();
     // The leader records pair tiles (the peer's half is complete: cluster
     // barrier at the end of the body).
     if (warp == 0 && go != kGoJoin) {
-      unsigned long long* dbg = p.dbg ? p.dbg + 8ull * static_cast<unsigned long long>(sh.rc.cmd.block) : nullptr;
-      if (dbg && lane == 0) dbg[0] = gtimer();
-      const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, n_blocks, busy, touched_key);
-      if (dbg && lane == 0) dbg[1] = gtimer();
+      const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, n_blocks, busy, sh.touched_key);
       if (done) cur_key = 0ull;  // the atom is done: rescan rather than claim from it
       handoff = done == 2;
     }
@@ -1246,7 +1218,6 @@ struct gpuos_dev {
   unsigned* version = nullptr;
   int* fence = nullptr;
   unsigned* tc_busy = nullptr;
-  unsigned long long* dbg = nullptr;  // gpuos_dev_debug_stamps (profiling only)
   DevCtl* ctl = nullptr;
   int* phys2log = nullptr;
   unsigned long long* gt_scratch = nullptr;
@@ -1574,7 +1545,6 @@ int gpuos_dev_start(gpuos_dev* d) {
   p.version = d->version;
   p.fence = d->fence;
   p.tc_busy = d->tc_busy;
-  p.dbg = d->dbg;
   p.ctl = d->ctl;
   p.phys2log = d->phys2log;
   p.ring = d->ring_d;
@@ -1844,7 +1814,6 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   p.version = d->version;
   p.fence = d->fence;
   p.tc_busy = d->tc_busy;
-  p.dbg = d->dbg;
   p.ctl = d->ctl;
   p.phys2log = d->phys2log;
   p.ring = d->ring_d;
@@ -2046,20 +2015,6 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
     ++n;
   }
   return n;
-}
-
-// Profiling hook (not part of the ABI header): per-block worker timestamps
-// (body end, accounted, claimed, joined; globaltimer) plus the claiming
-// CTA, 5 words per block id, for the next runs of this handle.
-int gpuos_dev_debug_stamps(gpuos_dev* d, uint64_t blocks, void** ptr) {
-  if (!d || !ptr) return fail(GPUOS_E_CONFIG, "null argument");
-  CUDA_TRY(cudaSetDevice(d->device));
-  if (d->dbg) cudaFree(d->dbg);
-  d->dbg = nullptr;
-  if (blocks) CUDA_TRY(cudaMalloc(&d->dbg, 8 * 8 * blocks));
-  if (blocks) CUDA_TRY(cudaMemset(d->dbg, 0, 8 * 8 * blocks));
-  *ptr = d->dbg;
-  return GPUOS_OK;
 }
 
 int gpuos_dev_get_stats(gpuos_dev* d, gpuos_dev_stats* out) {
