@@ -142,3 +142,35 @@ def test_chained_launches_with_contention_on_replay(api):
     assert a["report"] == b["report"]
     for app in a["report"]["apps"][:2]:
         assert app["completed"] >= app["offered"] - 1
+
+
+def test_chain_depth_limits_and_validation(api):
+    """chain_depth bounds how many kernels ride behind the running one; it
+    is validated like the reference's other knobs (ConfigError, code 2)."""
+    from paper_2504_15465_b200 import models
+
+    kernels = models.llama3_8b_decode(256)[:12]
+    cfg = {"name": "m", "device": {"gpc_count": 2, "tpcs_per_gpc": 37}, "policy": "full_system",
+           "horizon_ms": 50.0, "seed": 1, "scheduler": {"dvfs": False, "chain_launches": True},
+           "apps": [{"id": "t", "priority": "hp", "quota": 74, "slo_ms": 100.0,
+                     "arrival": {"times_ms": [0.0]}, "kernels": kernels}]}
+    outstanding = {}
+    for depth in (1, 4):
+        r = api.run({"scenario": {"config": cfg}, "backend": "replay", "log": True,
+                     "set": {"chain_depth": depth}})
+        assert r["report"]["apps"][0]["completed"] == 1
+        # Dispatched but not yet completed atoms at every dispatch: the
+        # running kernel plus at most `depth` chained behind it.
+        live, worst = set(), 0
+        for line in r["log"].splitlines():
+            f = line.split()
+            if f[0] == "D":
+                live.add(int(f[2]))
+                worst = max(worst, len(live))
+            elif f[0] == "C":
+                live.discard(int(f[2]))
+        outstanding[depth] = worst
+    assert outstanding[1] == 2 and outstanding[4] == 5
+    with pytest.raises(api.GpuosError) as e:
+        api.run({"scenario": {"config": cfg}, "backend": "replay", "set": {"chain_depth": 0}})
+    assert e.value.code == 2
