@@ -73,6 +73,7 @@ void apply_knob(ScenarioConfig& c, const std::string& k, const json& v) {
   else if (k == "block_revocation") s.block_revocation = flag();
   else if (k == "chain_launches") s.chain_launches = flag();
   else if (k == "chain_depth") s.chain_depth = v.get<int>();
+  else if (k == "chain_best_effort") s.chain_best_effort = flag();
   else if (k == "atom_duration_us") s.atom_duration = duration_from_us(v.get<double>());
   else if (k == "steal_horizon_us") s.steal_horizon = duration_from_us(v.get<double>());
   else if (k == "max_outstanding_atoms") s.max_outstanding_atoms = v.get<int>();

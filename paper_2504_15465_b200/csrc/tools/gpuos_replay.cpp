@@ -55,6 +55,7 @@ void set_knob(ScenarioConfig& c, const std::string& kv) {
   else if (k == "block_revocation") s.block_revocation = truthy(v);
   else if (k == "chain_launches") s.chain_launches = truthy(v);
   else if (k == "chain_depth") s.chain_depth = std::atoi(v.c_str());
+  else if (k == "chain_best_effort") s.chain_best_effort = truthy(v);
   else if (k == "atom_duration_us") s.atom_duration = duration_from_us(x);
   else if (k == "steal_horizon_us") s.steal_horizon = duration_from_us(x);
   else if (k == "max_outstanding_atoms") s.max_outstanding_atoms = std::atoi(v.c_str());
