@@ -49,3 +49,35 @@ def test_live_model_configs_complete(api, cuda_device, name):
     tl = r["b200"]["timeline"]
     for m0, m1, t0, t1 in zip(tl["mask0"], tl["mask1"], tl["touched0"], tl["touched1"]):
         assert (t0 & ~m0) == 0 and (t1 & ~m1) == 0 and (t0 | t1) != 0
+
+
+def test_live_decode_kernels_chain_on_the_device(api, cuda_device):
+    """Llama-3-8B decode alone with chain_launches: nearly every kernel of a
+    token is submitted before its predecessor's last block ends (it rides
+    behind it on the device), and the token latency beats host-paced
+    launches of the same trace on the same device."""
+    import json
+    import statistics
+
+    cfg = workloads.without_apps(workloads.hybrid(200.0), "rn50_train")
+    p50 = {}
+    for chain in (False, True):
+        req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
+               "timeline": True, "b200": {"chunk_cap": 256},
+               "set": {"block_revocation": True, "chain_launches": chain}}
+        with api.Session(req) as s:
+            s.run()
+            r = s.run()
+        lat = [json.loads(x)["latency_us"] for x in r["request_log"].splitlines() if json.loads(x)["completed"]]
+        assert len(lat) >= 5
+        p50[chain] = statistics.median(lat)
+        if chain:
+            tl = r["b200"]["timeline"]
+            order = sorted(range(len(tl["kernel"])), key=lambda i: tl["dev_first"][i])
+            pairs = [(a, b) for a, b in zip(order, order[1:])
+                     if tl["dev_first"][b] - tl["dev_last"][a] < 100_000]  # same token
+            early = sum(1 for a, b in pairs if tl["submit"][b] < tl["dev_last"][a])
+            assert early >= 0.8 * len(pairs), (early, len(pairs))
+            for a, b in pairs:  # chained kernels never overlap their predecessor
+                assert tl["dev_first"][b] >= tl["dev_last"][a]
+    assert p50[True] < 0.9 * p50[False], p50
