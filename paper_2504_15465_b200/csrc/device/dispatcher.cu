@@ -455,6 +455,13 @@ struct RoundCmd {
 constexpr int kRoundCmdWords64 = sizeof(RoundCmd) / 8;
 static_assert(sizeof(RoundCmd) % 8 == 0, "RoundCmd copied as 64-bit words");
 
+// Pair bodies' descriptors start with their two TMA tensor maps (128 B each):
+// fetch them into this SM's tensor-map cache ahead of the body's first load.
+__device__ __forceinline__ void prefetch_tile_maps(unsigned long long desc) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(desc) : "memory");
+  asm volatile("prefetch.tensormap [%0];" ::"l"(desc + 128) : "memory");
+}
+
 enum WorkerGo : int { kGoExit = 0, kGoOwn = 1, kGoPair = 2, kGoJoin = 3 };
 
 // Spreading pair tiles: a leader whose TPC's tensor cores already run a
@@ -1101,6 +1108,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
 #pragma unroll
           for (int w = 0; w < kRoundCmdWords64; ++w) st_cluster_u64(peer_join_rc + 8 * w, src[w]);
           mbar_arrive_remote(peer_join_full);
+          prefetch_tile_maps(sh.rc.cmd.args[0]);  // while the peer joins
           // The peer takes it at its next decision point; only an abort
           // (quit, hang guard) can leave it untaken.
           for (unsigned polls = 0; !mbar_test_cluster(&sh.joined, joins & 1u); ++polls) {
@@ -1113,6 +1121,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
         } else if (go == kGoJoin) {
           sh.rc = sh.join_rc;
           mbar_arrive_remote(leader_joined);
+          prefetch_tile_maps(sh.rc.cmd.args[0]);
         }
         sh.go = go;
         sh.t_start = gtimer();
