@@ -110,6 +110,10 @@ class B200Runtime {
   // to a kernel id: called for every kernel of a scenario before the
   // dispatcher starts, so no allocation or fill kernel runs beside it.
   void prepare(const SimKernelSpec& spec) { (void)resolve_body(spec); }
+  // Records a kernel's workspace need without allocating: called for every
+  // kernel before prepare(), so a workspace shared by kernels of different
+  // sizes is allocated once at the largest.
+  void reserve(const SimKernelSpec& spec);
 
   void start();
   float stop(bool drain);  // returns the worker kernel's CUDA-event ms
@@ -156,6 +160,7 @@ class B200Runtime {
   int tpcs_ = 0;
   bool running_ = false;
   std::unordered_map<std::uint32_t, Workspace> ws_;
+  std::unordered_map<std::uint32_t, std::uint64_t> ws_reserve_;  // words, from reserve()
   std::vector<std::uint32_t*> trace_of_;  // per kernel id
   // Trace pool: fixed-size chunks kept across runs (allocating during a
   // live run would stall it), zeroed between runs.

@@ -86,9 +86,22 @@ int B200Runtime::workers_per_tpc() const {
   return t.workers_per_tpc;
 }
 
+void B200Runtime::reserve(const SimKernelSpec& spec) {
+  const BodyRef& b = spec.body;
+  if (b.kind != BodyKind::Stream || b.p0 <= 0) return;
+  const std::uint64_t cap = b.p2 > 0 ? static_cast<std::uint64_t>(b.p2)
+                                     : static_cast<std::uint64_t>(opt_.stream_chunk_cap);
+  std::uint64_t& r = ws_reserve_[b.workspace];
+  r = std::max<std::uint64_t>(r, static_cast<std::uint64_t>(b.p0) * cap);
+}
+
 B200Runtime::Workspace& B200Runtime::workspace(std::uint32_t id, std::uint64_t words) {
   Workspace& w = ws_[id];
   if (w.words >= words) return w;
+  if (!w.src) {
+    const auto it = ws_reserve_.find(id);
+    if (it != ws_reserve_.end()) words = std::max(words, it->second);
+  }
   // Buffers may be referenced by atoms in flight: never reallocate.
   if (w.src) throw ConfigError("workspace " + std::to_string(id) + " is smaller than a later kernel needs");
   words = (words + 3) & ~3ull;

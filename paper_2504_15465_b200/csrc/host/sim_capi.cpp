@@ -22,20 +22,26 @@ namespace {
 // Allocate every tenant kernel's operands before the dispatcher starts (no
 // allocation or initialisation kernel may run beside the resident workers).
 void prepare_bodies(B200Runtime& rt, const ScenarioConfig& cfg) {
-  auto prep = [&](const RequestTemplate& tmpl) {
-    for (const KernelRecord& k : tmpl.kernels) {
-      SimKernelSpec spec;
-      spec.total_blocks = k.total_blocks();
-      spec.block_duration_at_fmax = k.block_duration_at_fmax;
-      spec.sensitivity_s = k.sensitivity_s;
-      spec.occupancy_per_tpc = k.occupancy_per_tpc;
-      spec.body = k.body;
-      rt.prepare(spec);
+  const std::vector<AppWorkload> apps = resolve_workloads(cfg);
+  for (const bool allocate : {false, true}) {  // sizes first, then allocation
+    auto prep = [&](const RequestTemplate& tmpl) {
+      for (const KernelRecord& k : tmpl.kernels) {
+        SimKernelSpec spec;
+        spec.total_blocks = k.total_blocks();
+        spec.block_duration_at_fmax = k.block_duration_at_fmax;
+        spec.sensitivity_s = k.sensitivity_s;
+        spec.occupancy_per_tpc = k.occupancy_per_tpc;
+        spec.body = k.body;
+        if (allocate)
+          rt.prepare(spec);
+        else
+          rt.reserve(spec);
+      }
+    };
+    for (const AppWorkload& w : apps) {
+      prep(w.request);
+      for (const RequestTemplate& t : w.per_request) prep(t);
     }
-  };
-  for (const AppWorkload& w : resolve_workloads(cfg)) {
-    prep(w.request);
-    for (const RequestTemplate& t : w.per_request) prep(t);
   }
 }
 

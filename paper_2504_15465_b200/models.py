@@ -91,9 +91,11 @@ class Builder:
             "body": {"kind": "gemv_bf16", "ws": self._next(), "p": [n, k, splits]}})
 
     def stream(self, nbytes) -> None:
-        """Elementwise kernel moving `nbytes` (read + written)."""
-        words = STREAM_WORDS
-        blocks = max(1, math.ceil(nbytes / (8 * words)))
+        """Elementwise kernel moving `nbytes` (read + written): blocks of at
+        most STREAM_WORDS u32, sized (in 1 KiB steps) to the bytes moved, so
+        a 16 KB RMSNorm is one 16 KB block, not a 128 KB one."""
+        blocks = max(1, math.ceil(nbytes / (8 * STREAM_WORDS)))
+        words = min(STREAM_WORDS, max(256, math.ceil(nbytes / (8 * blocks) / 256) * 256))
         self.kernels.append({
             "blocks": blocks, "block_us": round(8 * words / (TPC_GBS / 4 * 1e3), 3), "s": 0.2, "occ": 4,
             "body": {"kind": "stream", "ws": self.stream_ws, "p": [words, 0, 256]}})
