@@ -80,6 +80,8 @@ struct alignas(128) DevAtom {
   unsigned long long t_first, t_last;   // second line: per-block records
   unsigned long long touched[2];
   unsigned long long t_seen, t_armed;   // ingest instrumentation (globaltimer)
+  unsigned gate;                        // early-armed chained GEMV: 1 until its predecessor ends
+  unsigned armed;                       // claim armed (blocks claimable or claimed)
   unsigned char entry[GPUOS_MAX_TPCS];  // resident-list index per TPC
 };
 static_assert(offsetof(DevAtom, succ) + 4 <= 128, "hot fields must share one line");
@@ -182,6 +184,7 @@ constexpr int kIngestBatch = 8;  // two 512-byte reads per poll
 struct IngestSubmit {
   unsigned slot, seq;
   unsigned pred;  // chained: predecessor slot + 1 (0: none)
+  unsigned early; // chained and armed at once behind a closed gate
   unsigned long long mask[2];
   unsigned long long key;
 };
@@ -293,6 +296,20 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           a->done = 0;
           a->succ = 0;
           a->chain = (aux & kAuxChainHead) ? kChainHead : 0u;
+          // Early start: a chained GEMV is armed at once behind a closed gate
+          // -- its blocks stream W while the predecessor runs and read x
+          // when the predecessor's finisher opens the gate. Only at a
+          // priority no higher than the predecessor's, so the
+          // predecessor's unclaimed blocks always win a free slot first.
+          // The predecessor must be armed already: its unclaimed blocks then
+          // win every slot before ours, so our waiting blocks cannot starve
+          // it (an unarmed predecessor could find every worker parked at
+          // our gate).
+          const bool early = pred != 0u && body == GPUOS_BODY_GEMV_BF16 &&
+                             prio <= p.atoms[pred - 1u].prio &&
+                             ld_relaxed_gpu(&p.atoms[pred - 1u].armed) != 0u;
+          a->gate = early ? 1u : 0u;
+          a->armed = 0u;
           a->tag = tag;
           a->trace = reinterpret_cast<unsigned*>(trace);
           a->mask[0] = mask0;
@@ -308,6 +325,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           s.slot = slot;
           s.seq = seq;
           s.pred = pred;
+          s.early = a->gate;
           s.mask[0] = mask0;
           s.mask[1] = mask1;
           s.key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
@@ -385,9 +403,10 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
       for (int i = 0; i < n_sub; ++i) {
         const IngestSubmit s = subs[i];
         DevAtom* a = p.atoms + s.slot;
-        if (lane == 0 && s.pred == 0u) {
+        if (lane == 0 && (s.pred == 0u || s.early)) {
           st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
           a->t_armed = t_armed;
+          a->armed = 1u;
         }
         chained = chained || s.pred != 0u;
         for (int t = lane; t < p.logical_tpcs; t += 32) {
@@ -408,9 +427,15 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
             if (s.pred == 0u) continue;
             DevAtom* a = p.atoms + s.slot;
             if (atomicCAS(&p.atoms[s.pred - 1u].succ, 0u, s.slot + 1u) == kSuccDone) {
-              // Predecessor already finished: arm here (woken below).
-              st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
-              a->t_armed = gtimer();
+              // Predecessor already finished: arm here (woken below), or
+              // open an early successor's gate.
+              if (s.early) {
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&a->gate), "r"(0u) : "memory");
+              } else {
+                st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
+                a->t_armed = gtimer();
+                a->armed = 1u;
+              }
             }
           }
         }
@@ -671,6 +696,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   // (the other workers are woken for the rest).
   RoundCmd ho;
   int handoff = 0;
+  unsigned look = 0;  // lane 0: successor's successor armed early (slot + 1)
   chain = __shfl_sync(0xffffffffu, chain, 0);
   if (chain & kChainHead) {
     unsigned next = 0;
@@ -678,6 +704,13 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       // Registered before we looked: nothing to race with (registration
       // happens once), and the acquire above ordered its fields.
       next = pre != 0u ? pre : atom_exch_acq_rel32(&a->succ, kSuccDone);
+      if (next != 0u && ld_relaxed_gpu(&p.atoms[next - 1u].gate) != 0u) {
+        // Early-started successor (armed at ingest): our outputs, acquired
+        // through the count above, are released to its gate waiters.
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&p.atoms[next - 1u].gate), "r"(0u)
+                     : "memory");
+        next = 0;
+      }
       if (next != 0u) {
         bf.load(p.atoms + (next - 1u));
         DevAtom* b = p.atoms + (next - 1u);
@@ -690,6 +723,22 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
                           bprio >= floor_prio && (!body_is_pair(bbody) || rank == 0u);
         st_relaxed_gpu64(&b->claim, (static_cast<unsigned long long>(bseq) << 32) | (here ? 1u : 0u));
         b->t_armed = gtimer();
+        b->armed = 1u;
+        // Lookahead: b's own registered successor, if a GEMV that may start
+        // early, is armed now behind a closed gate (b opens it).
+        const unsigned cn = ld_acquire_gpu(&b->succ);
+        if (cn != 0u && cn != kSuccDone) {
+          DevAtom* c = p.atoms + (cn - 1u);
+          if (c->body == GPUOS_BODY_GEMV_BF16 && c->prio <= bprio && ld_relaxed_gpu(&c->gate) == 0u &&
+              ld_relaxed_gpu(&c->armed) == 0u) {
+            c->gate = 1u;
+            fence_acq_rel_gpu();  // the gate before the claim
+            st_relaxed_gpu64(&c->claim, static_cast<unsigned long long>(c->seq) << 32);
+            c->t_armed = gtimer();
+            c->armed = 1u;
+            look = cn;
+          }
+        }
         if (here) {
           handoff = 1;
 #pragma unroll
@@ -709,12 +758,13 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
     }
     next = __shfl_sync(0xffffffffu, next, 0);
     handoff = __shfl_sync(0xffffffffu, handoff, 0);
-    if (next != 0u) {
+    look = __shfl_sync(0xffffffffu, look, 0);
+    if (next != 0u || look != 0u) {
       __syncwarp();
-      fence_acq_rel_gpu();  // every lane: the armed claim before its version bumps
-      const DevAtom* b = p.atoms + (next - 1u);
+      fence_acq_rel_gpu();  // every lane: the armed claims before the version bumps
       for (int t = lane; t < p.logical_tpcs; t += 32) {
-        const unsigned long long m = b->mask[t >> 6];
+        const unsigned long long m = (next ? p.atoms[next - 1u].mask[t >> 6] : 0ull) |
+                                     (look ? p.atoms[look - 1u].mask[t >> 6] : 0ull);
         if ((m >> (t & 63)) & 1ull) red_relaxed_gpu_add(p.version + t, 1u);
       }
     }
@@ -767,10 +817,11 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
 }
 
 __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned rank,
-                                         StreamPipe& pipe, GemmPipe& gemm, GemvPipe& gemv) {
+                                         StreamPipe& pipe, GemmPipe& gemm, GemvPipe& gemv,
+                                         const DevAtom* atoms) {
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
-    case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv); break;
+    case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, &atoms[rc.slot].gate); break;
     case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
     case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm); break;
@@ -1131,7 +1182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
     __syncthreads();
     const int go = sh.go;
     if (go == kGoExit) break;
-    run_body(sh.rc, tid, rank, pipe, gemm, gemv);  // pair tiles end with a cluster barrier
+    run_body(sh.rc, tid, rank, pipe, gemm, gemv, p.atoms);  // pair tiles end with a cluster barrier
     if (go == kGoPair || go == kGoJoin) ++joins;
     if (tc_hold && tid == 0) {
       if (atomicSub(p.tc_busy + tpc, 1u) == 1u) atomicSub(&p.ctl->tc_active, 1u);
@@ -1752,6 +1803,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     x.lo = a.lo;
     ids[static_cast<size_t>(i)] = d->next_atom_id++;
     x.chain = (a.flags & GPUOS_ATOM_CHAIN_HEAD) ? kChainHead : 0u;
+    x.armed = pred[static_cast<size_t>(i)] >= 0 ? 0u : 1u;
     if (pred[static_cast<size_t>(i)] >= 0) {
       x.claim |= x.count;  // unarmed until the predecessor's last block
       atoms[static_cast<size_t>(pred[static_cast<size_t>(i)])].succ = static_cast<unsigned>(i) + 1u;

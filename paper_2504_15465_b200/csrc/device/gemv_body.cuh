@@ -96,7 +96,11 @@ __device__ __forceinline__ unsigned tmem_ld1(unsigned taddr) {
 }
 
 // Both CTAs of the pair, all threads; rank 0 is the leader.
-__device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned rank, GemvPipe& G) {
+// `gate`: the atom's early-start gate (dispatcher.cu): while it is 1 the
+// block streams its first stages of W but loads no x (the predecessor is
+// still producing it).
+__device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned rank, GemvPipe& G,
+                                           const unsigned* gate) {
   const GemvDesc* D = reinterpret_cast<const GemvDesc*>(c.args[0]);
   // Block b: row tile b % row_tiles, K split b / row_tiles (decode shapes
   // have few row tiles; splitting K keeps every TPC streaming W).
@@ -121,7 +125,29 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->x) : "memory");
     const int w_row = static_cast<int>(blk * kGemvTile + rank * kGemmHalf);
     const int x_row = static_cast<int>(rank * kGemvXRows);  // rank 1: all zero fill
-    for (unsigned j = 0; j < nk; ++j) {
+    // Early start: W for the first stages now, their x once the gate opens.
+    unsigned pre = 0;
+    if (ld_acquire_gpu(gate) != 0u) {
+      pre = nk < S ? nk : S;
+      for (unsigned j = 0; j < pre; ++j) {
+        const unsigned long long k = g0 + j;
+        const unsigned s = static_cast<unsigned>(k % S);
+        const unsigned long long r = k / S;
+        if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
+        if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemvStageBytes);
+        tma_load_2d_pair(G.tiles + s * kGemvStageBytes, &D->w, static_cast<int>((kb0 + j) * kGemmBK), w_row,
+                         G.full + s);
+      }
+      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+      // x was written through the generic proxy; the TMA reads it.
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      for (unsigned j = 0; j < pre; ++j) {
+        const unsigned s = static_cast<unsigned>((g0 + j) % S);
+        tma_load_2d_pair(G.tiles + s * kGemvStageBytes + kGemvWBytes, &D->x,
+                         static_cast<int>((kb0 + j) * kGemmBK), x_row, G.full + s);
+      }
+    }
+    for (unsigned j = pre; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;

@@ -10,7 +10,9 @@ dependent kernel starts without a host round trip. Checked here:
   * both arming paths -- successor registered before the predecessor ends
     (the finisher arms it) and after (the ingest warp arms it) -- and a
     successor whose predecessor was already polled (runs at once);
-  * batch mode chains and the argument errors.
+  * batch mode chains and the argument errors;
+  * early start: a chained GEMV whose x is its predecessor's output streams
+    W before the predecessor ends and reads x only when its gate opens.
 """
 from __future__ import annotations
 
@@ -204,3 +206,40 @@ def test_chain_removes_the_host_round_trip(api, cuda_device):
     med = float(np.median(gaps))
     print(f"serial host round trip {serial * 1e6:.1f} us/kernel; chained gap median {med / 1e3:.2f} us")
     assert med < 0.5 * (serial * 1e9 - 1000)
+
+
+@pytest.mark.parametrize("n1,k,n2,splits", [(8192, 4096, 4096, 4), (2048, 1024, 28672, 1)])
+def test_early_started_gemv_reads_its_predecessors_output(api, cuda_device, n1, k, n2, splits):
+    """y1 = W1 x (bf16 out) then y2 = W2 y1, chained: y2 must equal the
+    product with the y1 the device wrote (y1 starts as NaN, so an x read
+    before the gate opened shows up)."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(n1 + n2)
+    w1 = (torch.rand(n1, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    x = (torch.rand(k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w2 = (torch.rand(n2, n1, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    y1 = torch.full((n1,), float("nan"), device="cuda", dtype=torch.bfloat16)
+    y2 = torch.full((n2,), float("nan"), device="cuda")
+    with api.Device(workers_per_sm=2) as dev:
+        d1, b1 = dev.gemv_desc(w1.data_ptr(), x.data_ptr(), y1.data_ptr(), n1, k, bf16_out=True, k_splits=splits)
+        d2, b2 = dev.gemv_desc(w2.data_ptr(), y1.data_ptr(), y2.data_ptr(), n2, n1, k_splits=splits)
+        for rep in range(3):
+            # (no torch kernel can run beside the resident dispatcher: fill
+            # and check between runs)
+            y1.fill_(float("nan"))
+            y2.fill_(float("nan"))
+            torch.cuda.synchronize()
+            dev.start()
+            a = dev.submit(0, b1, range(74), 30, api.GPUOS_BODY_GEMV_BF16, [d1], chain_head=True)
+            b = dev.submit(0, b2, range(74), 30, api.GPUOS_BODY_GEMV_BF16, [d2], after=a)
+            done = wait_all(dev, 2)
+            dev.stop()
+            assert [c.atom_id for c in done] == [a, b]
+            y1h = y1.double().cpu()
+            ref = (w2.double().cpu() @ y1h).float()
+            assert not torch.isnan(y1h).any()
+            err = ((y2.cpu() - ref).abs().max() / ref.abs().max()).item()
+            assert err < 1e-3, (rep, err)
+        dev.free(d1)
+        dev.free(d2)

@@ -54,8 +54,9 @@ def test_live_model_configs_complete(api, cuda_device, name):
 def test_live_decode_kernels_chain_on_the_device(api, cuda_device):
     """Llama-3-8B decode alone with chain_launches: nearly every kernel of a
     token is submitted before its predecessor's last block ends (it rides
-    behind it on the device), and the token latency beats host-paced
-    launches of the same trace on the same device."""
+    behind it on the device), only GEMVs start before their predecessor
+    ends (early start behind a gate), and the token latency beats
+    host-paced launches of the same trace on the same device."""
     import json
     import statistics
 
@@ -73,11 +74,13 @@ def test_live_decode_kernels_chain_on_the_device(api, cuda_device):
         p50[chain] = statistics.median(lat)
         if chain:
             tl = r["b200"]["timeline"]
-            order = sorted(range(len(tl["kernel"])), key=lambda i: tl["dev_first"][i])
+            order = sorted(range(len(tl["kernel"])), key=lambda i: tl["kernel"][i])  # launch order
             pairs = [(a, b) for a, b in zip(order, order[1:])
                      if tl["dev_first"][b] - tl["dev_last"][a] < 100_000]  # same token
             early = sum(1 for a, b in pairs if tl["submit"][b] < tl["dev_last"][a])
             assert early >= 0.8 * len(pairs), (early, len(pairs))
-            for a, b in pairs:  # chained kernels never overlap their predecessor
-                assert tl["dev_first"][b] >= tl["dev_last"][a]
+            kern = models.llama3_8b_decode(1024)
+            for a, b in pairs:  # only a GEMV starts early (behind its gate)
+                if kern[tl["kernel"][b] % len(kern)]["body"]["kind"] != "gemv_bf16":
+                    assert tl["dev_first"][b] >= tl["dev_last"][a]
     assert p50[True] < 0.9 * p50[False], p50
