@@ -59,7 +59,10 @@ __device__ __forceinline__ void tma_load_im2col_pair(void* dst, const CUtensorMa
 
 // Both CTAs of the pair, all threads; rank 0 is the leader. Shares the GEMM
 // pipe (stage = 16 KiB A + 16 KiB B, same barriers and TMEM columns).
-__device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G) {
+// `gate`: early-start gate, as in body_gemm2 (weights first, activations
+// once the predecessor has written them).
+__device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G,
+                                           const unsigned* gate) {
   const ConvDesc* D = reinterpret_cast<const ConvDesc*>(c.args[0]);
   const unsigned pt = static_cast<unsigned>(c.block) % D->pair_tiles;
   const unsigned kt = static_cast<unsigned>(c.block) / D->pair_tiles;
@@ -84,7 +87,27 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
     const int k_row = static_cast<int>(kt * n_tile + rank * (n_tile / 2));
     const unsigned tx = 2 * (kGemmABytes + n_tile / 2 * kGemmBK * 2);  // both CTAs' A and B halves
     const unsigned cb_count = D->c_blocks;
-    for (unsigned j = 0; j < nk; ++j) {
+    // Weights for the first stages first, then activations once the atom's
+    // gate is open (early start; otherwise the gate read overlaps).
+    const unsigned pre = nk < S ? nk : S;
+    for (unsigned j = 0; j < pre; ++j) {
+      const unsigned s = static_cast<unsigned>((g0 + j) % S);
+      if ((g0 + j) / S >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>(((g0 + j) / S - 1) & 1));
+      if (rank == 0) mbar_expect_tx(G.full + s, tx);
+      tma_load_2d_pair(G.tiles + s * kGemmStageBytes + kGemmABytes, &D->wgt, static_cast<int>(j * kGemmBK),
+                       k_row, G.full + s);
+    }
+    while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    for (unsigned j = 0; j < pre; ++j) {
+      const unsigned tap = j / cb_count, cb = j - tap * cb_count;
+      const unsigned rr = tap / D->s, ss = tap - rr * D->s;
+      const unsigned s = static_cast<unsigned>((g0 + j) % S);
+      tma_load_im2col_pair(G.tiles + s * kGemmStageBytes, &D->act, static_cast<int>(cb * kGemmBK), w0, h0,
+                           static_cast<int>(n0), static_cast<unsigned short>(ss),
+                           static_cast<unsigned short>(rr), G.full + s);
+    }
+    for (unsigned j = pre; j < nk; ++j) {
       const unsigned tap = j / cb_count, cb = j - tap * cb_count;
       const unsigned rr = tap / D->s, ss = tap - rr * D->s;
       const unsigned long long k = g0 + j;

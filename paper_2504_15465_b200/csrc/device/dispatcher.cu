@@ -166,6 +166,11 @@ __device__ __forceinline__ unsigned long long field64(unsigned lo, unsigned hi) 
   return static_cast<unsigned long long>(lo) | (static_cast<unsigned long long>(hi) << 32);
 }
 
+__device__ __forceinline__ bool body_is_pair(unsigned body) {
+  return body == GPUOS_BODY_GEMM_BF16 || body == GPUOS_BODY_GEMV_BF16 ||
+         body == GPUOS_BODY_CONV_BF16;
+}
+
 // ------------------------------------------------------------ ingest warp
 // Ring entries are read kIngestBatch at a time: two 512-byte PCIe reads per
 // poll (lane l loads 16 B: entry head + l/8, words 4(l%8)..4(l%8)+3), so a
@@ -305,7 +310,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           // win every slot before ours, so our waiting blocks cannot starve
           // it (an unarmed predecessor could find every worker parked at
           // our gate).
-          const bool early = pred != 0u && body == GPUOS_BODY_GEMV_BF16 &&
+          const bool early = pred != 0u && body_is_pair(body) &&
                              prio <= p.atoms[pred - 1u].prio &&
                              ld_relaxed_gpu(&p.atoms[pred - 1u].armed) != 0u;
           a->gate = early ? 1u : 0u;
@@ -588,11 +593,6 @@ __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long 
   return got ? static_cast<long long>(off) : -1;
 }
 
-__device__ __forceinline__ bool body_is_pair(unsigned body) {
-  return body == GPUOS_BODY_GEMM_BF16 || body == GPUOS_BODY_GEMV_BF16 ||
-         body == GPUOS_BODY_CONV_BF16;
-}
-
 // Warp 0 of the CTA that ran `rc`: record the block on its atom and, for the
 // atom's last block, publish the completion and retire its resident keys.
 // Returns 0 (more blocks to go), 1 (atom done) or 2 (atom done, and `rc`
@@ -729,7 +729,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         const unsigned cn = ld_acquire_gpu(&b->succ);
         if (cn != 0u && cn != kSuccDone) {
           DevAtom* c = p.atoms + (cn - 1u);
-          if (c->body == GPUOS_BODY_GEMV_BF16 && c->prio <= bprio && ld_relaxed_gpu(&c->gate) == 0u &&
+          if (body_is_pair(c->body) && c->prio <= bprio && ld_relaxed_gpu(&c->gate) == 0u &&
               ld_relaxed_gpu(&c->armed) == 0u) {
             c->gate = 1u;
             fence_acq_rel_gpu();  // the gate before the claim
@@ -822,9 +822,9 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
     case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, &atoms[rc.slot].gate); break;
-    case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm); break;
+    case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm, &atoms[rc.slot].gate); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
-    case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm); break;
+    case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm, &atoms[rc.slot].gate); break;
     default: break;
   }
 }

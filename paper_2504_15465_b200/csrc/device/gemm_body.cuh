@@ -266,7 +266,11 @@ __device__ __forceinline__ void epilogue_staged(const GemmPipe& G, int tid, unsi
 }
 
 // Both CTAs of the pair, all threads; rank 0 is the leader.
-__device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G) {
+// `gate`: the atom's early-start gate (dispatcher.cu): while it is 1 the
+// tile loads its first stages of B (weights) but no A (the predecessor is
+// still producing the activations).
+__device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G,
+                                           const unsigned* gate) {
   const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
   const unsigned m_tiles = D->m_tiles, n_tiles = D->n_tiles, n_tile = D->n_tile;
   const unsigned blk = static_cast<unsigned>(c.block);
@@ -297,7 +301,22 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
     const int a_row = static_cast<int>(mt * kGemmTile + rank * kGemmHalf);
     const int b_row = static_cast<int>(nt * n_tile + rank * (n_tile / 2));
     const unsigned tx = 2 * (kGemmABytes + n_tile / 2 * kGemmBK * 2);  // both CTAs' A and B halves
-    for (unsigned j = 0; j < nk; ++j) {
+    // B (weights) for the first stages first, then A once the atom's gate
+    // is open (early start; otherwise the gate read overlaps the B loads).
+    const unsigned pre = nk < S ? nk : S;
+    for (unsigned j = 0; j < pre; ++j) {
+      const unsigned s = static_cast<unsigned>((g0 + j) % S);
+      if ((g0 + j) / S >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>(((g0 + j) / S - 1) & 1));
+      if (rank == 0) mbar_expect_tx(G.full + s, tx);
+      tma_load_2d_pair(G.tiles + s * kGemmStageBytes + kGemmABytes, &D->b, static_cast<int>(j * kGemmBK),
+                       b_row, G.full + s);
+    }
+    while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // A: generic-proxy writes, TMA reads
+    for (unsigned j = 0; j < pre; ++j)
+      tma_load_2d_pair(G.tiles + static_cast<unsigned>((g0 + j) % S) * kGemmStageBytes, &D->a,
+                       static_cast<int>(j * kGemmBK), a_row, G.full + static_cast<unsigned>((g0 + j) % S));
+    for (unsigned j = pre; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;

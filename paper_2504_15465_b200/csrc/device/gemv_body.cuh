@@ -125,27 +125,25 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->x) : "memory");
     const int w_row = static_cast<int>(blk * kGemvTile + rank * kGemmHalf);
     const int x_row = static_cast<int>(rank * kGemvXRows);  // rank 1: all zero fill
-    // Early start: W for the first stages now, their x once the gate opens.
-    unsigned pre = 0;
-    if (ld_acquire_gpu(gate) != 0u) {
-      pre = nk < S ? nk : S;
-      for (unsigned j = 0; j < pre; ++j) {
-        const unsigned long long k = g0 + j;
-        const unsigned s = static_cast<unsigned>(k % S);
-        const unsigned long long r = k / S;
-        if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
-        if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemvStageBytes);
-        tma_load_2d_pair(G.tiles + s * kGemvStageBytes, &D->w, static_cast<int>((kb0 + j) * kGemmBK), w_row,
-                         G.full + s);
-      }
-      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
-      // x was written through the generic proxy; the TMA reads it.
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      for (unsigned j = 0; j < pre; ++j) {
-        const unsigned s = static_cast<unsigned>((g0 + j) % S);
-        tma_load_2d_pair(G.tiles + s * kGemvStageBytes + kGemvWBytes, &D->x,
-                         static_cast<int>((kb0 + j) * kGemmBK), x_row, G.full + s);
-      }
+    // W for the first stages first, then x once the atom's gate is open:
+    // an early-started block streams W while its predecessor still writes
+    // x; for any other block the gate read overlaps the W loads.
+    const unsigned pre = nk < S ? nk : S;
+    for (unsigned j = 0; j < pre; ++j) {
+      const unsigned long long k = g0 + j;
+      const unsigned s = static_cast<unsigned>(k % S);
+      const unsigned long long r = k / S;
+      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
+      if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemvStageBytes);
+      tma_load_2d_pair(G.tiles + s * kGemvStageBytes, &D->w, static_cast<int>((kb0 + j) * kGemmBK), w_row,
+                       G.full + s);
+    }
+    while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic-proxy writes, TMA reads
+    for (unsigned j = 0; j < pre; ++j) {
+      const unsigned s = static_cast<unsigned>((g0 + j) % S);
+      tma_load_2d_pair(G.tiles + s * kGemvStageBytes + kGemvWBytes, &D->x,
+                       static_cast<int>((kb0 + j) * kGemmBK), x_row, G.full + s);
     }
     for (unsigned j = pre; j < nk; ++j) {
       const unsigned long long k = g0 + j;

@@ -243,3 +243,53 @@ def test_early_started_gemv_reads_its_predecessors_output(api, cuda_device, n1, 
             assert err < 1e-3, (rep, err)
         dev.free(d1)
         dev.free(d2)
+
+
+def test_early_started_gemm_and_conv_read_their_predecessors_output(api, cuda_device):
+    """C1 = A B1^T (bf16) then C2 = C1 B2^T; X1 = conv(X0) (bf16 NHWC) then
+    X2 = conv(X1): each second kernel chained and started early (weights
+    first); the intermediates start as NaN."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    m, k, n1, n2 = 1024, 512, 768, 640
+    a = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    b1 = (torch.rand(n1, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    b2 = (torch.rand(n2, n1, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    c1 = torch.full((m, n1), float("nan"), device="cuda", dtype=torch.bfloat16)
+    c2 = torch.full((m, n2), float("nan"), device="cuda")
+    nb, hw, ch = 4, 14, 128
+    x0 = (torch.rand(nb, hw, hw, ch, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    wa = (torch.rand(ch, 3, 3, ch, device="cuda", generator=g) * 0.2 - 0.1).to(torch.bfloat16)
+    wb = (torch.rand(ch, 3, 3, ch, device="cuda", generator=g) * 0.2 - 0.1).to(torch.bfloat16)
+    x1 = torch.full((nb, hw, hw, ch), float("nan"), device="cuda", dtype=torch.bfloat16)
+    x2 = torch.full((nb, hw, hw, ch), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    with api.Device(workers_per_sm=2) as dev:
+        g1, gb1, _, _ = dev.gemm_desc(a.data_ptr(), b1.data_ptr(), c1.data_ptr(), m, n1, k, bf16_out=True)
+        g2, gb2, _, _ = dev.gemm_desc(c1.data_ptr(), b2.data_ptr(), c2.data_ptr(), m, n2, n1)
+        v1, vb1, _, _ = dev.conv_desc(x0.data_ptr(), wa.data_ptr(), x1.data_ptr(), nb, hw, hw, ch, ch, 3, 3, 1, 1,
+                                      bf16_out=True)
+        v2, vb2, _, _ = dev.conv_desc(x1.data_ptr(), wb.data_ptr(), x2.data_ptr(), nb, hw, hw, ch, ch, 3, 3, 1, 1)
+        dev.start()
+        ga = dev.submit(0, gb1, range(74), 30, api.GPUOS_BODY_GEMM_BF16, [g1], chain_head=True)
+        gb = dev.submit(0, gb2, range(74), 30, api.GPUOS_BODY_GEMM_BF16, [g2], after=ga)
+        ca = dev.submit(0, vb1, range(74), 30, api.GPUOS_BODY_CONV_BF16, [v1], chain_head=True)
+        cb = dev.submit(0, vb2, range(74), 30, api.GPUOS_BODY_CONV_BF16, [v2], after=ca)
+        done = wait_all(dev, 4)
+        dev.stop()
+        for d in (g1, g2, v1, v2):
+            dev.free(d)
+    order = [c.atom_id for c in done]
+    assert order.index(ga) < order.index(gb) and order.index(ca) < order.index(cb)
+    c1h = c1.double().cpu()
+    assert not torch.isnan(c1h).any()
+    ref = c1h @ b2.double().cpu().T
+    err = ((c2.double().cpu() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-3, err
+    x1h = x1.double().cpu()
+    assert not torch.isnan(x1h).any()
+    refx = torch.nn.functional.conv2d(x1h.permute(0, 3, 1, 2), wb.double().cpu().permute(0, 3, 1, 2),
+                                      padding=1).permute(0, 2, 3, 1)
+    errx = ((x2.double().cpu() - refx).abs().max() / refx.abs().max()).item()
+    assert errx < 1e-3, errx
