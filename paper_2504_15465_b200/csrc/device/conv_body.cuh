@@ -89,7 +89,7 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
     const unsigned cb_count = D->c_blocks;
     // Weights for the first stages first, then activations once the atom's
     // gate is open (early start; otherwise the gate read overlaps).
-    const unsigned pre = nk < S ? nk : S;
+    const unsigned pre = gate ? (nk < S ? nk : S) : 0u;  // (no gate: loads in stage order)
     for (unsigned j = 0; j < pre; ++j) {
       const unsigned s = static_cast<unsigned>((g0 + j) % S);
       if ((g0 + j) / S >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>(((g0 + j) / S - 1) & 1));
@@ -97,8 +97,10 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
       tma_load_2d_pair(G.tiles + s * kGemmStageBytes + kGemmABytes, &D->wgt, static_cast<int>(j * kGemmBK),
                        k_row, G.full + s);
     }
-    while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (gate) {
+      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     for (unsigned j = 0; j < pre; ++j) {
       const unsigned tap = j / cb_count, cb = j - tap * cb_count;
       const unsigned rr = tap / D->s, ss = tap - rr * D->s;

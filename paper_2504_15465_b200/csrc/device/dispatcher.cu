@@ -63,7 +63,8 @@ enum Op : unsigned { kOpSubmit = 1, kOpPause = 2, kOpResume = 3, kOpFence = 4,
 struct alignas(128) DevAtom {
   unsigned long long claim;  // +0  seq << 32 | next slice offset (fetch-add)
   unsigned count;            // +8  slices = blocks x parts
-  unsigned paused;           // +12 (claim, count, paused): one 16-byte load
+  unsigned paused;           // +12 (claim, count, paused): one 16-byte load.
+                             //     bit 0: paused; bit 1 (kGatedBit): early start, gate closed
   long long lo;              // +16 first block
   unsigned body;             // +24
   unsigned parts;            // +28 slices per block
@@ -95,6 +96,7 @@ static_assert(offsetof(DevAtom, chain) % 8 == 0 && offsetof(DevAtom, succ) == of
 // successor: exactly one does, and a successor registered after the
 // predecessor finished is armed by the ingest warp itself.
 constexpr unsigned kSuccDone = 0xffffffffu;
+constexpr unsigned kGatedBit = 2u;  // DevAtom::paused: a claimer's hint that `gate` may be closed
 constexpr unsigned kChainHead = 1u;
 constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head
 
@@ -290,7 +292,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           // key cannot carry into the sequence bits, and arming overwrites it.
           a->claim = (static_cast<unsigned long long>(seq) << 32) | count;
           a->count = count;
-          a->paused = 0;
+          a->paused = 0;  // (the early-start bit is set below)
           a->lo = lo;
           a->body = body;
           a->parts = parts;
@@ -314,6 +316,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
                              prio <= p.atoms[pred - 1u].prio &&
                              ld_relaxed_gpu(&p.atoms[pred - 1u].armed) != 0u;
           a->gate = early ? 1u : 0u;
+          a->paused = early ? kGatedBit : 0u;
           a->armed = 0u;
           a->tag = tag;
           a->trace = reinterpret_cast<unsigned*>(trace);
@@ -361,7 +364,10 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
         // Shuffles are warp-collective: read every field before lane-0 work.
         const unsigned slot = get(kFSlot);
         DevAtom* a = p.atoms + slot;
-        if (lane == 0) atomicExch(&a->paused, op == kOpPause ? 1u : 0u);
+        if (lane == 0) {
+          if (op == kOpPause) atomicOr(&a->paused, 1u);
+          else atomicAnd(&a->paused, ~1u);
+        }
         // Workers drain one atom on a fast path while their TPC's version is
         // unchanged, so pause and resume both bump it.
         // Lane 0 wrote the mask if the atom arrived in this batch: read it
@@ -436,6 +442,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
               // open an early successor's gate.
               if (s.early) {
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&a->gate), "r"(0u) : "memory");
+                atomicAnd(&a->paused, ~kGatedBit);
               } else {
                 st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
                 a->t_armed = gtimer();
@@ -481,6 +488,8 @@ struct RoundCmd {
   unsigned long long key;       // resident key of the atom
   unsigned slot;
   unsigned count;               // slices of the atom (1: single-block fast path)
+  unsigned gated;               // the atom was early-started: its body checks the gate
+  unsigned pad;
 };
 constexpr int kRoundCmdWords64 = sizeof(RoundCmd) / 8;
 static_assert(sizeof(RoundCmd) % 8 == 0, "RoundCmd copied as 64-bit words");
@@ -709,6 +718,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         // through the count above, are released to its gate waiters.
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&p.atoms[next - 1u].gate), "r"(0u)
                      : "memory");
+        atomicAnd(&p.atoms[next - 1u].paused, ~kGatedBit);
         next = 0;
       }
       if (next != 0u) {
@@ -719,7 +729,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         const int bprio = static_cast<int>(bf.seq_prio >> 32);
         const unsigned bcount = static_cast<unsigned>(bf.count_paused);
         const unsigned bbody = static_cast<unsigned>(bf.body_parts);
-        const bool here = (((tpc < 64 ? bf.mask[0] : bf.mask[1]) >> (tpc & 63)) & 1ull) && (bf.count_paused >> 32) == 0u &&
+        const bool here = (((tpc < 64 ? bf.mask[0] : bf.mask[1]) >> (tpc & 63)) & 1ull) && ((bf.count_paused >> 32) & 1ull) == 0u &&
                           bprio >= floor_prio && (!body_is_pair(bbody) || rank == 0u);
         st_relaxed_gpu64(&b->claim, (static_cast<unsigned long long>(bseq) << 32) | (here ? 1u : 0u));
         b->t_armed = gtimer();
@@ -732,6 +742,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
           if (body_is_pair(c->body) && c->prio <= bprio && ld_relaxed_gpu(&c->gate) == 0u &&
               ld_relaxed_gpu(&c->armed) == 0u) {
             c->gate = 1u;
+            atomicOr(&c->paused, kGatedBit);
             fence_acq_rel_gpu();  // the gate before the claim
             st_relaxed_gpu64(&c->claim, static_cast<unsigned long long>(c->seq) << 32);
             c->t_armed = gtimer();
@@ -752,6 +763,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
                    (static_cast<unsigned long long>(~bseq) << 24) | (next - 1u);
           ho.slot = next - 1u;
           ho.count = bcount;
+          ho.gated = 0u;  // armed by this finisher: not early
           if (bcount == 1u) next = 0;  // nothing left for other workers: no wake-up
         }
       }
@@ -819,12 +831,14 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
 __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned rank,
                                          StreamPipe& pipe, GemmPipe& gemm, GemvPipe& gemv,
                                          const DevAtom* atoms) {
+  // Only an early-started atom's blocks check its gate (weights first).
+  const unsigned* gate = rc.gated ? &atoms[rc.slot].gate : nullptr;
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
-    case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, &atoms[rc.slot].gate); break;
-    case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm, &atoms[rc.slot].gate); break;
+    case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, gate); break;
+    case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm, gate); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
-    case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm, &atoms[rc.slot].gate); break;
+    case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm, gate); break;
     default: break;
   }
 }
@@ -986,7 +1000,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               f_a[4] = ld_relaxed_gpu64(&a->args[4]);
               eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
                          static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
-                         static_cast<unsigned>(cp >> 32) == 0u &&
+                         ((cp >> 32) & 1ull) == 0u &&
                          static_cast<int>(k >> 56) >= floor_prio;
             }
             // Candidates of this snapshot, best first: a claim lost to other
@@ -1004,6 +1018,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               // The winner's count and body travel with the arbitration.
               const int win = __ffs(__ballot_sync(0xffffffffu, eligible && k == key)) - 1;
               const unsigned wcount = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp), win);
+              const unsigned wgated = __shfl_sync(0xffffffffu, static_cast<unsigned>(f_cp >> 32), win) & kGatedBit;
               const unsigned long long wbp = __shfl_sync(0xffffffffu, f_bp, win);
               const bool pair = body_is_pair(static_cast<unsigned>(wbp));
               // GEMV tiles are HBM-bound (their MMAs are a few percent of
@@ -1073,6 +1088,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                   sh.rc.key = key;
                   sh.rc.slot = static_cast<unsigned>(key & 0xffffffull);
                   sh.rc.count = wcount;
+                  sh.rc.gated = wgated;
                 }
               }
               break;
@@ -1093,6 +1109,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
                 sh.rc.slot = slot;
                 sh.rc.key = key;
                 sh.rc.count = ld_relaxed_gpu(&a->count);
+                sh.rc.gated = ld_relaxed_gpu(&a->paused) & kGatedBit;
               }
               const unsigned parts = sh.rc.cmd.parts;
               sh.rc.cmd.block = sh.rc.lo + off / parts;

@@ -303,7 +303,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
     const unsigned tx = 2 * (kGemmABytes + n_tile / 2 * kGemmBK * 2);  // both CTAs' A and B halves
     // B (weights) for the first stages first, then A once the atom's gate
     // is open (early start; otherwise the gate read overlaps the B loads).
-    const unsigned pre = nk < S ? nk : S;
+    const unsigned pre = gate ? (nk < S ? nk : S) : 0u;  // (no gate: loads in stage order)
     for (unsigned j = 0; j < pre; ++j) {
       const unsigned s = static_cast<unsigned>((g0 + j) % S);
       if ((g0 + j) / S >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>(((g0 + j) / S - 1) & 1));
@@ -311,8 +311,10 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
       tma_load_2d_pair(G.tiles + s * kGemmStageBytes + kGemmABytes, &D->b, static_cast<int>(j * kGemmBK),
                        b_row, G.full + s);
     }
-    while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // A: generic-proxy writes, TMA reads
+    if (gate) {
+      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // A: generic-proxy writes, TMA reads
+    }
     for (unsigned j = 0; j < pre; ++j)
       tma_load_2d_pair(G.tiles + static_cast<unsigned>((g0 + j) % S) * kGemmStageBytes, &D->a,
                        static_cast<int>(j * kGemmBK), a_row, G.full + static_cast<unsigned>((g0 + j) % S));

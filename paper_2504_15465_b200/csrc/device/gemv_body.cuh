@@ -128,7 +128,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
     // W for the first stages first, then x once the atom's gate is open:
     // an early-started block streams W while its predecessor still writes
     // x; for any other block the gate read overlaps the W loads.
-    const unsigned pre = nk < S ? nk : S;
+    const unsigned pre = gate ? (nk < S ? nk : S) : 0u;  // (no gate: loads in stage order)
     for (unsigned j = 0; j < pre; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
@@ -138,8 +138,10 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       tma_load_2d_pair(G.tiles + s * kGemvStageBytes, &D->w, static_cast<int>((kb0 + j) * kGemmBK), w_row,
                        G.full + s);
     }
-    while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic-proxy writes, TMA reads
+    if (gate) {
+      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic-proxy writes, TMA reads
+    }
     for (unsigned j = 0; j < pre; ++j) {
       const unsigned s = static_cast<unsigned>((g0 + j) % S);
       tma_load_2d_pair(G.tiles + s * kGemvStageBytes + kGemvWBytes, &D->x,
