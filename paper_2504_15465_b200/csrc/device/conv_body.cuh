@@ -98,7 +98,7 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
                        k_row, G.full + s);
     }
     if (gate) {
-      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+      while (ld_acquire_gpu(gate) & 2u) __nanosleep(64);  // DevAtom::paused, kGatedBit
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     for (unsigned j = 0; j < pre; ++j) {

@@ -64,7 +64,8 @@ struct alignas(128) DevAtom {
   unsigned long long claim;  // +0  seq << 32 | next slice offset (fetch-add)
   unsigned count;            // +8  slices = blocks x parts
   unsigned paused;           // +12 (claim, count, paused): one 16-byte load.
-                             //     bit 0: paused; bit 1 (kGatedBit): early start, gate closed
+                             //     bit 0: paused; bit 1 (kGatedBit): early-started, gate
+                             //     closed (its tiles wait for it to clear before reading x / A)
   long long lo;              // +16 first block
   unsigned body;             // +24
   unsigned parts;            // +28 slices per block
@@ -81,7 +82,7 @@ struct alignas(128) DevAtom {
   unsigned long long t_first, t_last;   // second line: per-block records
   unsigned long long touched[2];
   unsigned long long t_seen, t_armed;   // ingest instrumentation (globaltimer)
-  unsigned gate;                        // early-armed chained GEMV: 1 until its predecessor ends
+  unsigned pad1;
   unsigned armed;                       // claim armed (blocks claimable or claimed)
   unsigned char entry[GPUOS_MAX_TPCS];  // resident-list index per TPC
 };
@@ -96,7 +97,13 @@ static_assert(offsetof(DevAtom, chain) % 8 == 0 && offsetof(DevAtom, succ) == of
 // successor: exactly one does, and a successor registered after the
 // predecessor finished is armed by the ingest warp itself.
 constexpr unsigned kSuccDone = 0xffffffffu;
-constexpr unsigned kGatedBit = 2u;  // DevAtom::paused: a claimer's hint that `gate` may be closed
+constexpr unsigned kGatedBit = 2u;  // DevAtom::paused: early start, gate closed
+
+// Opens an early-started atom's gate (release: the predecessor's outputs,
+// which the caller has acquired, become visible to the gate's waiters).
+__device__ __forceinline__ void open_gate(unsigned* paused) {
+  asm volatile("red.release.gpu.global.and.b32 [%0], %1;" ::"l"(paused), "r"(~kGatedBit) : "memory");
+}
 constexpr unsigned kChainHead = 1u;
 constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head
 
@@ -315,7 +322,6 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           const bool early = pred != 0u && body_is_pair(body) &&
                              prio <= p.atoms[pred - 1u].prio &&
                              ld_relaxed_gpu(&p.atoms[pred - 1u].armed) != 0u;
-          a->gate = early ? 1u : 0u;
           a->paused = early ? kGatedBit : 0u;
           a->armed = 0u;
           a->tag = tag;
@@ -333,7 +339,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           s.slot = slot;
           s.seq = seq;
           s.pred = pred;
-          s.early = a->gate;
+          s.early = early ? 1u : 0u;
           s.mask[0] = mask0;
           s.mask[1] = mask1;
           s.key = (static_cast<unsigned long long>(prio & 0xff) << 56) |
@@ -441,8 +447,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
               // Predecessor already finished: arm here (woken below), or
               // open an early successor's gate.
               if (s.early) {
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&a->gate), "r"(0u) : "memory");
-                atomicAnd(&a->paused, ~kGatedBit);
+                open_gate(&a->paused);
               } else {
                 st_relaxed_gpu64(&a->claim, static_cast<unsigned long long>(s.seq) << 32);
                 a->t_armed = gtimer();
@@ -713,12 +718,10 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       // Registered before we looked: nothing to race with (registration
       // happens once), and the acquire above ordered its fields.
       next = pre != 0u ? pre : atom_exch_acq_rel32(&a->succ, kSuccDone);
-      if (next != 0u && ld_relaxed_gpu(&p.atoms[next - 1u].gate) != 0u) {
-        // Early-started successor (armed at ingest): our outputs, acquired
-        // through the count above, are released to its gate waiters.
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&p.atoms[next - 1u].gate), "r"(0u)
-                     : "memory");
-        atomicAnd(&p.atoms[next - 1u].paused, ~kGatedBit);
+      if (next != 0u && (ld_relaxed_gpu(&p.atoms[next - 1u].paused) & kGatedBit)) {
+        // Early-started successor: our outputs, acquired through the count
+        // above, are released to its gate waiters.
+        open_gate(&p.atoms[next - 1u].paused);
         next = 0;
       }
       if (next != 0u) {
@@ -739,12 +742,14 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         const unsigned cn = ld_acquire_gpu(&b->succ);
         if (cn != 0u && cn != kSuccDone) {
           DevAtom* c = p.atoms + (cn - 1u);
-          if (body_is_pair(c->body) && c->prio <= bprio && ld_relaxed_gpu(&c->gate) == 0u &&
-              ld_relaxed_gpu(&c->armed) == 0u) {
-            c->gate = 1u;
-            atomicOr(&c->paused, kGatedBit);
-            fence_acq_rel_gpu();  // the gate before the claim
-            st_relaxed_gpu64(&c->claim, static_cast<unsigned long long>(c->seq) << 32);
+          if (body_is_pair(c->body) && c->prio <= bprio && ld_relaxed_gpu(&c->armed) == 0u) {
+            // Armed claim and closed gate in one 16-byte store: a claimer
+            // never sees one without the other.
+            const unsigned long long cc = static_cast<unsigned long long>(c->count) |
+                                          (static_cast<unsigned long long>(kGatedBit) << 32);
+            asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(&c->claim),
+                         "l"(static_cast<unsigned long long>(c->seq) << 32), "l"(cc)
+                         : "memory");
             c->t_armed = gtimer();
             c->armed = 1u;
             look = cn;
@@ -832,7 +837,7 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
                                          StreamPipe& pipe, GemmPipe& gemm, GemvPipe& gemv,
                                          const DevAtom* atoms) {
   // Only an early-started atom's blocks check its gate (weights first).
-  const unsigned* gate = rc.gated ? &atoms[rc.slot].gate : nullptr;
+  const unsigned* gate = rc.gated ? &atoms[rc.slot].paused : nullptr;
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
     case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, gate); break;

@@ -312,7 +312,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
                        b_row, G.full + s);
     }
     if (gate) {
-      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+      while (ld_acquire_gpu(gate) & 2u) __nanosleep(64);  // DevAtom::paused, kGatedBit
       asm volatile("fence.proxy.async.global;" ::: "memory");  // A: generic-proxy writes, TMA reads
     }
     for (unsigned j = 0; j < pre; ++j)

@@ -139,7 +139,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
                        G.full + s);
     }
     if (gate) {
-      while (ld_acquire_gpu(gate) != 0u) __nanosleep(64);
+      while (ld_acquire_gpu(gate) & 2u) __nanosleep(64);  // DevAtom::paused, kGatedBit
       asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic-proxy writes, TMA reads
     }
     for (unsigned j = 0; j < pre; ++j) {
