@@ -19,12 +19,13 @@
 //   key: highest priority, then oldest atom -- the reference's refill rule
 //   (device.cpp:188-206). There is no lower-priority bypass: a lane-parallel
 //   max over eligible atoms picks exactly one.
-// * Lane 0 claims a block with a CAS on the atom's claim word
-//   (seq << 32 | next offset); the sequence tag makes a stale key for a
-//   recycled slot fail the CAS instead of stealing a block.
+// * Lane 0 claims a block with a fetch-add on the atom's claim word
+//   (seq << 32 | next offset); the sequence tag tells a stale key for a
+//   recycled slot apart (its offset is run for the slot's new occupant).
 // * All 8 warps run the body; warp 0 then accounts the block and, for the
-//   atom's last block, removes its resident keys and writes the completion
-//   record (device timestamps, TPCs touched) into host-mapped memory.
+//   atom's last block, arms a chained successor (or opens its early-start
+//   gate), writes the completion record (device timestamps, TPCs touched)
+//   into host-mapped memory and removes its resident keys.
 // * Block-granular revocation: fence[tpc] is a minimum priority; raising it
 //   stops stolen atoms from starting new blocks there without a relaunch.
 #include <cuda_runtime.h>
@@ -79,7 +80,7 @@ struct alignas(128) DevAtom {
   unsigned long long mask[2];  // +104
   unsigned chain;            // +120 kChainHead: completion arms a successor
   unsigned succ;             // +124 chained successor: slot + 1, kSuccDone once finished
-  unsigned long long t_first, t_last;   // second line: per-block records
+  unsigned long long t_first, t_last;   // second line: first slice's start (t_last unused)
   unsigned long long touched[2];
   unsigned long long t_seen, t_armed;   // ingest instrumentation (globaltimer)
   unsigned pad1;
