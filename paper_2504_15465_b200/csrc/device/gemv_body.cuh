@@ -219,9 +219,22 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       if (last_split) {
         const unsigned row = blk * kGemvTile + static_cast<unsigned>(tid);
         if (row < D->n) {
+          // Up to 16 splits: every partial load in flight at once (one L2
+          // round trip, not one per split), summed in split order.
           float acc = 0.f;
-          for (unsigned sp = 0; sp < D->splits; ++sp)
-            acc += __ldcg(D->partial + static_cast<size_t>(sp) * D->n + row);
+          const unsigned splits = D->splits;
+          if (splits <= 16) {
+            float v[16];
+#pragma unroll
+            for (unsigned sp = 0; sp < 16; ++sp)
+              v[sp] = sp < splits ? __ldcg(D->partial + static_cast<size_t>(sp) * D->n + row) : 0.f;
+#pragma unroll
+            for (unsigned sp = 0; sp < 16; ++sp)
+              if (sp < splits) acc += v[sp];
+          } else {
+            for (unsigned sp = 0; sp < splits; ++sp)
+              acc += __ldcg(D->partial + static_cast<size_t>(sp) * D->n + row);
+          }
           if (bf16_y)
             reinterpret_cast<__nv_bfloat16*>(D->y)[row] = __float2bfloat16_rn(acc);
           else
