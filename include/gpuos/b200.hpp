@@ -207,7 +207,7 @@ class B200Device final : public Device {
   bool supports_chaining() const override { return true; }
   AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,
                         const std::vector<int>& tpcs, int priority, bool atomized,
-                        std::uint64_t tag, bool chain_head) override;
+                        std::uint64_t tag, bool chain_head, bool no_early = false) override;
 
   B200Runtime& runtime() { return *rt_; }
   // Clears per-run state so one device (and its workspaces) serves many runs.

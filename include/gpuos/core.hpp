@@ -185,9 +185,12 @@ class Device {
   // `chain_head` lets a later atom be chained behind this one. Completions
   // still arrive in chain order. Backends without it never see the call.
   virtual bool supports_chaining() const { return false; }
+  // `no_early`: a tensor-core successor must not start its weight loads
+  // before `after` completes (the predecessor may run for seconds).
   virtual AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,
                                 const std::vector<int>& tpcs, int priority,
-                                bool atomized, std::uint64_t tag, bool chain_head);
+                                bool atomized, std::uint64_t tag, bool chain_head,
+                                bool no_early = false);
 };
 
 }  // namespace gpuos

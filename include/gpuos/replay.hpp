@@ -37,7 +37,7 @@ class DeviceEngine final : public Device {
   bool supports_chaining() const override { return true; }
   AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,
                         const std::vector<int>& tpcs, int priority, bool atomized,
-                        std::uint64_t tag, bool chain_head) override;
+                        std::uint64_t tag, bool chain_head, bool no_early = false) override;
   SimTime request_frequency(FreqMhz f) override;
   void schedule_call(SimTime t, std::function<void()> fn) override;
   void set_atom_complete_handler(

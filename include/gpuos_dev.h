@@ -131,6 +131,11 @@ typedef struct gpuos_atom_desc {
 #define GPUOS_ATOM_CHAIN_HEAD 1u /* a successor may be chained behind this
                                     atom (its completion then arms it: one
                                     extra L2 atomic on the last block)    */
+#define GPUOS_ATOM_NO_EARLY 2u   /* a chained tensor-core atom that must not
+                                    start early (weights before its
+                                    predecessor ends): set when the
+                                    predecessor may run longer than the
+                                    bodies' 2 s pipeline hang guard     */
 
 typedef struct gpuos_completion {
   uint32_t atom_id;          /* id returned by gpuos_dev_submit_atom        */

@@ -85,6 +85,7 @@ class AtomDesc(C.Structure):
 
 
 GPUOS_ATOM_CHAIN_HEAD = 1
+GPUOS_ATOM_NO_EARLY = 2
 
 
 class Completion(C.Structure):
@@ -276,7 +277,7 @@ class Device:
     @staticmethod
     def desc(lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
              trace: int | None = None, parts: int = 1, after: int | None = None,
-             chain_head: bool = False) -> AtomDesc:
+             chain_head: bool = False, no_early: bool = False) -> AtomDesc:
         """One atom. `after`: atom id of a predecessor this atom is chained
         behind (armed on the device when the predecessor's last block ends);
         the predecessor must have been submitted with chain_head=True."""
@@ -291,7 +292,7 @@ class Device:
             d.args[i] = int(a)
         d.trace = trace
         d.after = 0 if after is None else after + 1
-        d.flags = GPUOS_ATOM_CHAIN_HEAD if chain_head else 0
+        d.flags = (GPUOS_ATOM_CHAIN_HEAD if chain_head else 0) | (GPUOS_ATOM_NO_EARLY if no_early else 0)
         return d
 
     def run_batch(self, descs: list[AtomDesc]) -> float:
@@ -303,8 +304,8 @@ class Device:
 
     def submit(self, lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
                trace: int | None = None, parts: int = 1, after: int | None = None,
-               chain_head: bool = False) -> int:
-        d = self.desc(lo, hi, tpcs, priority, body, args, tag, trace, parts, after, chain_head)
+               chain_head: bool = False, no_early: bool = False) -> int:
+        d = self.desc(lo, hi, tpcs, priority, body, args, tag, trace, parts, after, chain_head, no_early)
         aid = C.c_uint32()
         self._check(self._lib.gpuos_dev_submit_atom(self._h, C.byref(d), C.byref(aid)))
         return aid.value

@@ -106,7 +106,9 @@ __device__ __forceinline__ void open_gate(unsigned* paused) {
   asm volatile("red.release.gpu.global.and.b32 [%0], %1;" ::"l"(paused), "r"(~kGatedBit) : "memory");
 }
 constexpr unsigned kChainHead = 1u;
-constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head
+constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head | no early
+constexpr unsigned kAuxNoEarly = 0x40000000u;
+constexpr unsigned kNoEarly = 2u;                 // DevAtom::chain: GPUOS_ATOM_NO_EARLY
 
 struct DevCtl {
   unsigned quit;
@@ -292,7 +294,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
         const unsigned body = get(kFBody);
         const unsigned pred = get(kFPred);
         const unsigned aux = get(kFAux);
-        const unsigned parts = aux & ~kAuxChainHead;
+        const unsigned parts = aux & ~(kAuxChainHead | kAuxNoEarly);
         DevAtom* a = p.atoms + slot;
         if (lane == 0) {
           // Exhausted (offset == count) until armed in phase B: a stale
@@ -310,7 +312,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           a->prio = prio;
           a->done = 0;
           a->succ = 0;
-          a->chain = (aux & kAuxChainHead) ? kChainHead : 0u;
+          a->chain = ((aux & kAuxChainHead) ? kChainHead : 0u) | ((aux & kAuxNoEarly) ? kNoEarly : 0u);
           // Early start: a chained GEMV is armed at once behind a closed gate
           // -- its blocks stream W while the predecessor runs and read x
           // when the predecessor's finisher opens the gate. Only at a
@@ -320,7 +322,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           // win every slot before ours, so our waiting blocks cannot starve
           // it (an unarmed predecessor could find every worker parked at
           // our gate).
-          const bool early = pred != 0u && body_is_pair(body) &&
+          const bool early = pred != 0u && body_is_pair(body) && !(aux & kAuxNoEarly) &&
                              prio <= p.atoms[pred - 1u].prio &&
                              ld_relaxed_gpu(&p.atoms[pred - 1u].armed) != 0u;
           a->paused = early ? kGatedBit : 0u;
@@ -743,7 +745,8 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         const unsigned cn = ld_acquire_gpu(&b->succ);
         if (cn != 0u && cn != kSuccDone) {
           DevAtom* c = p.atoms + (cn - 1u);
-          if (body_is_pair(c->body) && c->prio <= bprio && ld_relaxed_gpu(&c->armed) == 0u) {
+          if (body_is_pair(c->body) && !(c->chain & kNoEarly) && c->prio <= bprio &&
+              ld_relaxed_gpu(&c->armed) == 0u) {
             // Armed claim and closed gate in one 16-byte store: a claimer
             // never sees one without the other.
             const unsigned long long cc = static_cast<unsigned long long>(c->count) |
@@ -1796,7 +1799,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   const uint32_t id_base = d->next_atom_id;
   for (int i = 0; i < n; ++i) {
     const gpuos_atom_desc& a = descs[i];
-    if (a.flags & ~GPUOS_ATOM_CHAIN_HEAD) return fail(GPUOS_E_CONFIG, "unknown atom flags");
+    if (a.flags & ~(GPUOS_ATOM_CHAIN_HEAD | GPUOS_ATOM_NO_EARLY)) return fail(GPUOS_E_CONFIG, "unknown atom flags");
     if (a.after != 0) {
       // Only atoms of this batch exist: the predecessor is an earlier entry.
       const int64_t j = static_cast<int64_t>(a.after - 1u) - static_cast<int64_t>(id_base);
@@ -1825,7 +1828,8 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     x.body = a.body;
     x.lo = a.lo;
     ids[static_cast<size_t>(i)] = d->next_atom_id++;
-    x.chain = (a.flags & GPUOS_ATOM_CHAIN_HEAD) ? kChainHead : 0u;
+    x.chain = ((a.flags & GPUOS_ATOM_CHAIN_HEAD) ? kChainHead : 0u) |
+              ((a.flags & GPUOS_ATOM_NO_EARLY) ? kNoEarly : 0u);
     x.armed = pred[static_cast<size_t>(i)] >= 0 ? 0u : 1u;
     if (pred[static_cast<size_t>(i)] >= 0) {
       x.claim |= x.count;  // unarmed until the predecessor's last block
@@ -1954,7 +1958,8 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
     if (((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) && d->tpc_resident[t] >= kResident)
       return fail(GPUOS_E_FULL, "TPC " + std::to_string(t) + " already holds 32 resident atoms");
   if (d->free_slots.empty()) return fail(GPUOS_E_FULL, "atom table full");
-  if (a->flags & ~GPUOS_ATOM_CHAIN_HEAD) return fail(GPUOS_E_CONFIG, "unknown atom flags");
+  if (a->flags & ~(GPUOS_ATOM_CHAIN_HEAD | GPUOS_ATOM_NO_EARLY))
+    return fail(GPUOS_E_CONFIG, "unknown atom flags");
   // Chaining: a live predecessor (not yet polled) arms this atom on the
   // device; one that already completed leaves nothing to wait for.
   uint32_t pred_slot = 0, pred_seq = 0;
@@ -1984,7 +1989,8 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   data[kFPrio] = static_cast<uint32_t>(map_priority(a->priority));
   put64(data, kFLo, static_cast<uint64_t>(a->lo));
   data[kFCount] = static_cast<uint32_t>((a->hi - a->lo) * parts);
-  data[kFAux] = parts | ((a->flags & GPUOS_ATOM_CHAIN_HEAD) ? kAuxChainHead : 0u);
+  data[kFAux] = parts | ((a->flags & GPUOS_ATOM_CHAIN_HEAD) ? kAuxChainHead : 0u) |
+                ((a->flags & GPUOS_ATOM_NO_EARLY) ? kAuxNoEarly : 0u);
   data[kFBody] = a->body;
   put64(data, kFMask0, a->tpc_mask[0]);
   put64(data, kFMask1, a->tpc_mask[1]);

@@ -466,7 +466,7 @@ AtomId B200Device::submit_atom(KernelId kernel, long lo, long hi, const std::vec
 
 AtomId B200Device::submit_chained(AtomId after, KernelId kernel, long lo, long hi,
                                   const std::vector<int>& tpcs, int priority, bool atomized,
-                                  std::uint64_t tag, bool chain_head) {
+                                  std::uint64_t tag, bool chain_head, bool no_early) {
   const SimKernelSpec& spec = kernels_.at(kernel);
   if (tpcs.empty()) throw ConfigError("atom needs a non-empty TPC set");
   if (lo < 0 || hi <= lo || hi > spec.total_blocks)
@@ -489,7 +489,7 @@ AtomId B200Device::submit_chained(AtomId after, KernelId kernel, long lo, long h
   d.atomized = atomized ? 1 : 0;
   d.parts = r.parts;
   d.after = after == kNoAtom ? 0u : after + 1u;
-  d.flags = chain_head ? GPUOS_ATOM_CHAIN_HEAD : 0u;
+  d.flags = (chain_head ? GPUOS_ATOM_CHAIN_HEAD : 0u) | (no_early ? GPUOS_ATOM_NO_EARLY : 0u);
   std::uint32_t id = 0;
   check(gpuos_dev_submit_atom(rt_->handle(), &d, &id), "gpuos_dev_submit_atom");
   AtomTimeline tl{};

@@ -83,7 +83,7 @@ Duration reference_kernel_latency(const SimKernelSpec& spec, int t, FreqMhz f,
 }
 
 AtomId Device::submit_chained(AtomId, KernelId, long, long, const std::vector<int>&, int, bool,
-                              std::uint64_t, bool) {
+                              std::uint64_t, bool, bool) {
   throw InvariantError("this backend does not chain kernels");
 }
 

@@ -117,7 +117,8 @@ AtomId DeviceEngine::submit_atom(KernelId kernel, long lo, long hi,
 
 AtomId DeviceEngine::submit_chained(AtomId after, KernelId kernel, long lo, long hi,
                                     const std::vector<int>& tpcs, int priority,
-                                    bool atomized, std::uint64_t tag, bool /*chain_head*/) {
+                                    bool atomized, std::uint64_t tag, bool /*chain_head*/,
+                                    bool /*no_early*/) {
   if (after == kNoAtom || atoms_.at(after).finished)
     return submit_atom(kernel, lo, hi, tpcs, priority, atomized, tag);
   if (atoms_[after].succ != kNoAtom) throw InvariantError("atom already has a successor");

@@ -293,3 +293,33 @@ def test_early_started_gemm_and_conv_read_their_predecessors_output(api, cuda_de
                                       padding=1).permute(0, 2, 3, 1)
     errx = ((x2.double().cpu() - refx).abs().max() / refx.abs().max()).item()
     assert errx < 1e-3, errx
+
+
+def test_no_early_keeps_a_chained_gemv_behind_its_predecessor(api, cuda_device):
+    """GPUOS_ATOM_NO_EARLY: the chained GEMV is armed only when its
+    predecessor completes (no block starts before the predecessor's last
+    ends), and still reads the predecessor's output."""
+    import torch
+
+    n1, k, n2 = 8192, 4096, 4096
+    g = torch.Generator(device="cuda").manual_seed(5)
+    w1 = (torch.rand(n1, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    x = (torch.rand(k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w2 = (torch.rand(n2, n1, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    y1 = torch.full((n1,), float("nan"), device="cuda", dtype=torch.bfloat16)
+    y2 = torch.full((n2,), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    with api.Device(workers_per_sm=2) as dev:
+        d1, b1 = dev.gemv_desc(w1.data_ptr(), x.data_ptr(), y1.data_ptr(), n1, k, bf16_out=True, k_splits=4)
+        d2, b2 = dev.gemv_desc(w2.data_ptr(), y1.data_ptr(), y2.data_ptr(), n2, n1, k_splits=4)
+        dev.start()
+        a = dev.submit(0, b1, range(74), 30, api.GPUOS_BODY_GEMV_BF16, [d1], chain_head=True)
+        b = dev.submit(0, b2, range(74), 30, api.GPUOS_BODY_GEMV_BF16, [d2], after=a, no_early=True)
+        done = wait_all(dev, 2)
+        dev.stop()
+        dev.free(d1)
+        dev.free(d2)
+    check_order(done, [a, b])
+    ref = (w2.double().cpu() @ y1.double().cpu()).float()
+    err = ((y2.cpu() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-3, err
