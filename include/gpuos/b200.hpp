@@ -202,7 +202,7 @@ class B200Device final : public Device {
   const std::map<FreqMhz, Duration>& freq_residency() const override { return residency_; }
   long blocks_executed(KernelId k) const override { return executed_.at(k); }
 
-  void set_tpc_fence(const std::vector<int>& tpcs, int min_priority) override;
+  void set_tpc_fence(const std::vector<int>& tpcs, int min_priority, std::uint64_t owner_tag) override;
   bool preempts_stolen() const override { return true; }
   bool supports_chaining() const override { return true; }
   AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,
@@ -216,6 +216,9 @@ class B200Device final : public Device {
   float last_kernel_ms() const { return last_ms_; }
   std::int64_t run_wall_ns() const { return run_wall_ns_; }
   const std::vector<SimKernelSpec>& kernels() const { return kernels_; }
+  // submit_atom calls that found a TPC's resident list (32) or the atom
+  // table full and waited for completions (last run).
+  std::int64_t backpressure_waits() const { return backpressure_waits_; }
 
  private:
   SimTime host_now() const;
@@ -242,6 +245,7 @@ class B200Device final : public Device {
   std::function<void(const AtomCompletion&)> on_complete_;
   SimTime horizon_ = -1;
   double busy_tpc_ns_ = 0.0;
+  std::int64_t backpressure_waits_ = 0;
   std::map<FreqMhz, Duration> residency_;
   float last_ms_ = 0.f;
   std::int64_t run_wall_ns_ = 0;

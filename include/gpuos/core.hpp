@@ -175,7 +175,11 @@ class Device {
   // work, so blocks of atoms below `min_priority` must stop starting there
   // (block-granular revocation). The replay backend models the reference,
   // which revokes only at atom boundaries, and ignores it.
-  virtual void set_tpc_fence(const std::vector<int>& /*tpcs*/, int /*min_priority*/) {}
+  // Block-granular revocation (live extension): on these TPCs only atoms
+  // of `owner_tag` (the owning tenant's submit tag) or of priority >=
+  // min_priority start new blocks (min_priority 0 lifts the fence).
+  virtual void set_tpc_fence(const std::vector<int>& /*tpcs*/, int /*min_priority*/,
+                             std::uint64_t /*owner_tag*/) {}
   // Live-backend hook: true when TPCs holding only foreign stolen atoms may
   // be handed back to their owner immediately (device priority arbitration
   // preempts at the next block boundary).

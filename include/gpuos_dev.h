@@ -46,9 +46,9 @@ extern "C" {
 #define GPUOS_RESIDENT_PER_TPC 32
 
 /* ------------------------------------------------------------ config flags */
-/* start() launches only the ingest warp; atoms submitted before
- * gpuos_dev_launch_workers() are staged on the device, so the worker
- * kernel's CUDA-event time covers execution alone (batch measurements).  */
+/* start() prepares the run but does not launch the dispatcher; atoms
+ * submitted before gpuos_dev_launch_workers() wait in the submit ring (at
+ * most ring_entries of them), so the kernel starts with a backlog.        */
 #define GPUOS_DEV_DEFER_WORKERS 1u
 
 /* ------------------------------------------------------------ body kinds */
@@ -84,7 +84,12 @@ typedef struct gpuos_dev_config {
   int32_t ring_entries;     /* host->device submit ring [4096]            */
   int32_t idle_sleep_ns;    /* worker back-off while idle [256]           */
   uint32_t flags;           /* GPUOS_DEV_* flags                          */
-  int32_t reserved;
+  int32_t pipeline_timeout_ms; /* bound on one tensor-core pipeline wait
+                               (TMA / MMA / accumulator mbarriers) [2000];
+                               on expiry the device raises a fault, the
+                               dispatcher drains out and the host gets
+                               GPUOS_E_TIMEOUT -- no context-killing trap.
+                               Early-start gate waits are not bounded.   */
 } gpuos_dev_config;
 
 typedef struct gpuos_dev_topology {
@@ -126,6 +131,11 @@ typedef struct gpuos_atom_desc {
                                 runs at once. poll() never reports an atom
                                 before its predecessor.                     */
   uint32_t flags;            /* GPUOS_ATOM_*                                */
+  uint32_t tenant;           /* 1 + the submitting tenant's id (< 65535), or
+                                0: none. A TPC's owner (gpuos_dev_set_tpc_owner)
+                                starts its own atoms there whatever its
+                                fence floor.                               */
+  uint32_t reserved;
 } gpuos_atom_desc;
 
 #define GPUOS_ATOM_CHAIN_HEAD 1u /* a successor may be chained behind this
@@ -162,15 +172,24 @@ typedef struct gpuos_dev_stats {
                                 time minus this is launch + teardown)      */
   int64_t first_block_ns;    /* last run: first worker entry .. first block
                                 start (per-CTA setup: TMEM, barriers)      */
+  uint64_t tpc_busy_ns;      /* summed over logical TPCs: time with >= 1
+                                running block (the reference's
+                                tpc_busy_integral, device.cpp:264-275),
+                                sampled on the device by the ingest warp  */
+  uint32_t fault;            /* last run's device fault code (0: none;
+                                1: a pipeline wait expired)               */
+  uint32_t reserved;
 } gpuos_dev_stats;
 
 int gpuos_dev_open(const gpuos_dev_config* cfg, struct gpuos_dev** out);
 int gpuos_dev_close(struct gpuos_dev* dev);
 int gpuos_dev_get_topology(struct gpuos_dev* dev, gpuos_dev_topology* out);
 
-/* Launch the persistent dispatcher (ingest + worker kernels). */
+/* Launch the persistent dispatcher: ONE kernel (k_worker; its cluster 0
+ * hosts the ingest warp), launched from a helper thread so a profiler that
+ * serialises the launch (ncu) still lets this thread feed the ring.       */
 int gpuos_dev_start(struct gpuos_dev* dev);
-/* With GPUOS_DEV_DEFER_WORKERS: launch the worker kernel now. */
+/* With GPUOS_DEV_DEFER_WORKERS: launch the dispatcher kernel now. */
 int gpuos_dev_launch_workers(struct gpuos_dev* dev);
 /* Batch mode (dispatcher stopped): stage n atoms directly into the device
  * tables and run the worker kernel alone until all complete. Returns its
@@ -194,6 +213,16 @@ int gpuos_dev_set_tpc_fence(struct gpuos_dev* dev, int32_t tpc,
 /* Same for every TPC in the mask, as one ring entry. */
 int gpuos_dev_set_fence_mask(struct gpuos_dev* dev, const uint64_t mask[2],
                              int32_t min_priority);
+/* The device-resident TPC-ownership table: every TPC in the mask gets
+ * `owner` (1 + tenant id, 0: none) and a fence floor. Atoms of the owner
+ * (gpuos_atom_desc::tenant == owner) start blocks there at any priority;
+ * other atoms only at priority >= min_priority (0 lifts the fence). This
+ * is block-granular revocation: a busy owner's quota stops accepting
+ * other tenants' stolen blocks without fencing the owner's own atoms that
+ * span its quota and stolen TPCs (reference: the ledger's owner field and
+ * revocation, scheduler.hpp:61-66, scheduler.cpp:239-270).              */
+int gpuos_dev_set_tpc_owner(struct gpuos_dev* dev, const uint64_t mask[2], uint32_t owner,
+                            int32_t min_priority);
 /* Non-blocking; returns the number of completions written to out[0..max). */
 int gpuos_dev_poll(struct gpuos_dev* dev, gpuos_completion* out, int32_t max);
 int64_t gpuos_dev_now_ns(struct gpuos_dev* dev);

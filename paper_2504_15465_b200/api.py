@@ -45,7 +45,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_set_tpc_fence", "gpuos_dev_poll", "gpuos_dev_now_ns", "gpuos_dev_in_flight",
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
-    "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask",
+    "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask", "gpuos_dev_set_tpc_owner",
     "gpuos_dev_gemm_desc", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
 ]
 SIM_SYMBOLS = [
@@ -67,7 +67,7 @@ class DevConfig(C.Structure):
     _fields_ = [("device_ordinal", C.c_int32), ("workers_per_sm", C.c_int32),
                 ("logical_tpcs", C.c_int32), ("atom_slots", C.c_int32),
                 ("ring_entries", C.c_int32), ("idle_sleep_ns", C.c_int32),
-                ("flags", C.c_uint32), ("reserved", C.c_int32)]
+                ("flags", C.c_uint32), ("pipeline_timeout_ms", C.c_int32)]
 
 
 class DevTopology(C.Structure):
@@ -81,7 +81,8 @@ class AtomDesc(C.Structure):
     _fields_ = [("lo", C.c_int64), ("hi", C.c_int64), ("tpc_mask", C.c_uint64 * 2),
                 ("priority", C.c_int32), ("body", C.c_uint32), ("args", C.c_uint64 * 5),
                 ("tag", C.c_uint64), ("trace", C.c_void_p), ("atomized", C.c_int32),
-                ("parts", C.c_uint32), ("after", C.c_uint32), ("flags", C.c_uint32)]
+                ("parts", C.c_uint32), ("after", C.c_uint32), ("flags", C.c_uint32),
+                ("tenant", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 GPUOS_ATOM_CHAIN_HEAD = 1
@@ -100,7 +101,8 @@ class DevStats(C.Structure):
     _fields_ = [("blocks_executed", C.c_uint64), ("atoms_completed", C.c_uint64),
                 ("worker_busy_ns", C.c_uint64), ("claim_retries", C.c_uint64),
                 ("kernel_elapsed_ns", C.c_int64), ("ingest_entries", C.c_int64),
-                ("worker_span_ns", C.c_int64), ("first_block_ns", C.c_int64)]
+                ("worker_span_ns", C.c_int64), ("first_block_ns", C.c_int64),
+                ("tpc_busy_ns", C.c_uint64), ("fault", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 _lib: C.CDLL | None = None
@@ -126,6 +128,7 @@ def library() -> C.CDLL:
         "gpuos_dev_set_atom_paused": (C.c_int, [P, C.c_uint32, C.c_int]),
         "gpuos_dev_set_tpc_fence": (C.c_int, [P, C.c_int32, C.c_int32]),
         "gpuos_dev_set_fence_mask": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int32]),
+        "gpuos_dev_set_tpc_owner": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_uint32, C.c_int32]),
         "gpuos_dev_poll": (C.c_int, [P, C.POINTER(Completion), C.c_int32]),
         "gpuos_dev_now_ns": (C.c_int64, [P]),
         "gpuos_dev_in_flight": (C.c_int32, [P]),
@@ -277,11 +280,13 @@ class Device:
     @staticmethod
     def desc(lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
              trace: int | None = None, parts: int = 1, after: int | None = None,
-             chain_head: bool = False, no_early: bool = False) -> AtomDesc:
+             chain_head: bool = False, no_early: bool = False, tenant: int = 0) -> AtomDesc:
         """One atom. `after`: atom id of a predecessor this atom is chained
         behind (armed on the device when the predecessor's last block ends);
-        the predecessor must have been submitted with chain_head=True."""
+        the predecessor must have been submitted with chain_head=True.
+        `tenant`: 1 + the submitting tenant's id (0: none), see set_owner."""
         d = AtomDesc()
+        d.tenant = tenant
         d.parts = parts
         d.lo, d.hi, d.priority, d.body, d.tag = lo, hi, priority, body, tag
         m = [0, 0]
@@ -304,8 +309,9 @@ class Device:
 
     def submit(self, lo: int, hi: int, tpcs, priority: int, body: int, args, tag: int = 0,
                trace: int | None = None, parts: int = 1, after: int | None = None,
-               chain_head: bool = False, no_early: bool = False) -> int:
-        d = self.desc(lo, hi, tpcs, priority, body, args, tag, trace, parts, after, chain_head, no_early)
+               chain_head: bool = False, no_early: bool = False, tenant: int = 0) -> int:
+        d = self.desc(lo, hi, tpcs, priority, body, args, tag, trace, parts, after, chain_head, no_early,
+                      tenant)
         aid = C.c_uint32()
         self._check(self._lib.gpuos_dev_submit_atom(self._h, C.byref(d), C.byref(aid)))
         return aid.value
@@ -364,6 +370,14 @@ class Device:
         for t in tpcs:
             m[t >> 6] |= 1 << (t & 63)
         self._check(self._lib.gpuos_dev_set_fence_mask(self._h, m, min_priority))
+
+    def set_owner(self, tpcs, owner: int, min_priority: int) -> None:
+        """TPC-ownership table: `owner` (1 + tenant id) starts its atoms on
+        these TPCs at any priority, other atoms need >= min_priority."""
+        m = (C.c_uint64 * 2)()
+        for t in tpcs:
+            m[t >> 6] |= 1 << (t & 63)
+        self._check(self._lib.gpuos_dev_set_tpc_owner(self._h, m, owner, min_priority))
 
     def poll(self, max_n: int = 256) -> list[Completion]:
         buf = (Completion * max_n)()

@@ -36,6 +36,7 @@
 #include <chrono>
 #include <memory>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <string>
@@ -106,6 +107,20 @@ __device__ __forceinline__ void open_gate(unsigned* paused) {
   asm volatile("red.release.gpu.global.and.b32 [%0], %1;" ::"l"(paused), "r"(~kGatedBit) : "memory");
 }
 constexpr unsigned kChainHead = 1u;
+
+// The TPC-ownership table (gpuos_dev_set_tpc_owner): fence[t] = owner << 16
+// | floor, owner = 1 + tenant id (0: none). An atom starts blocks on t when
+// its priority reaches the floor or it belongs to the owner -- the owner's
+// atoms that span its quota and stolen TPCs run at the stolen priority
+// and would otherwise be fenced off their own quota. An atom's tenant
+// travels in DevAtom::paused bits 16..31 (read with the claim word).
+__device__ __forceinline__ bool fence_admits(int fence, int prio, unsigned tenant) {
+  const unsigned owner = static_cast<unsigned>(fence) >> 16;
+  return prio >= (fence & 0xff) || (owner != 0u && owner == tenant);
+}
+__device__ __forceinline__ unsigned tenant_of(unsigned long long count_paused) {
+  return static_cast<unsigned>(count_paused >> 48);
+}
 constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head | no early
 constexpr unsigned kAuxNoEarly = 0x40000000u;
 constexpr unsigned kNoEarly = 2u;                 // DevAtom::chain: GPUOS_ATOM_NO_EARLY
@@ -124,6 +139,8 @@ struct DevCtl {
   unsigned long long t_first_block;    // earliest block start
   unsigned tc_active;                  // TPCs whose tensor cores run a pair tile
   unsigned idle_leaders;               // leaders waiting with nothing eligible
+  unsigned fault;                      // first device fault (kFault*; 0: none)
+  unsigned pad2;
 };
 
 // 128-byte submit-ring entry: four 32-byte sectors, each = 7 data words +
@@ -164,6 +181,11 @@ struct Params {
   int idle_sleep_ns;
   unsigned smem_bytes;  // dynamic shared memory per worker (STREAM / GEMM rings)
   unsigned tmem_cols;   // TMEM columns each worker owns (GEMM accumulator)
+  unsigned ingest;      // live mode: cluster 0 runs the ingest warp (0: batch mode)
+  unsigned pad0;
+  unsigned long long wait_bound_ns;  // bodies' pipeline-wait bound (fault after it)
+  unsigned* tpc_occ;                 // [tpcs] blocks running on the TPC (workers +-1)
+  unsigned long long* tpc_busy;      // [tpcs] ns with >= 1 running block (ingest's sampler)
 };
 
 __device__ __forceinline__ void st_release_gpu64(unsigned long long* p, unsigned long long v) {
@@ -224,20 +246,66 @@ __device__ __forceinline__ void st_relaxed_gpu64(unsigned long long* p, unsigned
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// 64 registers: it shares an SM sub-partition with four worker warps.
-__global__ void __maxnreg__(64) k_ingest(Params p) {
+// Shared memory of the ingest warp (carved from the dynamic region of the
+// ingest cluster's CTA 0, which runs no bodies).
+struct IngestShared {
   // Shadow occupancy of every TPC's resident list. Only this warp inserts
   // keys, so an entry whose shadow bit is clear is certainly empty; workers
   // clear entries behind its back, which the shadow learns on refresh.
-  __shared__ unsigned shadow[GPUOS_MAX_TPCS];
+  unsigned shadow[GPUOS_MAX_TPCS];
   // Entries chosen in the current batch whose keys are not stored yet (a
   // refresh from the list must not hand them out twice). TPC t is only ever
   // touched by lane t % 32, so neither array needs synchronisation.
-  __shared__ unsigned pend[GPUOS_MAX_TPCS];
-  __shared__ IngestSubmit subs[kIngestBatch];
-  const unsigned lane = threadIdx.x;
+  unsigned pend[GPUOS_MAX_TPCS];
+  IngestSubmit subs[kIngestBatch];
+};
+
+// TPC utilisation with the reference's definition (device.cpp:264-275,
+// sim.cpp:423-426): the time integral of "TPCs with >= 1 running block".
+// Workers add +-1 to tpc_occ[t] around every block (fire-and-forget
+// reductions, nothing on their path); the ingest warp samples the counters
+// between ring polls (every ~1-2 us, against blocks of 10s of us) and
+// integrates per TPC, lane t % 32 owning TPC t.
+struct OccSampler {
+  unsigned long long busy[(GPUOS_MAX_TPCS + 31) / 32] = {};
+  unsigned prev = 0;  // bit i: TPC lane + 32 i was occupied at the last sample
+  unsigned long long t_prev = 0;
+  __device__ __forceinline__ void sample(const Params& p, unsigned lane) {
+    const unsigned long long now = gtimer();
+    unsigned cur = 0;
+#pragma unroll
+    for (int i = 0; i < (GPUOS_MAX_TPCS + 31) / 32; ++i) {
+      const int t = static_cast<int>(lane) + 32 * i;
+      if (t < p.logical_tpcs) {
+        if (((prev >> i) & 1u) && t_prev != 0) busy[i] += now - t_prev;
+        if (ld_relaxed_gpu(p.tpc_occ + t) != 0u) cur |= 1u << i;
+      }
+    }
+    prev = cur;
+    t_prev = now;
+  }
+  __device__ __forceinline__ void flush(const Params& p, unsigned lane) {
+    sample(p, lane);
+#pragma unroll
+    for (int i = 0; i < (GPUOS_MAX_TPCS + 31) / 32; ++i) {
+      const int t = static_cast<int>(lane) + 32 * i;
+      if (t < p.logical_tpcs) p.tpc_busy[t] = busy[i];
+    }
+  }
+};
+
+// The ingest warp: warp 0 of the ingest cluster's CTA 0 (live mode). It is
+// part of the worker grid, so the dispatcher is ONE self-contained launch
+// (ncu and compute-sanitizer can replay it; nothing depends on two kernels
+// being co-resident).
+__device__ __forceinline__ void ingest_loop(const Params& p, IngestShared& ish) {
+  unsigned* shadow = ish.shadow;
+  unsigned* pend = ish.pend;
+  IngestSubmit* subs = ish.subs;
+  const unsigned lane = threadIdx.x & 31u;
   for (int t = lane; t < GPUOS_MAX_TPCS; t += 32) shadow[t] = pend[t] = 0u;  // lists start empty
   __syncwarp();
+  OccSampler occ;
   unsigned long long head = 0;
   unsigned polls = 0;
   for (;;) {
@@ -251,6 +319,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
     const unsigned el = lane >> 3;  // entry of this lane's 16 bytes (and el + 4)
     const uint4 va = ld_relaxed_sys_v4(p.ring[(head + el) % p.ring_cap].w + 4 * (lane & 7));
     const uint4 vb = ld_relaxed_sys_v4(p.ring[(head + 4 + el) % p.ring_cap].w + 4 * (lane & 7));
+    occ.sample(p, lane);  // (its L2 loads overlap the ring's PCIe reads)
     // Sector s of entry e ends with its ticket: word 8s+7 = lane 8e+2s+1, .w
     const bool tka = (lane & 1u) == 0u || va.w == static_cast<unsigned>(head + el + 1);
     const bool tkb = (lane & 1u) == 0u || vb.w == static_cast<unsigned>(head + 4 + el + 1);
@@ -281,7 +350,9 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
       if (op == kOpSubmit) {
         const unsigned slot = get(kFSlot);
         const unsigned seq = get(kFSeq);
-        const int prio = static_cast<int>(get(kFPrio));
+        const unsigned prio_word = get(kFPrio);  // prio | tenant << 16
+        const int prio = static_cast<int>(prio_word & 0xffu);
+        const unsigned tenant_bits = prio_word & 0xffff0000u;
         const unsigned long long mask0 = field64(get(kFMask0), get(kFMask0 + 1));
         const unsigned long long mask1 = field64(get(kFMask1), get(kFMask1 + 1));
         unsigned long long args[5];
@@ -325,7 +396,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
           const bool early = pred != 0u && body_is_pair(body) && !(aux & kAuxNoEarly) &&
                              prio <= p.atoms[pred - 1u].prio &&
                              ld_relaxed_gpu(&p.atoms[pred - 1u].armed) != 0u;
-          a->paused = early ? kGatedBit : 0u;
+          a->paused = tenant_bits | (early ? kGatedBit : 0u);
           a->armed = 0u;
           a->tag = tag;
           a->trace = reinterpret_cast<unsigned*>(trace);
@@ -390,7 +461,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
         bump1 |= __shfl_sync(0xffffffffu, m1, 0);
       } else if (op == kOpFence) {
         const int t = static_cast<int>(get(kFAux));
-        const int floor_prio = static_cast<int>(get(kFPrio));
+        const int floor_prio = static_cast<int>(get(kFPrio) & 0xffu);  // (no owner)
         if (t >= 0 && t < p.logical_tpcs) {
           if (lane == 0) atomicExch(p.fence + t, floor_prio);
           if (t < 64) bump0 |= 1ull << t; else bump1 |= 1ull << (t - 64);
@@ -398,7 +469,7 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
       } else if (op == kOpFenceMask) {
         const unsigned long long m0 = field64(get(kFMask0), get(kFMask0 + 1));
         const unsigned long long m1 = field64(get(kFMask1), get(kFMask1 + 1));
-        const int floor_prio = static_cast<int>(get(kFPrio));
+        const int floor_prio = static_cast<int>((get(kFPrio) & 0xffu) | (get(kFAux) << 16));  // owner
         for (int t = lane; t < p.logical_tpcs; t += 32) {
           const unsigned long long m = t < 64 ? m0 : m1;
           if ((m >> (t & 63)) & 1ull) atomicExch(p.fence + t, floor_prio);
@@ -476,6 +547,17 @@ __global__ void __maxnreg__(64) k_ingest(Params p) {
     __syncwarp();
     if (stop) break;
   }
+  // Drain: keep integrating utilisation until the workers leave.
+  for (unsigned k = 0;; ++k) {
+    occ.sample(p, lane);
+    if ((k & 7u) == 7u &&
+        (ld_relaxed_gpu(&p.ctl->quit) ||
+         (ld_relaxed_gpu(&p.ctl->drain) && ld_relaxed_gpu_s32(&p.ctl->outstanding) == 0) ||
+         gtimer() > p.ctl->deadline))
+      break;
+    __nanosleep(1000);
+  }
+  occ.flush(p, lane);
 }
 
 // ------------------------------------------------------------ worker CTAs
@@ -528,7 +610,16 @@ struct WorkerShared {
   int go;                       // WorkerGo
   unsigned long long touched_key;  // warp 0: atom whose `touched` word has this TPC
   unsigned tmem_base;           // this worker's TMEM columns (tcgen05.alloc)
+  WaitGuard guard;              // the bodies' bounded pipeline waits
 };
+
+// Lane 0 broadcasts a field of sh.rc it wrote itself; the other lanes do
+// not touch the shared copy (a volatile load cannot be speculated).
+__device__ __forceinline__ unsigned lane0_field(const unsigned& f, unsigned lane) {
+  unsigned v = 0u;
+  if (lane == 0) v = *static_cast<const volatile unsigned*>(&f);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
 
 __device__ __forceinline__ unsigned atom_add_acq_rel32(unsigned* p, unsigned v) {
   unsigned old;
@@ -736,7 +827,8 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         const unsigned bcount = static_cast<unsigned>(bf.count_paused);
         const unsigned bbody = static_cast<unsigned>(bf.body_parts);
         const bool here = (((tpc < 64 ? bf.mask[0] : bf.mask[1]) >> (tpc & 63)) & 1ull) && ((bf.count_paused >> 32) & 1ull) == 0u &&
-                          bprio >= floor_prio && (!body_is_pair(bbody) || rank == 0u);
+                          fence_admits(floor_prio, bprio, tenant_of(bf.count_paused)) &&
+                          (!body_is_pair(bbody) || rank == 0u);
         st_relaxed_gpu64(&b->claim, (static_cast<unsigned long long>(bseq) << 32) | (here ? 1u : 0u));
         b->t_armed = gtimer();
         b->armed = 1u;
@@ -749,8 +841,9 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
               ld_relaxed_gpu(&c->armed) == 0u) {
             // Armed claim and closed gate in one 16-byte store: a claimer
             // never sees one without the other.
+            const unsigned cpz = (ld_relaxed_gpu(&c->paused) & 0xffff0000u) | kGatedBit;  // (tenant kept)
             const unsigned long long cc = static_cast<unsigned long long>(c->count) |
-                                          (static_cast<unsigned long long>(kGatedBit) << 32);
+                                          (static_cast<unsigned long long>(cpz) << 32);
             asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(&c->claim),
                          "l"(static_cast<unsigned long long>(c->seq) << 32), "l"(cc)
                          : "memory");
@@ -860,7 +953,7 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
 // warp (32 x 64). R = 104 keeps that SM able to host both workers: a pair
 // that cannot be co-placed there is never launched (measured at R = 103
 // with a 122-register ingest warp).
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid_constant__ Params p) {
   __shared__ WorkerShared sh;
   extern __shared__ __align__(1024) unsigned char dsmem[];
   const int tid = threadIdx.x;
@@ -869,24 +962,32 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   const unsigned rank = cluster_rank();
   unsigned sm = smid();
   int tpc = p.phys2log[sm >> 1];
+  // Live mode: cluster 0 is the ingest cluster. Its CTA 0's warp 0 runs the
+  // ingest warp for the kernel's lifetime; the TPC it lands on keeps one
+  // worker pair (of W) for bodies.
+  const bool ingest_cluster = p.ingest != 0u && blockIdx.x < 2u;
   if (tid == 0) {
     atomicMin(&p.ctl->t_enter, gtimer());
-    st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 ? 0x80000000u : 0u));
+    st_release_sys(p.alive + blockIdx.x, (sm + 1) | (tpc < 0 || ingest_cluster ? 0x80000000u : 0u));
     atomicAdd(&p.ctl->arrived, 1u);
   }
-  if (tpc < 0) {
-    // TPC not exposed to the scheduler (both CTAs of the pair). Give up the
-    // TMEM allocation permit at once (an SM does not start a second CTA of a
-    // TMEM-using kernel while the first still holds it: measured, every
-    // unexposed SM then hosted one worker), then stay until every worker
-    // CTA has started: leaving at once would free this SM for a cluster
-    // meant for an exposed TPC, leaving that TPC short.
+  if (tpc < 0 || ingest_cluster) {
+    // No bodies here (a TPC not exposed to the scheduler, or the ingest
+    // cluster). Give up the TMEM allocation permit at once (an SM does not
+    // start a second CTA of a TMEM-using kernel while the first still holds
+    // it: measured, every unexposed SM then hosted one worker), then stay
+    // until every worker CTA has started: leaving at once would free this SM
+    // for a cluster meant for an exposed TPC, leaving that TPC short. Only
+    // one thread needs to stay for the CTA to stay resident.
     if (warp == 1) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    if (ingest_cluster && rank == 0 && warp == 0) {
+      ingest_loop(p, *reinterpret_cast<IngestShared*>(dsmem));
+      return;
+    }
     if (tid == 0)
       while (ld_relaxed_gpu(&p.ctl->arrived) < gridDim.x && !ld_relaxed_gpu(&p.ctl->quit) &&
              gtimer() < p.ctl->deadline)
         __nanosleep(1000);
-    __syncthreads();
     return;
   }
 
@@ -896,6 +997,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   gemm_pipe_init(gemm, dsmem, p.smem_bytes, p.tmem_cols, tid);
   GemvPipe gemv;
   gemv_pipe_init(gemv, dsmem, p.smem_bytes, p.tmem_cols, tid);
+  if (tid == 0) sh.guard = WaitGuard{&p.ctl->fault, &p.ctl->quit, p.wait_bound_ns};
+  gemm.guard = gemv.guard = &sh.guard;
   if (tid == 0) {
     mbar_init(&sh.join_full, 1);
     mbar_init(&sh.joined, 1);
@@ -906,6 +1009,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
   // 512 / W columns so the W workers of an SM never contend.
   if (warp == 1) tmem_alloc2(&sh.tmem_base, p.tmem_cols);
   tc_fence_before();
+  __syncthreads();     // (the CTA-level order of the allocation's shared write)
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   gemm.tmem = gemv.tmem = sh.tmem_base;
@@ -950,7 +1054,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
         // here (account_block); a pair tile takes the tensor reservation.
         handoff = false;
         cur_key = 0ull;
-        cur_body = __shfl_sync(0xffffffffu, sh.rc.cmd.body, 0);
+        cur_body = lane0_field(sh.rc.cmd.body, lane);
         go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
         if (go == kGoPair && cur_body != GPUOS_BODY_GEMV_BF16 && lane == 0) {
           if (atomicAdd(p.tc_busy + tpc, 1u) == 0u) atomicAdd(&p.ctl->tc_active, 1u);
@@ -1010,7 +1114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
               eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
                          static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
                          ((cp >> 32) & 1ull) == 0u &&
-                         static_cast<int>(k >> 56) >= floor_prio;
+                         fence_admits(floor_prio, static_cast<int>(k >> 56), tenant_of(cp));
             }
             // Candidates of this snapshot, best first: a claim lost to other
             // workers (the atom ran out) moves on to the next candidate
@@ -1127,7 +1231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
             cur_key = stale ? 0ull : key;
             cur_slot = slot;
             cur_ver = ver;
-            cur_body = __shfl_sync(0xffffffffu, sh.rc.cmd.body, 0);
+            cur_body = lane0_field(sh.rc.cmd.body, lane);  // (lane 0 wrote it)
             spread_since = 0;
             go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
             // A peer reaches a 2-SM block only by adopting a recycled slot
@@ -1202,7 +1306,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
         }
         sh.go = go;
         sh.t_start = gtimer();
-        if (go != kGoExit && first_start == ~0ull) first_start = sh.t_start;
+        if (go != kGoExit) {
+          if (first_start == ~0ull) first_start = sh.t_start;
+          red_relaxed_gpu_add(p.tpc_occ + tpc, 1u);  // utilisation sampler (OccSampler)
+        }
       }
     }
     __syncthreads();
@@ -1215,12 +1322,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(Params p) {
       tc_hold = false;
     }
     __syncthreads();
+    if (tid == 0) red_relaxed_gpu_add(p.tpc_occ + tpc, ~0u);  // -1: the block has ended
     // The leader records pair tiles (the peer's half is complete: cluster
     // barrier at the end of the body).
     if (warp == 0 && go != kGoJoin) {
       const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, n_blocks, busy, sh.touched_key);
       if (done) cur_key = 0ull;  // the atom is done: rescan rather than claim from it
       handoff = done == 2;
+      __syncwarp();  // every lane has read sh.t_start / sh.rc before lane 0 rewrites them
     }
   }
   if (tid == 0) {
@@ -1288,6 +1397,9 @@ struct HostAtom {
   bool has_succ = false;     // a successor is chained behind it
   uint32_t pred_slot = 0;    // chained: predecessor's slot and sequence
   uint32_t pred_seq = 0;     // (0: not chained)
+  uint64_t succ_ring = 0;    // ring entries the device must have consumed before
+                             // this slot may be reused (its successor's entry
+                             // registers on it by slot number)
 };
 
 }  // namespace
@@ -1296,7 +1408,7 @@ struct gpuos_dev {
   gpuos_dev_config cfg{};
   gpuos_dev_topology topo{};
   int device = 0;
-  cudaStream_t s_ingest = nullptr, s_work = nullptr, s_side = nullptr;
+  cudaStream_t s_work = nullptr, s_side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   // device tables
   DevAtom* atoms = nullptr;
@@ -1307,6 +1419,15 @@ struct gpuos_dev {
   DevCtl* ctl = nullptr;
   int* phys2log = nullptr;
   unsigned long long* gt_scratch = nullptr;
+  unsigned* tpc_occ = nullptr;              // [T] running blocks (utilisation sampler)
+  unsigned long long* tpc_busy = nullptr;   // [T] sampled busy ns
+  // The dispatcher kernel is launched from this thread: under a profiler
+  // that serialises launches (ncu) the launch call blocks until the kernel
+  // ends, and the kernel only ends once this handle's owner has fed the
+  // ring and drained it.
+  std::thread launcher;
+  std::atomic<int> launch_rc{0};            // 0 pending, 1 launched, < 0 failed
+  std::string launch_error;
   // mapped host memory
   RingEntry* ring_h = nullptr;
   RingEntry* ring_d = nullptr;
@@ -1323,6 +1444,10 @@ struct gpuos_dev {
   uint32_t next_seq = 1;
   uint32_t next_atom_id = 0;
   std::deque<uint32_t> free_slots;  // FIFO: a freed slot is reused last
+  // Completed chain heads whose successor's ring entry the device has not
+  // consumed yet: (ring entries that must be consumed, slot).
+  std::deque<std::pair<uint64_t, uint32_t>> deferred_free;
+  int64_t exit_check_ns = 0;        // poll(): last check that the kernel still runs
   std::vector<HostAtom> slots;
   std::unordered_map<uint32_t, uint32_t> slot_of;  // live atom id -> slot
   std::vector<int> tpc_resident;  // keys currently resident per logical TPC
@@ -1344,7 +1469,8 @@ int publish(gpuos_dev* d, const uint32_t* data /*28 words*/) {
   const int64_t deadline = steady_ns() + 10'000'000'000LL;
   while (d->ring_head - __atomic_load_n(d->consumed_h, __ATOMIC_ACQUIRE) >=
          static_cast<uint64_t>(d->cfg.ring_entries)) {
-    if (!d->running) return fail(GPUOS_E_FULL, "submit ring full and dispatcher stopped");
+    if (!d->running || !d->workers_launched)
+      return fail(GPUOS_E_FULL, "submit ring full and dispatcher not running");
     if (steady_ns() > deadline) return fail(GPUOS_E_TIMEOUT, "submit ring stalled");
   }
   RingEntry* e = d->ring_h + (d->ring_head % d->cfg.ring_entries);
@@ -1408,6 +1534,55 @@ void record_spans(gpuos_dev* d, const DevCtl& c) {
       ok && c.t_first_block != ~0ull ? static_cast<int64_t>(c.t_first_block - c.t_enter) : 0;
 }
 
+unsigned tmem_cols_for(int workers_per_sm);
+
+Params make_params(gpuos_dev* d, bool ingest) {
+  Params p{};
+  p.atoms = d->atoms;
+  p.resident = d->resident;
+  p.version = d->version;
+  p.fence = d->fence;
+  p.tc_busy = d->tc_busy;
+  p.ctl = d->ctl;
+  p.phys2log = d->phys2log;
+  p.ring = d->ring_d;
+  p.comp = d->comp_d;
+  p.consumed = d->consumed_d;
+  p.alive = d->alive_d;
+  p.ring_cap = static_cast<unsigned>(d->cfg.ring_entries);
+  p.comp_cap = static_cast<unsigned>(d->cfg.atom_slots);
+  p.logical_tpcs = d->cfg.logical_tpcs;
+  p.idle_sleep_ns = d->cfg.idle_sleep_ns;
+  p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
+  p.tmem_cols = tmem_cols_for(d->cfg.workers_per_sm);
+  p.ingest = ingest ? 1u : 0u;
+  p.wait_bound_ns = static_cast<unsigned long long>(d->cfg.pipeline_timeout_ms) * 1000000ull;
+  p.tpc_occ = d->tpc_occ;
+  p.tpc_busy = d->tpc_busy;
+  return p;
+}
+
+// Kernel-exit bookkeeping shared by stop() and run_batch(): counters,
+// spans, the sampled TPC-busy integral and the device fault word.
+int collect_run(gpuos_dev* d, float ms, DevCtl& ctl) {
+  CUDA_TRY(cudaMemcpy(&ctl, d->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost));
+  std::vector<unsigned long long> busy(static_cast<size_t>(d->cfg.logical_tpcs), 0ull);
+  CUDA_TRY(cudaMemcpy(busy.data(), d->tpc_busy, sizeof(unsigned long long) * busy.size(),
+                      cudaMemcpyDeviceToHost));
+  d->stats.blocks_executed += ctl.blocks;
+  d->stats.worker_busy_ns += ctl.busy_ns;
+  d->stats.claim_retries += ctl.retries;
+  d->stats.kernel_elapsed_ns = static_cast<int64_t>(ms * 1e6);
+  for (unsigned long long b : busy) d->stats.tpc_busy_ns += b;
+  d->stats.fault = ctl.fault;
+  record_spans(d, ctl);
+  return GPUOS_OK;
+}
+
+const char* fault_name(unsigned f) {
+  return f == 1u ? "a tensor-core pipeline wait expired (pipeline_timeout_ms)" : "unknown fault";
+}
+
 // UMMA N for a pair tile over `cols` output columns: 64, 128 or 256.
 unsigned narrow_tile(int64_t cols) { return cols <= 64 ? 64u : cols <= 128 ? 128u : kGemmTile; }
 
@@ -1448,6 +1623,11 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   if (cfg.atom_slots <= 0) cfg.atom_slots = 4096;
   if (cfg.ring_entries <= 0) cfg.ring_entries = 4096;
   if (cfg.idle_sleep_ns <= 0) cfg.idle_sleep_ns = 128;
+  if (cfg.pipeline_timeout_ms <= 0) {
+    // (GPUOS_PIPELINE_TIMEOUT_MS: longer bounds for runs under sanitizers)
+    const char* env = std::getenv("GPUOS_PIPELINE_TIMEOUT_MS");
+    cfg.pipeline_timeout_ms = env != nullptr && std::atoi(env) > 0 ? std::atoi(env) : 2000;
+  }
   if (cfg.workers_per_sm > 2)
     return fail(GPUOS_E_CONFIG, "workers_per_sm must be 1 or 2 (TMEM-owning workers per SM)");
   if (cfg.atom_slots > (1 << 24)) return fail(GPUOS_E_CONFIG, "atom_slots must be < 2^24");
@@ -1468,13 +1648,9 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
 
   // Size each worker's shared memory so that exactly W workers fit per SM.
   const int smem_sm = static_cast<int>(prop.sharedMemPerMultiprocessor);
-  // Headroom for the per-CTA reserved shared memory of the workers and of
-  // the co-resident ingest CTA.
-  // (the ingest CTA holds ~3 KB of static shared memory including its 1 KB
-  // reserve; the workers of the SM it shares must leave room for it. A
-  // cluster-launched pair needs more slack than the arithmetic suggests:
-  // with 6 KB per worker the pair that must share the ingest's TPC is never
-  // placed, measured; 8 KB places all.)
+  // Headroom for the per-CTA reserved shared memory (a cluster-launched
+  // pair needs more slack than the arithmetic suggests: measured with the
+  // former separate ingest kernel, 8 KB places every pair).
   int smem_worker = std::min<int>(static_cast<int>(prop.sharedMemPerBlockOptin) - 2048,
                                   smem_sm / cfg.workers_per_sm - 8192);
   smem_worker = std::max(smem_worker - smem_worker % 1024, 0);
@@ -1492,11 +1668,9 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   d->grid = prop.multiProcessorCount * cfg.workers_per_sm;
 
   CUDA_TRY(cudaFuncSetAttribute(k_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_worker));
-  // Both kernels must ask for the same L1/shared carveout, or the SM that
-  // hosts the ingest warp cannot also host workers (measured:
-  // csrc/tools/residency_probe.cu).
+  // Max shared carveout: operand init kernels that run beside the resident
+  // dispatcher ask for the same one (csrc/tools/residency_probe.cu).
   CUDA_TRY(cudaFuncSetAttribute(k_worker, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  CUDA_TRY(cudaFuncSetAttribute(k_ingest, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_worker, kWorkerThreads, smem_worker));
   // The occupancy calculator reports 1 CTA/SM for any kernel that uses
@@ -1507,7 +1681,6 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
     return fail(GPUOS_E_CONFIG, "worker occupancy is " + std::to_string(per_sm) +
                                     " CTAs/SM, expected " + std::to_string(cfg.workers_per_sm));
 
-  CUDA_TRY(cudaStreamCreateWithFlags(&d->s_ingest, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&d->s_work, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&d->s_side, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreate(&d->ev_start));
@@ -1523,6 +1696,10 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   CUDA_TRY(cudaMalloc(&d->ctl, sizeof(DevCtl)));
   CUDA_TRY(cudaMalloc(&d->phys2log, sizeof(int) * phys_tpcs));
   CUDA_TRY(cudaMalloc(&d->gt_scratch, sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&d->tpc_occ, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMalloc(&d->tpc_busy, sizeof(unsigned long long) * T));
+  CUDA_TRY(cudaMemset(d->tpc_occ, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->tpc_busy, 0, sizeof(unsigned long long) * T));
   std::vector<int> p2l(phys_tpcs, -1);
   for (int t = 0; t < cfg.logical_tpcs; ++t) p2l[t] = t;
   CUDA_TRY(cudaMemcpy(d->phys2log, p2l.data(), sizeof(int) * phys_tpcs, cudaMemcpyHostToDevice));
@@ -1550,6 +1727,7 @@ int gpuos_dev_close(gpuos_dev* d) {
     float ms = 0;
     gpuos_dev_stop(d, 0, &ms);
   }
+  if (d->launcher.joinable()) d->launcher.join();
   cudaFree(d->atoms);
   cudaFree(d->resident);
   cudaFree(d->version);
@@ -1558,13 +1736,14 @@ int gpuos_dev_close(gpuos_dev* d) {
   cudaFree(d->ctl);
   cudaFree(d->phys2log);
   cudaFree(d->gt_scratch);
+  cudaFree(d->tpc_occ);
+  cudaFree(d->tpc_busy);
   cudaFreeHost(d->ring_h);
   cudaFreeHost(d->comp_h);
   cudaFreeHost(d->consumed_h);
   cudaFreeHost(d->alive_h);
   if (d->ev_start) cudaEventDestroy(d->ev_start);
   if (d->ev_stop) cudaEventDestroy(d->ev_stop);
-  if (d->s_ingest) cudaStreamDestroy(d->s_ingest);
   if (d->s_work) cudaStreamDestroy(d->s_work);
   if (d->s_side) cudaStreamDestroy(d->s_side);
   delete d;
@@ -1584,12 +1763,17 @@ int gpuos_dev_start(gpuos_dev* d) {
   if (!d) return fail(GPUOS_E_CONFIG, "null device");
   if (d->running) return fail(GPUOS_E_STATE, "dispatcher already running");
   if (d->in_flight != 0) return fail(GPUOS_E_STATE, "atoms still in flight");
+  if (d->cfg.workers_per_sm != 2)
+    return fail(GPUOS_E_CONFIG, "live mode needs workers_per_sm = 2: cluster 0 hosts the ingest warp "
+                                "and its TPC keeps the other worker pair (W = 1 runs batch mode only)");
   CUDA_TRY(cudaSetDevice(d->device));
   const size_t T = static_cast<size_t>(d->cfg.logical_tpcs);
   CUDA_TRY(cudaMemset(d->resident, 0, sizeof(unsigned long long) * T * kResident));
   CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
   CUDA_TRY(cudaMemset(d->tc_busy, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->tpc_occ, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->tpc_busy, 0, sizeof(unsigned long long) * T));
   std::memset(d->ring_h, 0, sizeof(RingEntry) * d->cfg.ring_entries);
   std::memset(d->comp_h, 0, sizeof(CompRec) * d->cfg.atom_slots);
   std::memset(d->alive_h, 0, sizeof(unsigned) * d->grid);
@@ -1597,6 +1781,8 @@ int gpuos_dev_start(gpuos_dev* d) {
   d->ring_head = 0;
   d->live.clear();
   d->slot_of.clear();
+  for (const auto& f : d->deferred_free) d->free_slots.push_back(f.second);
+  d->deferred_free.clear();
   std::fill(d->tpc_resident.begin(), d->tpc_resident.end(), 0);
 
   // Calibrate device globaltimer against the host origin (+- half an RTT),
@@ -1625,28 +1811,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   CUDA_TRY(cudaMemcpyAsync(d->ctl, &ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, d->s_side));
   CUDA_TRY(cudaStreamSynchronize(d->s_side));
 
-  Params p{};
-  p.atoms = d->atoms;
-  p.resident = d->resident;
-  p.version = d->version;
-  p.fence = d->fence;
-  p.tc_busy = d->tc_busy;
-  p.ctl = d->ctl;
-  p.phys2log = d->phys2log;
-  p.ring = d->ring_d;
-  p.comp = d->comp_d;
-  p.consumed = d->consumed_d;
-  p.alive = d->alive_d;
-  p.ring_cap = static_cast<unsigned>(d->cfg.ring_entries);
-  p.comp_cap = static_cast<unsigned>(d->cfg.atom_slots);
-  p.logical_tpcs = d->cfg.logical_tpcs;
-  p.idle_sleep_ns = d->cfg.idle_sleep_ns;
-  p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
-  p.tmem_cols = tmem_cols_for(d->cfg.workers_per_sm);
-
-  d->params = p;
-  k_ingest<<<1, 32, 0, d->s_ingest>>>(p);
-  CUDA_TRY(cudaGetLastError());
+  d->params = make_params(d, true);
   d->running = true;
   d->workers_launched = false;
   if (d->cfg.flags & GPUOS_DEV_DEFER_WORKERS) return GPUOS_OK;
@@ -1655,16 +1820,38 @@ int gpuos_dev_start(gpuos_dev* d) {
 
 int gpuos_dev_launch_workers(gpuos_dev* d) {
   if (!d) return fail(GPUOS_E_CONFIG, "null device");
-  if (!d->running || d->workers_launched) return fail(GPUOS_E_STATE, "workers not launchable now");
-  CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
-  k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(d->params);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+  if (!d->running || d->workers_launched) return fail(GPUOS_E_STATE, "dispatcher not launchable now");
+  if (d->launcher.joinable()) d->launcher.join();
+  d->launch_rc.store(0);
+  d->launch_error.clear();
   d->workers_launched = true;
+  d->exit_check_ns = 0;
+  // One launch, from a helper thread (see gpuos_dev::launcher). Its events
+  // bracket the kernel on the work stream.
+  d->launcher = std::thread([d] {
+    cudaError_t e = cudaSetDevice(d->device);
+    if (e == cudaSuccess) e = cudaEventRecord(d->ev_start, d->s_work);
+    if (e == cudaSuccess) {
+      k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(d->params);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(d->ev_stop, d->s_work);
+    if (e != cudaSuccess) {
+      d->launch_error = std::string("dispatcher launch: ") + cudaGetErrorString(e);
+      d->launch_rc.store(-1, std::memory_order_release);
+    } else {
+      d->launch_rc.store(1, std::memory_order_release);
+    }
+  });
 
   // Every worker CTA must be resident, W per SM, 2W per logical TPC.
   const int64_t deadline = steady_ns() + 5'000'000'000LL;
   for (;;) {
+    if (d->launch_rc.load(std::memory_order_acquire) < 0) {
+      d->launcher.join();
+      d->running = false;
+      return fail(GPUOS_E_CUDA, d->launch_error);
+    }
     int ready = 0;
     for (int i = 0; i < d->grid; ++i)
       ready += __atomic_load_n(d->alive_h + i, __ATOMIC_ACQUIRE) != 0u;
@@ -1720,14 +1907,15 @@ int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
   if (!d) return fail(GPUOS_E_CONFIG, "null device");
   if (!d->running) return fail(GPUOS_E_STATE, "dispatcher not running");
   if (!d->workers_launched) {
-    // Deferred workers never launched: run them now so the drain completes.
+    // Deferred dispatcher never launched: run it now so the drain completes.
     if (drain) {
       const int lrc = gpuos_dev_launch_workers(d);
       if (lrc != GPUOS_OK) return lrc;
     } else {
-      d->workers_launched = true;  // nothing to wait for on the work stream
-      CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
-      CUDA_TRY(cudaEventRecord(d->ev_stop, d->s_work));
+      d->running = false;
+      d->last_elapsed_ms = 0.f;
+      if (elapsed_ms) *elapsed_ms = 0.f;
+      return GPUOS_OK;
     }
   }
   uint32_t data[28] = {};
@@ -1736,15 +1924,15 @@ int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
   if (rc != GPUOS_OK) drain = 0;
   if (!drain) {
     // Abort path: also raise the quit flag directly through the side stream,
-    // so workers stop even if the ingest warp never became resident.
+    // so workers stop even if the ingest warp is stuck.
     static const unsigned one = 1;
     cudaMemcpyAsync(&d->ctl->quit, &one, sizeof one, cudaMemcpyHostToDevice, d->s_side);
     cudaStreamSynchronize(d->s_side);
   }
   // Completions keep arriving while draining; the caller polls them after.
   const int64_t deadline = steady_ns() + (drain ? 300'000'000'000LL : 30'000'000'000LL);
-  while (cudaStreamQuery(d->s_work) == cudaErrorNotReady ||
-         cudaStreamQuery(d->s_ingest) == cudaErrorNotReady) {
+  while (d->launch_rc.load(std::memory_order_acquire) == 0 ||
+         cudaStreamQuery(d->s_work) == cudaErrorNotReady) {
     if (steady_ns() > deadline) {
       if (drain) {
         static const unsigned one = 1;
@@ -1757,22 +1945,20 @@ int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
     }
     std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
+  d->launcher.join();
   d->running = false;
+  if (d->launch_rc.load() < 0) return fail(GPUOS_E_CUDA, d->launch_error);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(d->s_work));
-  CUDA_TRY(cudaStreamSynchronize(d->s_ingest));
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, d->ev_start, d->ev_stop));
   d->last_elapsed_ms = ms;
   if (elapsed_ms) *elapsed_ms = ms;
   DevCtl ctl{};
-  CUDA_TRY(cudaMemcpy(&ctl, d->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost));
-  d->stats.blocks_executed += ctl.blocks;
-  d->stats.worker_busy_ns += ctl.busy_ns;
-  d->stats.claim_retries += ctl.retries;
-  d->stats.kernel_elapsed_ns = static_cast<int64_t>(ms * 1e6);
+  if (const int crc = collect_run(d, ms, ctl); crc != GPUOS_OK) return crc;
   d->stats.ingest_entries += static_cast<int64_t>(*d->consumed_h);
-  record_spans(d, ctl);
+  if (ctl.fault != 0u)
+    return fail(GPUOS_E_TIMEOUT, std::string("device fault: ") + fault_name(ctl.fault));
   if (drain && ctl.outstanding != 0)
     return fail(GPUOS_E_INVARIANT, "drained with atoms outstanding");
   return GPUOS_OK;
@@ -1800,6 +1986,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   for (int i = 0; i < n; ++i) {
     const gpuos_atom_desc& a = descs[i];
     if (a.flags & ~(GPUOS_ATOM_CHAIN_HEAD | GPUOS_ATOM_NO_EARLY)) return fail(GPUOS_E_CONFIG, "unknown atom flags");
+    if (a.tenant > 0xffffu) return fail(GPUOS_E_CONFIG, "tenant must be < 65536");
     if (a.after != 0) {
       // Only atoms of this batch exist: the predecessor is an earlier entry.
       const int64_t j = static_cast<int64_t>(a.after - 1u) - static_cast<int64_t>(id_base);
@@ -1825,6 +2012,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
     x.parts = parts;
     x.seq = seq;
     x.prio = prio;
+    x.paused = a.tenant << 16;
     x.body = a.body;
     x.lo = a.lo;
     ids[static_cast<size_t>(i)] = d->next_atom_id++;
@@ -1857,6 +2045,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   }
   // Host bookkeeping: slots 0..n-1 in flight, completions consumed by poll().
   d->free_slots.clear();
+  d->deferred_free.clear();
   for (int s = d->cfg.atom_slots - 1; s >= n; --s) d->free_slots.push_back(static_cast<uint32_t>(s));
   const int64_t now = gpuos_dev_now_ns(d);
   d->slot_of.clear();
@@ -1895,25 +2084,10 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   ctl.outstanding = n;
   ctl.deadline = ~0ull >> 1;
   CUDA_TRY(cudaMemcpy(d->ctl, &ctl, sizeof ctl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(d->tpc_occ, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->tpc_busy, 0, sizeof(unsigned long long) * T));
 
-  Params p{};
-  p.atoms = d->atoms;
-  p.resident = d->resident;
-  p.version = d->version;
-  p.fence = d->fence;
-  p.tc_busy = d->tc_busy;
-  p.ctl = d->ctl;
-  p.phys2log = d->phys2log;
-  p.ring = d->ring_d;
-  p.comp = d->comp_d;
-  p.consumed = d->consumed_d;
-  p.alive = d->alive_d;
-  p.ring_cap = static_cast<unsigned>(d->cfg.ring_entries);
-  p.comp_cap = static_cast<unsigned>(d->cfg.atom_slots);
-  p.logical_tpcs = T;
-  p.idle_sleep_ns = d->cfg.idle_sleep_ns;
-  p.smem_bytes = static_cast<unsigned>(d->topo.smem_per_worker);
-  p.tmem_cols = tmem_cols_for(d->cfg.workers_per_sm);
+  const Params p = make_params(d, false);  // every cluster works; no ring
   CUDA_TRY(cudaEventRecord(d->ev_start, d->s_work));
   k_worker<<<d->grid, kWorkerThreads, d->topo.smem_per_worker, d->s_work>>>(p);
   CUDA_TRY(cudaGetLastError());
@@ -1924,12 +2098,9 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   if (elapsed_ms) *elapsed_ms = ms;
   d->last_elapsed_ms = ms;
   DevCtl after{};
-  CUDA_TRY(cudaMemcpy(&after, d->ctl, sizeof after, cudaMemcpyDeviceToHost));
-  d->stats.blocks_executed += after.blocks;
-  d->stats.worker_busy_ns += after.busy_ns;
-  d->stats.claim_retries += after.retries;
-  d->stats.kernel_elapsed_ns = static_cast<int64_t>(ms * 1e6);
-  record_spans(d, after);
+  if (const int crc = collect_run(d, ms, after); crc != GPUOS_OK) return crc;
+  if (after.fault != 0u)
+    return fail(GPUOS_E_TIMEOUT, std::string("device fault: ") + fault_name(after.fault));
   if (after.outstanding != 0) return fail(GPUOS_E_INVARIANT, "batch finished with atoms outstanding");
   return GPUOS_OK;
 }
@@ -1957,9 +2128,17 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   for (int t = 0; t < T; ++t)
     if (((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) && d->tpc_resident[t] >= kResident)
       return fail(GPUOS_E_FULL, "TPC " + std::to_string(t) + " already holds 32 resident atoms");
+  if (!d->deferred_free.empty()) {
+    const uint64_t consumed = __atomic_load_n(d->consumed_h, __ATOMIC_ACQUIRE);
+    while (!d->deferred_free.empty() && d->deferred_free.front().first <= consumed) {
+      d->free_slots.push_back(d->deferred_free.front().second);
+      d->deferred_free.pop_front();
+    }
+  }
   if (d->free_slots.empty()) return fail(GPUOS_E_FULL, "atom table full");
   if (a->flags & ~(GPUOS_ATOM_CHAIN_HEAD | GPUOS_ATOM_NO_EARLY))
     return fail(GPUOS_E_CONFIG, "unknown atom flags");
+  if (a->tenant > 0xffffu) return fail(GPUOS_E_CONFIG, "tenant must be < 65536");
   // Chaining: a live predecessor (not yet polled) arms this atom on the
   // device; one that already completed leaves nothing to wait for.
   uint32_t pred_slot = 0, pred_seq = 0;
@@ -1986,7 +2165,7 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   data[kFOp] = kOpSubmit;
   data[kFSlot] = slot;
   data[kFSeq] = seq;
-  data[kFPrio] = static_cast<uint32_t>(map_priority(a->priority));
+  data[kFPrio] = static_cast<uint32_t>(map_priority(a->priority)) | (a->tenant << 16);
   put64(data, kFLo, static_cast<uint64_t>(a->lo));
   data[kFCount] = static_cast<uint32_t>((a->hi - a->lo) * parts);
   data[kFAux] = parts | ((a->flags & GPUOS_ATOM_CHAIN_HEAD) ? kAuxChainHead : 0u) |
@@ -2010,13 +2189,19 @@ int gpuos_dev_submit_atom(gpuos_dev* d, const gpuos_atom_desc* a, uint32_t* atom
   h.has_succ = false;
   h.pred_slot = pred_slot;
   h.pred_seq = pred_seq;
+  h.succ_ring = 0;
   const int rc = publish(d, data);
   if (rc != GPUOS_OK) {
     h.live = false;
     d->free_slots.push_front(slot);
     return rc;
   }
-  if (chained) d->slots[pred_slot].has_succ = true;
+  if (chained) {
+    // The device registers this atom on the predecessor's slot when it
+    // ingests this entry: the slot must not be recycled before that.
+    d->slots[pred_slot].has_succ = true;
+    d->slots[pred_slot].succ_ring = d->ring_head;
+  }
   d->slot_of[id] = slot;
   for (int t = 0; t < T; ++t)
     if ((a->tpc_mask[t >> 6] >> (t & 63)) & 1ull) ++d->tpc_resident[t];
@@ -2053,6 +2238,18 @@ int gpuos_dev_set_fence_mask(gpuos_dev* d, const uint64_t mask[2], int32_t min_p
   put64(data, kFMask0, mask[0]);
   put64(data, kFMask1, mask[1]);
   data[kFPrio] = min_priority <= 0 ? 0u : static_cast<uint32_t>(map_priority(min_priority));
+  return publish(d, data);
+}
+
+int gpuos_dev_set_tpc_owner(gpuos_dev* d, const uint64_t mask[2], uint32_t owner, int32_t min_priority) {
+  if (!d || !mask) return fail(GPUOS_E_CONFIG, "null argument");
+  if (owner > 0xffffu) return fail(GPUOS_E_CONFIG, "owner must be < 65536");
+  uint32_t data[28] = {};
+  data[kFOp] = kOpFenceMask;
+  put64(data, kFMask0, mask[0]);
+  put64(data, kFMask1, mask[1]);
+  data[kFPrio] = min_priority <= 0 ? 0u : static_cast<uint32_t>(map_priority(min_priority));
+  data[kFAux] = owner;
   return publish(d, data);
 }
 
@@ -2097,12 +2294,32 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
       if ((h.mask[t >> 6] >> (t & 63)) & 1ull) --d->tpc_resident[t];
     h.live = false;
     d->slot_of.erase(h.atom_id);
-    d->free_slots.push_back(slot);
+    if (h.succ_ring > __atomic_load_n(d->consumed_h, __ATOMIC_ACQUIRE))
+      d->deferred_free.emplace_back(h.succ_ring, slot);  // successor not ingested yet
+    else
+      d->free_slots.push_back(slot);
     d->live[i] = d->live.back();  // O(1) removal; order is irrelevant
     d->live.pop_back();
     --d->in_flight;
     ++d->stats.atoms_completed;
     ++n;
+  }
+  if (n == 0 && d->in_flight > 0 && d->running && d->launch_rc.load(std::memory_order_acquire) == 1) {
+    // Nothing new: make sure the dispatcher still runs (a device fault or
+    // the hang guard ends it early), at most once per millisecond.
+    const int64_t now = steady_ns();
+    if (now - d->exit_check_ns > 1'000'000) {
+      d->exit_check_ns = now;
+      const cudaError_t q = cudaStreamQuery(d->s_work);
+      if (q != cudaErrorNotReady) {
+        unsigned fault = 0;
+        cudaMemcpy(&fault, &d->ctl->fault, sizeof fault, cudaMemcpyDeviceToHost);
+        if (fault != 0u)
+          return fail(GPUOS_E_TIMEOUT, std::string("dispatcher stopped on a device fault: ") + fault_name(fault));
+        return fail(GPUOS_E_INVARIANT, q == cudaSuccess ? "dispatcher exited with atoms in flight"
+                                                        : std::string("dispatcher failed: ") + cudaGetErrorString(q));
+      }
+    }
   }
   return n;
 }

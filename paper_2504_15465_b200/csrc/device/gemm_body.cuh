@@ -55,6 +55,16 @@ struct alignas(128) GemmDesc {
 };
 constexpr unsigned kGemmOutBf16 = 1u;
 
+struct WaitGuard {
+  unsigned* fault;              // DevCtl::fault (0: none)
+  unsigned* quit;               // DevCtl::quit
+  unsigned long long bound_ns;  // per wait
+};
+constexpr unsigned kFaultPipeline = 1u;  // an mbarrier wait expired
+__device__ __forceinline__ void raise_fault(const WaitGuard& g, unsigned code) {
+  atomicCAS(g.fault, 0u, code);
+  atomicExch(g.quit, 1u);
+}
 struct GemmPipe {
   unsigned char* tiles;          // stages x 32 KiB (A half, B half), 1024-aligned
   unsigned long long* full;      // [kGemmMaxStages]
@@ -65,11 +75,17 @@ struct GemmPipe {
   unsigned tmem;                 // TMEM base address of this worker's columns
   unsigned accum_used;           // tiles completed by this CTA (accum parity)
   unsigned long long kb_used;    // K slices streamed by this CTA so far
+  const WaitGuard* guard;        // in shared memory (slow path only)
 };
 
-// mbarrier wait that traps after 2 s instead of hanging the persistent
-// kernel (a trap aborts the context; the host sees a CUDA error).
-__device__ __forceinline__ void mbar_wait_bounded(unsigned long long* b, unsigned parity) {
+// Pipeline waits are bounded so a stuck tile cannot hang the persistent
+// kernel. On expiry the wait raises the dispatcher's fault word (first
+// fault wins) and its quit flag, then returns: the worker unwinds, the
+// kernel drains out, and the host reports GPUOS_E_TIMEOUT with the fault
+// code -- no `trap`, which would abort the CUDA context for every tenant.
+// After a fault every bounded wait returns at once.
+__device__ __forceinline__ void mbar_wait_bounded(unsigned long long* b, unsigned parity,
+                                                  const WaitGuard& g) {
   const unsigned a = smem_u32(b);
   unsigned ok = 0;
   unsigned long long t0 = 0;
@@ -81,11 +97,41 @@ __device__ __forceinline__ void mbar_wait_bounded(unsigned long long* b, unsigne
         : "memory");
     if (ok) return;
     if ((spins & 1023u) == 0) {
+      if (ld_relaxed_gpu(g.fault) != 0u) return;
       const unsigned long long t = gtimer();
-      if (t0 == 0) t0 = t;
-      else if (t - t0 > 2000000000ull) asm volatile("trap;");
+      if (t0 == 0) {
+        t0 = t;
+      } else if (t - t0 > g.bound_ns) {
+        raise_fault(g, kFaultPipeline);
+        return;
+      }
     }
   }
+}
+
+// One thread: spin until the gate opens (the TMA producer before its
+// activation loads, the MMA issuer before its first wait).
+__device__ __forceinline__ void gate_spin(const unsigned* gate, const WaitGuard& g) {
+  for (unsigned spins = 0; ld_acquire_gpu(gate) & 2u; ++spins) {
+    if ((spins & 63u) == 63u && ld_relaxed_gpu(g.quit) != 0u) break;
+    __nanosleep(64);
+  }
+}
+
+// An early-started tile's gate (DevAtom::paused bit 1): every thread that
+// is about to enter a bounded pipeline wait first waits here, unbounded
+// (the predecessor may legitimately run for a long time), so the bound
+// only ever measures the pipeline itself. Lane 0 of each warp polls; a
+// quit (hang guard, fault) releases the wait.
+__device__ __forceinline__ void gate_wait(const unsigned* gate, const WaitGuard& g) {
+  if (gate == nullptr) return;
+  if ((threadIdx.x & 31u) == 0u) {
+    for (unsigned spins = 0; ld_acquire_gpu(gate) & 2u; ++spins) {
+      if ((spins & 63u) == 63u && ld_relaxed_gpu(g.quit) != 0u) break;
+      __nanosleep(128);
+    }
+  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ void tc_fence_after() {
@@ -306,13 +352,13 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
     const unsigned pre = gate ? (nk < S ? nk : S) : 0u;  // (no gate: loads in stage order)
     for (unsigned j = 0; j < pre; ++j) {
       const unsigned s = static_cast<unsigned>((g0 + j) % S);
-      if ((g0 + j) / S >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>(((g0 + j) / S - 1) & 1));
+      if ((g0 + j) / S >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>(((g0 + j) / S - 1) & 1), *G.guard);
       if (rank == 0) mbar_expect_tx(G.full + s, tx);
       tma_load_2d_pair(G.tiles + s * kGemmStageBytes + kGemmABytes, &D->b, static_cast<int>(j * kGemmBK),
                        b_row, G.full + s);
     }
     if (gate) {
-      while (ld_acquire_gpu(gate) & 2u) __nanosleep(64);  // DevAtom::paused, kGatedBit
+      gate_spin(gate, *G.guard);  // DevAtom::paused, kGatedBit
       asm volatile("fence.proxy.async.global;" ::: "memory");  // A: generic-proxy writes, TMA reads
     }
     for (unsigned j = 0; j < pre; ++j)
@@ -322,7 +368,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;
-      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
+      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1), *G.guard);
       unsigned char* st = G.tiles + s * kGemmStageBytes;
       if (rank == 0) mbar_expect_tx(G.full + s, tx);
       const int kc = static_cast<int>(j * kGemmBK);
@@ -330,13 +376,14 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
       tma_load_2d_pair(st + kGemmABytes, &D->b, kc, b_row, G.full + s);
     }
   } else if (tid == 32 && rank == 0) {
+    if (gate) gate_spin(gate, *G.guard);  // the bounded waits measure the pipeline only
     // MMA issuer: one thread of the leader drives both SMs' tensor cores.
     tc_fence_after();
     const unsigned idesc = umma_idesc_bf16(kGemmTile, n_tile);
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
-      mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1));
+      mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1), *G.guard);
       tc_fence_after();
       if (tm && j == 0) tm[1] = gtimer();
       const unsigned a0 = smem_u32(G.tiles + s * kGemmStageBytes);
@@ -352,7 +399,8 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
 
   // Epilogue: all 8 warps of both CTAs. Warp w reads TMEM lanes 32(w%4)..+31
   // (this CTA's 128 tile rows) and column half w/4.
-  mbar_wait_bounded(G.accum, G.accum_used & 1u);
+  gate_wait(gate, *G.guard);  // (unbounded: the predecessor may run long)
+  mbar_wait_bounded(G.accum, G.accum_used & 1u, *G.guard);
   tc_fence_after();
   if (tm && tid == 0) tm[2] = gtimer();
   const unsigned col0 = nt * n_tile;

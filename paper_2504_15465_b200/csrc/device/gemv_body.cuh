@@ -63,6 +63,7 @@ struct GemvPipe {
   unsigned accum_used;
   unsigned long long kb_used;
   unsigned tmem;
+  const WaitGuard* guard;        // in shared memory (slow path only)
 };
 
 // Once per CTA, all threads (barriers at smem + 256 .. 392; tiles share the
@@ -133,13 +134,13 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;
-      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
+      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1), *G.guard);
       if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemvStageBytes);
       tma_load_2d_pair(G.tiles + s * kGemvStageBytes, &D->w, static_cast<int>((kb0 + j) * kGemmBK), w_row,
                        G.full + s);
     }
     if (gate) {
-      while (ld_acquire_gpu(gate) & 2u) __nanosleep(64);  // DevAtom::paused, kGatedBit
+      gate_spin(gate, *G.guard);  // DevAtom::paused, kGatedBit
       asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic-proxy writes, TMA reads
     }
     for (unsigned j = 0; j < pre; ++j) {
@@ -151,7 +152,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
       const unsigned long long r = k / S;
-      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1));
+      if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1), *G.guard);
       unsigned char* st = G.tiles + s * kGemvStageBytes;
       if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemvStageBytes);
       const int kc = static_cast<int>((kb0 + j) * kGemmBK);
@@ -159,12 +160,13 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       tma_load_2d_pair(st + kGemvWBytes, &D->x, kc, x_row, G.full + s);
     }
   } else if (tid == 32 && rank == 0) {
+    if (gate) gate_spin(gate, *G.guard);  // the bounded waits measure the pipeline only
     tc_fence_after();
     const unsigned idesc = umma_idesc_bf16(kGemvTile, kGemvN);
     for (unsigned j = 0; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
-      mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1));
+      mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1), *G.guard);
       tc_fence_after();
       if (tm && j == 0) tm[1] = gtimer();
       const unsigned a0 = smem_u32(G.tiles + s * kGemvStageBytes);
@@ -178,7 +180,8 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
     umma2_commit_both(G.accum);
   }
   // Epilogue: warps 0-3 of both CTAs read TMEM column 0 (y) of their lanes.
-  mbar_wait_bounded(G.accum, G.accum_used & 1u);
+  gate_wait(gate, *G.guard);  // (unbounded: the predecessor may run long)
+  mbar_wait_bounded(G.accum, G.accum_used & 1u, *G.guard);
   tc_fence_after();
   if (tm && tid == 0) tm[2] = gtimer();
   const int warp = tid >> 5, lane = tid & 31;

@@ -445,6 +445,7 @@ void B200Device::reset_run() {
   timer_fns_.clear();
   now_ = 0;
   busy_tpc_ns_ = 0.0;
+  backpressure_waits_ = 0;
   residency_.clear();
 }
 
@@ -490,8 +491,24 @@ AtomId B200Device::submit_chained(AtomId after, KernelId kernel, long lo, long h
   d.parts = r.parts;
   d.after = after == kNoAtom ? 0u : after + 1u;
   d.flags = (chain_head ? GPUOS_ATOM_CHAIN_HEAD : 0u) | (no_early ? GPUOS_ATOM_NO_EARLY : 0u);
+  d.tenant = tag < 0xffffu ? static_cast<std::uint32_t>(tag) + 1u : 0u;  // the scheduler tags atoms with their app
   std::uint32_t id = 0;
-  check(gpuos_dev_submit_atom(rt_->handle(), &d, &id), "gpuos_dev_submit_atom");
+  // Back-pressure: a TPC holds at most 32 resident atoms and the atom table
+  // is finite (the reference has no cap). When either is full, collect
+  // completions (queued for step(), not delivered here: no re-entry into
+  // the scheduler) until the device frees room; every atom ahead of this
+  // one is already submitted, so room always comes.
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(60);
+  for (;;) {
+    const int rc = gpuos_dev_submit_atom(rt_->handle(), &d, &id);
+    if (rc == GPUOS_OK) break;
+    if (rc != GPUOS_E_FULL) raise(rc, "gpuos_dev_submit_atom");
+    ++backpressure_waits_;
+    pump();
+    if (std::chrono::steady_clock::now() > deadline)
+      throw InvariantError("submit_atom: no room on the device for 60 s");
+    std::this_thread::yield();
+  }
   AtomTimeline tl{};
   tl.atom = id;
   tl.tag = tag;
@@ -510,11 +527,12 @@ void B200Device::set_atom_paused(AtomId atom, bool paused) {
   check(gpuos_dev_set_atom_paused(rt_->handle(), atom, paused ? 1 : 0), "pause");
 }
 
-void B200Device::set_tpc_fence(const std::vector<int>& tpcs, int min_priority) {
+void B200Device::set_tpc_fence(const std::vector<int>& tpcs, int min_priority, std::uint64_t owner_tag) {
   if (!rt_->running() || tpcs.empty()) return;
   const auto m = mask_of(tpcs);
   const std::uint64_t mask[2] = {m[0], m[1]};
-  check(gpuos_dev_set_fence_mask(rt_->handle(), mask, min_priority), "fence");
+  const std::uint32_t owner = owner_tag < 0xffffu ? static_cast<std::uint32_t>(owner_tag) + 1u : 0u;
+  check(gpuos_dev_set_tpc_owner(rt_->handle(), mask, owner, min_priority), "fence");
 }
 
 SimTime B200Device::request_frequency(FreqMhz f) {
@@ -602,10 +620,10 @@ void B200Device::run_all() {
   pump();  // nothing should remain; keep the ring consistent regardless
   gpuos_dev_stats st{};
   gpuos_dev_get_stats(rt_->handle(), &st);
-  // Worker-slot time of this run in TPC-ns, counted up to the metrics
-  // horizon (blocks after it are scaled out pro rata).
-  double busy = static_cast<double>(st.worker_busy_ns - before.worker_busy_ns) /
-                rt_->workers_per_tpc();
+  // TPC-ns with >= 1 running block (the reference's definition,
+  // device.cpp:264-275), sampled on the device, counted up to the metrics
+  // horizon (time after it is scaled out pro rata).
+  double busy = static_cast<double>(st.tpc_busy_ns - before.tpc_busy_ns);
   if (horizon_ > 0 && now_ > horizon_) busy *= static_cast<double>(horizon_) / static_cast<double>(now_);
   busy_tpc_ns_ = busy;
   residency_[freq_.f_max()] = now_;
@@ -617,6 +635,7 @@ MirrorDevice::MirrorDevice(DeviceTopology topo, FrequencyDomain freq, PowerModel
     : replay_(topo, std::move(freq), power) {
   opt.trace_blocks = true;
   rt_ = std::make_unique<B200Runtime>(topo.total_tpcs(), opt);
+  rt_->reset_kernels();  // first trace chunk now: no allocation inside the live run
 }
 
 MirrorDevice::~MirrorDevice() = default;

@@ -11,6 +11,7 @@
 #include "gpuos/replay.hpp"
 #include "gpuos/scenario.hpp"
 #include "gpuos_dev.h"
+#include "gpuos_dev.h"
 #include "gpuos_sim.h"
 #include "json.hpp"
 
@@ -80,6 +81,7 @@ void apply_knob(ScenarioConfig& c, const std::string& k, const json& v) {
   else if (k == "chain_launches") s.chain_launches = flag();
   else if (k == "chain_depth") s.chain_depth = v.get<int>();
   else if (k == "chain_best_effort") s.chain_best_effort = flag();
+  else if (k == "atom_lookahead") s.atom_lookahead = flag();
   else if (k == "atom_duration_us") s.atom_duration = duration_from_us(v.get<double>());
   else if (k == "steal_horizon_us") s.steal_horizon = duration_from_us(v.get<double>());
   else if (k == "max_outstanding_atoms") s.max_outstanding_atoms = v.get<int>();
@@ -249,6 +251,13 @@ std::string run_session(gpuos_session* s, const json& overrides) {
     b["workers_per_tpc"] = dev.runtime().workers_per_tpc();
     b["logical_tpcs"] = cfg.topo.total_tpcs();
     b["tpc_busy_integral"] = dev.tpc_busy_integral();
+    b["backpressure_waits"] = dev.backpressure_waits();
+    {
+      gpuos_dev_stats st{};
+      gpuos_dev_get_stats(dev.runtime().handle(), &st);
+      b["worker_busy_ns_total"] = st.worker_busy_ns;  // (cumulative over the handle's runs)
+      b["tpc_busy_ns_total"] = st.tpc_busy_ns;
+    }
     long blocks = 0;
     for (std::size_t k = 0; k < dev.kernels().size(); ++k) blocks += dev.blocks_executed(static_cast<KernelId>(k));
     b["blocks"] = blocks;

@@ -56,3 +56,26 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+def run_atoms(api, dev, atoms, workers, body, args, trace=None, timeout=60.0):
+    """Executes (lo, hi, tpcs, prio) atoms of one body: live (ring + ingest
+    warp) with W = 2 workers per SM, batch mode with W = 1 (live mode needs
+    W = 2: the ingest cluster takes one of a TPC's two worker pairs)."""
+    import time
+
+    if workers == 2:
+        dev.start()
+        for lo, hi, tpcs, prio in atoms:
+            dev.submit(lo, hi, tpcs, prio, body, args, trace=trace)
+    else:
+        dev.run_batch([api.Device.desc(lo, hi, tpcs, prio, body, args, trace=trace)
+                       for lo, hi, tpcs, prio in atoms])
+    done = []
+    t0 = time.time()
+    while len(done) < len(atoms):
+        done += dev.poll()
+        assert time.time() - t0 < timeout, f"only {len(done)}/{len(atoms)} atoms completed"
+    if workers == 2:
+        dev.stop()
+    return done

@@ -320,6 +320,10 @@ def test_no_early_keeps_a_chained_gemv_behind_its_predecessor(api, cuda_device):
         dev.free(d1)
         dev.free(d2)
     check_order(done, [a, b])
+    by_id = {c.atom_id: c for c in done}
+    # Not armed early: no block of b starts before a's last block ends.
+    assert by_id[b].dev_first_start_ns >= by_id[a].dev_last_end_ns, (
+        by_id[b].dev_first_start_ns, by_id[a].dev_last_end_ns)
     ref = (w2.double().cpu() @ y1.double().cpu()).float()
     err = ((y2.cpu() - ref).abs().max() / ref.abs().max()).item()
     assert err < 1e-3, err

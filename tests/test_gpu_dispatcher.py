@@ -45,6 +45,10 @@ def test_topology_and_residency(api, cuda_device):
         assert t.workers_per_tpc == 4
         dev.start()  # fails loudly unless every SM hosts exactly W workers
         dev.stop()
+    with api.Device(workers_per_sm=1) as dev:
+        with pytest.raises(api.GpuosError) as e:
+            dev.start()  # live mode needs W = 2 (cluster 0 hosts the ingest warp)
+        assert e.value.code == -2
 
 
 @pytest.mark.parametrize("workers_per_sm", [1, 2])
@@ -68,12 +72,23 @@ def test_stream_atoms_exactly_once_placed_bit_exact(api, torch_mod, workers_per_
             tpcs = [73]
         specs.append((lo, hi, tpcs, rng.choice([10, 20, 30])))
     with api.Device(workers_per_sm=workers_per_sm) as dev:
-        dev.start()
-        for lo, hi, tpcs, prio in specs:
-            dev.submit(lo, hi, tpcs, prio, api.GPUOS_BODY_STREAM,
-                       [src.data_ptr(), dst.data_ptr(), words, salt, 0], trace=trace.data_ptr())
-        done = wait_all(dev, len(specs))
-        dev.stop()
+        if workers_per_sm == 2:
+            dev.start()  # live: ring + ingest warp (cluster 0) + workers
+            for lo, hi, tpcs, prio in specs:
+                dev.submit(lo, hi, tpcs, prio, api.GPUOS_BODY_STREAM,
+                           [src.data_ptr(), dst.data_ptr(), words, salt, 0], trace=trace.data_ptr())
+            done = wait_all(dev, len(specs))
+            dev.stop()
+        else:
+            # W = 1 runs batch mode only (live mode's ingest cluster would
+            # take a TPC's only worker pair); <= 32 atoms per TPC.
+            descs = [api.Device.desc(lo, hi, tpcs, prio, api.GPUOS_BODY_STREAM,
+                                     [src.data_ptr(), dst.data_ptr(), words, salt, 0], trace=trace.data_ptr())
+                     for lo, hi, tpcs, prio in specs]
+            dev.run_batch(descs[:30])
+            done = wait_all(dev, 30)
+            dev.run_batch(descs[30:])
+            done += wait_all(dev, len(specs) - 30)
     counts, sm = decode(trace)
     assert (counts == 1).all(), f"{int((counts == 0).sum())} missing, {int((counts > 1).sum())} duplicated"
     for (lo, hi, tpcs, _), c in zip(specs, sorted(done, key=lambda c: c.atom_id)):
@@ -198,6 +213,30 @@ def test_fence_revokes_tpcs_mid_atom(api, torch_mod):
     assert set(late.tolist()) <= {2, 3}
 
 
+def test_tpc_owner_keeps_its_own_stolen_priority_atoms(api, torch_mod):
+    """The TPC-ownership table: an owner fences its quota (TPCs 0-1) against
+    other tenants' stolen-priority atoms, while its own atom -- priority 10
+    because it also spans stolen TPCs 2-3 -- keeps starting blocks there."""
+    torch = torch_mod
+    blocks = 800
+    own = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+    other = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+    with api.Device() as dev:
+        dev.start()
+        dev.set_owner([0, 1], owner=1, min_priority=11)
+        time.sleep(0.0005)
+        dev.submit(0, blocks, [0, 1, 2, 3], 10, api.GPUOS_BODY_SPIN, [50_000], trace=own.data_ptr(), tenant=1)
+        dev.submit(0, blocks, [0, 1, 2, 3], 10, api.GPUOS_BODY_SPIN, [50_000], trace=other.data_ptr(), tenant=2)
+        wait_all(dev, 2)
+        dev.set_owner([0, 1], owner=0, min_priority=0)
+        dev.stop()
+    c_own, sm_own = decode(own)
+    c_oth, sm_oth = decode(other)
+    assert (c_own == 1).all() and (c_oth == 1).all()
+    assert set((sm_own >> 1).tolist()) == {0, 1, 2, 3}  # the owner's atom used its quota
+    assert set((sm_oth >> 1).tolist()) <= {2, 3}        # the other tenant's never did
+
+
 def test_slot_recycling_many_small_atoms(api, torch_mod):
     """10k one-to-three-block atoms through a 64-slot atom table: slots are
     reused while stale resident keys are still visible; the sequence-tagged
@@ -283,3 +322,21 @@ def test_batch_mode_priority_and_placement(api, torch_mod):
     for i in range(30):
         assert set((sm[i * 100:(i + 1) * 100] >> 1).tolist()) <= {i % 74, (i * 7) % 74}
     assert sorted(c.blocks for c in done) == [100] * 30
+
+
+def test_tpc_busy_sampler_matches_known_occupancy(api, cuda_device):
+    """TPC utilisation with the reference's definition (device.cpp:264-275):
+    the device integrates "TPCs with >= 1 running block". 10 TPCs run 1 ms
+    SPIN blocks back to back (4 workers each, 20 waves) while the other 64
+    stay idle: the integral is ~10 TPCs x the atom's span."""
+    with api.Device(workers_per_sm=2) as dev:
+        dev.start()
+        before = dev.stats().tpc_busy_ns
+        blocks = 10 * 4 * 20
+        dev.submit(0, blocks, list(range(10, 20)), 20, api.GPUOS_BODY_SPIN, [1_000_000])
+        (c,) = wait_all(dev, 1)
+        dev.stop()
+        busy = dev.stats().tpc_busy_ns - before
+    span = c.dev_last_end_ns - c.dev_first_start_ns
+    assert 19e6 <= span <= 23e6, span
+    assert 0.95 * 10 * span <= busy <= 10 * span + 10 * 0.5e6, (busy, span)

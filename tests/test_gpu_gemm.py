@@ -18,6 +18,7 @@ import time
 import numpy as np
 import pytest
 
+from conftest import run_atoms
 from oracle.policy import stream_expect
 
 pytestmark = pytest.mark.gpu
@@ -83,11 +84,7 @@ def test_gemm_atoms_match_reference(api, cuda_device, m, n, k, bf16_out, workers
         assert blocks == -(-m // tm) * -(-n // tn)
         trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
         atoms = random_atoms(rng, blocks, min(blocks, 7))
-        dev.start()
-        for lo, hi, tpcs, prio in atoms:
-            dev.submit(lo, hi, tpcs, prio, api.GPUOS_BODY_GEMM_BF16, [desc], trace=trace.data_ptr())
-        wait_all(dev, len(atoms))
-        dev.stop()
+        run_atoms(api, dev, atoms, workers, api.GPUOS_BODY_GEMM_BF16, [desc], trace=trace.data_ptr())
         dev.free(desc)
     tr = trace.cpu().numpy().view(np.uint32)
     assert ((tr >> 16) == 1).all(), "a tile did not run exactly once"

@@ -12,6 +12,8 @@ import time
 import numpy as np
 import pytest
 
+from conftest import run_atoms
+
 pytestmark = pytest.mark.gpu
 
 
@@ -49,17 +51,23 @@ def test_gemv_atoms_match_reference(api, cuda_device, n, k, bf16_out, workers, s
         cuts = sorted(rng.sample(range(1, blocks), min(6, blocks - 1)))
         atoms = [(lo, hi, sorted(rng.sample(range(74), rng.choice([1, 5, 74]))), rng.choice([10, 20, 30]))
                  for lo, hi in zip([0] + cuts, cuts + [blocks])]
-        dev.start()
-        for lo, hi, tpcs, prio in atoms:
-            dev.submit(lo, hi, tpcs, prio, api.GPUOS_BODY_GEMV_BF16, [desc], trace=trace.data_ptr())
-        wait_all(dev, len(atoms))
-        # The same descriptor serves the next decode step: new x, same pointers.
         x2 = (torch.rand(k, generator=g) * 2 - 1).to(torch.bfloat16)
-        X.copy_(x2.cuda())
-        torch.cuda.current_stream().synchronize()  # not the device: the dispatcher is resident
-        dev.submit(0, blocks, list(range(74)), 20, api.GPUOS_BODY_GEMV_BF16, [desc])
-        wait_all(dev, 1)
-        dev.stop()
+        if workers == 2:
+            dev.start()
+            for lo, hi, tpcs, prio in atoms:
+                dev.submit(lo, hi, tpcs, prio, api.GPUOS_BODY_GEMV_BF16, [desc], trace=trace.data_ptr())
+            wait_all(dev, len(atoms))
+            # The same descriptor serves the next decode step: new x, same pointers.
+            X.copy_(x2.cuda())
+            torch.cuda.current_stream().synchronize()  # not the device: the dispatcher is resident
+            dev.submit(0, blocks, list(range(74)), 20, api.GPUOS_BODY_GEMV_BF16, [desc])
+            wait_all(dev, 1)
+            dev.stop()
+        else:  # W = 1: batch mode (see conftest.run_atoms)
+            run_atoms(api, dev, atoms, workers, api.GPUOS_BODY_GEMV_BF16, [desc], trace=trace.data_ptr())
+            X.copy_(x2.cuda())
+            torch.cuda.synchronize()
+            run_atoms(api, dev, [(0, blocks, list(range(74)), 20)], workers, api.GPUOS_BODY_GEMV_BF16, [desc])
         dev.free(desc)
     tr = trace.cpu().numpy().view(np.uint32)
     assert ((tr >> 16) == 1).all()
