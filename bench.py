@@ -132,7 +132,8 @@ def barrier():
 
 def reference_arm(args, cfgs: list[dict], rank: int, world: int) -> None:
     """The unmodified reference on this box's host cores (rank 0 only): every
-    rank's scenario, each as parallel replicas over an equal share of cores."""
+    rank's scenario, each as parallel replicas over an equal share of cores;
+    each step a bounded ~5 s sample."""
     if rank != 0:
         return
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
@@ -141,7 +142,62 @@ def reference_arm(args, cfgs: list[dict], rank: int, world: int) -> None:
     if not os.path.exists(exe):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
         return
-    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_baseline(cfgs, seconds=0.0)
+    steps = [cpu_baseline(cfgs, seconds=args.sample_s) for _ in range(args.steps)]
+    be = sum(s["value"] * s["wall_s"] for s in steps)
+    wall = sum(s["wall_s"] for s in steps)
+    value = be / wall
+    cb = dict(steps[-1], value=value, wall_s=wall)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "BE atoms/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": bench_config(cfgs[0], args, world),
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "BE atoms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def host_cores() -> int:
+    """Cores this process may run on (the affinity mask, not the machine)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def bench_config(cfg: dict, args, world: int) -> dict:
+    """The `config` object both arms print (identical dicts: same scenario,
+    same replica layout)."""
+    return {"workload": cfg["name"] + (" (BASELINE config #5, per GPU)" if args.workload == "box8"
+                                       else " (BASELINE config #1)"),
+            "tenants": [a["id"] + (" (LC)" if a["priority"] == "hp" else " (BE)") for a in cfg["apps"]],
+            "tpcs": 74, "time_scale": args.time_scale, "horizon_ms": cfg["horizon_ms"],
+            "l2": "inputs larger than L2 (STREAM workspaces >> 126 MB)",
+            "parallelism": f"replicas x{world}"}
+
+
+def cpu_baseline(cfgs: list[dict], cores: int | None = None, seconds: float = 10.0) -> dict:
+    """Bounded sample of the reference on this box's host (rank 0, N=1): the
+    compiled reference simulator (oracle/_ref/ref_bench) on the same
+    scenario(s), `cores` independent replicas in parallel (one per core)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return {"value": None, "unit": "BE atoms/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    cores = cores or host_cores()
     per = max(1, cores // len(cfgs))
     paths = []
     for c in cfgs:
@@ -149,55 +205,21 @@ def reference_arm(args, cfgs: list[dict], rank: int, world: int) -> None:
             json.dump(c, f)
             paths.append(f.name)
 
-    def step(reps):
+    def run(reps):
         procs = [subprocess.Popen([exe, "--config", p, "--threads", str(per), "--reps", str(reps)],
                                   stdout=subprocess.PIPE, text=True) for p in paths]
         outs = [json.loads(p.communicate()[0]) for p in procs]
         return {"be_atoms": sum(o["be_atoms"] for o in outs), "wall_s": max(o["wall_s"] for o in outs),
                 "hp_p99_ns": max(o["hp_p99_ns"] for o in outs)}
 
-    probe = step(1)
-    reps = max(1, int(5.0 / max(probe["wall_s"], 1e-3)))  # ~5 s of wall time per step
-    for _ in range(args.warmup):
-        step(1)
-    steps = [step(reps) for _ in range(args.steps)]
-    be = sum(s["be_atoms"] for s in steps)
-    wall = sum(s["wall_s"] for s in steps)
-    value = be / wall
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "BE atoms/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": ", ".join(c["name"] for c in cfgs),
-                   "tenants": [a["id"] for a in cfgs[0]["apps"]],
-                   "tpcs": cfgs[0]["device"]["gpc_count"] * cfgs[0]["device"]["tpcs_per_gpc"]},
-        "cpu_baseline": {"value": value, "unit": "BE atoms/s", "cores": per * len(cfgs), "kind": "reference",
-                         "sample": f"{reps} x {per} replicas of each of {len(cfgs)} scenario(s) per step "
-                                   f"(reference discrete-event simulator, wall clock)"},
-        "e2e": {"value": value, "unit": "BE atoms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "lc_p99_ms_simulated": steps[-1]["hp_p99_ns"] / 1e6,
-    }))
-
-
-def cpu_baseline(cfg: dict) -> dict:
-    """Bounded sample of the reference on this box's host (rank 0, N=1)."""
-    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
-    if not os.path.exists(exe):
-        return {"value": None, "unit": "BE atoms/s", "cores": 0, "kind": "reference",
-                "sample": "oracle/_ref not built"}
-    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
-        json.dump(cfg, f)
-        path = f.name
-    one = json.loads(subprocess.run([exe, "--config", path, "--threads", "1", "--reps", "1"],
-                                    capture_output=True, text=True, check=True).stdout)
-    reps = max(1, int(10.0 / max(one["wall_s"], 1e-3)))
-    r = json.loads(subprocess.run([exe, "--config", path, "--threads", "1", "--reps", str(reps)],
-                                  capture_output=True, text=True, check=True).stdout)
-    return {"value": r["be_atoms"] / r["wall_s"], "unit": "BE atoms/s", "cores": 1, "kind": "reference",
-            "sample": f"{reps} sequential runs of the scenario on 1 core "
-                      f"({r['wall_s']:.1f} s; reference simulator, simulated LC p99 "
-                      f"{r['hp_p99_ns'] / 1e6:.3f} ms)"}
+    one = run(1)
+    reps = max(1, int(seconds / max(one["wall_s"], 1e-3)))
+    r = run(reps)
+    return {"value": r["be_atoms"] / r["wall_s"], "unit": "BE atoms/s", "cores": per * len(cfgs),
+            "kind": "reference", "cpu_model": cpu_model(), "wall_s": r["wall_s"], "reps": reps,
+            "sample": f"{reps} runs of each of {len(cfgs)} scenario(s) on each of {per} parallel "
+                      f"replica threads ({r['wall_s']:.1f} s; reference discrete-event simulator, "
+                      f"simulated LC p99 {r['hp_p99_ns'] / 1e6:.3f} ms)"}
 
 
 def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
@@ -282,13 +304,8 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (reference Figure-7 trace, time-scaled; STREAM bodies over seeded u32 workspaces)",
-        "config": {"workload": cfg["name"] + (" (BASELINE config #5, per GPU)" if args.workload == "box8"
-                                              else " (BASELINE config #1)"),
-                   "tenants": [a["id"] + (" (LC)" if a["priority"] == "hp" else " (BE)") for a in cfg["apps"]],
-                   "tpcs": 74, "time_scale": args.time_scale, "horizon_ms": cfg["horizon_ms"],
-                   "workers_per_sm": args.workers_per_sm,
-                   "l2": "inputs larger than L2 (STREAM workspaces >> 126 MB)",
-                   "parallelism": f"replicas x{world}"},
+        "config": bench_config(cfg, args, world),
+        "workers_per_sm": args.workers_per_sm,
         "lc_p99_ms": lc_p99, "lc_p99_alone_ms": lc_alone, "lc_p99_vs_alone": lc_p99 / lc_alone,
         "lc_slo_ms": cfg["apps"][0]["slo_ms"],
         "be_blocks_per_s": be_blocks_all / (max_ms * 1e-3),
@@ -302,7 +319,11 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
             "be_atoms_per_s": sum(s["atoms"]["be"] for s in ref_sem) / (ref_sem_ms * 1e-3),
             "be_blocks_per_s": sum(be_blocks_of(s) for s in ref_sem) / (ref_sem_ms * 1e-3)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "frac": achieved / pk["hbm_gbs"], "traffic": live_traffic(),
+                     "traffic_note": "DRAM read+write of one live k_worker launch of this scenario "
+                                     "under ncu (profiles/ncu_traffic_r02.json); algorithmic bytes "
+                                     "of that launch in traffic_algorithmic",
+                     "traffic_algorithmic": live_traffic("algorithmic_bytes"),
                      "kernel": "k_worker (persistent dispatcher, stacked run, CUDA events)",
                      "peak_source": pk["source"]},
         "roofline_saturated": sat,
@@ -317,11 +338,11 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
             "publish_to_first_block_us_p50": probe["publish_to_first_block_ns"]["p50"] / 1e3,
             "pipelined_ns_per_atom": probe["pipelined_ns_per_atom"],
             "note": "empty one-block atoms through the live ring (gpuos_probe_dispatch)"},
-        "cpu_baseline": cpu_baseline(cfg) if world == 1 else None,
+        "cpu_baseline": cpu_baseline([cfg]) if world == 1 else None,
         "e2e": {"value": e2e_atoms_all / e2e_s_max, "unit": "BE atoms/s",
                 "h2d_bytes_per_step": e2e[0]["b200"]["h2d_bytes"],
                 "d2h_bytes_per_step": e2e[0]["b200"]["d2h_bytes"]},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": args.steps,  # one self-contained k_worker launch per step
         "clocks": clocks.summary(),
     }
     print(json.dumps(line))
@@ -365,6 +386,16 @@ def ncu_traffic(name: str, config: str):
     except (OSError, KeyError, ValueError):
         return None
     return t["dram_read"] + t["dram_write"] if t.get("config") == config else None
+
+
+def live_traffic(key: str = "dram"):
+    """The live stacked run's DRAM bytes per k_worker launch from the committed
+    ncu capture of the same scenario (profiles/ncu_traffic_r02.json)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")))["fig7_live"]
+    except (OSError, KeyError, ValueError):
+        return None
+    return t["dram_read"] + t["dram_write"] if key == "dram" else t[key]
 
 
 def guarded(fn):
@@ -532,6 +563,26 @@ def conv_saturation(api, local: int, args) -> dict:
             "peak_source": pk["source"]}
 
 
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks of this same
+    command line, one per GPU (RANK / LOCAL_RANK / WORLD_SIZE /
+    MASTER_ADDR=127.0.0.1 / MASTER_PORT in the environment, exactly what
+    torchrun would set). Rank 0's stdout is the bench line; the others'
+    stdout is discarded. Returns the worst exit code."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    return max(abs(p.wait()) for p in procs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -546,15 +597,21 @@ def main():
                     help="skip the model-trace runs of configs #2/#3")
     ap.add_argument("--workload", choices=["fig7", "box8"], default="fig7",
                     help="fig7: BASELINE config #1; box8: config #5 (8 tenants per GPU)")
+    ap.add_argument("--sample-s", type=float, default=5.0,
+                    help="reference arm: seconds of simulator work per step")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     rank, world, local = dist_init()
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
     if args.workload == "box8":
         cfg = workloads.tenant_set(rank, args.time_scale, args.horizon_ms)
     else:
         cfg = workloads.fig7_b200(args.time_scale, args.horizon_ms)
     if args.impl == "reference":
         cfgs = ([workloads.tenant_set(r, args.time_scale, args.horizon_ms) for r in range(world)]
-                if args.workload == "box8" else [cfg])
+                if args.workload == "box8" else [cfg] * world)
         reference_arm(args, cfgs, rank, world)
     else:
         ours(args, cfg, rank, world, local)

@@ -124,11 +124,12 @@ def build(verbose: bool = False) -> dict[str, str]:
         if _stale(exe, [src] + libs + headers):
             _run(cc + [src] + libs + ["-o", exe])
         out[name] = exe
-    probe = os.path.join(BIN, "topo_probe")
-    psrc = os.path.join(CSRC, "tools", "topo_probe.cu")
-    if _stale(probe, [psrc]):
-        _run([NVCC] + ARCH + ["-O2", "-std=c++17", psrc, "-o", probe])
-    out["topo_probe"] = probe
+    for name in ("topo_probe", "racecheck_alloc_probe"):
+        probe = os.path.join(BIN, name)
+        psrc = os.path.join(CSRC, "tools", name + ".cu")
+        if _stale(probe, [psrc]):
+            _run([NVCC] + ARCH + ["-O2", "-lineinfo", "-std=c++17", psrc, "-o", probe])
+        out[name] = probe
     if verbose:
         for k, v in out.items():
             print(f"{k}: {v}")
