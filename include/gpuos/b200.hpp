@@ -79,7 +79,16 @@ struct VerifyReport {
   long misplaced = 0;    // blocks run on an SM outside the atom's TPC set
   long bad_words = 0;    // body output words differing from the oracle
   long checked_words = 0;
-  bool ok() const { return missing == 0 && duplicated == 0 && misplaced == 0 && bad_words == 0; }
+  // Tensor-core bodies (GEMM / GEMV / conv): sampled output elements of every
+  // fully executed kernel against a float64 restatement of the same bf16
+  // operands (tolerance: one bf16 rounding of the result plus fp32
+  // accumulation, 2^-8 |ref| + 1e-5 sum |a b|).
+  long tensor_kernels = 0;
+  long tensor_checked = 0;
+  long tensor_bad = 0;
+  bool ok() const {
+    return missing == 0 && duplicated == 0 && misplaced == 0 && bad_words == 0 && tensor_bad == 0;
+  }
 };
 
 // Owns one dispatcher handle plus the tenant workspaces.
@@ -147,10 +156,14 @@ class B200Runtime {
   Workspace& workspace(std::uint32_t id, std::uint64_t words);
   Resolved resolve_body(const SimKernelSpec& spec);
   struct TensorBody {  // operands + descriptor of a tensor-core kernel shape
-    std::vector<void*> bufs;
+    std::vector<void*> bufs;  // gemm: A, B, C; gemv: W, x, y; conv: x, w, y
     void* desc = nullptr;
     std::int64_t blocks = 0;
+    BodyRef ref;              // kind + shape (verify_kernels)
   };
+  // Sampled float64 check of a tensor body's output (verify_kernels).
+  void verify_tensor(const TensorBody& t, VerifyReport& rep);
+  std::unordered_map<std::uint64_t, const TensorBody*> tensor_of_desc_;
   const TensorBody& tensor_body(const BodyRef& b);
   std::map<std::string, TensorBody> tensors_;
   void ensure_trace(KernelId kid, long blocks);

@@ -61,11 +61,11 @@ __device__ __forceinline__ void tma_load_im2col_pair(void* dst, const CUtensorMa
 // pipe (stage = 16 KiB A + 16 KiB B, same barriers and TMEM columns).
 // `gate`: early-start gate, as in body_gemm2 (weights first, activations
 // once the predecessor has written them).
-__device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G,
-                                           const unsigned* gate) {
-  const ConvDesc* D = reinterpret_cast<const ConvDesc*>(c.args[0]);
-  const unsigned pt = static_cast<unsigned>(c.block) % D->pair_tiles;
-  const unsigned kt = static_cast<unsigned>(c.block) / D->pair_tiles;
+template <class NextTile>
+__device__ __forceinline__ void conv2_tile(const ConvDesc* D, unsigned blk, int tid, unsigned rank,
+                                           GemmPipe& G, const unsigned* gate, NextTile& next_tile) {
+  const unsigned pt = blk % D->pair_tiles;
+  const unsigned kt = blk / D->pair_tiles;
   const unsigned m0 = pt * kGemmTile + rank * kGemmHalf;  // this CTA's first output pixel
   const unsigned pq = D->p * D->q;
   const unsigned n0 = m0 / pq, rem = m0 - n0 * pq;
@@ -75,6 +75,7 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
   const unsigned S = G.stages;
   const unsigned long long g0 = G.kb_used;
   if (S == 0) {
+    if (tid == 0 && rank == 0) next_tile(true);  // (ends the run)
     cluster_sync_all();
     return;
   }
@@ -122,6 +123,7 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
                            static_cast<unsigned short>(ss), static_cast<unsigned short>(rr), G.full + s);
       tma_load_2d_pair(stg + kGemmABytes, &D->wgt, static_cast<int>(j * kGemmBK), k_row, G.full + s);
     }
+    if (rank == 0) next_tile();  // claim + post the run's next tile (body_gemm2)
   } else if (tid == 32 && rank == 0) {
     if (gate) gate_spin(gate, *G.guard);  // the bounded waits measure the pipeline only
     tc_fence_after();
@@ -153,7 +155,22 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
   tc_fence_before();
   G.kb_used = g0 + nk;
   G.accum_used += 1;
-  cluster_sync_all();  // both halves written, both TMEMs read
+  cluster_sync_all();  // both halves written, both TMEMs read; the next tile posted
+}
+
+// A pair run of conv tiles (see PairTiles, gemm_body.cuh).
+template <class NextTile>
+__device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G,
+                                           const unsigned* gate, const PairTiles& run,
+                                           NextTile& next_tile) {
+  const ConvDesc* D = reinterpret_cast<const ConvDesc*>(c.args[0]);
+  long long blk = c.block;
+  for (;;) {
+    conv2_tile(D, static_cast<unsigned>(blk), tid, rank, G, gate, next_tile);
+    blk = *run.run_next;
+    if (blk < 0) break;
+    gate = nullptr;
+  }
 }
 
 }  // namespace gpuos_dev_impl

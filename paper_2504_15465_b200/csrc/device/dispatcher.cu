@@ -601,8 +601,22 @@ enum WorkerGo : int { kGoExit = 0, kGoOwn = 1, kGoPair = 2, kGoJoin = 3 };
 // second pair just starts a little later and overlaps its partner's epilogue.
 constexpr unsigned long long kSpreadNs = 4000;
 
+// A pair run (PairTiles, gemm_body.cuh): the leader's claim context for
+// GEMM / conv tiles claimed inside the body after the run's first tile.
+struct PairRun {
+  DevAtom* atom;                // atom the run may claim from (null: a single tile)
+  unsigned long long key;       // its resident key (sequence for claim_block)
+  long long lo;                 // its first block
+  unsigned count;               // its slices
+  unsigned ver;                 // the TPC's candidate-set version at the first claim
+  unsigned extra;               // tiles claimed inside the body (beyond the first)
+  unsigned pad;
+  long long next;               // posted next block, -1: end of run (leader writes both CTAs')
+};
+
 struct WorkerShared {
   RoundCmd rc;                  // this CTA's block for the round
+  PairRun run;                  // pair run state (leader) / posted next tile (both)
   RoundCmd join_rc;             // peer: pair tile posted by the leader
   unsigned long long t_start;
   unsigned long long join_full; // mbarrier (peer): leader posted join_rc
@@ -701,6 +715,49 @@ __device__ __forceinline__ long long claim_block(DevAtom* a, unsigned long long 
   return got ? static_cast<long long>(off) : -1;
 }
 
+// The leader's producer thread, after the last load of a pair tile: claim
+// the run's next tile and post it to both CTAs (PairTiles, gemm_body.cuh).
+// The run continues only while the TPC's candidate set is unchanged (no new
+// atom, fence or pause here since the first claim: otherwise the pair goes
+// back to full arbitration, which may pick a higher-priority atom) and, as
+// in the arbitration's spreading rule, only if no idle leader elsewhere
+// would start the tile sooner (some leader idle and the atom has fewer
+// tiles in flight than TPCs). Our own unfinished tile keeps the atom from
+// completing, so its slot cannot be recycled under the claim (no stale
+// case). A claimed tile is traced here; the run's tiles are counted done
+// with the first one (account_block, `extra`).
+struct NextTile {
+  const Params& p;
+  PairRun& run;
+  unsigned peer_next;  // shared::cluster address of the peer's run.next
+  int tpc;
+  unsigned sm;
+  __device__ __forceinline__ void operator()(bool stop = false) const {
+    long long nb = -1;
+    DevAtom* a = run.atom;
+    if (!stop && a != nullptr && ld_acquire_gpu(p.version + tpc) == run.ver) {
+      bool ok = true;
+      if (ld_relaxed_gpu(&p.ctl->idle_leaders) != 0u) {
+        const unsigned in_flight = static_cast<unsigned>(ld_relaxed_gpu64(&a->claim)) - ld_relaxed_gpu(&a->done);
+        const unsigned width = __popcll(ld_relaxed_gpu64(&a->mask[0])) + __popcll(ld_relaxed_gpu64(&a->mask[1]));
+        ok = in_flight >= width;
+      }
+      if (ok) {
+        bool stale = false;
+        unsigned got = 0;
+        const long long off = claim_block(a, run.key, run.count, 1u, p.ctl, stale, got);
+        if (off >= 0) {
+          nb = run.lo + off;
+          ++run.extra;
+          if (a->trace != nullptr) atomicAdd(a->trace + nb, 0x10000u + sm + 1u);
+        }
+      }
+    }
+    run.next = nb;
+    st_cluster_u64(peer_next, static_cast<unsigned long long>(nb));
+  }
+};
+
 // Warp 0 of the CTA that ran `rc`: record the block on its atom and, for the
 // atom's last block, publish the completion and retire its resident keys.
 // Returns 0 (more blocks to go), 1 (atom done) or 2 (atom done, and `rc`
@@ -728,7 +785,7 @@ __device__ __forceinline__ unsigned atom_exch_acq_rel32(unsigned* p, unsigned v)
 
 __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
                                              unsigned long long t_start, int tpc, unsigned sm,
-                                             unsigned rank, unsigned lane,
+                                             unsigned rank, unsigned lane, unsigned extra,
                                              unsigned long long& n_blocks,
                                              unsigned long long& busy,
                                              unsigned long long& touched_key) {
@@ -761,7 +818,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
     if (a->trace != nullptr)
       atomicAdd(a->trace + rc.cmd.block * rc.cmd.parts + rc.cmd.part, 0x10000u + sm + 1u);
     busy += t_end - t_start;
-    ++n_blocks;
+    n_blocks += 1u + extra;
     if (single) {
       // The body's output (and trace) precede the completion record; a
       // chain head fences after arming its successor (off its path).
@@ -783,7 +840,8 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       // acq_rel: this block's records (and the body's output stores, ordered
       // by the CTA barrier before this) precede the count; the last finisher
       // observes every other block's records.
-      last = atom_add_acq_rel32(&a->done, 1u) + 1u == rc.count;
+      // (A pair run counts its in-body tiles here too: `extra`.)
+      last = atom_add_acq_rel32(&a->done, 1u + extra) + 1u + extra == rc.count;
       if (last) {
         s_t1 = gtimer();  // every block has ended (each counted after its end)
         finisher_fields();
@@ -932,15 +990,16 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
 
 __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned rank,
                                          StreamPipe& pipe, GemmPipe& gemm, GemvPipe& gemv,
-                                         const DevAtom* atoms) {
+                                         const DevAtom* atoms, PairRun& run, const NextTile& nt) {
   // Only an early-started atom's blocks check its gate (weights first).
   const unsigned* gate = rc.gated ? &atoms[rc.slot].paused : nullptr;
+  const PairTiles tiles{&run.next};
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
     case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, gate); break;
-    case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm, gate); break;
+    case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm, gate, tiles, nt); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
-    case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm, gate); break;
+    case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm, gate, tiles, nt); break;
     default: break;
   }
 }
@@ -1019,6 +1078,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
   const unsigned peer_join_rc = map_rank(&sh.join_rc, 1);
   const unsigned peer_join_full = map_rank(&sh.join_full, 1);
   const unsigned leader_joined = map_rank(&sh.joined, 0);
+  const unsigned peer_run_next = map_rank(&sh.run.next, 1);
   unsigned joins = 0;  // pair tiles this CTA has run (join_full / joined parity)
   // Warp 0's draining state: the atom it last claimed from and the TPC's
   // candidate-set version at that time. While the version is unchanged no
@@ -1056,6 +1116,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
         cur_key = 0ull;
         cur_body = lane0_field(sh.rc.cmd.body, lane);
         go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
+        if (lane == 0) {
+          sh.run.atom = nullptr;  // a single tile: no pair run
+          sh.run.extra = 0u;
+        }
         if (go == kGoPair && cur_body != GPUOS_BODY_GEMV_BF16 && lane == 0) {
           if (atomicAdd(p.tc_busy + tpc, 1u) == 0u) atomicAdd(&p.ctl->tc_active, 1u);
           tc_hold = true;
@@ -1227,6 +1291,15 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
               const unsigned parts = sh.rc.cmd.parts;
               sh.rc.cmd.block = sh.rc.lo + off / parts;
               sh.rc.cmd.part = static_cast<unsigned>(off % parts);
+              // GEMM / conv tiles claimed by a leader start a pair run.
+              const unsigned b = sh.rc.cmd.body;
+              sh.run.atom = rank == 0 && !stale && (b == GPUOS_BODY_GEMM_BF16 || b == GPUOS_BODY_CONV_BF16)
+                                ? p.atoms + slot : nullptr;
+              sh.run.key = key;
+              sh.run.lo = sh.rc.lo;
+              sh.run.count = sh.rc.count;
+              sh.run.ver = ver;
+              sh.run.extra = 0u;
             }
             cur_key = stale ? 0ull : key;
             cur_slot = slot;
@@ -1315,7 +1388,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
     __syncthreads();
     const int go = sh.go;
     if (go == kGoExit) break;
-    run_body(sh.rc, tid, rank, pipe, gemm, gemv, p.atoms);  // pair tiles end with a cluster barrier
+    {
+      const NextTile nt{p, sh.run, peer_run_next, tpc, sm};
+      run_body(sh.rc, tid, rank, pipe, gemm, gemv, p.atoms, sh.run, nt);  // pair tiles end with a cluster barrier
+    }
     if (go == kGoPair || go == kGoJoin) ++joins;
     if (tc_hold && tid == 0) {
       if (atomicSub(p.tc_busy + tpc, 1u) == 1u) atomicSub(&p.ctl->tc_active, 1u);
@@ -1326,7 +1402,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
     // The leader records pair tiles (the peer's half is complete: cluster
     // barrier at the end of the body).
     if (warp == 0 && go != kGoJoin) {
-      const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, n_blocks, busy, sh.touched_key);
+      const unsigned extra = go == kGoPair ? lane0_field(sh.run.extra, lane) : 0u;
+      const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, extra, n_blocks, busy,
+                                     sh.touched_key);
       if (done) cur_key = 0ull;  // the atom is done: rescan rather than claim from it
       handoff = done == 2;
       __syncwarp();  // every lane has read sh.t_start / sh.rc before lane 0 rewrites them

@@ -311,15 +311,29 @@ __device__ __forceinline__ void epilogue_staged(const GemmPipe& G, int tid, unsi
   }
 }
 
+// A pair run: after the first tile (claimed by the dispatcher's arbitration)
+// the pair keeps claiming tiles of the same atom inside the body. The
+// leader's producer thread claims the next tile right after issuing the
+// current tile's last load (the claim's L2 round trip overlaps the last
+// stages and the epilogue) and posts it to both CTAs' `next` word; the
+// tile's closing cluster barrier publishes it (barrier.cluster arrive.release
+// / wait.acquire), so no extra handshake, arbitration, peer join or per-tile
+// accounting sits between two tiles of a run. `next_tile` (dispatcher.cu,
+// PairRun) returns the next absolute block or -1 (atom drained, or the TPC's
+// candidate set changed: the pair goes back to full arbitration).
+// `run_next`: this CTA's copy of the posted block.
+struct PairTiles {
+  volatile long long* run_next;
+};
+
 // Both CTAs of the pair, all threads; rank 0 is the leader.
 // `gate`: the atom's early-start gate (dispatcher.cu): while it is 1 the
 // tile loads its first stages of B (weights) but no A (the predecessor is
 // still producing the activations).
-__device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G,
-                                           const unsigned* gate) {
-  const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
+template <class NextTile>
+__device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int tid, unsigned rank,
+                                           GemmPipe& G, const unsigned* gate, NextTile& next_tile) {
   const unsigned m_tiles = D->m_tiles, n_tiles = D->n_tiles, n_tile = D->n_tile;
-  const unsigned blk = static_cast<unsigned>(c.block);
   // Grouped raster: blocks walk 8 M-tiles down an N column before moving
   // right, so ~150 concurrent tiles touch 8 A panels and ~18 B panels (fits
   // L2) instead of every A panel (8192^3: DRAM reads 3x the operands).
@@ -333,6 +347,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   const unsigned S = G.stages;
   const unsigned long long g0 = G.kb_used;
   if (S == 0) {  // host validated; never on the path
+    if (tid == 0 && rank == 0) next_tile(true);  // (ends the run)
     cluster_sync_all();
     return;
   }
@@ -375,6 +390,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
       tma_load_2d_pair(st, &D->a, kc, a_row, G.full + s);
       tma_load_2d_pair(st + kGemmABytes, &D->b, kc, b_row, G.full + s);
     }
+    if (rank == 0) next_tile();  // claim + post the run's next tile (both CTAs)
   } else if (tid == 32 && rank == 0) {
     if (gate) gate_spin(gate, *G.guard);  // the bounded waits measure the pipeline only
     // MMA issuer: one thread of the leader drives both SMs' tensor cores.
@@ -415,8 +431,23 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   G.kb_used = g0 + nk;
   G.accum_used += 1;
   // Both halves of the tile are written (and both TMEMs read) before the
-  // leader records the tile or issues the next tile's MMAs.
+  // leader records the tile or issues the next tile's MMAs; the posted next
+  // tile is visible in both CTAs after it.
   cluster_sync_all();
+}
+
+template <class NextTile>
+__device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned rank, GemmPipe& G,
+                                           const unsigned* gate, const PairTiles& run,
+                                           NextTile& next_tile) {
+  const GemmDesc* D = reinterpret_cast<const GemmDesc*>(c.args[0]);
+  long long blk = c.block;
+  for (;;) {
+    gemm2_tile(D, static_cast<unsigned>(blk), tid, rank, G, gate, next_tile);
+    blk = *run.run_next;
+    if (blk < 0) break;
+    gate = nullptr;  // (open: the run's first tile waited for it)
+  }
 }
 
 }  // namespace gpuos_dev_impl

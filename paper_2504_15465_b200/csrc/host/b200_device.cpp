@@ -4,6 +4,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <set>
 #include <thread>
 
 #include "gpuos/b200.hpp"
@@ -177,7 +178,84 @@ const B200Runtime::TensorBody& B200Runtime::tensor_body(const BodyRef& b) {
                               static_cast<int32_t>(st), GPUOS_CONV_OUT_BF16, &t.desc, &t.blocks, &po, &qo),
           "conv descriptor");
   }
-  return tensors_.emplace(key, t).first->second;
+  t.ref = b;
+  const TensorBody& out = tensors_.emplace(key, t).first->second;
+  tensor_of_desc_[reinterpret_cast<std::uint64_t>(out.desc)] = &out;
+  return out;
+}
+
+namespace {
+float bf16_to_float(std::uint16_t v) {
+  const std::uint32_t u = static_cast<std::uint32_t>(v) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+}  // namespace
+
+void B200Runtime::verify_tensor(const TensorBody& t, VerifyReport& rep) {
+  // Up to 48 sampled outputs per kernel, each recomputed in float64 from
+  // the operands read back from HBM (only the rows / windows it needs).
+  const BodyRef& b = t.ref;
+  std::uint64_t rng = mix64(reinterpret_cast<std::uint64_t>(t.desc));
+  auto next = [&](std::uint64_t n) { rng = mix64(rng); return n ? rng % n : 0ull; };
+  auto fetch = [&](const void* base, std::uint64_t elem, std::uint64_t n, std::vector<std::uint16_t>& out) {
+    out.resize(n);
+    check(gpuos_dev_copy(dev_, out.data(), static_cast<const std::uint16_t*>(base) + elem, n * 2, 2),
+          "verify download");
+  };
+  auto judge = [&](double got, double ref, double mag) {
+    ++rep.tensor_checked;
+    if (!(std::fabs(got - ref) <= std::ldexp(std::fabs(ref), -8) + 1e-5 * mag + 1e-6)) ++rep.tensor_bad;
+  };
+  std::vector<std::uint16_t> ra, rb, out1;
+  constexpr int kSamples = 48;
+  ++rep.tensor_kernels;
+  if (b.kind == BodyKind::GemmBf16 || b.kind == BodyKind::GemvBf16) {
+    const bool gemm = b.kind == BodyKind::GemmBf16;
+    const std::uint64_t M = gemm ? static_cast<std::uint64_t>(b.p0) : 1;
+    const std::uint64_t N = static_cast<std::uint64_t>(gemm ? b.p1 : b.p0);
+    const std::uint64_t K = static_cast<std::uint64_t>(gemm ? b.p2 : b.p1);
+    for (int i = 0; i < kSamples; ++i) {
+      const std::uint64_t m = next(M), n = next(N);
+      fetch(t.bufs[0], gemm ? m * K : n * K, K, ra);   // A row m / W row n
+      fetch(t.bufs[1], gemm ? n * K : 0, K, rb);       // B row n / x
+      fetch(t.bufs[2], gemm ? m * N + n : n, 1, out1);
+      double ref = 0, mag = 0;
+      for (std::uint64_t k = 0; k < K; ++k) {
+        const double p = static_cast<double>(bf16_to_float(ra[k])) * bf16_to_float(rb[k]);
+        ref += p;
+        mag += std::fabs(p);
+      }
+      judge(bf16_to_float(out1[0]), ref, mag);
+    }
+    return;
+  }
+  // conv: x [n, h, w, c], w [k, r, s, cb], y [n, P, Q, k] (NHWC, bf16)
+  const std::int64_t n = b.p0, h = b.p1, w = b.p2, c = b.param(3), k = b.param(4), r = b.param(5),
+                     sd = b.param(6), pad = b.param(7), st = std::max<std::int64_t>(1, b.param(8));
+  const std::int64_t cb = (c + 63) / 64 * 64;
+  const std::int64_t P = (h + 2 * pad - r) / st + 1, Q = (w + 2 * pad - sd) / st + 1;
+  for (int i = 0; i < kSamples / 4; ++i) {
+    const std::int64_t in = static_cast<std::int64_t>(next(n)), p = static_cast<std::int64_t>(next(P)),
+                       q = static_cast<std::int64_t>(next(Q)), kk = static_cast<std::int64_t>(next(k));
+    fetch(t.bufs[1], static_cast<std::uint64_t>(kk * r * sd * cb), static_cast<std::uint64_t>(r * sd * cb), rb);
+    double ref = 0, mag = 0;
+    for (std::int64_t rr = 0; rr < r; ++rr)
+      for (std::int64_t ss = 0; ss < sd; ++ss) {
+        const std::int64_t y = p * st - pad + rr, x = q * st - pad + ss;
+        if (y < 0 || y >= h || x < 0 || x >= w) continue;
+        fetch(t.bufs[0], static_cast<std::uint64_t>(((in * h + y) * w + x) * c), static_cast<std::uint64_t>(c), ra);
+        for (std::int64_t ci = 0; ci < c; ++ci) {
+          const double v = static_cast<double>(bf16_to_float(ra[ci])) *
+                           bf16_to_float(rb[static_cast<std::size_t>((rr * sd + ss) * cb + ci)]);
+          ref += v;
+          mag += std::fabs(v);
+        }
+      }
+    fetch(t.bufs[2], static_cast<std::uint64_t>(((in * P + p) * Q + q) * k + kk), 1, out1);
+    judge(bf16_to_float(out1[0]), ref, mag);
+  }
 }
 
 void B200Runtime::ensure_trace(KernelId kid, long blocks) {
@@ -355,6 +433,7 @@ VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs
   VerifyReport rep;
   // Chunks of each workspace that some executed block wrote.
   std::unordered_map<std::uint64_t, std::vector<char>> touched;  // args[1] -> chunks
+  std::set<std::uint64_t> verified;  // tensor descriptors already value-checked
   std::vector<std::uint32_t> trace;
   for (std::size_t k = 0; k < specs.size(); ++k) {
     if (k >= has_resolved_.size() || !has_resolved_[k]) continue;
@@ -369,6 +448,10 @@ VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs
     trace.assign(static_cast<std::size_t>(blocks * parts), 0u);
     check(gpuos_dev_copy(dev_, trace.data(), r.trace, blocks * parts * 4ull, 2), "trace download");
     std::vector<char>* tc = nullptr;
+    bool complete = true;  // every block of the kernel placed and run once
+    long covered = 0;
+    for (const auto& rg : pl.ranges) covered += rg.second - rg.first;
+    if (covered != blocks) complete = false;
     if (r.body == GPUOS_BODY_STREAM) {
       auto& v = touched[r.args[1]];
       v.resize(static_cast<std::size_t>(r.chunks), 0);
@@ -391,7 +474,14 @@ VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs
             ++rep.misplaced;
         }
         if (tc && whole) (*tc)[static_cast<std::size_t>(b % r.chunks)] = 1;
+        complete = complete && whole;
       }
+    }
+    // A tensor-core kernel every block of which ran: its output values.
+    if (complete && (r.body == GPUOS_BODY_GEMM_BF16 || r.body == GPUOS_BODY_GEMV_BF16 ||
+                     r.body == GPUOS_BODY_CONV_BF16)) {
+      const auto it = tensor_of_desc_.find(r.args[0]);
+      if (it != tensor_of_desc_.end() && verified.insert(r.args[0]).second) verify_tensor(*it->second, rep);
     }
   }
   // Body outputs against the CPU restatement.

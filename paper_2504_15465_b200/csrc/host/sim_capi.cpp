@@ -156,7 +156,8 @@ json verify_json(const VerifyReport& v) {
   return json{{"kernels", v.kernels},   {"blocks", v.blocks},
               {"missing", v.missing},   {"duplicated", v.duplicated},
               {"misplaced", v.misplaced}, {"bad_words", v.bad_words},
-              {"checked_words", v.checked_words}, {"ok", v.ok()}};
+              {"checked_words", v.checked_words}, {"tensor_kernels", v.tensor_kernels},
+              {"tensor_checked", v.tensor_checked}, {"tensor_bad", v.tensor_bad}, {"ok", v.ok()}};
 }
 
 }  // namespace

@@ -105,7 +105,28 @@ def cases() -> list[tuple[str, list[str]]]:
                                          "--set", "stealing=0", "--set", "dvfs=0"]))
     for seed in range(1, 13):
         out.append((f"random_{seed}", ["--config", f"scenarios/random_{seed}.json"]))
+    # The B200-form BASELINE configs the bench and the live runs use (short
+    # horizons): #1 fig7-b200, #5 one 8-tenant set per rank, #2 infer4 and
+    # #3 hybrid on random-init model kernel traces.
+    for name in B200_SCENARIOS:
+        out.append((name, ["--config", f"scenarios/{name}.json"]))
     return out
+
+
+def b200_scenarios() -> dict[str, dict]:
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_2504_15465_b200 import workloads
+
+    return {"fig7_b200_x10": workloads.fig7_b200(10.0, 2000.0),
+            "box8_rank0": workloads.tenant_set(0, 10.0, 500.0),
+            "box8_rank1": workloads.tenant_set(1, 10.0, 500.0),
+            "infer4_300ms": workloads.infer4(300.0),
+            "hybrid_300ms": workloads.hybrid(300.0)}
+
+
+B200_SCENARIOS = ("fig7_b200_x10", "box8_rank0", "box8_rank1", "infer4_300ms", "hybrid_300ms")
 
 
 def digest_cases() -> list[tuple[str, list[str]]]:
@@ -140,6 +161,9 @@ def main() -> None:
     for seed in range(1, 13):
         with open(os.path.join(HERE, "scenarios", f"random_{seed}.json"), "w") as f:
             json.dump(random_scenario(seed), f, indent=1)
+    for name, cfg in b200_scenarios().items():
+        with open(os.path.join(HERE, "scenarios", f"{name}.json"), "w") as f:
+            json.dump(cfg, f, separators=(",", ":"))
     write_gz(os.path.join(HERE, "vectors.jsonl.gz"), ref("ref_vectors", []))
     index = {}
     for name, args in cases():

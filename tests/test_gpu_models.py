@@ -29,6 +29,8 @@ def test_mirror_resnet50_and_bert_traces(api, cuda_device):
     v = r["verify"]
     assert v["ok"], v
     assert v["missing"] == v["duplicated"] == v["misplaced"] == 0
+    # conv / GEMM / GEMV outputs sampled against float64 (verify_tensor)
+    assert v["tensor_kernels"] > 0 and v["tensor_checked"] > 0 and v["tensor_bad"] == 0, v
     assert r["gpu_atoms"] == r["atoms"]["hp"] + r["atoms"]["be"] > 0
     replay = api.run({"scenario": {"config": cfg}, "backend": "replay", "log": True})
     assert r["log"] == replay["log"]
@@ -38,10 +40,14 @@ def test_mirror_resnet50_and_bert_traces(api, cuda_device):
 def test_live_model_configs_complete(api, cuda_device, name):
     cfg = workloads.infer4(150.0) if name == "infer4" else workloads.hybrid(150.0)
     req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
-           "timeline": True, "b200": {"chunk_cap": 256}, "set": {"block_revocation": True}}
+           "timeline": True, "verify": True, "b200": {"chunk_cap": 256, "trace": True},
+           "set": {"block_revocation": True}}
     with api.Session(req) as s:
         s.run()
         r = s.run()
+    v = r["verify"]
+    assert v["ok"], v
+    assert v["tensor_kernels"] > 0 and v["tensor_checked"] > 0, v
     for a in r["report"]["apps"]:
         assert a["completed"] > 0
         if a["high_priority"]:  # requests still in flight at the horizon are not counted

@@ -28,9 +28,21 @@ MIRROR = {
     "inf-train_2s": {"scenario": {"preset": "inf-train"}, "horizon_ms": 2000},
     "inf-inf_mps_like_1s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 1000, "policy": "mps_like"},
     "inf-inf_time_slice_1s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 1000, "policy": "time_slice"},
+    "inf-inf_mig_like_1s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 1000, "policy": "mig_like"},
+    "inf-inf_priority_only_1s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 1000,
+                                 "policy": "priority_only"},
+    "inf-inf_reef_like_1s": {"scenario": {"preset": "inf-inf"}, "horizon_ms": 1000, "policy": "reef_like"},
     "cli_smoke": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "cli_smoke.json")}},
     "random_7": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "random_7.json")}},
+    "random_3": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "random_3.json")}},
+    # B200-form BASELINE configs: #1 and one rank of #5 (STREAM bodies), #2
+    # and #3 on model traces (tensor-core bodies, values checked in float64).
+    "fig7_b200_x10": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "fig7_b200_x10.json")}},
+    "box8_rank0": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "box8_rank0.json")}},
+    "infer4_300ms": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "infer4_300ms.json")}},
+    "hybrid_300ms": {"scenario": {"config_path": os.path.join(GOLDEN, "scenarios", "hybrid_300ms.json")}},
 }
+TENSOR_CASES = {"infer4_300ms", "hybrid_300ms"}
 
 
 @pytest.mark.parametrize("name", sorted(MIRROR))
@@ -44,7 +56,10 @@ def test_mirror_executes_reference_schedule_on_b200(api, cuda_device, name):
     assert v["ok"], v
     assert v["missing"] == v["duplicated"] == v["misplaced"] == v["bad_words"] == 0
     assert r["gpu_atoms"] == r["atoms"]["hp"] + r["atoms"]["be"]
-    assert v["checked_words"] > 0
+    if name in TENSOR_CASES:
+        assert v["tensor_kernels"] > 0 and v["tensor_checked"] > 0 and v["tensor_bad"] == 0, v
+    else:
+        assert v["checked_words"] > 0
 
 
 def live_request(**kw):
