@@ -443,10 +443,15 @@ def right_sizing_summary(local: int, args) -> dict:
     r = rightsize.sweep(device=local, slip=1.04, quick=True, reps=2, workers_per_sm=args.workers_per_sm)
     return {"slip": r["slip"], "grid": r["grid"], "mean_capacity_savings": r["mean_capacity_savings"],
             "max_slowdown": r["max_slowdown"], "weighted_r2": r["weighted_r2"],
+            "b200_mean_capacity_savings": r["b200_mean_capacity_savings"],
+            "b200_max_slowdown": r["b200_max_slowdown"],
             "bodies": [{k: b[k] for k in ("body", "t_star", "slowdown", "capacity_savings", "r2")}
+                       | {"b200_t_star": b["b200"]["t_star"], "b200_slowdown": b["b200"]["slowdown"],
+                          "b200_capacity_savings": b["b200"]["capacity_savings"]}
                        for b in r["bodies"]],
             "note": "t* = choose_tpcs_wave(fit_scaling(l(1), l(74)), slip 1.04) on device-timed "
-                    "single-atom runs; slowdown = measured l(t*) / l(74)"}
+                    "single-atom runs (the reference's right-sizer); b200_t_star = the measured-curve "
+                    "chooser (l(1), l(37), plateau l(74)); slowdown = measured l(t*) / l(74)"}
 
 
 def policy_rows(local: int) -> dict:

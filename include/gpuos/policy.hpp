@@ -6,6 +6,7 @@
 // citations on each declaration point at the behaviour reproduced).
 #pragma once
 
+#include <algorithm>
 #include <compare>
 #include <map>
 #include <string>
@@ -91,6 +92,9 @@ class LatencyPredictor {
   int next_ordinal(int queue_id);
   bool has_any(const OperatorKey& key) const;
   std::string dump_store(int queue_id) const;
+  // Warm start (B200 sessions): take `other`'s learned tables, queue ids
+  // mapped through `queue_map` (other's id -> this predictor's id).
+  void absorb(const LatencyPredictor& other, const std::map<int, int>& queue_map);
 
  private:
   struct Ewma {
@@ -113,7 +117,20 @@ struct ScalingFit {
   double m_ns = 0.0;
   double b_ns = 0.0;
   bool valid = false;
+  // B200 extension (0 in the reference): latency floor of the measured
+  // curve, l(t) = max(m/t + b, floor_ns). HBM-bound bodies plateau once
+  // enough TPCs saturate the memory system (STREAM from 48 of 74 TPCs);
+  // the two-point l = m/t + b cannot see that and keeps them at full width.
+  double floor_ns = 0.0;
+  double at(int t) const {
+    const double l = m_ns / t + b_ns;
+    return floor_ns > 0.0 ? std::max(l, floor_ns) : l;
+  }
 };
+// Three-point fit of a measured curve (B200 extension): m, b through
+// (1, l1) and (t_mid, l_mid), floor = the full-width latency lT, so the
+// model follows the compute-bound slope and stops at the measured plateau.
+ScalingFit fit_scaling_plateau(Duration l1, int t_mid, Duration l_mid, Duration lT, int T);
 
 ScalingFit fit_scaling(Duration l1, Duration lT, int T);      // rightsizer.cpp:8-19
 int filter_cap(long total_blocks, int occupancy_per_tpc,
@@ -123,12 +140,33 @@ int choose_tpcs(const ScalingFit& fit, int t_alloc, double slip_k,
 int choose_tpcs_wave(const ScalingFit& fit, int t_alloc, double slip_k,
                      long blocks, int occ);                     // :40-60
 
-enum class ProbeDecision { UseFull, ProbeOneTpc, UseFit };
+enum class ProbeDecision { UseFull, ProbeOneTpc, UseFit, ProbeWidth };
 
 struct RightsizerConfig {
   double slip_k = 1.1;
   int probe_depth_limit = 1;
+  // B200 extension (off = the reference's two probes and l = m/t + b): the
+  // right-sizer works on the MEASURED curve -- after the full-width and
+  // one-TPC probes it bisects the width (ProbeWidth, on quiet dispatches
+  // like the one-TPC probe) between the widest measured width that misses
+  // the slip budget and the narrowest one that meets it, and picks the
+  // narrowest measured width within slip_k of the widest width's latency.
+  // HBM-bound bodies, whose latency plateaus once enough TPCs saturate the
+  // memory system, get the plateau's start; compute-bound ones keep the
+  // width their measured speed-up needs.
+  bool plateau = false;
 };
+
+// The measured-curve search (RightsizerConfig::plateau) over samples
+// (width, mean latency): `ok` = narrowest width within slip_k of the widest
+// sampled width's latency, `probe` = next width to measure (0: converged --
+// the bracket [widest miss, ok] is within max(1, ok / 16) TPCs).
+struct MeasuredChoice {
+  int ok = 0;
+  int probe = 0;
+  int widest = 0;
+};
+MeasuredChoice choose_measured(const std::map<int, double>& mean_ns, double slip_k);
 
 // full width -> one-TPC probe -> fitted width (rightsizer.cpp:62-103).
 class Rightsizer {
@@ -140,6 +178,13 @@ class Rightsizer {
   void observe(const OperatorKey& key, int tpc_count, Duration latency);
   const ScalingFit* fit_for(const OperatorKey& key) const;
   int choose(const OperatorKey& key, int t_alloc, long blocks, int occ) const;
+  // Plateau mode: the next width to measure for `key` (0: none due).
+  int probe_width(const OperatorKey& key) const;
+  // Plateau mode: the measured-curve state of `key` (ok = 0: no samples).
+  MeasuredChoice measured(const OperatorKey& key) const;
+  // Warm start (B200 sessions): take `other`'s curves, queue ids mapped
+  // through `queue_map` (other's id -> this scheduler's id).
+  void absorb(const Rightsizer& other, const std::map<int, int>& queue_map);
   double weighted_r_squared(long* included = nullptr) const;
   const RightsizerConfig& config() const { return cfg_; }
 

@@ -84,6 +84,8 @@ struct RunHooks {
   std::function<void(const AtomCompletion&)> on_complete;
   // Called with the finished scheduler before the report is assembled.
   std::function<void(const Scheduler&)> on_finish;
+  // Called with the new scheduler before it runs (warm start).
+  std::function<void(Scheduler&)> on_start;
 };
 
 // Runs `cfg` on an existing device (its topology must match cfg.topo's TPC

@@ -243,6 +243,16 @@ int gpuos_dev_get_stats(struct gpuos_dev* dev, gpuos_dev_stats* out);
 int gpuos_dev_gemm_desc(struct gpuos_dev* dev, const void* a, const void* b, void* c,
                         int64_t m, int64_t n, int64_t k, int64_t ldc, uint32_t flags,
                         void** desc, int64_t* blocks, int32_t* tile_m, int32_t* tile_n);
+/* Split-K variant: k_splits > 1 also splits K (shapes with few output tiles
+ * and a long K, e.g. weight gradients): block b = (tile b % tiles, K split
+ * b / tiles), *blocks = tiles x splits; each split adds its fp32 tile into
+ * the tile's accumulator (vector float reductions in L2, so the fp32 sum
+ * order is the splits' arrival order) and the tile's last split writes C.
+ * One run of a descriptor at a time. k_splits <= 1 is gpuos_dev_gemm_desc.*/
+int gpuos_dev_gemm_desc_splitk(struct gpuos_dev* dev, const void* a, const void* b, void* c,
+                               int64_t m, int64_t n, int64_t k, int64_t ldc, uint32_t flags,
+                               int32_t k_splits, void** desc, int64_t* blocks, int32_t* tile_m,
+                               int32_t* tile_n);
 
 /* GEMV body descriptor (GPUOS_BODY_GEMV_BF16): y[N] = W[N,K] . x[K] with
  * bf16 W and x (16-byte aligned, K % 8 == 0), fp32 accumulation, fp32 y

@@ -60,6 +60,21 @@ int gpuos_choose_tpcs(double m_ns, double b_ns, int32_t valid, int32_t t_alloc,
 int gpuos_choose_tpcs_wave(double m_ns, double b_ns, int32_t valid,
                            int32_t t_alloc, double slip_k, int64_t blocks,
                            int32_t occ);
+/* B200 extension of the right-sizer (RightsizerConfig::plateau): the
+ * three-point measured-curve fit l(t) = max(m/t + b, floor) through
+ * (1, l1), (t_mid, l_mid) and the full-width plateau lT, and the wave-aware
+ * chooser on that model (floor_ns = 0 is exactly gpuos_choose_tpcs_wave). */
+int gpuos_fit_scaling_plateau(int64_t l1_ns, int32_t t_mid, int64_t l_mid_ns, int64_t lT_ns,
+                              int32_t T, double* m_ns, double* b_ns, double* floor_ns,
+                              int32_t* valid);
+int gpuos_choose_tpcs_wave_floor(double m_ns, double b_ns, double floor_ns, int32_t valid,
+                                 int32_t t_alloc, double slip_k, int64_t blocks, int32_t occ);
+/* The measured-curve right-sizer's search step (RightsizerConfig::plateau):
+ * n samples (width t[i], mean latency l_ns[i]) -> *ok = narrowest width
+ * within slip_k of the widest sample's latency, *probe = next width to
+ * measure (0: converged). */
+int gpuos_choose_measured(const int32_t* t, const double* l_ns, int32_t n, double slip_k,
+                          int32_t* ok, int32_t* probe);
 /* Block latency and the closed-form lone-kernel latency at frequency f_mhz
  * for the default A100-like table (540..1410 MHz). */
 int64_t gpuos_block_latency(int64_t d0_ns, double s, int32_t f_mhz);

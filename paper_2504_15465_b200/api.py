@@ -46,12 +46,13 @@ DEV_SYMBOLS = [
     "gpuos_dev_get_stats", "gpuos_dev_alloc", "gpuos_dev_free", "gpuos_dev_copy",
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask", "gpuos_dev_set_tpc_owner",
-    "gpuos_dev_gemm_desc", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
+    "gpuos_dev_gemm_desc", "gpuos_dev_gemm_desc_splitk", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
     "gpuos_free_text", "gpuos_sim_last_error", "gpuos_plan_atoms", "gpuos_should_atomize",
     "gpuos_filter_cap", "gpuos_fit_scaling", "gpuos_choose_tpcs", "gpuos_choose_tpcs_wave",
+    "gpuos_fit_scaling_plateau", "gpuos_choose_tpcs_wave_floor", "gpuos_choose_measured",
     "gpuos_block_latency", "gpuos_reference_kernel_latency", "gpuos_select_frequency",
     "gpuos_predictor_replay", "gpuos_probe_dispatch",
 ]
@@ -152,6 +153,9 @@ def library() -> C.CDLL:
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                           C.c_uint32, C.POINTER(P), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "gpuos_dev_gemm_desc_splitk": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                                 C.c_uint32, C.c_int32, C.POINTER(P), C.POINTER(C.c_int64),
+                                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "gpuos_session_open": (C.c_int, [C.c_char_p, C.POINTER(P)]),
         "gpuos_session_run": (C.c_int, [P, C.c_char_p, C.POINTER(C.c_void_p)]),
         "gpuos_session_close": (C.c_int, [P]),
@@ -166,6 +170,13 @@ def library() -> C.CDLL:
                                         C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
         "gpuos_choose_tpcs": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_int32,
                                         C.c_double, C.c_int32]),
+        "gpuos_fit_scaling_plateau": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int32,
+                                                C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+        "gpuos_choose_tpcs_wave_floor": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_int32, C.c_int32,
+                                                   C.c_double, C.c_int64, C.c_int32]),
+        "gpuos_choose_measured": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_double), C.c_int32, C.c_double,
+                                            C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "gpuos_choose_tpcs_wave": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_int32,
                                              C.c_double, C.c_int64, C.c_int32]),
         "gpuos_block_latency": (C.c_int64, [C.c_int64, C.c_double, C.c_int32]),
@@ -325,14 +336,15 @@ class Device:
             raise
 
     def gemm_desc(self, a: int, b: int, c: int, m: int, n: int, k: int, ldc: int | None = None,
-                  bf16_out: bool = False) -> tuple[int, int, int, int]:
+                  bf16_out: bool = False, k_splits: int = 1) -> tuple[int, int, int, int]:
         """Descriptor for GPUOS_BODY_GEMM_BF16 (C = A . B^T on tcgen05):
-        returns (device pointer for args[0], grid blocks, tile_m, tile_n)."""
+        returns (device pointer for args[0], grid blocks, tile_m, tile_n).
+        k_splits > 1: split-K (gpuos_dev_gemm_desc_splitk)."""
         desc, blocks = C.c_void_p(), C.c_int64()
         tm, tn = C.c_int32(), C.c_int32()
-        self._check(self._lib.gpuos_dev_gemm_desc(
+        self._check(self._lib.gpuos_dev_gemm_desc_splitk(
             self._h, a, b, c, m, n, k, n if ldc is None else ldc,
-            GPUOS_GEMM_OUT_BF16 if bf16_out else 0, C.byref(desc), C.byref(blocks),
+            GPUOS_GEMM_OUT_BF16 if bf16_out else 0, k_splits, C.byref(desc), C.byref(blocks),
             C.byref(tm), C.byref(tn)))
         return desc.value, blocks.value, tm.value, tn.value
 
@@ -447,6 +459,34 @@ def choose_tpcs(m: float, b: float, valid: bool, t_alloc: int, slip: float, cap:
 def choose_tpcs_wave(m: float, b: float, valid: bool, t_alloc: int, slip: float, blocks: int,
                      occ: int) -> int:
     return library().gpuos_choose_tpcs_wave(m, b, int(valid), t_alloc, slip, blocks, occ)
+
+
+def fit_scaling_plateau(l1: int, t_mid: int, l_mid: int, lT: int, T: int) -> tuple[float, float, float, bool]:
+    """B200 measured-curve fit: l(t) = max(m/t + b, floor) (policy.hpp)."""
+    m, b, fl, v = C.c_double(), C.c_double(), C.c_double(), C.c_int32()
+    rc = library().gpuos_fit_scaling_plateau(l1, t_mid, l_mid, lT, T, C.byref(m), C.byref(b), C.byref(fl),
+                                             C.byref(v))
+    if rc != 0:
+        raise GpuosError(rc, library().gpuos_sim_last_error().decode())
+    return m.value, b.value, fl.value, bool(v.value)
+
+
+def choose_tpcs_wave_floor(m: float, b: float, floor: float, valid: bool, t_alloc: int, slip: float,
+                           blocks: int, occ: int) -> int:
+    return library().gpuos_choose_tpcs_wave_floor(m, b, floor, int(valid), t_alloc, slip, blocks, occ)
+
+
+def choose_measured(samples: dict[int, float], slip: float) -> tuple[int, int]:
+    """Measured-curve right-sizer step: (narrowest width within the slip, next
+    width to probe or 0) from {width: mean latency ns}."""
+    ts = sorted(samples)
+    t_arr = (C.c_int32 * max(1, len(ts)))(*ts)
+    l_arr = (C.c_double * max(1, len(ts)))(*[float(samples[t]) for t in ts])
+    ok, probe = C.c_int32(), C.c_int32()
+    rc = library().gpuos_choose_measured(t_arr, l_arr, len(ts), slip, C.byref(ok), C.byref(probe))
+    if rc != 0:
+        raise GpuosError(rc, library().gpuos_sim_last_error().decode())
+    return ok.value, probe.value
 
 
 def block_latency(d0: int, s: float, f: int) -> int:

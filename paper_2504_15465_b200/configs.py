@@ -50,23 +50,35 @@ def per_app(results: list[dict]) -> dict[str, dict]:
 
 
 def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0,
-        chain: bool = True) -> dict[str, Any]:
+        chain: bool = True, knobs: dict | None = None, b200: dict | None = None,
+        cfg: dict | None = None) -> dict[str, Any]:
     """chain: HP tenants' dependent kernels chained on the device
-    (SchedulerConfig::chain_launches) instead of host-paced launches."""
-    cfg = workloads.infer4(horizon_ms) if name == "infer4" else workloads.hybrid(horizon_ms)
+    (SchedulerConfig::chain_launches) instead of host-paced launches.
+    knobs: extra scheduler knobs (apply_knob names) for the stacked and
+    alone runs; b200: extra B200Options."""
+    if cfg is None:
+        cfg = workloads.infer4(horizon_ms) if name == "infer4" else workloads.hybrid(horizon_ms)
+    knob_set = {"block_revocation": True, "chain_launches": chain} | (knobs or {})
+    # warm_start: the scheduler keeps what it learned (predictor, right-sizer
+    # curves) from one run to the next, like the long-lived process it is;
+    # every measured run, stacked, alone or static, starts warm.
     req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
-           "b200": {"chunk_cap": 256, "device": device},
-           "set": {"block_revocation": True, "chain_launches": chain}}
+           "b200": {"chunk_cap": 256, "device": device} | (b200 or {}),
+           "set": knob_set, "warm_start": True}
     with api.Session(req) as s:
         s.run()
         s.run()  # warm: operands allocated, predictor and right-sizer state learned
         live = [s.run() for _ in range(reps)]
+        rsz = [r.get("rightsizer") for r in live if r.get("rightsizer")]
         alone = {}
         for a in cfg["apps"]:
             others = [b["id"] for b in cfg["apps"] if b["id"] != a["id"]]
             solo = workloads.without_apps(cfg, *others)
             alone[a["id"]] = per_app([s.run(scenario={"config": solo}) for _ in range(reps)])[a["id"]]
-        static = per_app([s.run(scenario={"config": workloads.variant(cfg, stealing=False, atomizer=False)})
+        # The equivalent static partition: each tenant on its quota, no
+        # stealing, no atomization, no right-sizing.
+        static = per_app([s.run(scenario={"config": workloads.variant(cfg, stealing=False, atomizer=False)},
+                                set=dict(knob_set, rightsizer=False))
                           for _ in range(reps)])
     stacked = per_app(live)
     apps = {}
@@ -82,8 +94,14 @@ def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0,
         if a["priority"] == "be" and st.get("per_s") and sp.get("per_s"):
             row["throughput_vs_static"] = st["per_s"] / sp["per_s"]
         apps[i] = row
-    return {"config": name, "horizon_ms": horizon_ms, "reps": reps, "chain_launches": chain, "apps": apps,
-            "tpc_utilization": sum(r["report"]["tpc_utilization"] for r in live) / len(live)}
+    out = {"config": name, "horizon_ms": horizon_ms, "reps": reps, "chain_launches": chain, "apps": apps,
+           "knobs": knob_set, "tpc_utilization": sum(r["report"]["tpc_utilization"] for r in live) / len(live)}
+    if rsz:
+        used = sum(x["tpc_ns_used"] for x in rsz)
+        unsized = sum(x["tpc_ns_unsized"] for x in rsz)
+        out["rightsizer"] = {"capacity_savings": 1.0 - used / unsized if unsized else 0.0,
+                             "plateau": rsz[0]["plateau"]}
+    return out
 
 
 POLICIES = ["full_system", "mps_like", "mig_like", "time_slice", "priority_only", "reef_like"]

@@ -2452,6 +2452,12 @@ int gpuos_dev_host_alloc(gpuos_dev* d, uint64_t bytes, void** ptr) {
 int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int64_t m,
                         int64_t n, int64_t k, int64_t ldc, uint32_t flags, void** desc,
                         int64_t* blocks, int32_t* tile_m, int32_t* tile_n) {
+  return gpuos_dev_gemm_desc_splitk(d, a, b, c, m, n, k, ldc, flags, 1, desc, blocks, tile_m, tile_n);
+}
+
+int gpuos_dev_gemm_desc_splitk(gpuos_dev* d, const void* a, const void* b, void* c, int64_t m,
+                               int64_t n, int64_t k, int64_t ldc, uint32_t flags, int32_t k_splits,
+                               void** desc, int64_t* blocks, int32_t* tile_m, int32_t* tile_n) {
   if (!d || !a || !b || !c || !desc) return fail(GPUOS_E_CONFIG, "null argument");
   if (m <= 0 || n <= 0 || k <= 0 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return fail(GPUOS_E_CONFIG, "GEMM shape out of range");
@@ -2490,13 +2496,33 @@ int gpuos_dev_gemm_desc(gpuos_dev* d, const void* a, const void* b, void* c, int
   h.n_tile = n_tile;
   h.flags = flags & kGemmOutBf16;
   h.timing = nullptr;
+  // Split-K (wide-K, few-tile shapes such as weight gradients): K slices
+  // per split rounded so every split is non-empty.
+  const unsigned nk = static_cast<unsigned>((k + kGemmBK - 1) / kGemmBK);
+  const unsigned want = std::clamp<unsigned>(k_splits <= 0 ? 1u : static_cast<unsigned>(k_splits), 1u, nk);
+  h.tiles = h.m_tiles * h.n_tiles;
+  h.k_slices_per_split = (nk + want - 1) / want;
+  h.splits = (nk + h.k_slices_per_split - 1) / h.k_slices_per_split;
+  if (h.splits == 1) h.k_slices_per_split = nk;
+  // One allocation: descriptor, split counters and fp32 tile accumulators
+  // (both zeroed; the last split of a tile re-zeroes its accumulator).
+  const size_t counters_off = (sizeof(GemmDesc) + 255) & ~size_t{255};
+  const size_t partial_off = (counters_off + 4ull * h.tiles + 255) & ~size_t{255};
+  const size_t acc_bytes = 4ull * h.tiles * kGemmTile * static_cast<size_t>(n_tile);
+  const size_t total = h.splits > 1 ? partial_off + acc_bytes : sizeof(GemmDesc);
   void* p = nullptr;
   CUDA_TRY(cudaSetDevice(d->device));
-  CUDA_TRY(cudaMallocAsync(&p, sizeof(GemmDesc), d->s_side));
+  CUDA_TRY(cudaMallocAsync(&p, total, d->s_side));
+  if (h.splits > 1) {
+    h.arrivals = reinterpret_cast<unsigned*>(static_cast<char*>(p) + counters_off);
+    h.partial = reinterpret_cast<float*>(static_cast<char*>(p) + partial_off);
+    CUDA_TRY(cudaMemsetAsync(h.arrivals, 0, 4ull * h.tiles, d->s_side));
+    CUDA_TRY(cudaMemsetAsync(h.partial, 0, acc_bytes, d->s_side));
+  }
   CUDA_TRY(cudaMemcpyAsync(p, &h, sizeof(GemmDesc), cudaMemcpyHostToDevice, d->s_side));
   CUDA_TRY(cudaStreamSynchronize(d->s_side));
   *desc = p;
-  if (blocks) *blocks = static_cast<int64_t>(h.m_tiles) * h.n_tiles;
+  if (blocks) *blocks = static_cast<int64_t>(h.tiles) * h.splits;
   if (tile_m) *tile_m = static_cast<int32_t>(kGemmTile);
   if (tile_n) *tile_n = static_cast<int32_t>(n_tile);
   return GPUOS_OK;

@@ -52,6 +52,17 @@ struct alignas(128) GemmDesc {
   unsigned m, n, k, ldc;
   unsigned m_tiles, n_tiles, n_tile, flags;  // n_tile: 64, 128 or 256 columns; flags bit 0: bf16 output
   unsigned long long* timing;    // optional: 4 globaltimer stamps per tile (profiling)
+  // Split-K (splits > 1): block b = (tile b % tiles, K split b / tiles); a
+  // split adds its fp32 tile into the tile's accumulator with vector float
+  // reductions in L2 (red.global.add.v4.f32: every split's adds run in
+  // parallel; the order of the fp32 sums is the arrival order), and the
+  // tile's last split (self-resetting arrival counter) converts the
+  // accumulator to C and zeroes it for the next run. (A first cut stored
+  // per-split partials and let the last split sum them: that reduction
+  // read splits x 64-256 KB in one CTA, 0.8 ms for 98 splits.)
+  unsigned splits, k_slices_per_split, tiles, pad0;
+  float* partial;                // [tiles][256][n_tile] fp32 accumulators (zero between runs)
+  unsigned* arrivals;            // [tiles]
 };
 constexpr unsigned kGemmOutBf16 = 1u;
 
@@ -330,10 +341,65 @@ struct PairTiles {
 // `gate`: the atom's early-start gate (dispatcher.cu): while it is 1 the
 // tile loads its first stages of B (weights) but no A (the predecessor is
 // still producing the activations).
+// Split-K: this CTA's 128 accumulator rows added into the tile's fp32
+// accumulator in L2 (all 8 warps; warp w: TMEM lanes 32 (w % 4).., column
+// half w / 4), 16 bytes per reduction.
+__device__ __forceinline__ void epilogue_red_f32(const GemmPipe& G, int tid, float* acc, unsigned cta_row0,
+                                                 unsigned n_tile) {
+  const int warp = tid >> 5, lane = tid & 31;
+  const unsigned q = static_cast<unsigned>(warp & 3), h = static_cast<unsigned>(warp >> 2);
+  constexpr unsigned half = kGemmTile / 2;
+  float* row = acc + static_cast<size_t>(cta_row0 + q * 32u + static_cast<unsigned>(lane)) * n_tile;
+#pragma unroll 1
+  for (unsigned pc = 0; pc < half; pc += 32) {
+    const unsigned col0 = h * half + pc;
+    if (col0 >= n_tile) break;  // warp-uniform: narrow tiles
+    unsigned v[32];
+    tmem_ld32(G.tmem + ((q * 32u) << 16) + col0, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + col0 + 4 * i),
+                   "f"(__uint_as_float(v[4 * i])), "f"(__uint_as_float(v[4 * i + 1])),
+                   "f"(__uint_as_float(v[4 * i + 2])), "f"(__uint_as_float(v[4 * i + 3]))
+                   : "memory");
+  }
+}
+
+// Split-K, the tile's last split (leader CTA, 256 threads): the fp32
+// accumulator -> C (ragged edges masked), and back to zero for the next run.
+// 16 threads per row of 64 columns, 16 bytes each.
+__device__ __forceinline__ void gemm_reduce_tile(const GemmDesc* D, unsigned tile, unsigned mt, unsigned nt,
+                                                 int tid) {
+  const unsigned n_tile = D->n_tile;
+  float* base = D->partial + static_cast<size_t>(tile) * kGemmTile * n_tile;
+  const bool bf16_out = (D->flags & kGemmOutBf16) != 0;
+  const unsigned vecs = n_tile / 4;               // float4 per row
+  const unsigned per_pass = 256u / vecs;          // rows per pass
+#pragma unroll 4
+  for (unsigned r0 = 0; r0 < kGemmTile; r0 += per_pass) {
+    const unsigned r = r0 + static_cast<unsigned>(tid) / vecs;
+    const unsigned c4 = static_cast<unsigned>(tid) % vecs;
+    float4* src = reinterpret_cast<float4*>(base + static_cast<size_t>(r) * n_tile + 4 * c4);
+    const float4 v = __ldcg(src);
+    __stcg(src, make_float4(0.f, 0.f, 0.f, 0.f));
+    const unsigned grow = mt * kGemmTile + r, gcol = nt * n_tile + 4 * c4;
+    if (grow >= D->m || gcol >= D->n) continue;
+    const float a4[4] = {v.x, v.y, v.z, v.w};
+    const size_t o = static_cast<size_t>(grow) * D->ldc + gcol;
+    for (unsigned e = 0; e < 4 && gcol + e < D->n; ++e) {
+      if (bf16_out) reinterpret_cast<__nv_bfloat16*>(D->c)[o + e] = __float2bfloat16_rn(a4[e]);
+      else reinterpret_cast<float*>(D->c)[o + e] = a4[e];
+    }
+  }
+}
+
 template <class NextTile>
-__device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int tid, unsigned rank,
+__device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk_in, int tid, unsigned rank,
                                            GemmPipe& G, const unsigned* gate, NextTile& next_tile) {
   const unsigned m_tiles = D->m_tiles, n_tiles = D->n_tiles, n_tile = D->n_tile;
+  // Split-K: this block's output tile and K range.
+  const unsigned blk = D->splits > 1 ? blk_in % D->tiles : blk_in;
+  const unsigned split = D->splits > 1 ? blk_in / D->tiles : 0u;
   // Grouped raster: blocks walk 8 M-tiles down an N column before moving
   // right, so ~150 concurrent tiles touch 8 A panels and ~18 B panels (fits
   // L2) instead of every A panel (8192^3: DRAM reads 3x the operands).
@@ -343,7 +409,10 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int 
   const unsigned gm = m_tiles - first_m < kGroup ? m_tiles - first_m : kGroup;
   const unsigned in_group = blk - group * kGroup * n_tiles;
   const unsigned mt = first_m + in_group % gm, nt = in_group / gm;
-  const unsigned nk = (D->k + kGemmBK - 1) / kGemmBK;
+  const unsigned nk_all = (D->k + kGemmBK - 1) / kGemmBK;
+  const unsigned kb0 = split * D->k_slices_per_split;
+  const unsigned nk = D->splits > 1 ? (kb0 + D->k_slices_per_split < nk_all ? D->k_slices_per_split : nk_all - kb0)
+                                    : nk_all;
   const unsigned S = G.stages;
   const unsigned long long g0 = G.kb_used;
   if (S == 0) {  // host validated; never on the path
@@ -352,7 +421,7 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int 
     return;
   }
 
-  unsigned long long* tm = D->timing != nullptr && rank == 0 ? D->timing + 4ull * blk : nullptr;
+  unsigned long long* tm = D->timing != nullptr && rank == 0 ? D->timing + 4ull * blk_in : nullptr;
   if (tm && tid == 0) tm[0] = gtimer();
   if (tid == 0) {
     // TMA producer (both CTAs). The descriptor was written by a host copy
@@ -369,7 +438,7 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int 
       const unsigned s = static_cast<unsigned>((g0 + j) % S);
       if ((g0 + j) / S >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>(((g0 + j) / S - 1) & 1), *G.guard);
       if (rank == 0) mbar_expect_tx(G.full + s, tx);
-      tma_load_2d_pair(G.tiles + s * kGemmStageBytes + kGemmABytes, &D->b, static_cast<int>(j * kGemmBK),
+      tma_load_2d_pair(G.tiles + s * kGemmStageBytes + kGemmABytes, &D->b, static_cast<int>((kb0 + j) * kGemmBK),
                        b_row, G.full + s);
     }
     if (gate) {
@@ -378,7 +447,7 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int 
     }
     for (unsigned j = 0; j < pre; ++j)
       tma_load_2d_pair(G.tiles + static_cast<unsigned>((g0 + j) % S) * kGemmStageBytes, &D->a,
-                       static_cast<int>(j * kGemmBK), a_row, G.full + static_cast<unsigned>((g0 + j) % S));
+                       static_cast<int>((kb0 + j) * kGemmBK), a_row, G.full + static_cast<unsigned>((g0 + j) % S));
     for (unsigned j = pre; j < nk; ++j) {
       const unsigned long long k = g0 + j;
       const unsigned s = static_cast<unsigned>(k % S);
@@ -386,7 +455,7 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int 
       if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1), *G.guard);
       unsigned char* st = G.tiles + s * kGemmStageBytes;
       if (rank == 0) mbar_expect_tx(G.full + s, tx);
-      const int kc = static_cast<int>(j * kGemmBK);
+      const int kc = static_cast<int>((kb0 + j) * kGemmBK);
       tma_load_2d_pair(st, &D->a, kc, a_row, G.full + s);
       tma_load_2d_pair(st + kGemmABytes, &D->b, kc, b_row, G.full + s);
     }
@@ -420,9 +489,15 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int 
   tc_fence_after();
   if (tm && tid == 0) tm[2] = gtimer();
   const unsigned col0 = nt * n_tile;
-  epilogue_staged(G, tid, mt * kGemmTile + rank * kGemmHalf, col0, D->m,
-                  D->n - col0 < n_tile ? D->n : col0 + n_tile, D->ldc,
-                  (D->flags & kGemmOutBf16) != 0, reinterpret_cast<void*>(D->c));
+  if (D->splits > 1) {
+    // This split's contribution, added into the tile's fp32 accumulator.
+    epilogue_red_f32(G, tid, D->partial + static_cast<size_t>(blk) * kGemmTile * n_tile, rank * kGemmHalf,
+                     n_tile);
+  } else {
+    epilogue_staged(G, tid, mt * kGemmTile + rank * kGemmHalf, col0, D->m,
+                    D->n - col0 < n_tile ? D->n : col0 + n_tile, D->ldc,
+                    (D->flags & kGemmOutBf16) != 0, reinterpret_cast<void*>(D->c));
+  }
   tc_fence_before();  // the next tile's MMAs overwrite this accumulator
   if (tm) {
     __syncthreads();
@@ -434,6 +509,22 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk, int 
   // leader records the tile or issues the next tile's MMAs; the posted next
   // tile is visible in both CTAs after it.
   cluster_sync_all();
+  if (D->splits > 1 && rank == 0) {
+    // Split-K: the tile's last split converts the accumulator.
+    __shared__ int last_split;
+    if (tid == 0) {
+      __threadfence();  // this split's reductions (both CTAs, via the cluster barrier)
+      const unsigned before = atomicAdd(D->arrivals + blk, 1u);
+      last_split = before == D->splits - 1;
+      if (last_split) {
+        __threadfence();
+        D->arrivals[blk] = 0u;  // ready for the kernel's next run
+      }
+    }
+    __syncthreads();
+    if (last_split) gemm_reduce_tile(D, blk, mt, nt, tid);
+    __syncthreads();  // (last_split is read before thread 0 rewrites it)
+  }
 }
 
 template <class NextTile>

@@ -145,12 +145,14 @@ const B200Runtime::TensorBody& B200Runtime::tensor_body(const BodyRef& b) {
   };
   if (b.kind == BodyKind::GemmBf16) {
     const std::int64_t M = b.p0, N = b.p1, K = b.p2;
-    if (M <= 0 || N <= 0 || K <= 0) throw ConfigError("gemm_bf16 needs p = [M, N, K]");
+    if (M <= 0 || N <= 0 || K <= 0) throw ConfigError("gemm_bf16 needs p = [M, N, K(, k_splits)]");
     void* A = tensor(static_cast<std::uint64_t>(M) * K, true);
     void* B = tensor(static_cast<std::uint64_t>(N) * K, true);
     void* C = tensor(static_cast<std::uint64_t>(M) * N, false);
     int32_t tm = 0, tn = 0;
-    check(gpuos_dev_gemm_desc(dev_, A, B, C, M, N, K, N, GPUOS_GEMM_OUT_BF16, &t.desc, &t.blocks, &tm, &tn),
+    const std::int64_t splits = std::max<std::int64_t>(1, b.param(3));  // p[3]: split-K
+    check(gpuos_dev_gemm_desc_splitk(dev_, A, B, C, M, N, K, N, GPUOS_GEMM_OUT_BF16, static_cast<int32_t>(splits),
+                                     &t.desc, &t.blocks, &tm, &tn),
           "gemm descriptor");
   } else if (b.kind == BodyKind::GemvBf16) {
     const std::int64_t N = b.p0, K = b.p1, splits = std::max<std::int64_t>(1, b.p2);

@@ -143,6 +143,20 @@ ScalingFit fit_scaling(Duration l1, Duration lT, int T) {  // :8-19
   return f;
 }
 
+ScalingFit fit_scaling_plateau(Duration l1, int t_mid, Duration l_mid, Duration lT, int T) {
+  if (t_mid < 2) throw ConfigError("plateau fit needs t_mid >= 2");
+  if (l1 <= 0 || l_mid <= 0 || lT <= 0) throw ConfigError("fit latencies must be > 0");
+  if (l1 < l_mid) return fit_scaling(l1, lT, T);  // no speed-up to 1..t_mid: two-point
+  ScalingFit f = fit_scaling(l1, l_mid, t_mid);
+  if (f.b_ns < 0.0) {  // (super-linear to t_mid: pure m/t through the mid point)
+    f.b_ns = 0.0;
+    f.m_ns = static_cast<double>(l_mid) * t_mid;
+  }
+  f.valid = true;
+  f.floor_ns = static_cast<double>(std::min(l_mid, lT));
+  return f;
+}
+
 int filter_cap(long total_blocks, int occupancy_per_tpc, int total_tpcs) {  // :21-26
   if (total_blocks < 1 || occupancy_per_tpc < 1)
     throw ConfigError("filter_cap inputs must be >= 1");
@@ -169,14 +183,23 @@ int choose_tpcs_wave(const ScalingFit& fit, int t_alloc, double slip_k,
   if (!fit.valid) return t_full;
   const long max_waves = (blocks + occ - 1) / occ;
   if (fit.m_ns <= 0.0) return static_cast<int>(std::min<long>(t_full, max_waves));
-  const double budget = slip_k * (fit.m_ns / t_full + fit.b_ns);
+  // (floor_ns is 0 for the reference's fit: at(t) = m/t + b exactly.)
+  const double budget = slip_k * fit.at(t_full);
+  // Measured plateau well above the compute curve at full width: the body
+  // is bound by a shared resource (HBM), not by its TPCs' throughput, so
+  // block waves do not set its latency -- the smallest width whose compute
+  // part fits the budget is where the plateau starts.
+  if (fit.floor_ns > 0.0 && fit.floor_ns > 1.02 * (fit.m_ns / t_full + fit.b_ns) && budget > fit.b_ns) {
+    const int t = static_cast<int>(std::ceil(fit.m_ns / (budget - fit.b_ns)));
+    return std::clamp(t, 1, t_full);
+  }
   // Walk wave counts upward; only breakpoint widths change latency.
   int chosen = t_full;
   for (long waves = 1; waves <= max_waves; ++waves) {
     const long per_wave = (blocks + waves - 1) / waves;
     const int width = static_cast<int>((per_wave + occ - 1) / occ);
     if (width > t_full) continue;
-    if (fit.m_ns / width + fit.b_ns > budget) break;
+    if (fit.at(width) > budget) break;
     chosen = width;
     if (width == 1) break;
   }
@@ -187,9 +210,61 @@ ProbeDecision Rightsizer::decide(const OperatorKey& key, int queue_depth,
                                  bool slo_slack_ok) const {  // :62-72
   auto it = curves_.find(key);
   if (it == curves_.end() || !it->second.has_wide) return ProbeDecision::UseFull;
-  if (it->second.has_one) return ProbeDecision::UseFit;
   const bool quiet = queue_depth < cfg_.probe_depth_limit && slo_slack_ok;
+  if (cfg_.plateau) {  // measured-curve search (B200 extension)
+    const MeasuredChoice mc = measured(key);
+    if (mc.probe == 0 || !quiet) return ProbeDecision::UseFit;
+    return mc.probe == 1 ? ProbeDecision::ProbeOneTpc : ProbeDecision::ProbeWidth;
+  }
+  if (it->second.has_one) return ProbeDecision::UseFit;
   return quiet ? ProbeDecision::ProbeOneTpc : ProbeDecision::UseFull;
+}
+
+MeasuredChoice choose_measured(const std::map<int, double>& mean_ns, double slip_k) {
+  MeasuredChoice mc;
+  if (mean_ns.empty()) return mc;
+  mc.widest = mean_ns.rbegin()->first;
+  const double budget = slip_k * mean_ns.rbegin()->second;
+  mc.ok = mc.widest;
+  for (const auto& [t, l] : mean_ns)
+    if (l <= budget) {
+      mc.ok = t;
+      break;
+    }
+  int miss = 0;  // widest measured width below `ok` that misses the budget
+  for (const auto& [t, l] : mean_ns)
+    if (t < mc.ok && l > budget) miss = t;
+  if (mc.ok == 1) return mc;
+  if (miss == 0) {
+    mc.probe = 1;  // the one-TPC probe first (as the reference)
+    return mc;
+  }
+  if (mc.ok - miss > std::max(1, mc.ok / 16)) mc.probe = (miss + mc.ok) / 2;
+  return mc;
+}
+
+MeasuredChoice Rightsizer::measured(const OperatorKey& key) const {
+  auto it = curves_.find(key);
+  if (it == curves_.end()) return {};
+  std::map<int, double> mean;
+  for (const auto& [t, s] : it->second.samples) mean[t] = s.first / static_cast<double>(s.second);
+  return choose_measured(mean, cfg_.slip_k);
+}
+
+int Rightsizer::probe_width(const OperatorKey& key) const { return measured(key).probe; }
+
+void Rightsizer::absorb(const Rightsizer& other, const std::map<int, int>& queue_map) {
+  for (const auto& [key, c] : other.curves_) {
+    const auto q = queue_map.find(key.queue_id);
+    if (q != queue_map.end()) curves_[OperatorKey{q->second, key.ordinal}] = c;
+  }
+}
+
+void LatencyPredictor::absorb(const LatencyPredictor& other, const std::map<int, int>& queue_map) {
+  for (const auto& [key, table] : other.tables_) {
+    const auto q = queue_map.find(key.queue_id);
+    if (q != queue_map.end()) tables_[OperatorKey{q->second, key.ordinal}] = table;
+  }
 }
 
 void Rightsizer::observe(const OperatorKey& key, int tpc_count,
@@ -218,6 +293,10 @@ const ScalingFit* Rightsizer::fit_for(const OperatorKey& key) const {  // :92-96
 
 int Rightsizer::choose(const OperatorKey& key, int t_alloc, long blocks,
                        int occ) const {  // :98-103
+  if (cfg_.plateau) {  // measured-curve mode: the narrowest width within the slip
+    const MeasuredChoice mc = measured(key);
+    if (mc.ok > 0) return std::clamp(mc.ok, 1, std::min(t_alloc, filter_cap(blocks, occ, t_alloc)));
+  }
   const ScalingFit* f = fit_for(key);
   if (f == nullptr) return std::min(t_alloc, filter_cap(blocks, occ, t_alloc));
   return choose_tpcs_wave(*f, t_alloc, cfg_.slip_k, blocks, occ);
@@ -231,7 +310,7 @@ double r_squared(const ScalingFit& fit,
   mean /= static_cast<double>(points.size());
   double res = 0.0, tot = 0.0;
   for (const auto& [t, l] : points) {
-    const double model = fit.m_ns / t + fit.b_ns;
+    const double model = fit.at(t);
     res += (l - model) * (l - model);
     tot += (l - mean) * (l - mean);
   }

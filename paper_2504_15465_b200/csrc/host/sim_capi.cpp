@@ -87,6 +87,8 @@ void apply_knob(ScenarioConfig& c, const std::string& k, const json& v) {
   else if (k == "max_outstanding_atoms") s.max_outstanding_atoms = v.get<int>();
   else if (k == "slip_k") s.rightsizer.slip_k = v.get<double>();
   else if (k == "probe_depth_limit") s.rightsizer.probe_depth_limit = v.get<int>();
+  else if (k == "rightsizer_plateau") s.rightsizer.plateau = flag();
+  else if (k == "rightsize_hp") s.rightsize_hp = flag();
   else if (k == "dvfs_slip_k") s.dvfs.slip_k = v.get<double>();
   else if (k == "ewma_beta") s.predictor.ewma_beta = v.get<double>();
   else if (k == "default_unknown_us") s.predictor.default_unknown = duration_from_us(v.get<double>());
@@ -166,6 +168,14 @@ struct gpuos_session {
   json request;
   std::string backend;  // replay | b200 | mirror
   std::unique_ptr<B200Device> b200;
+  // Warm start ("warm_start": true): what the last run's scheduler learned
+  // (predictor tables, right-sizer curves), keyed back to app ids.
+  struct Learned {
+    LatencyPredictor pred;
+    Rightsizer rs;
+    std::vector<std::string> apps;
+  };
+  std::unique_ptr<Learned> learned;
 };
 
 namespace {
@@ -200,7 +210,44 @@ std::string run_session(gpuos_session* s, const json& overrides) {
           << '\n';
     };
   }
+  double rs_used = 0.0, rs_unsized = 0.0;
+  const bool warm = merged.value("warm_start", false);
+  std::vector<std::string> app_ids;
+  for (const AppWorkload& a : cfg.apps) app_ids.push_back(a.spec.app_id);
+  if (warm && s->learned) {
+    hooks.on_start = [&](Scheduler& sc) {
+      std::map<int, int> qmap;  // learned app index -> this run's index, by app id
+      for (std::size_t i = 0; i < s->learned->apps.size(); ++i)
+        for (std::size_t j = 0; j < app_ids.size(); ++j)
+          if (s->learned->apps[i] == app_ids[j]) qmap[static_cast<int>(i)] = static_cast<int>(j);
+      sc.warm_start(s->learned->pred, s->learned->rs, qmap);
+    };
+  }
   hooks.on_finish = [&](const Scheduler& sc) {
+    if (warm) {
+      // Merge: keep what earlier runs learned for apps absent from this one.
+      auto next = std::make_unique<gpuos_session::Learned>(
+          gpuos_session::Learned{LatencyPredictor(cfg.sched.predictor), Rightsizer(cfg.sched.rightsizer), {}});
+      std::vector<std::string> ids = s->learned ? s->learned->apps : std::vector<std::string>{};
+      for (const std::string& id : app_ids)
+        if (std::find(ids.begin(), ids.end(), id) == ids.end()) ids.push_back(id);
+      auto map_to = [&](const std::vector<std::string>& from) {
+        std::map<int, int> m;
+        for (std::size_t i = 0; i < from.size(); ++i)
+          m[static_cast<int>(i)] = static_cast<int>(std::find(ids.begin(), ids.end(), from[i]) - ids.begin());
+        return m;
+      };
+      if (s->learned) {
+        next->pred.absorb(s->learned->pred, map_to(s->learned->apps));
+        next->rs.absorb(s->learned->rs, map_to(s->learned->apps));
+      }
+      next->pred.absorb(sc.predictor(), map_to(app_ids));
+      next->rs.absorb(sc.rightsizer(), map_to(app_ids));
+      next->apps = ids;
+      s->learned = std::move(next);
+    }
+    rs_used = sc.rightsized_tpc_ns();
+    rs_unsized = sc.unsized_tpc_ns();
     app_atoms.assign(sc.app_count(), 0);
     for (const PredictionLogEntry& e : sc.prediction_log()) {
       (e.high_priority ? hp_atoms : be_atoms) += 1;
@@ -325,6 +372,10 @@ std::string run_session(gpuos_session* s, const json& overrides) {
     throw ConfigError("backend must be replay, b200 or mirror");
   }
   out["report"] = json::parse(res.report.to_json());
+  if (cfg.sched.rightsizer_enabled)
+    out["rightsizer"] = json{{"tpc_ns_used", rs_used}, {"tpc_ns_unsized", rs_unsized},
+                             {"capacity_savings", rs_unsized > 0.0 ? 1.0 - rs_used / rs_unsized : 0.0},
+                             {"plateau", cfg.sched.rightsizer.plateau}};
   if (want_requests) out["request_log"] = res.request_log;
   if (want_log) out["log"] = log.str();
   out["atoms"] = json{{"hp", hp_atoms}, {"be", be_atoms}, {"per_app", app_atoms}};
@@ -522,6 +573,40 @@ int gpuos_choose_tpcs_wave(double m, double b, int32_t valid, int32_t t_alloc, d
   int r = -2;
   guarded([&] { r = choose_tpcs_wave(ScalingFit{m, b, valid != 0}, t_alloc, slip, blocks, occ); });
   return r;
+}
+
+int gpuos_fit_scaling_plateau(int64_t l1, int32_t t_mid, int64_t l_mid, int64_t lT, int32_t T, double* m,
+                              double* b, double* floor_ns, int32_t* valid) {
+  return guarded([&] {
+    const ScalingFit f = fit_scaling_plateau(l1, t_mid, l_mid, lT, T);
+    *m = f.m_ns;
+    *b = f.b_ns;
+    *floor_ns = f.floor_ns;
+    *valid = f.valid ? 1 : 0;
+  });
+}
+
+int gpuos_choose_tpcs_wave_floor(double m, double b, double floor_ns, int32_t valid, int32_t t_alloc,
+                                 double slip, int64_t blocks, int32_t occ) {
+  int r = -2;
+  guarded([&] {
+    ScalingFit f{m, b, valid != 0};
+    f.floor_ns = floor_ns;
+    r = choose_tpcs_wave(f, t_alloc, slip, blocks, occ);
+  });
+  return r;
+}
+
+int gpuos_choose_measured(const int32_t* t, const double* l_ns, int32_t n, double slip_k, int32_t* ok,
+                          int32_t* probe) {
+  return guarded([&] {
+    if ((n > 0 && (!t || !l_ns)) || !ok || !probe) throw ConfigError("null argument");
+    std::map<int, double> mean;
+    for (int32_t i = 0; i < n; ++i) mean[t[i]] = l_ns[i];
+    const MeasuredChoice mc = choose_measured(mean, slip_k);
+    *ok = mc.ok;
+    *probe = mc.probe;
+  });
 }
 
 int64_t gpuos_block_latency(int64_t d0, double s, int32_t f) {

@@ -44,8 +44,23 @@ def conv_blocks(n, h, w, c, k, r, s, pad, stride) -> tuple[int, int, int]:
     return math.ceil(n * P * Q / 256) * math.ceil(k / n_tile(k)), P, Q
 
 
-def gemm_blocks(m, n, k) -> int:
-    return math.ceil(m / 256) * math.ceil(n / n_tile(n))
+def gemm_splits(k, splits) -> int:
+    """Effective K splits of gpuos_dev_gemm_desc_splitk (every split non-empty)."""
+    nk = math.ceil(k / 64)
+    per = math.ceil(nk / max(1, min(splits, nk)))
+    return math.ceil(nk / per)
+
+
+def gemm_blocks(m, n, k, splits=1) -> int:
+    return math.ceil(m / 256) * math.ceil(n / n_tile(n)) * gemm_splits(k, splits)
+
+
+def wgrad_splits(m, n, k, target=296) -> int:
+    """Split-K for a weight gradient (few output tiles, K = n P Q): enough
+    splits for `target` blocks (two waves of the 148 worker pairs), each
+    split at least 32 K steps of 64."""
+    tiles = math.ceil(m / 256) * math.ceil(n / n_tile(n))
+    return max(1, min(math.ceil(target / tiles), math.ceil(k / 64) // 32))
 
 
 def gemv_blocks(n, k, splits) -> int:
@@ -75,11 +90,12 @@ class Builder:
             "body": {"kind": "conv_bf16", "ws": self._next(), "p": [n, h, w, c, k, r, s, pad, stride]}})
         return P, Q
 
-    def gemm(self, m, n, k) -> None:
+    def gemm(self, m, n, k, splits=1) -> None:
+        sp = gemm_splits(k, splits)
         self.kernels.append({
-            "blocks": gemm_blocks(m, n, k),
-            "block_us": round(2.0 * 256 * n_tile(n) * k / (TPC_TFLOPS * 1e6), 3), "s": 0.9, "occ": 2,
-            "body": {"kind": "gemm_bf16", "ws": self._next(), "p": [m, n, k]}})
+            "blocks": gemm_blocks(m, n, k, sp),
+            "block_us": round(2.0 * 256 * n_tile(n) * k / sp / (TPC_TFLOPS * 1e6), 3), "s": 0.9, "occ": 2,
+            "body": {"kind": "gemm_bf16", "ws": self._next(), "p": [m, n, k] + ([sp] if sp > 1 else [])}})
 
     def gemv(self, n, k, splits=1) -> None:
         """occ 1: HBM-bound, so the occupancy filter (blocks / occ TPCs at
@@ -142,8 +158,15 @@ def resnet50_infer(batch: int = 1, ws_base: int = 0) -> list[dict]:
 
 def resnet50_train(batch: int = 64, ws_base: int = 0) -> list[dict]:
     """Forward, backward (for every conv: data-gradient conv of the same
-    FLOPs and weight-gradient GEMM [k, r s c] reduced over n p q), ReLU/BN
-    backward elementwise, and an SGD-momentum update over 25.6 M fp32 params."""
+    FLOPs and weight-gradient GEMM reduced over n p q), ReLU/BN backward
+    elementwise, and an SGD-momentum update over 25.6 M fp32 params.
+
+    The weight gradient dW[k, r s c] = dY^T . X_col has few output tiles and
+    a K of n P Q (up to 800 K at batch 64): it is computed transposed,
+    dW^T[r s c, k] (M = r s c, N = k: a 64-wide UMMA N for k = 64), with
+    split-K over n P Q -- as cuDNN does -- so it spreads over the TPCs
+    instead of 13 tiles running 8 ms each on 7 TPCs (round-2 measurement,
+    tools/train_breakdown.py)."""
     b = Builder(ws_base)
     convs = _resnet_forward(b, batch)
     b.gemm(batch, 1000, 2048)
@@ -152,7 +175,8 @@ def resnet50_train(batch: int = 64, ws_base: int = 0) -> list[dict]:
         P = (h + 2 * pad - r) // stride + 1
         if c >= 64:                                      # no data gradient for the stem input
             b.conv(n, P, P, k, c, r, s, (r - 1) // 2, 1)  # dgrad (same FLOPs as forward)
-        b.gemm(k, r * s * math.ceil(c / 64) * 64, n * P * P)  # wgrad
+        m_w, n_w, k_w = r * s * c, k, n * P * P              # (stem: its 8 padded input channels)
+        b.gemm(m_w, n_w, k_w, wgrad_splits(m_w, n_w, k_w))    # wgrad (transposed, split-K)
         b.stream(n * P * P * k * 2 * 3)                  # BN / ReLU backward
     b.stream(25_600_000 * 4 * 5)                         # SGD with momentum: w, g, m read; w, m written
     return b.kernels

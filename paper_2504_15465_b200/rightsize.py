@@ -13,7 +13,12 @@ C ABI (the same functions the gpuos:: Rightsizer calls):
   R^2 of the fit over every measured t                 rightsizer.cpp:105-119
 
 and l(t*) is measured to report the real slowdown against the full width and
-the capacity saved (1 - t*/74). occ = blocks a TPC advances at once: 2W
+the capacity saved (1 - t*/74). Beside it, the B200 measured-curve chooser
+(RightsizerConfig::plateau, the live scheduler's mode) runs its search on
+the same body: from l(74) and l(1) it bisects the width, measuring what it
+asks for, and picks the narrowest measured width within the slip of l(74)
+-- HBM-bound bodies, whose latency stops falling once enough TPCs saturate
+the memory system, get the width where the plateau starts instead of 74. occ = blocks a TPC advances at once: 2W
 worker slots for 1-SM bodies (STREAM); 1 for pair bodies (GEMM, GEMV): a
 TPC has one pair of tensor cores, which its W pairs share.
 
@@ -91,6 +96,16 @@ def default_bodies(dev: api.Device, torch, keep: list) -> list[Body]:
         keep.append(("desc", desc))
         out.append(Body(f"gemm_bf16 {m}x{n}x{k}", api.GPUOS_BODY_GEMM_BF16, [desc], blocks, 1,
                         f"{2 * m * n * k / 1e9:.1f} GFLOP"))
+    # ResNet-50 training-batch 3x3 convolutions (stage 2 and stage 3), NHWC
+    for (cn, h, w_, c, kk) in ((64, 28, 28, 128, 128), (64, 14, 14, 256, 256)):
+        x, wt = bf16(cn, h, w_, c), bf16(kk, 3, 3, c)
+        yv = torch.empty(cn, h, w_, kk, device="cuda", dtype=torch.bfloat16)
+        keep.append(yv)
+        desc, blocks, P, Q = dev.conv_desc(x.data_ptr(), wt.data_ptr(), yv.data_ptr(), cn, h, w_, c, kk, 3, 3,
+                                           1, 1, bf16_out=True)
+        keep.append(("desc", desc))
+        out.append(Body(f"conv_bf16 n{cn} {h}x{w_}x{c} k{kk} 3x3", api.GPUOS_BODY_CONV_BF16, [desc], blocks, 1,
+                        f"{2 * cn * P * Q * kk * 9 * c / 1e9:.1f} GFLOP"))
     n, k = 28672, 4096  # Llama-3-8B gate+up projection at batch 1
     w, x = bf16(n, k), bf16(k)
     y = torch.zeros(n, device="cuda")
@@ -127,6 +142,19 @@ def sweep(device: int = 0, slip: float = 1.04, quick: bool = False, reps: int = 
             t_star = api.choose_tpcs_wave(m, b, valid, FULL, slip, body.blocks, body.occ)
             if t_star not in lat:
                 lat[t_star] = atom_latency_ns(dev, body, t_star, reps)
+            # The live scheduler's measured-curve search (RightsizerConfig::
+            # plateau), run on this body: starting from the full-width and
+            # one-TPC probes, measure the width it asks for until it converges.
+            seen = {FULL: lat[FULL], 1: lat[1]}
+            probes = []
+            while True:
+                t_b200, probe = api.choose_measured(seen, slip)
+                if probe == 0 or len(probes) >= 8:
+                    break
+                if probe not in lat:
+                    lat[probe] = atom_latency_ns(dev, body, probe, reps)
+                seen[probe] = lat[probe]
+                probes.append(probe)
             rows.append({
                 "body": body.name, "work": body.work, "blocks": body.blocks, "occ": body.occ,
                 "latency_us": {str(t): round(v / 1e3, 2) for t, v in sorted(lat.items())},
@@ -134,6 +162,9 @@ def sweep(device: int = 0, slip: float = 1.04, quick: bool = False, reps: int = 
                 "r2": r2, "t_star": t_star,
                 "slowdown": lat[t_star] / lat[FULL],
                 "capacity_savings": 1.0 - t_star / FULL,
+                "b200": {"probes": probes,
+                         "t_star": t_b200, "slowdown": lat[t_b200] / lat[FULL],
+                         "capacity_savings": 1.0 - t_b200 / FULL},
             })
         for item in keep:
             if isinstance(item, tuple):
@@ -148,6 +179,8 @@ def sweep(device: int = 0, slip: float = 1.04, quick: bool = False, reps: int = 
         "slip": slip, "grid": grid, "reps": reps, "bodies": rows,
         "mean_capacity_savings": statistics.mean(r["capacity_savings"] for r in rows),
         "max_slowdown": max(r["slowdown"] for r in rows),
+        "b200_mean_capacity_savings": statistics.mean(r["b200"]["capacity_savings"] for r in rows),
+        "b200_max_slowdown": max(r["b200"]["slowdown"] for r in rows),
         "weighted_r2": (sum(r["r2"] * exec_time(r) for r in rows if r["r2"] is not None) / wsum)
         if wsum else None,
     }

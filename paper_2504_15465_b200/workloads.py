@@ -122,12 +122,15 @@ def infer4(horizon_ms: float = 2000.0, rps: tuple = (120.0, 120.0, 40.0, 40.0),
 
 
 def hybrid(horizon_ms: float = 2000.0, tokens_per_s: float = 60.0, slo_ms: float = 25.0,
-           train_batch: int = 64, tpcs: int = 74) -> dict:
+           train_batch: int = 256, tpcs: int = 74) -> dict:
     """BASELINE config #3, hybrid stacking: Llama-3-8B bf16 decode at batch 1
     (latency-critical, Poisson token requests, one request = one token's 258
     kernels over 15 GB of weights) with ResNet-50 training (best-effort,
-    closed loop, forward + backward + SGD) on one B200; mid-kernel
-    reallocation through TPC stealing, atomization and block revocation."""
+    closed loop, forward + backward + SGD, batch 256 -- the per-GPU ImageNet
+    batch; at batch 64 most kernels have too few tiles to use more than
+    the tenant's quota: 1.26x from 37 to 74 TPCs alone vs 1.52x at 256,
+    tools/train_breakdown.py) on one B200; mid-kernel reallocation through
+    TPC stealing, atomization and block revocation."""
     from . import models
 
     return {

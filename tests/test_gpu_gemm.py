@@ -155,3 +155,42 @@ def test_gemm_batch_large(api, cuda_device):
     tflops = 2 * m * n * k / (ms * 1e-3) / 1e12
     print(f"batch GEMM 4096^3: {ms:.3f} ms, {tflops:.0f} TFLOP/s")
     assert tflops > 100  # sanity: the tensor-core path ran
+
+
+@pytest.mark.parametrize("m,n,k,splits,bf16_out,workers", [
+    (576, 64, 12544, 6, True, 2),     # stage-1 3x3 weight gradient shape (transposed), 64-wide tiles
+    (300, 200, 4160, 5, False, 2),    # ragged M / N, K split unevenly (65 slices over 5 splits)
+    (1024, 512, 8192, 16, False, 1),  # 1 worker per SM
+    (256, 1000, 2048, 3, True, 2),
+])
+def test_gemm_split_k_matches_reference(api, cuda_device, m, n, k, splits, bf16_out, workers):
+    """Split-K GEMM (gpuos_dev_gemm_desc_splitk): block b = (tile b % tiles,
+    split b / tiles); the tile's last split sums the fp32 partials in split
+    order. Random atoms over random TPC sets, run twice (the arrival
+    counters reset themselves), every block exactly once."""
+    import torch
+
+    a, b, ref = operands(torch, m, n, k, seed=m + n + k + splits)
+    rng = random.Random(splits)
+    with api.Device(workers_per_sm=workers) as dev:
+        c = torch.full((m, n), float("nan"), device="cuda",
+                       dtype=torch.bfloat16 if bf16_out else torch.float32)
+        desc, blocks, tm, tn = dev.gemm_desc(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k,
+                                             bf16_out=bf16_out, k_splits=splits)
+        tiles = -(-m // tm) * -(-n // tn)
+        nk = -(-k // 64)
+        per = -(-nk // splits)
+        assert blocks == tiles * -(-nk // per)
+        for rep in range(2):
+            c.fill_(float("nan"))
+            trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+            atoms = random_atoms(rng, blocks, min(blocks, 9))
+            run_atoms(api, dev, atoms, workers, api.GPUOS_BODY_GEMM_BF16, [desc], trace=trace.data_ptr())
+            torch.cuda.synchronize()
+            tr = trace.cpu().numpy().view(np.uint32)
+            assert ((tr >> 16) == 1).all(), "a block did not run exactly once"
+            sm = (tr & 0xFFFF).astype(np.int64) - 1
+            for lo, hi, tpcs, _ in atoms:
+                assert set((sm[lo:hi] >> 1).tolist()) <= set(tpcs)
+            check(c, ref, bf16_out)
+        dev.free(desc)

@@ -1,0 +1,36 @@
+"""Config #3 (hybrid decode + training) under scheduler variants: decode p99
+vs alone and training throughput vs its static partition per variant.
+
+    python tools/hybrid_variants.py [--horizon-ms 1000] [--reps 3] [--only A,B]"""
+import argparse
+import json
+import sys
+
+sys.path.insert(0, ".")
+from paper_2504_15465_b200 import configs  # noqa: E402
+
+RS = {"rightsizer": True, "rightsizer_plateau": True, "dvfs": False}
+VARIANTS = {
+    "A": ({}, {}),
+    "B": (RS, {}),
+    "C": (dict(RS, slip_k=1.04), {}),
+    "D": (dict(RS, slip_k=1.2), {}),
+}
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--horizon-ms", type=float, default=1000.0)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--only", default=",".join(VARIANTS))
+ap.add_argument("--config", default="hybrid")
+args = ap.parse_args()
+for name in args.only.split(","):
+    knobs, b200 = VARIANTS[name]
+    r = configs.run(args.config, horizon_ms=args.horizon_ms, reps=args.reps, knobs=knobs, b200=b200)
+    row = {"variant": name, "knobs": knobs, "b200": b200, "tpc_utilization": r["tpc_utilization"],
+           "rightsizer": r.get("rightsizer")}
+    for app, a in r["apps"].items():
+        row[app] = {k: a.get(k) for k in ("p99_vs_alone", "throughput_vs_static", "slo_attainment")}
+        row[app].update({"p99_ms": a["stacked"].get("p99_ms"), "alone_p99": a["alone"].get("p99_ms"),
+                         "per_s": a["stacked"].get("per_s"), "static_per_s": a["static"].get("per_s"),
+                         "alone_per_s": a["alone"].get("per_s")})
+    print(json.dumps(row), flush=True)
