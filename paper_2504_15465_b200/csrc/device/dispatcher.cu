@@ -602,7 +602,7 @@ enum WorkerGo : int { kGoExit = 0, kGoOwn = 1, kGoPair = 2, kGoJoin = 3 };
 constexpr unsigned long long kSpreadNs = 4000;
 
 // A pair run (PairTiles, gemm_body.cuh): the leader's claim context for
-// GEMM / conv tiles claimed inside the body after the run's first tile.
+// GEMM / conv / GEMV tiles claimed inside the body after the run's first tile.
 struct PairRun {
   DevAtom* atom;                // atom the run may claim from (null: a single tile)
   unsigned long long key;       // its resident key (sequence for claim_block)
@@ -610,7 +610,7 @@ struct PairRun {
   unsigned count;               // its slices
   unsigned ver;                 // the TPC's candidate-set version at the first claim
   unsigned extra;               // tiles claimed inside the body (beyond the first)
-  unsigned pad;
+  unsigned spread;              // GEMM / conv: the spreading rule applies (not GEMV)
   long long next;               // posted next block, -1: end of run (leader writes both CTAs')
 };
 
@@ -737,7 +737,7 @@ struct NextTile {
     DevAtom* a = run.atom;
     if (!stop && a != nullptr && ld_acquire_gpu(p.version + tpc) == run.ver) {
       bool ok = true;
-      if (ld_relaxed_gpu(&p.ctl->idle_leaders) != 0u) {
+      if (run.spread && ld_relaxed_gpu(&p.ctl->idle_leaders) != 0u) {
         const unsigned in_flight = static_cast<unsigned>(ld_relaxed_gpu64(&a->claim)) - ld_relaxed_gpu(&a->done);
         const unsigned width = __popcll(ld_relaxed_gpu64(&a->mask[0])) + __popcll(ld_relaxed_gpu64(&a->mask[1]));
         ok = in_flight >= width;
@@ -996,7 +996,7 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
   const PairTiles tiles{&run.next};
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
-    case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, gate); break;
+    case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, gate, tiles, nt); break;
     case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm, gate, tiles, nt); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
     case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm, gate, tiles, nt); break;
@@ -1291,10 +1291,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
               const unsigned parts = sh.rc.cmd.parts;
               sh.rc.cmd.block = sh.rc.lo + off / parts;
               sh.rc.cmd.part = static_cast<unsigned>(off % parts);
-              // GEMM / conv tiles claimed by a leader start a pair run.
+              // Pair tiles (GEMM / conv / GEMV) claimed by a leader start a
+              // pair run; GEMV runs skip the spreading rule (HBM-bound: both
+              // pairs of a TPC stream at once).
               const unsigned b = sh.rc.cmd.body;
-              sh.run.atom = rank == 0 && !stale && (b == GPUOS_BODY_GEMM_BF16 || b == GPUOS_BODY_CONV_BF16)
-                                ? p.atoms + slot : nullptr;
+              sh.run.atom = rank == 0 && !stale && body_is_pair(b) ? p.atoms + slot : nullptr;
+              sh.run.spread = b != GPUOS_BODY_GEMV_BF16;
               sh.run.key = key;
               sh.run.lo = sh.rc.lo;
               sh.run.count = sh.rc.count;

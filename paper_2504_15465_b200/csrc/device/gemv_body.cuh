@@ -54,6 +54,9 @@ struct alignas(128) GemvDesc {
   unsigned long long* timing;    // optional: 4 globaltimer stamps per block (profiling)
 };
 
+// (tools/corun_probe.py writes `timing` at this offset for profiling)
+static_assert(offsetof(GemvDesc, timing) == 312, "GemvDesc layout");
+
 struct GemvPipe {
   unsigned char* tiles;          // stages x 18 KiB, 1024-aligned
   unsigned long long* full;      // [kGemvMaxStages]
@@ -100,13 +103,13 @@ __device__ __forceinline__ unsigned tmem_ld1(unsigned taddr) {
 // `gate`: the atom's early-start gate (dispatcher.cu): while it is 1 the
 // block streams its first stages of W but loads no x (the predecessor is
 // still producing it).
-__device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned rank, GemvPipe& G,
-                                           const unsigned* gate) {
-  const GemvDesc* D = reinterpret_cast<const GemvDesc*>(c.args[0]);
+template <class NextTile>
+__device__ __forceinline__ void gemv2_tile(const GemvDesc* D, unsigned block, int tid, unsigned rank, GemvPipe& G,
+                                           const unsigned* gate, NextTile& next_tile) {
   // Block b: row tile b % row_tiles, K split b / row_tiles (decode shapes
   // have few row tiles; splitting K keeps every TPC streaming W).
-  const unsigned blk = static_cast<unsigned>(c.block) % D->row_tiles;
-  const unsigned split = static_cast<unsigned>(c.block) / D->row_tiles;
+  const unsigned blk = block % D->row_tiles;
+  const unsigned split = block / D->row_tiles;
   const unsigned nk_all = (D->k + kGemmBK - 1) / kGemmBK;
   const unsigned kb0 = split * D->k_slices_per_block;
   const unsigned kb1 = kb0 + D->k_slices_per_block < nk_all ? kb0 + D->k_slices_per_block : nk_all;
@@ -114,10 +117,11 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
   const unsigned S = G.stages;
   const unsigned long long g0 = G.kb_used;
   if (S == 0 || nk == 0) {  // host validated; never on the path
+    if (tid == 0 && rank == 0) next_tile(true);  // (ends the run)
     cluster_sync_all();
     return;
   }
-  unsigned long long* tm = D->timing != nullptr && rank == 0 ? D->timing + 4ull * c.block : nullptr;
+  unsigned long long* tm = D->timing != nullptr && rank == 0 ? D->timing + 4ull * block : nullptr;
   if (tm && tid == 0) tm[0] = gtimer();
   if (tid == 0) {
     // TMA producer (both CTAs); descriptor written by a host copy while
@@ -159,6 +163,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
       tma_load_2d_pair(st, &D->w, kc, w_row, G.full + s);
       tma_load_2d_pair(st + kGemvWBytes, &D->x, kc, x_row, G.full + s);
     }
+    if (rank == 0) next_tile();  // claim + post the run's next block (both CTAs)
   } else if (tid == 32 && rank == 0) {
     if (gate) gate_spin(gate, *G.guard);  // the bounded waits measure the pipeline only
     tc_fence_after();
@@ -247,6 +252,22 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
     }
   }
   if (tm && tid == 0) tm[3] = gtimer();
+}
+
+// A pair run of GEMV blocks (PairTiles, gemm_body.cuh): the leader claims
+// the next block after the current one's last load; no arbitration, peer
+// join or per-block accounting between two blocks of a run.
+template <class NextTile>
+__device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned rank, GemvPipe& G,
+                                           const unsigned* gate, const PairTiles& run, NextTile& next_tile) {
+  const GemvDesc* D = reinterpret_cast<const GemvDesc*>(c.args[0]);
+  long long blk = c.block;
+  for (;;) {
+    gemv2_tile(D, static_cast<unsigned>(blk), tid, rank, G, gate, next_tile);
+    blk = *run.run_next;
+    if (blk < 0) break;
+    gate = nullptr;  // (open: the run's first block waited for it)
+  }
 }
 
 }  // namespace gpuos_dev_impl

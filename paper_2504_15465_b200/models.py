@@ -201,7 +201,8 @@ def bert_base_infer(batch: int = 8, seq: int = 128, ws_base: int = 0) -> list[di
     return b.kernels
 
 
-def llama3_8b_decode(context: int = 1024, ws_base: int = 0) -> list[dict]:
+def llama3_8b_decode(context: int = 1024, ws_base: int = 0,
+                     splits: tuple = (6, 8, 1, 9)) -> list[dict]:
     """One token: 32 layers of RMSNorm, QKV / O / gate-up / down GEMVs (split-K
     so every TPC streams weights), attention over a `context`-long KV cache
     (8 KV heads x 128), SiLU-mul; then the final norm and the LM head.
@@ -214,13 +215,13 @@ def llama3_8b_decode(context: int = 1024, ws_base: int = 0) -> list[dict]:
     d, kv, ffn, vocab = 4096, 1024, 14336, 128256
     for _ in range(32):
         b.stream(d * 2 * 2)                              # RMSNorm
-        b.gemv(d + 2 * kv, d, 6)                         # QKV (144 blocks)
+        b.gemv(d + 2 * kv, d, splits[0])                 # QKV (144 blocks)
         b.stream(context * kv * 2 * 2 + d * 2 * 2)       # RoPE + attention over K and V
-        b.gemv(d, d, 8)                                  # output projection (128 blocks)
+        b.gemv(d, d, splits[1])                          # output projection (128 blocks)
         b.stream(d * 2 * 3)                              # residual + RMSNorm
-        b.gemv(2 * ffn, d, 1)                            # gate + up (112 blocks)
+        b.gemv(2 * ffn, d, splits[2])                    # gate + up (112 blocks)
         b.stream(2 * ffn * 2 + ffn * 2)                  # SiLU(gate) * up
-        b.gemv(d, ffn, 9)                                # down projection (144 blocks)
+        b.gemv(d, ffn, splits[3])                        # down projection (144 blocks)
     b.stream(d * 2 * 2)                                  # final norm
     b.gemv(vocab, d, 1)                                  # LM head
     return b.kernels

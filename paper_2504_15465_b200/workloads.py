@@ -122,7 +122,7 @@ def infer4(horizon_ms: float = 2000.0, rps: tuple = (120.0, 120.0, 40.0, 40.0),
 
 
 def hybrid(horizon_ms: float = 2000.0, tokens_per_s: float = 60.0, slo_ms: float = 25.0,
-           train_batch: int = 256, tpcs: int = 74) -> dict:
+           train_batch: int = 256, tpcs: int = 74, decode_splits: tuple = (6, 8, 1, 9)) -> dict:
     """BASELINE config #3, hybrid stacking: Llama-3-8B bf16 decode at batch 1
     (latency-critical, Poisson token requests, one request = one token's 258
     kernels over 15 GB of weights) with ResNet-50 training (best-effort,
@@ -141,7 +141,7 @@ def hybrid(horizon_ms: float = 2000.0, tokens_per_s: float = 60.0, slo_ms: float
         "apps": [
             {"id": "llama_decode", "priority": "hp", "quota": tpcs // 2, "slo_ms": slo_ms,
              "arrival": {"poisson_rps": tokens_per_s, "seed_offset": 0},
-             "kernels": models.llama3_8b_decode(1024, ws_base=0)},
+             "kernels": models.llama3_8b_decode(1024, ws_base=0, splits=decode_splits)},
             {"id": "rn50_train", "priority": "be", "quota": tpcs - tpcs // 2,
              "arrival": "closed_loop", "kernels": models.resnet50_train(train_batch, ws_base=100_000)},
         ],
