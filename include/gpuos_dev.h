@@ -266,9 +266,20 @@ int gpuos_dev_gemm_desc_splitk(struct gpuos_dev* dev, const void* a, const void*
  * addresses. Release with gpuos_dev_free. No reference counterpart
  * (device.hpp:39-47).                                                    */
 #define GPUOS_GEMV_OUT_BF16 1u
+/* W pre-packed by gpuos_dev_gemv_pack (each ring stage one contiguous
+ * 16 KiB range): pass the packed buffer as w.                            */
+#define GPUOS_GEMV_W_PACKED 2u
 int gpuos_dev_gemv_desc(struct gpuos_dev* dev, const void* w, const void* x, void* y,
                         int64_t n, int64_t k, uint32_t flags, int32_t k_splits, void** desc,
                         int64_t* blocks);
+
+/* Repacks row-major bf16 W [n, k] into the GEMV's packed layout
+ * [ceil(n/128)][ceil(k/64)][128][64] (zero beyond n, k) on the side
+ * stream; dst holds GPUOS_GEMV_PACKED_BYTES(n, k) bytes. Weights are packed
+ * once, when a tenant loads them.                                        */
+int gpuos_dev_gemv_pack(struct gpuos_dev* dev, void* dst, const void* src, int64_t n, int64_t k);
+#define GPUOS_GEMV_PACKED_BYTES(n, k) \
+  ((uint64_t)(((n) + 127) / 128) * (uint64_t)(((k) + 63) / 64) * 128u * 64u * 2u)
 
 /* Convolution body descriptor (GPUOS_BODY_CONV_BF16): y = conv2d(x, w),
  * x NHWC bf16 [n, h, wd, c] (c % 8 == 0), w bf16 [k][r][s][cb] with cb = c

@@ -35,6 +35,8 @@ GPUOS_BODY_SPIN = 3
 GPUOS_BODY_GEMV_BF16 = 4
 GPUOS_BODY_CONV_BF16 = 5
 GPUOS_GEMM_OUT_BF16 = 1
+GPUOS_GEMV_OUT_BF16 = 1
+GPUOS_GEMV_W_PACKED = 2
 GPUOS_E_FULL = -5
 GPUOS_DEV_DEFER_WORKERS = 1
 
@@ -47,6 +49,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask", "gpuos_dev_set_tpc_owner",
     "gpuos_dev_gemm_desc", "gpuos_dev_gemm_desc_splitk", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
+    "gpuos_dev_gemv_pack",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -148,6 +151,7 @@ def library() -> C.CDLL:
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                                           C.POINTER(C.c_int32)]),
         "gpuos_dev_fill_bf16": (C.c_int, [P, P, C.c_uint64, C.c_uint64]),
+        "gpuos_dev_gemv_pack": (C.c_int, [P, P, P, C.c_int64, C.c_int64]),
         "gpuos_dev_gemv_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_uint32, C.c_int32,
                                           C.POINTER(P), C.POINTER(C.c_int64)]),
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
@@ -349,14 +353,25 @@ class Device:
         return desc.value, blocks.value, tm.value, tn.value
 
     def gemv_desc(self, w: int, x: int, y: int, n: int, k: int, bf16_out: bool = False,
-                  k_splits: int = 1) -> tuple[int, int]:
+                  k_splits: int = 1, packed: bool = False) -> tuple[int, int]:
         """Descriptor for GPUOS_BODY_GEMV_BF16 (y = W . x, decode GEMV):
         returns (device pointer for args[0], grid blocks). k_splits > 1
-        splits K; the last block of each row tile reduces the partials."""
+        splits K; the last block of each row tile reduces the partials.
+        packed: `w` is a gemv_pack()ed copy of W."""
         desc, blocks = C.c_void_p(), C.c_int64()
-        self._check(self._lib.gpuos_dev_gemv_desc(self._h, w, x, y, n, k, 1 if bf16_out else 0,
+        flags = (GPUOS_GEMV_OUT_BF16 if bf16_out else 0) | (GPUOS_GEMV_W_PACKED if packed else 0)
+        self._check(self._lib.gpuos_dev_gemv_desc(self._h, w, x, y, n, k, flags,
                                                   k_splits, C.byref(desc), C.byref(blocks)))
         return desc.value, blocks.value
+
+    @staticmethod
+    def gemv_packed_bytes(n: int, k: int) -> int:
+        return -(-n // 128) * -(-k // 64) * 128 * 64 * 2
+
+    def gemv_pack(self, dst: int, src: int, n: int, k: int) -> None:
+        """Row-major bf16 W [n, k] -> the GEMV's packed layout (each ring
+        stage one contiguous 16 KiB range; gemv_packed_bytes(n, k))."""
+        self._check(self._lib.gpuos_dev_gemv_pack(self._h, dst, src, n, k))
 
     def conv_desc(self, x: int, w: int, y: int, n: int, h: int, wd: int, c: int, k: int, r: int,
                   s: int, pad: int, stride: int, bf16_out: bool = False) -> tuple[int, int, int, int]:

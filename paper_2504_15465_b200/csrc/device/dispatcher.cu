@@ -1426,6 +1426,24 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
 
 __global__ void k_gtimer(unsigned long long* out) { *out = gtimer(); }
 
+// Packed GEMV weights (kGemvPacked): rows of 64 bf16; packed row
+// ((h nk + j) 128 + i) = W row 128 h + i, columns 64 j .. 64 j + 63, zero
+// beyond N or K.
+__host__ __device__ inline long long gemv_packed_rows(long long n, long long k) {
+  return (n + kGemmHalf - 1) / kGemmHalf * ((k + kGemmBK - 1) / kGemmBK) * kGemmHalf;
+}
+__global__ void k_gemv_pack(unsigned short* dst, const unsigned short* src, long long n, long long k,
+                            long long total) {
+  const long long nk = (k + kGemmBK - 1) / kGemmBK;
+  for (long long e = blockIdx.x * 256ll + threadIdx.x; e < total; e += gridDim.x * 256ll) {
+    const long long prow = e / kGemmBK, c = e % kGemmBK;
+    const long long i = prow % kGemmHalf, hj = prow / kGemmHalf;
+    const long long h = hj / nk, j = hj % nk;
+    const long long row = h * kGemmHalf + i, col = j * kGemmBK + c;
+    dst[e] = row < n && col < k ? src[row * k + col] : static_cast<unsigned short>(0);
+  }
+}
+
 // Uniform [-1, 1) bf16 fill from a counter hash (tenant operand init).
 __global__ void k_fill_bf16(unsigned short* p, unsigned long long n, unsigned long long seed) {
   for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
@@ -2530,6 +2548,18 @@ int gpuos_dev_gemm_desc_splitk(gpuos_dev* d, const void* a, const void* b, void*
   return GPUOS_OK;
 }
 
+int gpuos_dev_gemv_pack(gpuos_dev* d, void* dst, const void* src, int64_t n, int64_t k) {
+  if (!d || !dst || !src) return fail(GPUOS_E_CONFIG, "null argument");
+  if (n <= 0 || k <= 0 || n > 0x7fffffff || k > 0x7fffffff) return fail(GPUOS_E_CONFIG, "GEMV shape out of range");
+  const int64_t total = gemv_packed_rows(n, k) * kGemmBK;
+  CUDA_TRY(cudaSetDevice(d->device));
+  k_gemv_pack<<<1184, 256, 0, d->s_side>>>(static_cast<unsigned short*>(dst),
+                                            static_cast<const unsigned short*>(src), n, k, total);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(d->s_side));
+  return GPUOS_OK;
+}
+
 int gpuos_dev_gemv_desc(gpuos_dev* d, const void* w, const void* x, void* y, int64_t n, int64_t k,
                         uint32_t flags, int32_t k_splits, void** desc, int64_t* blocks) {
   if (!d || !w || !x || !y || !desc) return fail(GPUOS_E_CONFIG, "null argument");
@@ -2554,7 +2584,22 @@ int gpuos_dev_gemv_desc(gpuos_dev* d, const void* w, const void* x, void* y, int
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   };
   // x is a one-row tensor read with a 16-row box: rows >= 1 are zero fill.
-  if (make(&h.w, w, n, kGemmHalf) != CUDA_SUCCESS || make(&h.x, x, 1, kGemvXRows) != CUDA_SUCCESS)
+  // Packed W: a [rows, 64] tensor whose 128-row boxes are contiguous 16 KiB.
+  const bool packed = (flags & GPUOS_GEMV_W_PACKED) != 0;
+  CUresult wr;
+  if (packed) {
+    const int64_t prow = gemv_packed_rows(n, k);
+    const cuuint64_t dims[2] = {kGemmBK, static_cast<cuuint64_t>(prow)};
+    const cuuint64_t strides[1] = {kGemmBK * 2};
+    const cuuint32_t box[2] = {kGemmBK, kGemmHalf};
+    const cuuint32_t estr[2] = {1, 1};
+    wr = encode(&h.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    wr = make(&h.w, w, n, kGemmHalf);
+  }
+  if (wr != CUDA_SUCCESS || make(&h.x, x, 1, kGemvXRows) != CUDA_SUCCESS)
     return fail(GPUOS_E_CONFIG, "cuTensorMapEncodeTiled rejected the GEMV operands");
   h.y = reinterpret_cast<unsigned long long>(y);
   h.n = static_cast<unsigned>(n);
@@ -2565,7 +2610,7 @@ int gpuos_dev_gemv_desc(gpuos_dev* d, const void* w, const void* x, void* y, int
   h.k_slices_per_block = (nk + splits - 1) / splits;
   h.splits = (nk + h.k_slices_per_block - 1) / h.k_slices_per_block;
   h.blocks = h.row_tiles * h.splits;
-  h.flags = flags & kGemvOutBf16;
+  h.flags = flags & (kGemvOutBf16 | kGemvPacked);
   // One allocation: descriptor, then the split counters (zeroed), then the
   // partial sums; gpuos_dev_free(desc) releases all of it.
   const size_t counters_off = sizeof(GemvDesc);

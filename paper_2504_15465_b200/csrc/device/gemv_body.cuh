@@ -39,9 +39,12 @@ constexpr unsigned kGemvXBytes = kGemvXRows * kGemmBK * 2;   // 2 KiB
 constexpr unsigned kGemvStageBytes = kGemvWBytes + kGemvXBytes;
 constexpr unsigned kGemvMaxStages = 8;
 constexpr unsigned kGemvOutBf16 = 1u;
+// W pre-packed (gpuos_dev_gemv_pack): [ceil(N/128)][ceil(K/64)][128][64],
+// every ring stage's 16 KiB one contiguous HBM range.
+constexpr unsigned kGemvPacked = 2u;
 
 struct alignas(128) GemvDesc {
-  CUtensorMap w;                 // W [N, K] bf16: box {64, 128}, SWIZZLE_128B
+  CUtensorMap w;                 // W [N, K] bf16: box {64, 128}, SWIZZLE_128B (packed: [rows, 64])
   CUtensorMap x;                 // x [1, K] bf16: box {64, 16}, SWIZZLE_128B (rows >= 1 zero)
   unsigned long long y;
   unsigned n, k, blocks, flags;  // flags: kGemvOutBf16
@@ -128,7 +131,13 @@ __device__ __forceinline__ void gemv2_tile(const GemvDesc* D, unsigned block, in
     // this persistent kernel runs: acquire it into the tensor-map proxy.
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->w) : "memory");
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->x) : "memory");
+    // Packed W: the 128-row half-tile's K slice j starts at packed row
+    // ((2 blk + rank) nk_all + j) 128, column 0.
+    const bool packed = (D->flags & kGemvPacked) != 0;
     const int w_row = static_cast<int>(blk * kGemvTile + rank * kGemmHalf);
+    const int p_row = static_cast<int>(((2u * blk + rank) * nk_all + kb0) * kGemmHalf);
+    auto w_c0 = [&](unsigned j) { return packed ? 0 : static_cast<int>((kb0 + j) * kGemmBK); };
+    auto w_c1 = [&](unsigned j) { return packed ? p_row + static_cast<int>(j * kGemmHalf) : w_row; };
     const int x_row = static_cast<int>(rank * kGemvXRows);  // rank 1: all zero fill
     // W for the first stages first, then x once the atom's gate is open:
     // an early-started block streams W while its predecessor still writes
@@ -140,8 +149,7 @@ __device__ __forceinline__ void gemv2_tile(const GemvDesc* D, unsigned block, in
       const unsigned long long r = k / S;
       if (r >= 1) mbar_wait_bounded(G.empty + s, static_cast<unsigned>((r - 1) & 1), *G.guard);
       if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemvStageBytes);
-      tma_load_2d_pair(G.tiles + s * kGemvStageBytes, &D->w, static_cast<int>((kb0 + j) * kGemmBK), w_row,
-                       G.full + s);
+      tma_load_2d_pair(G.tiles + s * kGemvStageBytes, &D->w, w_c0(j), w_c1(j), G.full + s);
     }
     if (gate) {
       gate_spin(gate, *G.guard);  // DevAtom::paused, kGatedBit
@@ -160,7 +168,7 @@ __device__ __forceinline__ void gemv2_tile(const GemvDesc* D, unsigned block, in
       unsigned char* st = G.tiles + s * kGemvStageBytes;
       if (rank == 0) mbar_expect_tx(G.full + s, 2 * kGemvStageBytes);
       const int kc = static_cast<int>((kb0 + j) * kGemmBK);
-      tma_load_2d_pair(st, &D->w, kc, w_row, G.full + s);
+      tma_load_2d_pair(st, &D->w, w_c0(j), w_c1(j), G.full + s);
       tma_load_2d_pair(st + kGemvWBytes, &D->x, kc, x_row, G.full + s);
     }
     if (rank == 0) next_tile();  // claim + post the run's next block (both CTAs)

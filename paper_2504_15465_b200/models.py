@@ -202,15 +202,18 @@ def bert_base_infer(batch: int = 8, seq: int = 128, ws_base: int = 0) -> list[di
 
 
 def llama3_8b_decode(context: int = 1024, ws_base: int = 0,
-                     splits: tuple = (6, 8, 1, 9)) -> list[dict]:
+                     splits: tuple = (3, 4, 1, 4)) -> list[dict]:
     """One token: 32 layers of RMSNorm, QKV / O / gate-up / down GEMVs (split-K
     so every TPC streams weights), attention over a `context`-long KV cache
     (8 KV heads x 128), SiLU-mul; then the final norm and the LM head.
-    Split counts put each GEMV in about one wave of the 146 worker pairs
-    (W = 2): a block's fixed cost (first TMA load ~3 us, epilogue and
-    split-K reduction ~2 us) is then paid once per pair per kernel
-    (scratch measurements, cold weights: down projection 38 -> 25 us at
-    9 splits instead of 16)."""
+    `splits` (QKV, O, gate-up, down) size each GEMV to about one wave of one
+    worker pair per TPC (72 / 64 / 112 / 64 blocks): stacked with a
+    best-effort tenant, whose tiles hold the TPCs' other pairs, a decode GEMV
+    still runs in one wave. Sized to both pairs (6, 8, 1, 9: 144 / 128 / 112
+    / 144 blocks) decode alone is 6 % faster but stacked 24 % slower, as the
+    second wave waits for best-effort tiles (tools/hybrid_breakdown.py: QKV
+    17.7 us alone / 29.6 us stacked vs 20.1 / 21.8; token p50 4.71 / 6.13 ms
+    vs 5.02 / 5.73 ms)."""
     b = Builder(ws_base)
     d, kv, ffn, vocab = 4096, 1024, 14336, 128256
     for _ in range(32):

@@ -122,7 +122,7 @@ def infer4(horizon_ms: float = 2000.0, rps: tuple = (120.0, 120.0, 40.0, 40.0),
 
 
 def hybrid(horizon_ms: float = 2000.0, tokens_per_s: float = 60.0, slo_ms: float = 25.0,
-           train_batch: int = 256, tpcs: int = 74, decode_splits: tuple = (6, 8, 1, 9)) -> dict:
+           train_batch: int = 256, tpcs: int = 74, decode_splits: tuple = (3, 4, 1, 4)) -> dict:
     """BASELINE config #3, hybrid stacking: Llama-3-8B bf16 decode at batch 1
     (latency-critical, Poisson token requests, one request = one token's 258
     kernels over 15 GB of weights) with ResNet-50 training (best-effort,

@@ -26,13 +26,15 @@ def wait_all(dev, n, timeout=60.0):
     return done
 
 
-@pytest.mark.parametrize("n,k,bf16_out,workers,splits", [
-    (6144, 4096, False, 2, 1),   # Llama-3-8B QKV projection
-    (4096, 14336, True, 2, 1),   # down projection, bf16 y
-    (4096, 14336, True, 2, 16),  # down projection, split-K, bf16 y
-    (1000, 264, False, 1, 3),    # ragged last tile, K not a multiple of 64, split-K
+@pytest.mark.parametrize("n,k,bf16_out,workers,splits,packed", [
+    (6144, 4096, False, 2, 1, False),   # Llama-3-8B QKV projection
+    (4096, 14336, True, 2, 1, False),   # down projection, bf16 y
+    (4096, 14336, True, 2, 16, False),  # down projection, split-K, bf16 y
+    (1000, 264, False, 1, 3, False),    # ragged last tile, K not a multiple of 64, split-K
+    (6144, 4096, False, 2, 3, True),    # packed W (gpuos_dev_gemv_pack), split-K
+    (1000, 264, True, 2, 3, True),      # packed W, ragged N and K (zero-padded tiles)
 ])
-def test_gemv_atoms_match_reference(api, cuda_device, n, k, bf16_out, workers, splits):
+def test_gemv_atoms_match_reference(api, cuda_device, n, k, bf16_out, workers, splits, packed):
     import torch
 
     g = torch.Generator().manual_seed(n + k)
@@ -44,8 +46,12 @@ def test_gemv_atoms_match_reference(api, cuda_device, n, k, bf16_out, workers, s
                    dtype=torch.bfloat16 if bf16_out else torch.float32)
     rng = random.Random(k)
     with api.Device(workers_per_sm=workers) as dev:
+        if packed:
+            Wp = torch.full((dev.gemv_packed_bytes(n, k) // 2,), float("nan"), device="cuda", dtype=torch.bfloat16)
+            dev.gemv_pack(Wp.data_ptr(), W.data_ptr(), n, k)
+            W = Wp
         desc, blocks = dev.gemv_desc(W.data_ptr(), X.data_ptr(), y.data_ptr(), n, k, bf16_out=bf16_out,
-                                     k_splits=splits)
+                                     k_splits=splits, packed=packed)
         assert blocks == -(-n // 256) * min(splits, -(-k // 64))
         trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
         cuts = sorted(rng.sample(range(1, blocks), min(6, blocks - 1)))

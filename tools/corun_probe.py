@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--only", default="none,conv,gemm,spin")
     ap.add_argument("--timing", action="store_true", help="per-block stamps (GemvDesc::timing)")
     ap.add_argument("--gemv-tpcs", default="0-73")
+    ap.add_argument("--packed", action="store_true", help="W pre-packed (GPUOS_GEMV_W_PACKED)")
     ap.add_argument("--bg-tpcs", default="0-73")
     args = ap.parse_args()
     n, k, splits = (int(x) for x in args.shape.split(","))
@@ -45,8 +46,14 @@ def main():
     B = (torch.rand(4096, 4096, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
     Cm = torch.zeros(8192, 4096, device="cuda", dtype=torch.bfloat16)
     torch.cuda.synchronize()
+    ref = w.cpu().double() @ x.cpu().double()
     with api.Device(workers_per_sm=2) as dev:
-        gd, gblocks = dev.gemv_desc(w.data_ptr(), x.data_ptr(), y.data_ptr(), n, k, k_splits=splits)
+        wsrc = w
+        if args.packed:
+            wsrc = torch.empty(dev.gemv_packed_bytes(n, k) // 2, device="cuda", dtype=torch.bfloat16)
+            dev.gemv_pack(wsrc.data_ptr(), w.data_ptr(), n, k)
+        gd, gblocks = dev.gemv_desc(wsrc.data_ptr(), x.data_ptr(), y.data_ptr(), n, k, k_splits=splits,
+                                    packed=args.packed)
         cd, cblocks, _, _ = dev.conv_desc(X.data_ptr(), Wc.data_ptr(), Y.data_ptr(), cn, ch, cw, cc, ck, 3, 3, 1, 1,
                                           bf16_out=True)
         md, mblocks, _, _ = dev.gemm_desc(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), 8192, 4096, 4096, bf16_out=True)
@@ -89,8 +96,11 @@ def main():
             while bg_live:
                 for c in dev.poll():
                     bg_live.discard(c.atom_id)
+            # (CPU check: no kernel runs beside the resident dispatcher)
+            err = ((y.cpu().double() - ref).abs().max() / ref.abs().max()).item()
+            assert err < 1e-3, err
             gb = n * k * 2 / 1e3
-            print(f"{name:5s} tpcs {args.gemv_tpcs} bg {args.bg_tpcs} gemv {n}x{k}/{splits} ({gblocks} blocks): armed->end p50 {statistics.median(totals):7.2f} us"
+            print(f"{name:5s} {'packed ' if args.packed else ''}tpcs {args.gemv_tpcs} bg {args.bg_tpcs} gemv {n}x{k}/{splits} ({gblocks} blocks): armed->end p50 {statistics.median(totals):7.2f} us"
                   f" ({gb / statistics.median(totals):6.0f} GB/s)  span p50 {statistics.median(spans):7.2f} us"
                   f"  p90 {sorted(totals)[int(0.9 * len(totals))]:7.2f}", flush=True)
             if phases:

@@ -132,7 +132,7 @@ def main():
     ap.add_argument("--horizon-ms", type=float, default=1000.0)
     ap.add_argument("--set", default="{}", help="extra scheduler knobs (JSON)")
     ap.add_argument("--b200", default="{}", help="extra B200Options (JSON)")
-    ap.add_argument("--splits", default="6,8,1,9", help="decode GEMV K splits (QKV, O, gate-up, down)")
+    ap.add_argument("--splits", default="3,4,1,4", help="decode GEMV K splits (QKV, O, gate-up, down)")
     ap.add_argument("--train-alone", action="store_true")
     args = ap.parse_args()
     splits = tuple(int(x) for x in args.splits.split(","))
