@@ -614,6 +614,14 @@ struct PairRun {
   long long next;               // posted next block, -1: end of run (leader writes both CTAs')
 };
 
+// A finished atom's bookkeeping held back while its handed-off successor
+// runs (account_block / write_done).
+struct PendingDone {
+  unsigned long long t0, t1, m0, m1, tag, ts, ta;  // t0, m0, m1: single-slice atoms (else read here)
+  unsigned slot, tk, n, flags;                     // flags: kPendValid | kPendSingle
+};
+constexpr unsigned kPendValid = 1u, kPendSingle = 2u;
+
 struct WorkerShared {
   RoundCmd rc;                  // this CTA's block for the round
   PairRun run;                  // pair run state (leader) / posted next tile (both)
@@ -625,6 +633,7 @@ struct WorkerShared {
   unsigned long long touched_key;  // warp 0: atom whose `touched` word has this TPC
   unsigned tmem_base;           // this worker's TMEM columns (tcgen05.alloc)
   WaitGuard guard;              // the bodies' bounded pipeline waits
+  PendingDone pend;             // warp 0: a handed-off predecessor's bookkeeping
 };
 
 // Lane 0 broadcasts a field of sh.rc it wrote itself; the other lanes do
@@ -783,12 +792,68 @@ __device__ __forceinline__ unsigned atom_exch_acq_rel32(unsigned* p, unsigned v)
   return old;
 }
 
+// A finished atom's bookkeeping: completion record, resident-list clears,
+// counters. After a handoff it is held back until the successor's block has
+// run (the next account_block writes it, after that block's own chain work),
+// so the successor starts without waiting for it.
+
+// All lanes of warp 0; `d` (shared memory) was filled by lane 0 before a
+// __syncwarp.
+__device__ __forceinline__ void write_done(const Params& p, PendingDone& d, unsigned lane) {
+  const DevAtom* a = p.atoms + d.slot;
+  if (lane == 0) {
+    // Completion record (the host is waiting on it), in the slot's own
+    // record: four 16-byte chunks, each three data words and the ticket
+    // (= seq). Each chunk is one PCIe write, so a chunk whose ticket matches
+    // is complete; no system-scope fence (~1 us) sits on the completion path.
+    const bool single = (d.flags & kPendSingle) != 0u;
+    CompRec* rec = p.comp + d.slot;
+    const unsigned long long t0 = single ? d.t0 : ld_relaxed_gpu64(&a->t_first);
+    const unsigned long long m0 = single ? d.m0 : ld_relaxed_gpu64(&a->touched[0]);
+    const unsigned long long m1 = single ? d.m1 : ld_relaxed_gpu64(&a->touched[1]);
+    const unsigned tk = d.tk;
+    const unsigned long long span = d.t1 - t0;
+    st_relaxed_sys_v4(rec->w + 0, d.n, static_cast<unsigned>(d.tag), static_cast<unsigned>(d.tag >> 32), tk);
+    st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
+                      span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
+    st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
+                      static_cast<unsigned>(m1), tk);
+    // t_seen / t_armed as ns before t_first (0 in batch mode).
+    st_relaxed_sys_v4(rec->w + 12, static_cast<unsigned>(m1 >> 32),
+                      d.ts ? static_cast<unsigned>(t0 - d.ts) : 0u,
+                      d.ta ? static_cast<unsigned>(t0 - d.ta) : 0u, tk);
+  }
+  // Device-side bookkeeping after the record; the host recycles this slot
+  // only after thousands of others, long after these land. Our key still
+  // occupies its list entries (only this finisher clears them, and the
+  // ingest warp fills only cleared entries): plain stores, no round trip.
+  for (int t = lane; t < p.logical_tpcs; t += 32) {
+    const unsigned long long m = a->mask[t >> 6];
+    if ((m >> (t & 63)) & 1ull)
+      st_relaxed_gpu64(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], 0ull);
+  }
+  if (lane == 0) {
+    // Plain reductions: atoms_done is read after the kernel ends, and the
+    // drain check only needs outstanding to reach zero eventually.
+    atomicAdd(&p.ctl->atoms_done, 1ull);
+    atomicSub(&p.ctl->outstanding, 1);
+    d.flags = 0u;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void flush_pending(const Params& p, PendingDone& d, unsigned lane) {
+  const unsigned f = __shfl_sync(0xffffffffu, lane == 0 ? d.flags : 0u, 0);
+  if (f & kPendValid) write_done(p, d, lane);
+}
+
 __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
                                              unsigned long long t_start, int tpc, unsigned sm,
                                              unsigned rank, unsigned lane, unsigned extra,
                                              unsigned long long& n_blocks,
                                              unsigned long long& busy,
-                                             unsigned long long& touched_key) {
+                                             unsigned long long& touched_key,
+                                             PendingDone& pend) {
   DevAtom* a = p.atoms + rc.slot;
   int last = 0;
   // A single-slice atom is complete with its only block: its first / last
@@ -849,7 +914,10 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
     }
   }
   last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return 0;
+  if (!last) {
+    flush_pending(p, pend, lane);
+    return 0;
+  }
   // Chain head: arm the registered successor (or mark this atom finished so
   // the ingest warp arms it) before anything else -- the successor's start
   // is the chain's critical path. The swap is acq_rel: our outputs (ordered
@@ -870,16 +938,24 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       // Registered before we looked: nothing to race with (registration
       // happens once), and the acquire above ordered its fields.
       next = pre != 0u ? pre : atom_exch_acq_rel32(&a->succ, kSuccDone);
-      if (next != 0u && (ld_relaxed_gpu(&p.atoms[next - 1u].paused) & kGatedBit)) {
+      // The successor's hot line, this TPC's fence and b's own registered
+      // successor are loaded together (one L2 round trip, not four in a
+      // row): this chain is the gap between two dependent kernels.
+      int floor_prio = 0;
+      unsigned cn = 0;
+      if (next != 0u) {
+        bf.load(p.atoms + (next - 1u));
+        floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
+        cn = ld_acquire_gpu(&p.atoms[next - 1u].succ);
+      }
+      if (next != 0u && ((bf.count_paused >> 32) & kGatedBit)) {
         // Early-started successor: our outputs, acquired through the count
         // above, are released to its gate waiters.
         open_gate(&p.atoms[next - 1u].paused);
         next = 0;
       }
       if (next != 0u) {
-        bf.load(p.atoms + (next - 1u));
         DevAtom* b = p.atoms + (next - 1u);
-        const int floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
         const unsigned bseq = static_cast<unsigned>(bf.seq_prio);
         const int bprio = static_cast<int>(bf.seq_prio >> 32);
         const unsigned bcount = static_cast<unsigned>(bf.count_paused);
@@ -892,7 +968,6 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         b->armed = 1u;
         // Lookahead: b's own registered successor, if a GEMV that may start
         // early, is armed now behind a closed gate (b opens it).
-        const unsigned cn = ld_acquire_gpu(&b->succ);
         if (cn != 0u && cn != kSuccDone) {
           DevAtom* c = p.atoms + (cn - 1u);
           if (body_is_pair(c->body) && !(c->chain & kNoEarly) && c->prio <= bprio &&
@@ -941,49 +1016,27 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       }
     }
   }
+  // The previous handoff's bookkeeping (its successor -- this block -- is
+  // past its own chain work now), then this atom's: written at once, or
+  // held back while the successor handed off here runs.
+  flush_pending(p, pend, lane);
   if (lane == 0) {
-    if (single && (chain & kChainHead)) __threadfence();
-    // Completion record (the host is waiting on it), in the slot's own
-    // record: four 16-byte chunks, each three data words and the ticket
-    // (= seq). Each chunk is one PCIe write, so a chunk whose ticket matches
-    // is complete; no system-scope fence (~1 us) sits on the completion path.
-    CompRec* rec = p.comp + rc.slot;
-    const unsigned long long t0 = single ? s_t0 : ld_relaxed_gpu64(&a->t_first);
-    const unsigned long long t1 = s_t1;
-    const unsigned long long m0 =
-        single ? (tpc < 64 ? 1ull << tpc : 0ull) : ld_relaxed_gpu64(&a->touched[0]);
-    const unsigned long long m1 =
-        single ? (tpc >= 64 ? 1ull << (tpc - 64) : 0ull) : ld_relaxed_gpu64(&a->touched[1]);
-    const unsigned tk = ~static_cast<unsigned>(rc.key >> 24);
-    const unsigned long long span = t1 - t0;
-    st_relaxed_sys_v4(rec->w + 0, rc.count / rc.cmd.parts,
-                      static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32), tk);
-    st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
-                      span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
-    st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
-                      static_cast<unsigned>(m1), tk);
-    // t_seen / t_armed as ns before t_first (0 in batch mode).
-    st_relaxed_sys_v4(rec->w + 12, static_cast<unsigned>(m1 >> 32),
-                      ts ? static_cast<unsigned>(t0 - ts) : 0u,
-                      ta ? static_cast<unsigned>(t0 - ta) : 0u, tk);
+    if (single && (chain & kChainHead)) __threadfence();  // outputs before the record
+    pend.slot = rc.slot;
+    pend.tk = ~static_cast<unsigned>(rc.key >> 24);
+    pend.n = rc.count / rc.cmd.parts;
+    pend.tag = tag;
+    pend.ts = ts;
+    pend.ta = ta;
+    pend.t0 = s_t0;
+    pend.t1 = s_t1;
+    pend.m0 = tpc < 64 ? 1ull << tpc : 0ull;
+    pend.m1 = tpc >= 64 ? 1ull << (tpc - 64) : 0ull;
+    pend.flags = kPendValid | (single ? kPendSingle : 0u);
   }
   __syncwarp();
-  // Device-side bookkeeping after the record; the host recycles this slot
-  // only after thousands of others, long after these land. Our key still
-  // occupies its list entries (only this finisher clears them, and the
-  // ingest warp fills only cleared entries): plain stores, no round trip.
-  for (int t = lane; t < p.logical_tpcs; t += 32) {
-    const unsigned long long m = a->mask[t >> 6];
-    if ((m >> (t & 63)) & 1ull)
-      st_relaxed_gpu64(p.resident + static_cast<size_t>(t) * kResident + a->entry[t], 0ull);
-  }
-  if (lane == 0) {
-    // Plain reductions: atoms_done is read after the kernel ends, and the
-    // drain check only needs outstanding to reach zero eventually.
-    atomicAdd(&p.ctl->atoms_done, 1ull);
-    atomicSub(&p.ctl->outstanding, 1);
-    if (handoff) rc = ho;  // (rc's old contents are no longer needed)
-  }
+  if (!handoff) write_done(p, pend, lane);
+  if (lane == 0 && handoff) rc = ho;  // (rc's old contents are no longer needed)
   __syncwarp();
   return 1 + handoff;
 }
@@ -1056,7 +1109,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
   gemm_pipe_init(gemm, dsmem, p.smem_bytes, p.tmem_cols, tid);
   GemvPipe gemv;
   gemv_pipe_init(gemv, dsmem, p.smem_bytes, p.tmem_cols, tid);
-  if (tid == 0) sh.guard = WaitGuard{&p.ctl->fault, &p.ctl->quit, p.wait_bound_ns};
+  if (tid == 0) {
+    sh.guard = WaitGuard{&p.ctl->fault, &p.ctl->quit, p.wait_bound_ns};
+    sh.pend.flags = 0u;
+  }
   gemm.guard = gemv.guard = &sh.guard;
   if (tid == 0) {
     mbar_init(&sh.join_full, 1);
@@ -1406,12 +1462,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
     if (warp == 0 && go != kGoJoin) {
       const unsigned extra = go == kGoPair ? lane0_field(sh.run.extra, lane) : 0u;
       const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, extra, n_blocks, busy,
-                                     sh.touched_key);
+                                     sh.touched_key, sh.pend);
       if (done) cur_key = 0ull;  // the atom is done: rescan rather than claim from it
       handoff = done == 2;
       __syncwarp();  // every lane has read sh.t_start / sh.rc before lane 0 rewrites them
     }
   }
+  if (warp == 0) flush_pending(p, sh.pend, lane);  // (a handoff always runs its block first: none left)
   if (tid == 0) {
     atomicAdd(&p.ctl->blocks, n_blocks);
     atomicAdd(&p.ctl->busy_ns, busy);
