@@ -216,6 +216,7 @@ class B200Device final : public Device {
   long blocks_executed(KernelId k) const override { return executed_.at(k); }
 
   void set_tpc_fence(const std::vector<int>& tpcs, int min_priority, std::uint64_t owner_tag) override;
+  void set_pair_fence(const std::vector<int>& tpcs, unsigned pair_slots, int min_priority) override;
   bool preempts_stolen() const override { return true; }
   bool supports_chaining() const override { return true; }
   AtomId submit_chained(AtomId after, KernelId kernel, long lo, long hi,

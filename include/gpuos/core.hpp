@@ -180,6 +180,11 @@ class Device {
   // min_priority start new blocks (min_priority 0 lifts the fence).
   virtual void set_tpc_fence(const std::vector<int>& /*tpcs*/, int /*min_priority*/,
                              std::uint64_t /*owner_tag*/) {}
+  // Pair fence (live extension): on these TPCs only the worker pairs in
+  // `pair_slots` (bit i: the TPC's i-th pair) refuse blocks below
+  // min_priority; the others accept every atom (0 lifts).
+  virtual void set_pair_fence(const std::vector<int>& /*tpcs*/, unsigned /*pair_slots*/,
+                              int /*min_priority*/) {}
   // Live-backend hook: true when TPCs holding only foreign stolen atoms may
   // be handed back to their owner immediately (device priority arbitration
   // preempts at the next block boundary).

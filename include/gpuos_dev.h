@@ -223,6 +223,15 @@ int gpuos_dev_set_fence_mask(struct gpuos_dev* dev, const uint64_t mask[2],
  * revocation, scheduler.hpp:61-66, scheduler.cpp:239-270).              */
 int gpuos_dev_set_tpc_owner(struct gpuos_dev* dev, const uint64_t mask[2], uint32_t owner,
                             int32_t min_priority);
+/* Pair fence: on every TPC in the mask, only the worker pairs whose slot
+ * bit is set in pair_slots (bit i: the TPC's i-th pair, W pairs per TPC)
+ * stop starting blocks of atoms below min_priority (0 lifts); the TPC's
+ * other pairs accept every atom. Replaces the TPC's owner entry. Lets a
+ * latency-critical tenant keep one pair per TPC free of best-effort tiles
+ * while best-effort work keeps the other (no reference counterpart: the
+ * reference's TPC is the unit of revocation, scheduler.cpp:239-270).     */
+int gpuos_dev_set_pair_fence(struct gpuos_dev* dev, const uint64_t mask[2], uint32_t pair_slots,
+                             int32_t min_priority);
 /* Non-blocking; returns the number of completions written to out[0..max). */
 int gpuos_dev_poll(struct gpuos_dev* dev, gpuos_completion* out, int32_t max);
 int64_t gpuos_dev_now_ns(struct gpuos_dev* dev);

@@ -49,7 +49,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask", "gpuos_dev_set_tpc_owner",
     "gpuos_dev_gemm_desc", "gpuos_dev_gemm_desc_splitk", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
-    "gpuos_dev_gemv_pack",
+    "gpuos_dev_gemv_pack", "gpuos_dev_set_pair_fence",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -152,6 +152,7 @@ def library() -> C.CDLL:
                                           C.POINTER(C.c_int32)]),
         "gpuos_dev_fill_bf16": (C.c_int, [P, P, C.c_uint64, C.c_uint64]),
         "gpuos_dev_gemv_pack": (C.c_int, [P, P, P, C.c_int64, C.c_int64]),
+        "gpuos_dev_set_pair_fence": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_uint32, C.c_int32]),
         "gpuos_dev_gemv_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_uint32, C.c_int32,
                                           C.POINTER(P), C.POINTER(C.c_int64)]),
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
@@ -405,6 +406,14 @@ class Device:
         for t in tpcs:
             m[t >> 6] |= 1 << (t & 63)
         self._check(self._lib.gpuos_dev_set_tpc_owner(self._h, m, owner, min_priority))
+
+    def set_pair_fence(self, tpcs, pair_slots: int, min_priority: int) -> None:
+        """Pair fence: only the TPCs' worker pairs in `pair_slots` (bit i =
+        slot i) refuse blocks below min_priority (0 lifts)."""
+        m = (C.c_uint64 * 2)()
+        for t in tpcs:
+            m[t >> 6] |= 1 << (t & 63)
+        self._check(self._lib.gpuos_dev_set_pair_fence(self._h, m, pair_slots, min_priority))
 
     def poll(self, max_n: int = 256) -> list[Completion]:
         buf = (Completion * max_n)()

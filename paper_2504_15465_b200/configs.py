@@ -40,12 +40,17 @@ def per_app(results: list[dict]) -> dict[str, dict]:
         for a, n in zip(r["report"]["apps"], r["atoms"]["per_app"]):
             atoms[a["app_id"]] = atoms.get(a["app_id"], 0) + n
     secs = sum(r["b200"]["run_wall_ns"] for r in results) * 1e-9
+    work: dict[str, float] = {}
+    for r in results:
+        for a, w in zip(r["report"]["apps"], r["b200"].get("work_us_per_app", [])):
+            work[a["app_id"]] = work.get(a["app_id"], 0.0) + w
     out = {}
     for app in set(lat) | set(done) | set(atoms):
         xs = lat.get(app, [])
         out[app] = {"completed": done.get(app, 0), "per_s": done.get(app, 0) / secs if secs else None,
                     "p50_ms": nearest_rank(xs, 50), "p99_ms": nearest_rank(xs, 99),
-                    "atoms": atoms.get(app, 0)}
+                    "atoms": atoms.get(app, 0),
+                    "work_us_per_s": work.get(app, 0.0) / secs if secs else None}
     return out
 
 
@@ -77,8 +82,13 @@ def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0,
             alone[a["id"]] = per_app([s.run(scenario={"config": solo}) for _ in range(reps)])[a["id"]]
         # The equivalent static partition: each tenant on its quota, no
         # stealing, no atomization, no right-sizing.
+        # (sharing mechanisms -- coexistence, pair fences -- off: nothing is
+        # shared in a static partition, and pair fences would only slow the
+        # best-effort tenant on its own quota)
+        static_set = dict(knob_set, rightsizer=False, be_coexist=False, hp_pair_reserve=False,
+                          hp_quota_full=False)
         static = per_app([s.run(scenario={"config": workloads.variant(cfg, stealing=False, atomizer=False)},
-                                set=dict(knob_set, rightsizer=False))
+                                set=static_set)
                           for _ in range(reps)])
     stacked = per_app(live)
     apps = {}
@@ -91,8 +101,12 @@ def run(name: str, horizon_ms: float = 2000.0, reps: int = 2, device: int = 0,
             lat = [json.loads(x)["latency_us"] / 1e3 for r in live for x in r["request_log"].splitlines()
                    if json.loads(x)["app"] == i and json.loads(x)["completed"]]
             row["slo_attainment"] = sum(v <= a["slo_ms"] for v in lat) / len(lat) if lat else None
-        if a["priority"] == "be" and st.get("per_s") and sp.get("per_s"):
-            row["throughput_vs_static"] = st["per_s"] / sp["per_s"]
+        if a["priority"] == "be" and st.get("work_us_per_s") and sp.get("work_us_per_s"):
+            # Executed work (blocks x calibrated block time) per second:
+            # completed iterations quantise a 1 s run to ~3 %.
+            row["throughput_vs_static"] = st["work_us_per_s"] / sp["work_us_per_s"]
+            if st.get("per_s") and sp.get("per_s"):
+                row["iterations_vs_static"] = st["per_s"] / sp["per_s"]
         apps[i] = row
     out = {"config": name, "horizon_ms": horizon_ms, "reps": reps, "chain_launches": chain, "apps": apps,
            "knobs": knob_set, "tpc_utilization": sum(r["report"]["tpc_utilization"] for r in live) / len(live)}

@@ -114,7 +114,12 @@ constexpr unsigned kChainHead = 1u;
 // atoms that span its quota and stolen TPCs run at the stolen priority
 // and would otherwise be fenced off their own quota. An atom's tenant
 // travels in DevAtom::paused bits 16..31 (read with the claim word).
-__device__ __forceinline__ bool fence_admits(int fence, int prio, unsigned tenant) {
+// Bits 8..15: the worker-pair slots of the TPC the floor applies to (0: all;
+// gpuos_dev_set_pair_fence). A TPC runs W worker pairs; each knows its slot
+// (WorkerShared::pair_slot, numbered in arrival order at launch).
+__device__ __forceinline__ bool fence_admits(int fence, int prio, unsigned tenant, unsigned pair_slot) {
+  const unsigned slots = (static_cast<unsigned>(fence) >> 8) & 0xffu;
+  if (slots != 0u && !((slots >> pair_slot) & 1u)) return true;
   const unsigned owner = static_cast<unsigned>(fence) >> 16;
   return prio >= (fence & 0xff) || (owner != 0u && owner == tenant);
 }
@@ -169,6 +174,7 @@ struct Params {
   unsigned* version;             // [tpcs] bumped when a TPC's candidates change
   int* fence;                    // [tpcs] minimum priority allowed to start
   unsigned* tc_busy;             // [tpcs] pair tiles running on the TPC's tensor cores
+  unsigned* pair_seq;            // [tpcs] worker pairs started on the TPC (pair slots)
   DevCtl* ctl;
   const int* phys2log;           // [physical tpcs]
   RingEntry* ring;               // mapped host memory
@@ -469,7 +475,8 @@ __device__ __forceinline__ void ingest_loop(const Params& p, IngestShared& ish) 
       } else if (op == kOpFenceMask) {
         const unsigned long long m0 = field64(get(kFMask0), get(kFMask0 + 1));
         const unsigned long long m1 = field64(get(kFMask1), get(kFMask1 + 1));
-        const int floor_prio = static_cast<int>((get(kFPrio) & 0xffu) | (get(kFAux) << 16));  // owner
+        // floor | pair-slot mask << 8 | owner << 16
+        const int floor_prio = static_cast<int>((get(kFPrio) & 0xffffu) | (get(kFAux) << 16));
         for (int t = lane; t < p.logical_tpcs; t += 32) {
           const unsigned long long m = t < 64 ? m0 : m1;
           if ((m >> (t & 63)) & 1ull) atomicExch(p.fence + t, floor_prio);
@@ -634,6 +641,7 @@ struct WorkerShared {
   unsigned tmem_base;           // this worker's TMEM columns (tcgen05.alloc)
   WaitGuard guard;              // the bodies' bounded pipeline waits
   PendingDone pend;             // warp 0: a handed-off predecessor's bookkeeping
+  unsigned pair_slot;           // this pair's slot on its TPC (pair fences)
 };
 
 // Lane 0 broadcasts a field of sh.rc it wrote itself; the other lanes do
@@ -853,7 +861,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
                                              unsigned long long& n_blocks,
                                              unsigned long long& busy,
                                              unsigned long long& touched_key,
-                                             PendingDone& pend) {
+                                             PendingDone& pend, unsigned pair_slot) {
   DevAtom* a = p.atoms + rc.slot;
   int last = 0;
   // A single-slice atom is complete with its only block: its first / last
@@ -961,7 +969,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         const unsigned bcount = static_cast<unsigned>(bf.count_paused);
         const unsigned bbody = static_cast<unsigned>(bf.body_parts);
         const bool here = (((tpc < 64 ? bf.mask[0] : bf.mask[1]) >> (tpc & 63)) & 1ull) && ((bf.count_paused >> 32) & 1ull) == 0u &&
-                          fence_admits(floor_prio, bprio, tenant_of(bf.count_paused)) &&
+                          fence_admits(floor_prio, bprio, tenant_of(bf.count_paused), pair_slot) &&
                           (!body_is_pair(bbody) || rank == 0u);
         st_relaxed_gpu64(&b->claim, (static_cast<unsigned long long>(bseq) << 32) | (here ? 1u : 0u));
         b->t_armed = gtimer();
@@ -1119,6 +1127,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
     mbar_init(&sh.joined, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (tid == 0 && rank == 0) {
+    // This pair's slot on its TPC (pair fences), for both CTAs; the
+    // cluster barrier below publishes the peer's copy.
+    const unsigned ps = atomicAdd(p.pair_seq + tpc, 1u);
+    sh.pair_slot = ps;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_rank(&sh.pair_slot, 1)), "r"(ps) : "memory");
+  }
   // TMEM for the pair's GEMM accumulators: allocated once for the CTA's
   // lifetime by warp 1 of both CTAs (cta_group::2: same columns in both),
   // 512 / W columns so the W workers of an SM never contend.
@@ -1128,6 +1143,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   gemm.tmem = gemv.tmem = sh.tmem_base;
+  const unsigned pslot = sh.pair_slot;
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
   unsigned long long first_start = ~0ull;
   // Remote addresses inside the pair.
@@ -1234,7 +1250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
               eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
                          static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
                          ((cp >> 32) & 1ull) == 0u &&
-                         fence_admits(floor_prio, static_cast<int>(k >> 56), tenant_of(cp));
+                         fence_admits(floor_prio, static_cast<int>(k >> 56), tenant_of(cp), pslot);
             }
             // Candidates of this snapshot, best first: a claim lost to other
             // workers (the atom ran out) moves on to the next candidate
@@ -1462,7 +1478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
     if (warp == 0 && go != kGoJoin) {
       const unsigned extra = go == kGoPair ? lane0_field(sh.run.extra, lane) : 0u;
       const int done = account_block(p, sh.rc, sh.t_start, tpc, sm, rank, lane, extra, n_blocks, busy,
-                                     sh.touched_key, sh.pend);
+                                     sh.touched_key, sh.pend, pslot);
       if (done) cur_key = 0ull;  // the atom is done: rescan rather than claim from it
       handoff = done == 2;
       __syncwarp();  // every lane has read sh.t_start / sh.rc before lane 0 rewrites them
@@ -1571,6 +1587,7 @@ struct gpuos_dev {
   unsigned* version = nullptr;
   int* fence = nullptr;
   unsigned* tc_busy = nullptr;
+  unsigned* pair_seq = nullptr;
   DevCtl* ctl = nullptr;
   int* phys2log = nullptr;
   unsigned long long* gt_scratch = nullptr;
@@ -1698,6 +1715,7 @@ Params make_params(gpuos_dev* d, bool ingest) {
   p.version = d->version;
   p.fence = d->fence;
   p.tc_busy = d->tc_busy;
+  p.pair_seq = d->pair_seq;
   p.ctl = d->ctl;
   p.phys2log = d->phys2log;
   p.ring = d->ring_d;
@@ -1848,6 +1866,7 @@ int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   CUDA_TRY(cudaMalloc(&d->version, sizeof(unsigned) * T));
   CUDA_TRY(cudaMalloc(&d->fence, sizeof(int) * T));
   CUDA_TRY(cudaMalloc(&d->tc_busy, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMalloc(&d->pair_seq, sizeof(unsigned) * T));
   CUDA_TRY(cudaMalloc(&d->ctl, sizeof(DevCtl)));
   CUDA_TRY(cudaMalloc(&d->phys2log, sizeof(int) * phys_tpcs));
   CUDA_TRY(cudaMalloc(&d->gt_scratch, sizeof(unsigned long long)));
@@ -1888,6 +1907,7 @@ int gpuos_dev_close(gpuos_dev* d) {
   cudaFree(d->version);
   cudaFree(d->fence);
   cudaFree(d->tc_busy);
+  cudaFree(d->pair_seq);
   cudaFree(d->ctl);
   cudaFree(d->phys2log);
   cudaFree(d->gt_scratch);
@@ -1927,6 +1947,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
   CUDA_TRY(cudaMemset(d->tc_busy, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->pair_seq, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->tpc_occ, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->tpc_busy, 0, sizeof(unsigned long long) * T));
   std::memset(d->ring_h, 0, sizeof(RingEntry) * d->cfg.ring_entries);
@@ -2233,6 +2254,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   CUDA_TRY(cudaMemset(d->version, 0, sizeof(unsigned) * T));
   CUDA_TRY(cudaMemset(d->fence, 0, sizeof(int) * T));
   CUDA_TRY(cudaMemset(d->tc_busy, 0, sizeof(unsigned) * T));
+  CUDA_TRY(cudaMemset(d->pair_seq, 0, sizeof(unsigned) * T));
   DevCtl ctl{};
   ctl.t_enter = ctl.t_first_block = ~0ull;
   ctl.drain = 1;
@@ -2393,6 +2415,17 @@ int gpuos_dev_set_fence_mask(gpuos_dev* d, const uint64_t mask[2], int32_t min_p
   put64(data, kFMask0, mask[0]);
   put64(data, kFMask1, mask[1]);
   data[kFPrio] = min_priority <= 0 ? 0u : static_cast<uint32_t>(map_priority(min_priority));
+  return publish(d, data);
+}
+
+int gpuos_dev_set_pair_fence(gpuos_dev* d, const uint64_t mask[2], uint32_t pair_slots, int32_t min_priority) {
+  if (!d || !mask) return fail(GPUOS_E_CONFIG, "null argument");
+  if (pair_slots > 0xffu) return fail(GPUOS_E_CONFIG, "pair_slots is an 8-bit mask");
+  uint32_t data[28] = {};
+  data[kFOp] = kOpFenceMask;
+  put64(data, kFMask0, mask[0]);
+  put64(data, kFMask1, mask[1]);
+  data[kFPrio] = (min_priority <= 0 ? 0u : static_cast<uint32_t>(map_priority(min_priority))) | (pair_slots << 8);
   return publish(d, data);
 }
 

@@ -627,6 +627,13 @@ void B200Device::set_tpc_fence(const std::vector<int>& tpcs, int min_priority, s
   check(gpuos_dev_set_tpc_owner(rt_->handle(), mask, owner, min_priority), "fence");
 }
 
+void B200Device::set_pair_fence(const std::vector<int>& tpcs, unsigned pair_slots, int min_priority) {
+  if (!rt_->running() || tpcs.empty()) return;
+  const auto m = mask_of(tpcs);
+  const std::uint64_t mask[2] = {m[0], m[1]};
+  check(gpuos_dev_set_pair_fence(rt_->handle(), mask, pair_slots, min_priority), "pair fence");
+}
+
 SimTime B200Device::request_frequency(FreqMhz f) {
   if (!freq_.supports(f)) throw ConfigError("unsupported frequency");
   return now_;  // DVFS actuation is out of scope; clocks stay at f_max

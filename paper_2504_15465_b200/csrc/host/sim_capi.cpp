@@ -82,6 +82,9 @@ void apply_knob(ScenarioConfig& c, const std::string& k, const json& v) {
   else if (k == "chain_depth") s.chain_depth = v.get<int>();
   else if (k == "chain_best_effort") s.chain_best_effort = flag();
   else if (k == "atom_lookahead") s.atom_lookahead = flag();
+  else if (k == "be_coexist") s.be_coexist = flag();
+  else if (k == "hp_pair_reserve") s.hp_pair_reserve = flag();
+  else if (k == "hp_quota_full") s.hp_quota_full = flag();
   else if (k == "atom_duration_us") s.atom_duration = duration_from_us(v.get<double>());
   else if (k == "steal_horizon_us") s.steal_horizon = duration_from_us(v.get<double>());
   else if (k == "max_outstanding_atoms") s.max_outstanding_atoms = v.get<int>();
@@ -317,6 +320,15 @@ std::string run_session(gpuos_session* s, const json& overrides) {
       if (r.body == 1u) stream_bytes += 8.0 * static_cast<double>(r.words) * static_cast<double>(a.hi - a.lo);
     }
     b["stream_bytes"] = stream_bytes;
+    // Executed work per tenant in calibrated block time (blocks x the
+    // kernel's block duration): a throughput measure that counts partial
+    // requests (a closed-loop training iteration is ~40 ms of a 1 s run).
+    std::vector<double> work_us(cfg.apps.size(), 0.0);
+    for (const AtomTimeline& a : dev.timeline())
+      if (a.tag < work_us.size())
+        work_us[a.tag] += static_cast<double>(a.hi - a.lo) *
+                          static_cast<double>(dev.kernels()[a.kernel].block_duration_at_fmax) * 1e-3;
+    b["work_us_per_app"] = work_us;
     if (want_timeline) {
       json tl = json::object();
       std::vector<long long> submit, complete, first, last, lo, hi, tag, prio, kern, ingest, armed;

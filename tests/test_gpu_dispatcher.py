@@ -340,3 +340,36 @@ def test_tpc_busy_sampler_matches_known_occupancy(api, cuda_device):
     span = c.dev_last_end_ns - c.dev_first_start_ns
     assert 19e6 <= span <= 23e6, span
     assert 0.95 * 10 * span <= busy <= 10 * span + 10 * 0.5e6, (busy, span)
+
+
+def test_pair_fence_keeps_one_pair_per_tpc(api, torch_mod):
+    """gpuos_dev_set_pair_fence: with pair slot 0 fenced against priority
+    < 21, a priority-20 atom of 1-SM blocks on one TPC runs on the slot-1
+    pair's two CTAs only (half the TPC's four workers: ~2x the span), while
+    a priority-30 atom still uses all four; lifting the fence restores it."""
+    torch = torch_mod
+    blocks, spin_ns = 16, 100_000
+
+    ideal = blocks * spin_ns / 1e3 / 4  # four workers
+
+    def span(dev, tpc, prio):
+        aid = dev.submit(0, blocks, [tpc], prio, api.GPUOS_BODY_SPIN, [spin_ns])
+        c = [x for x in wait_all(dev, 1) if x.atom_id == aid][0]
+        return (c.dev_last_end_ns - c.dev_first_start_ns) / 1e3
+
+    with api.Device() as dev:
+        dev.start()
+        # (the TPC hosting the ingest warp has one worker pair: skip it)
+        tpc = next(t for t in (40, 41, 42) if span(dev, t, 20) < 1.3 * ideal)
+        free = span(dev, tpc, 20)
+        dev.set_pair_fence([tpc], 1, 21)
+        time.sleep(0.0005)
+        fenced = span(dev, tpc, 20)
+        hp = span(dev, tpc, 30)
+        dev.set_pair_fence([tpc], 1, 0)
+        time.sleep(0.0005)
+        lifted = span(dev, tpc, 20)
+        dev.stop()
+    assert free < 1.3 * ideal and lifted < 1.3 * ideal, (free, lifted, ideal)
+    assert hp < 1.3 * ideal, (hp, ideal)
+    assert 1.8 * ideal < fenced < 2.6 * ideal, (fenced, ideal)

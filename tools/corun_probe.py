@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--only", default="none,conv,gemm,spin")
     ap.add_argument("--timing", action="store_true", help="per-block stamps (GemvDesc::timing)")
     ap.add_argument("--gemv-tpcs", default="0-73")
+    ap.add_argument("--workers", type=int, default=2)
     ap.add_argument("--packed", action="store_true", help="W pre-packed (GPUOS_GEMV_W_PACKED)")
     ap.add_argument("--bg-tpcs", default="0-73")
     args = ap.parse_args()
@@ -47,7 +48,7 @@ def main():
     Cm = torch.zeros(8192, 4096, device="cuda", dtype=torch.bfloat16)
     torch.cuda.synchronize()
     ref = w.cpu().double() @ x.cpu().double()
-    with api.Device(workers_per_sm=2) as dev:
+    with api.Device(workers_per_sm=args.workers) as dev:
         wsrc = w
         if args.packed:
             wsrc = torch.empty(dev.gemv_packed_bytes(n, k) // 2, device="cuda", dtype=torch.bfloat16)
@@ -100,7 +101,7 @@ def main():
             err = ((y.cpu().double() - ref).abs().max() / ref.abs().max()).item()
             assert err < 1e-3, err
             gb = n * k * 2 / 1e3
-            print(f"{name:5s} {'packed ' if args.packed else ''}tpcs {args.gemv_tpcs} bg {args.bg_tpcs} gemv {n}x{k}/{splits} ({gblocks} blocks): armed->end p50 {statistics.median(totals):7.2f} us"
+            print(f"{name:5s} W{args.workers} {'packed ' if args.packed else ''}tpcs {args.gemv_tpcs} bg {args.bg_tpcs} gemv {n}x{k}/{splits} ({gblocks} blocks): armed->end p50 {statistics.median(totals):7.2f} us"
                   f" ({gb / statistics.median(totals):6.0f} GB/s)  span p50 {statistics.median(spans):7.2f} us"
                   f"  p90 {sorted(totals)[int(0.9 * len(totals))]:7.2f}", flush=True)
             if phases:
