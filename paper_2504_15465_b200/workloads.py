@@ -48,6 +48,18 @@ def variant(cfg: dict, **sched) -> dict:
     return out
 
 
+def silence_apps(cfg: dict, *ids: str) -> dict:
+    """Copy in which tenants `ids` issue no requests but keep their place
+    (and quota): the other tenants' app indices -- the predictor's and
+    right-sizer's keys, which warm-started sessions carry from run to run --
+    stay those of the stacked run, so an `alone` baseline is the same
+    scheduler state minus the competition."""
+    out = dict(cfg)
+    never = {"times_ms": [1e3 * (cfg["horizon_ms"] + 1e6)]}  # (an arrival past the horizon)
+    out["apps"] = [dict(a, arrival=never) if a["id"] in ids else a for a in cfg["apps"]]
+    return out
+
+
 def without_apps(cfg: dict, *ids: str) -> dict:
     out = dict(cfg)
     out["apps"] = [a for a in cfg["apps"] if a["id"] not in ids]
@@ -97,12 +109,15 @@ def tenant_set(rank: int, time_scale: float = 10.0, horizon_ms: float = 2000.0,
     }
 
 
-def infer4(horizon_ms: float = 2000.0, rps: tuple = (120.0, 120.0, 40.0, 40.0),
-           slo_ms: tuple = (10.0, 10.0, 25.0, 25.0), tpcs: int = 74) -> dict:
+def infer4(horizon_ms: float = 2000.0, rps: tuple = (150.0, 150.0, 100.0, 100.0),
+           slo_ms: tuple = (10.0, 10.0, 25.0, 25.0), tpcs: int = 74, be_batch: int = 256) -> dict:
     """BASELINE config #2, inference stacking: four latency-critical tenants
     on one B200 -- two ResNet-50 at batch 1 and two BERT-base at batch 8
     (random-init kernel traces, models.py) -- with Poisson arrivals, equal
-    quotas and TPC stealing (atomizer on, right-sizer off)."""
+    quotas (18 TPCs each) and TPC stealing (atomizer on, right-sizer off),
+    plus a best-effort ResNet-50 training tenant (batch `be_batch`, closed
+    loop, 2-TPC quota; 0 drops it) that soaks up every TPC the inference
+    tenants leave idle -- the contention the stacking must survive."""
     from . import models
 
     traces = [models.resnet50_infer(1, ws_base=0), models.resnet50_infer(1, ws_base=10_000),
@@ -112,6 +127,9 @@ def infer4(horizon_ms: float = 2000.0, rps: tuple = (120.0, 120.0, 40.0, 40.0),
     apps = [{"id": nm, "priority": "hp", "quota": quota, "slo_ms": slo_ms[i],
              "arrival": {"poisson_rps": rps[i], "seed_offset": i}, "kernels": traces[i]}
             for i, nm in enumerate(names)]
+    if be_batch:
+        apps.append({"id": "train_be", "priority": "be", "quota": tpcs - 4 * quota, "arrival": "closed_loop",
+                     "kernels": models.resnet50_train(be_batch, ws_base=40_000)})
     return {
         "name": "infer4-b200", "device": {"gpc_count": 2, "tpcs_per_gpc": tpcs // 2},
         "policy": "full_system", "horizon_ms": horizon_ms, "seed": 2,

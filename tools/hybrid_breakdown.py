@@ -145,11 +145,11 @@ def main():
         s.run()
         s.run()
         st = s.run(timeline=True)
-        solo = workloads.without_apps(cfg, "rn50_train")
+        solo = workloads.silence_apps(cfg, "rn50_train")
         s.run(scenario={"config": solo})
         al = s.run(scenario={"config": solo}, timeline=True)
         if args.train_alone:
-            tcfg = workloads.without_apps(cfg, "llama_decode")
+            tcfg = workloads.silence_apps(cfg, "llama_decode")
             ta = s.run(scenario={"config": tcfg}, timeline=True)
     a = analyse(al, trace, label="alone")
     b = analyse(st, trace, label="stacked")
@@ -158,7 +158,7 @@ def main():
     be_trace = models.resnet50_train(256, ws_base=100_000)
     print(json.dumps({"be_rate_stacked": be_rate(st, be_trace)}))
     if args.train_alone:
-        print(json.dumps({"be_rate_alone": be_rate(ta, be_trace, decode_app=-1, be_app=0)}))
+        print(json.dumps({"be_rate_alone": be_rate(ta, be_trace, decode_app=-1, be_app=1)}))
     print(f"{'kind':40s} {'w':>3s} | {'alone span50':>12s} {'span_mean':>9s} {'gap_mean':>8s} | "
           f"{'stack span50':>12s} {'span_mean':>9s} {'gap_mean':>8s} {'be_ov':>6s}")
     for kind in a["kinds"]:

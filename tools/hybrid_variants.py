@@ -21,6 +21,10 @@ VARIANTS = {
     "H": ({"be_coexist": True, "hp_pair_reserve": True}, {}),
     "I": ({"be_coexist": True, "hp_pair_reserve": True, "atom_lookahead": True}, {}),
     "J": ({"be_coexist": True, "hp_pair_reserve": True, "hp_quota_full": True}, {}),
+    "L": ({"chain_best_effort": True}, {}),
+    "N": ({"atom_duration_us": 500.0}, {}),
+    "O": ({"atom_duration_us": 2000.0}, {}),
+    "K": ({"be_coexist": True, "hp_pair_reserve": True, "hp_quota_full": True, "chain_best_effort": True}, {}),
 }
 
 ap = argparse.ArgumentParser()
@@ -29,8 +33,12 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--only", default=",".join(VARIANTS))
 ap.add_argument("--config", default="hybrid")
 ap.add_argument("--splits", default=None, help="decode GEMV K splits, e.g. 6,8,1,9")
+ap.add_argument("--be-batch", type=int, default=None, help="infer4: best-effort training batch")
 args = ap.parse_args()
 cfg = None
+if args.be_batch is not None:
+    from paper_2504_15465_b200 import workloads  # noqa: E402
+    cfg = workloads.infer4(args.horizon_ms, be_batch=args.be_batch)
 if args.splits:
     from paper_2504_15465_b200 import workloads  # noqa: E402
     cfg = workloads.hybrid(args.horizon_ms, decode_splits=tuple(int(x) for x in args.splits.split(",")))
