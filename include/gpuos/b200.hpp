@@ -56,6 +56,10 @@ struct B200Options {
   // claimed slices, bounding how long a higher-priority atom waits for a
   // worker slot (0: whole blocks).
   std::int64_t quantum_ns = 0;
+  // DVFS actuation: request_frequency() locks the SM clock (NVML) to the
+  // power manager's choice. Off by default -- never on a pool whose
+  // operator manages clocks.
+  bool dvfs_actuate = false;
 };
 
 struct AtomTimeline {
@@ -210,7 +214,11 @@ class B200Device final : public Device {
   void run_all() override;
 
   void set_metrics_horizon(SimTime t) override { horizon_ = t; }
-  double energy_joules() const override { return 0.0; }
+  // GPU energy counter (NVML) over the last run_all(); 0 without NVML.
+  double energy_joules() const override { return energy_j_; }
+  // NVML samples at the end of the last run_all() (0 without NVML).
+  unsigned last_sm_mhz() const { return sm_mhz_; }
+  unsigned last_power_mw() const { return power_mw_; }
   double tpc_busy_integral() const override { return busy_tpc_ns_; }
   const std::map<FreqMhz, Duration>& freq_residency() const override { return residency_; }
   long blocks_executed(KernelId k) const override { return executed_.at(k); }
@@ -238,6 +246,10 @@ class B200Device final : public Device {
   SimTime host_now() const;
   void pump();
 
+  double energy_j_ = 0.0;
+  unsigned sm_mhz_ = 0, power_mw_ = 0;
+  FreqMhz locked_mhz_ = 0;  // dvfs_actuate: clock currently locked (0: none)
+  B200Options opt_;
   DeviceTopology topo_;
   FrequencyDomain freq_;
   std::unique_ptr<B200Runtime> rt_;

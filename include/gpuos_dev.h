@@ -322,6 +322,24 @@ int gpuos_dev_host_free(struct gpuos_dev* dev, void* ptr);
 
 const char* gpuos_dev_last_error(void);
 
+/* ---- power and clocks (NVML, loaded at run time) --------------------
+ * The reference models power and integrates it into energy
+ * (device.cpp:221-242) and its power manager picks frequencies
+ * (power_manager.cpp:27-105). On the B200 the energy is the GPU's own
+ * counter; a chosen frequency can be applied as a locked SM clock
+ * (B200Options::dvfs_actuate -- off wherever the operator manages clocks).
+ * By CUDA device ordinal; GPUOS_E_CUDA when NVML is unavailable.          */
+typedef struct gpuos_power_sample_t {
+  uint64_t energy_mj;            /* total energy since driver load, mJ     */
+  uint64_t clock_event_reasons;  /* NVML clocks-event (throttle) reasons   */
+  uint32_t sm_mhz, mem_mhz;      /* current clocks                         */
+  uint32_t power_mw;             /* current board power                    */
+  uint32_t reserved;
+} gpuos_power_sample_t;
+int gpuos_power_sample(int32_t cuda_device, gpuos_power_sample_t* out);
+/* Locks the SM clock to mhz (min = max); 0 restores default boosting.    */
+int gpuos_power_lock_sm_clock(int32_t cuda_device, uint32_t mhz);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,7 +49,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_memset", "gpuos_dev_last_error", "gpuos_dev_launch_workers", "gpuos_dev_consumed",
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask", "gpuos_dev_set_tpc_owner",
     "gpuos_dev_gemm_desc", "gpuos_dev_gemm_desc_splitk", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
-    "gpuos_dev_gemv_pack", "gpuos_dev_set_pair_fence",
+    "gpuos_dev_gemv_pack", "gpuos_dev_set_pair_fence", "gpuos_power_sample", "gpuos_power_lock_sm_clock",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",

@@ -517,13 +517,15 @@ VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs
 
 // ============================================================ B200Device
 B200Device::B200Device(DeviceTopology topo, FrequencyDomain freq, B200Options opt)
-    : topo_(topo), freq_(std::move(freq)) {
+    : opt_(opt), topo_(topo), freq_(std::move(freq)) {
   topo_.validate();
   freq_.validate();
   rt_ = std::make_unique<B200Runtime>(topo_.total_tpcs(), opt);
 }
 
-B200Device::~B200Device() = default;
+B200Device::~B200Device() {
+  if (locked_mhz_ != 0) gpuos_power_lock_sm_clock(opt_.device, 0);  // (best effort)
+}
 
 void B200Device::reset_run() {
   if (rt_->running()) throw InvariantError("reset_run while the dispatcher runs");
@@ -636,7 +638,15 @@ void B200Device::set_pair_fence(const std::vector<int>& tpcs, unsigned pair_slot
 
 SimTime B200Device::request_frequency(FreqMhz f) {
   if (!freq_.supports(f)) throw ConfigError("unsupported frequency");
-  return now_;  // DVFS actuation is out of scope; clocks stay at f_max
+  // Actuation (opt-in): the power manager's frequency as a locked SM clock
+  // (power_manager.cpp:27-105 decides; device.cpp:221-242 models the
+  // switch). Off: clocks stay where the operator set them.
+  if (opt_.dvfs_actuate && f != locked_mhz_) {
+    if (gpuos_power_lock_sm_clock(opt_.device, static_cast<std::uint32_t>(f)) != GPUOS_OK)
+      throw InvariantError("NVML could not lock the SM clock");
+    locked_mhz_ = f;
+  }
+  return now_;
 }
 
 void B200Device::schedule_call(SimTime t, std::function<void()> fn) {
@@ -701,6 +711,8 @@ bool B200Device::step() {
 void B200Device::run_all() {
   gpuos_dev_stats before{};
   gpuos_dev_get_stats(rt_->handle(), &before);
+  gpuos_power_sample_t p0{}, p1{};
+  const bool nvml = gpuos_power_sample(opt_.device, &p0) == GPUOS_OK;
   rt_->start();
   origin_ = gpuos_dev_now_ns(rt_->handle());
   now_ = 0;
@@ -725,7 +737,12 @@ void B200Device::run_all() {
   double busy = static_cast<double>(st.tpc_busy_ns - before.tpc_busy_ns);
   if (horizon_ > 0 && now_ > horizon_) busy *= static_cast<double>(horizon_) / static_cast<double>(now_);
   busy_tpc_ns_ = busy;
-  residency_[freq_.f_max()] = now_;
+  residency_[locked_mhz_ != 0 ? locked_mhz_ : freq_.f_max()] = now_;
+  if (nvml && gpuos_power_sample(opt_.device, &p1) == GPUOS_OK) {
+    energy_j_ = static_cast<double>(p1.energy_mj - p0.energy_mj) * 1e-3;
+    sm_mhz_ = p1.sm_mhz;
+    power_mw_ = p1.power_mw;
+  }
 }
 
 // ============================================================ MirrorDevice

@@ -154,6 +154,7 @@ B200Options b200_options(const json& o) {
   b.stream_min_words = o.value("min_words", b.stream_min_words);
   b.stream_chunk_cap = o.value("chunk_cap", b.stream_chunk_cap);
   b.quantum_ns = static_cast<std::int64_t>(o.value("quantum_us", 0.0) * 1000.0);
+  b.dvfs_actuate = o.value("dvfs_actuate", b.dvfs_actuate);
   return b;
 }
 
@@ -320,6 +321,9 @@ std::string run_session(gpuos_session* s, const json& overrides) {
       if (r.body == 1u) stream_bytes += 8.0 * static_cast<double>(r.words) * static_cast<double>(a.hi - a.lo);
     }
     b["stream_bytes"] = stream_bytes;
+    b["energy_j"] = dev.energy_joules();  // GPU energy counter over the run (NVML)
+    b["sm_mhz_end"] = dev.last_sm_mhz();
+    b["power_w_end"] = dev.last_power_mw() * 1e-3;
     // Executed work per tenant in calibrated block time (blocks x the
     // kernel's block duration): a throughput measure that counts partial
     // requests (a closed-loop training iteration is ~40 ms of a 1 s run).

@@ -48,10 +48,11 @@ def test_live_model_configs_complete(api, cuda_device, name):
     v = r["verify"]
     assert v["ok"], v
     assert v["tensor_kernels"] > 0 and v["tensor_checked"] > 0, v
-    for a in r["report"]["apps"]:
-        assert a["completed"] > 0
+    for i, a in enumerate(r["report"]["apps"]):
         if a["high_priority"]:  # requests still in flight at the horizon are not counted
-            assert a["completed"] >= a["offered"] - 3
+            assert a["completed"] > 0 and a["completed"] >= a["offered"] - 3
+        else:  # a best-effort training iteration may outlast a 150 ms run: it ran blocks
+            assert r["b200"]["work_us_per_app"][i] > 0
     tl = r["b200"]["timeline"]
     for m0, m1, t0, t1 in zip(tl["mask0"], tl["mask1"], tl["touched0"], tl["touched1"]):
         assert (t0 & ~m0) == 0 and (t1 & ~m1) == 0 and (t0 | t1) != 0
