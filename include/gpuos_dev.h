@@ -68,6 +68,10 @@ extern "C" {
                                    [256 b, 256 b + 256) of y = W . x (decode
                                    GEMV, HBM-bound, tensor-core MACs)      */
 
+/* Tenant-supplied bodies (include/gpuos_body.cuh), compiled into the
+ * dispatcher by the body plug-in build: ids GPUOS_BODY_USER0 + i; look one
+ * up by name with gpuos_dev_body_id. args[4] = GPUOS_GRID(gx, gy, gz).   */
+#define GPUOS_BODY_USER0 64u
 #define GPUOS_BODY_CONV_BF16 5u /* args: [0] = descriptor from
                                    gpuos_dev_conv_desc(); block b = 256
                                    output pixels x 256 output channels of an
@@ -321,6 +325,10 @@ int gpuos_dev_host_alloc(struct gpuos_dev* dev, uint64_t bytes, void** ptr);
 int gpuos_dev_host_free(struct gpuos_dev* dev, void* ptr);
 
 const char* gpuos_dev_last_error(void);
+
+/* Id of the tenant body GPUOS_USER_BODY(name) compiled into this library
+ * (GPUOS_BODY_USER0 + i); GPUOS_E_CONFIG if there is none. Host only.    */
+int gpuos_dev_body_id(const char* name, uint32_t* id);
 
 /* ---- power and clocks (NVML, loaded at run time) --------------------
  * The reference models power and integrates it into energy

@@ -37,6 +37,22 @@ GPUOS_BODY_CONV_BF16 = 5
 GPUOS_GEMM_OUT_BF16 = 1
 GPUOS_GEMV_OUT_BF16 = 1
 GPUOS_GEMV_W_PACKED = 2
+GPUOS_BODY_USER0 = 64
+
+
+def grid(gx: int, gy: int = 1, gz: int = 1) -> int:
+    """args[4] of a tenant body (GPUOS_GRID)."""
+    return gx | (gy << 21) | (gz << 42)
+
+
+def body_id(name: str) -> int:
+    """Id of the tenant body GPUOS_USER_BODY(name) compiled into the library."""
+    lib = library()
+    out = C.c_uint32()
+    rc = lib.gpuos_dev_body_id(name.encode(), C.byref(out))
+    if rc != 0:
+        raise GpuosError(rc, lib.gpuos_dev_last_error().decode())
+    return out.value
 GPUOS_E_FULL = -5
 GPUOS_DEV_DEFER_WORKERS = 1
 
@@ -50,6 +66,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask", "gpuos_dev_set_tpc_owner",
     "gpuos_dev_gemm_desc", "gpuos_dev_gemm_desc_splitk", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
     "gpuos_dev_gemv_pack", "gpuos_dev_set_pair_fence", "gpuos_power_sample", "gpuos_power_lock_sm_clock",
+    "gpuos_dev_body_id",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -153,6 +170,7 @@ def library() -> C.CDLL:
         "gpuos_dev_fill_bf16": (C.c_int, [P, P, C.c_uint64, C.c_uint64]),
         "gpuos_dev_gemv_pack": (C.c_int, [P, P, P, C.c_int64, C.c_int64]),
         "gpuos_dev_set_pair_fence": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_uint32, C.c_int32]),
+        "gpuos_dev_body_id": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint32)]),
         "gpuos_dev_gemv_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_uint32, C.c_int32,
                                           C.POINTER(P), C.POINTER(C.c_int64)]),
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,

@@ -49,6 +49,7 @@
 #include "gemv_body.cuh"
 #include "conv_body.cuh"
 #include "gpuos_dev.h"
+#include "gpuos_user_bodies.cuh"  // generated (build.py): tenant bodies
 #include "ptx.cuh"
 
 namespace gpuos_dev_impl {
@@ -1061,7 +1062,32 @@ __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned r
     case GPUOS_BODY_CONV_BF16: body_conv2(rc.cmd, tid, rank, gemm, gate, tiles, nt); break;
     case GPUOS_BODY_SPIN: body_spin(rc.cmd, tid); break;
     case GPUOS_BODY_GEMM_BF16: body_gemm2(rc.cmd, tid, rank, gemm, gate, tiles, nt); break;
-    default: break;
+    default:
+      if (rc.cmd.body >= GPUOS_BODY_USER0) {
+        // A tenant-supplied body (include/gpuos_body.cuh): the prelude's
+        // blockIdx recovery from the linear index, then the
+        // tenant's code on this CTA's 256 threads and shared tile region.
+        const unsigned long long g = rc.cmd.args[4];
+        gpuos_block b;
+        b.block = rc.cmd.block;
+        b.gx = static_cast<unsigned>(g & 0x1fffffull);
+        b.gy = static_cast<unsigned>((g >> 21) & 0x1fffffull);
+        b.gz = static_cast<unsigned>((g >> 42) & 0x1fffffull);
+        if (b.gx == 0u) b.gx = 1u;
+        if (b.gy == 0u) b.gy = 1u;
+        if (b.gz == 0u) b.gz = 1u;
+        const unsigned long long lin = static_cast<unsigned long long>(rc.cmd.block);
+        b.x = static_cast<unsigned>(lin % b.gx);
+        b.y = static_cast<unsigned>((lin / b.gx) % b.gy);
+        b.z = static_cast<unsigned>(lin / (static_cast<unsigned long long>(b.gx) * b.gy));
+        b.tid = tid;
+        b.part = rc.cmd.part;
+        b.parts = rc.cmd.parts;
+        b.smem = pipe.tiles;
+        b.smem_bytes = pipe.stages * kTile;
+        gpuos_user_bodies::run(rc.cmd.body - GPUOS_BODY_USER0, b, rc.cmd.args);
+      }
+      break;
   }
 }
 
@@ -1768,7 +1794,8 @@ unsigned tmem_cols_for(int workers_per_sm) {
 
 bool known_body(uint32_t b) {
   return b == GPUOS_BODY_STREAM || b == GPUOS_BODY_SPIN || b == GPUOS_BODY_GEMM_BF16 ||
-         b == GPUOS_BODY_GEMV_BF16 || b == GPUOS_BODY_CONV_BF16;
+         b == GPUOS_BODY_GEMV_BF16 || b == GPUOS_BODY_CONV_BF16 ||
+         (b >= GPUOS_BODY_USER0 && b - GPUOS_BODY_USER0 < gpuos_user_bodies::kCount);
 }
 
 // Argument checks the device bodies rely on (empty string: valid).
@@ -1786,6 +1813,16 @@ std::string body_args_error(const gpuos_atom_desc& a) {
 extern "C" {
 
 const char* gpuos_dev_last_error(void) { return g_last_error.c_str(); }
+
+int gpuos_dev_body_id(const char* name, uint32_t* id) {
+  if (!name || !id) return fail(GPUOS_E_CONFIG, "null argument");
+  for (unsigned i = 0; i < gpuos_user_bodies::kCount; ++i)
+    if (std::strcmp(gpuos_user_bodies::kNames[i], name) == 0) {
+      *id = GPUOS_BODY_USER0 + i;
+      return GPUOS_OK;
+    }
+  return fail(GPUOS_E_CONFIG, std::string("no tenant body named ") + name + " in this library");
+}
 
 int gpuos_dev_open(const gpuos_dev_config* cfg_in, gpuos_dev** out) {
   if (out == nullptr) return fail(GPUOS_E_CONFIG, "null out pointer");

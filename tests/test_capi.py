@@ -101,3 +101,29 @@ def test_ctypes_structs_match_the_header(api, tmp_path):
         py = structs[c_name]
         want = ctypes.sizeof(py) if field == "size" else getattr(py, field).offset
         assert int(value) == want, (c_name, field, value, want)
+
+
+def test_tenant_body_table(api):
+    """The built-in tenant bodies are registered by name (host table, no GPU)."""
+    ids = {n: api.body_id(n) for n in ("grid_probe", "rmsnorm_bf16", "silu_mul_bf16")}
+    assert sorted(ids.values()) == [api.GPUOS_BODY_USER0 + i for i in range(3)]
+    with pytest.raises(api.GpuosError) as e:
+        api.body_id("missing")
+    assert e.value.code == -2
+
+
+def test_body_table_generation(tmp_path):
+    """build.generate_body_table: GPUOS_USER_BODY(name) declarations of the
+    body sources get ids in sorted-name order; duplicates are an error."""
+    from paper_2504_15465_b200 import build
+
+    a = tmp_path / "a.cu"
+    a.write_text("GPUOS_USER_BODY(zeta) {}\nGPUOS_USER_BODY( alpha ) {}\n")
+    b = tmp_path / "b.cu"
+    b.write_text("// GPUOS_USER_BODY(not_at_line_start) is a comment\nGPUOS_USER_BODY(mid) {}\n")
+    text = open(build.generate_body_table([str(a), str(b)], str(tmp_path))).read()
+    assert "case 0: alpha(b, a);" in text and "case 1: mid(b, a);" in text and "case 2: zeta(b, a);" in text
+    assert "not_at_line_start" not in text.split("kNames")[1]
+    b.write_text("GPUOS_USER_BODY(alpha) {}\n")
+    with pytest.raises(RuntimeError):
+        build.generate_body_table([str(a), str(b)], str(tmp_path))
