@@ -44,7 +44,10 @@ struct alignas(128) ConvDesc {
   unsigned pixels;               // N P Q
   unsigned pair_tiles, k_tiles, c_blocks, flags;
   unsigned n_tile;               // output channels per block: 64, 128 or 256
+  unsigned pad0;
+  unsigned long long* timing;    // optional: 4 globaltimer stamps per tile (profiling, tools/conv_batch.py)
 };
+static_assert(offsetof(ConvDesc, timing) == 336, "ConvDesc layout (tools/conv_batch.py)");
 
 __device__ __forceinline__ void tma_load_im2col_pair(void* dst, const CUtensorMap* map, int c0, int w0,
                                                      int h0, int n0, unsigned short off_w,
@@ -79,6 +82,8 @@ __device__ __forceinline__ void conv2_tile(const ConvDesc* D, unsigned blk, int 
     cluster_sync_all();
     return;
   }
+  unsigned long long* tm = D->timing != nullptr && rank == 0 ? D->timing + 4ull * blk : nullptr;
+  if (tm && tid == 0) tm[0] = gtimer();
   if (tid == 0) {
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->act) : "memory");
     asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&D->wgt) : "memory");
@@ -133,6 +138,7 @@ __device__ __forceinline__ void conv2_tile(const ConvDesc* D, unsigned blk, int 
       const unsigned s = static_cast<unsigned>(k % S);
       mbar_wait_bounded(G.full + s, static_cast<unsigned>((k / S) & 1), *G.guard);
       tc_fence_after();
+      if (tm && j == 0) tm[1] = gtimer();
       const unsigned a0 = smem_u32(G.tiles + s * kGemmStageBytes);
       const unsigned b0 = a0 + kGemmABytes;
 #pragma unroll
@@ -147,15 +153,20 @@ __device__ __forceinline__ void conv2_tile(const ConvDesc* D, unsigned blk, int 
   gate_wait(gate, *G.guard);  // (unbounded: the predecessor may run long)
   mbar_wait_bounded(G.accum, G.accum_used & 1u, *G.guard);
   tc_fence_after();
+  if (tm && tid == 0) tm[2] = gtimer();
   // The tile's rows are consecutive rows of the [N P Q, K] output: the
   // GEMM body's staged, coalesced epilogue applies as is.
   const unsigned col0 = kt * D->n_tile;
   epilogue_staged(G, tid, m0, col0, D->pixels, D->k - col0 < D->n_tile ? D->k : col0 + D->n_tile, D->k,
                   (D->flags & kConvOutBf16) != 0, reinterpret_cast<void*>(D->y));
   tc_fence_before();
+  if (tm) {
+    __syncthreads();
+    if (tid == 0) tm[3] = gtimer();
+  }
   G.kb_used = g0 + nk;
   G.accum_used += 1;
-  cluster_sync_all();  // both halves written, both TMEMs read; the next tile posted
+  cluster_sync_tile_end();  // both halves written, both TMEMs read; the next tile posted
 }
 
 // A pair run of conv tiles (see PairTiles, gemm_body.cuh).

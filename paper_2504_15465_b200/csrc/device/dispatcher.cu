@@ -773,6 +773,9 @@ struct NextTile {
     }
     run.next = nb;
     st_cluster_u64(peer_next, static_cast<unsigned long long>(nb));
+    // (the tile-end barrier arrives relaxed: publish the post here, before
+    // this thread's epilogue stores)
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
   }
 };
 

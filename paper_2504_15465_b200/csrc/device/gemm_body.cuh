@@ -231,6 +231,17 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
+// End of a pair tile: a relaxed arrive, so the epilogue's global stores are
+// not made cluster-visible first (nothing in the pair reads them; the
+// finisher's fence and acq_rel count publish them to other consumers).
+// What the barrier must order -- TMEM reads before the next tile's MMAs
+// (tcgen05 fences around it), shared-memory staging before the next TMA
+// writes, and the posted next tile (NextTile fences its own store) -- does
+// not need the release.
+__device__ __forceinline__ void cluster_sync_tile_end() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
 
 // Called once per CTA by all threads (barrier memory at smem + 128 .. 256;
 // the STREAM ring's barriers occupy smem + 0 .. 128, tiles start at 1024).
@@ -508,7 +519,7 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk_in, i
   // Both halves of the tile are written (and both TMEMs read) before the
   // leader records the tile or issues the next tile's MMAs; the posted next
   // tile is visible in both CTAs after it.
-  cluster_sync_all();
+  cluster_sync_tile_end();
   if (D->splits > 1 && rank == 0) {
     // Split-K: the tile's last split converts the accumulator.
     __shared__ int last_split;
