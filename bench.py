@@ -511,9 +511,11 @@ def gemm_saturation(api, local: int, args) -> dict:
     with api.Device(device=local, workers_per_sm=args.workers_per_sm) as dev:
         desc, blocks, tm, tn = dev.gemm_desc(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k,
                                              bf16_out=True)
-        # Two back-to-back kernels in one launch (the dispatcher's ~13 us
-        # start is paid once per persistent-kernel lifetime in live mode).
-        kernels = 2
+        # One kernel per launch: at 8192^3 (~0.7 ms) the dispatcher's ~13 us
+        # start is ~2 %; two back-to-back copies measured lower (1484 vs
+        # 1540 TF/s: the second atom's tiles interleave with the first's and
+        # break the grouped raster's L2 reuse -- DRAM 2.07 GB for 0.81 GB).
+        kernels = 1
         descs = [api.Device.desc(i * blocks // n_atoms, (i + 1) * blocks // n_atoms, range(74), 20,
                                  api.GPUOS_BODY_GEMM_BF16, [desc]) for i in range(n_atoms)] * kernels
         for _ in range(5):  # best of 5 (MEASURED_PEAKS' cuBLAS figure is a best of 10)

@@ -163,6 +163,8 @@ class B200Runtime {
     std::vector<void*> bufs;  // gemm: A, B, C; gemv: W, x, y; conv: x, w, y
     void* desc = nullptr;
     std::int64_t blocks = 0;
+    std::uint32_t body = 0;          // device body id (tenant bodies)
+    std::uint64_t args[5] = {0, 0, 0, 0, 0};  // tenant bodies' atom args
     BodyRef ref;              // kind + shape (verify_kernels)
   };
   // Sampled float64 check of a tensor body's output (verify_kernels).

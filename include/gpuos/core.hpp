@@ -84,6 +84,10 @@ enum class BodyKind : std::uint32_t {
   Spin = 3,      // fixed-duration compute spin (calibration / control)
   GemvBf16 = 4,  // decode GEMV (HBM-bound), 256 rows of W per block
   ConvBf16 = 5,  // NHWC implicit-GEMM convolution on tcgen05
+  // Tenant-supplied bodies (include/gpuos_body.cuh, csrc/bodies): the device
+  // id comes from gpuos_dev_body_id by name.
+  RmsNormBf16 = 6,  // p = [rows, d]: one row per block
+  SiluMulBf16 = 7,  // p = [n, chunk]: ceil(n / chunk) blocks
 };
 
 struct BodyRef {

@@ -1156,13 +1156,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
     mbar_init(&sh.joined, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid == 0 && rank == 0) {
-    // This pair's slot on its TPC (pair fences), for both CTAs; the
-    // cluster barrier below publishes the peer's copy.
-    const unsigned ps = atomicAdd(p.pair_seq + tpc, 1u);
-    sh.pair_slot = ps;
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_rank(&sh.pair_slot, 1)), "r"(ps) : "memory");
-  }
+  // This pair's slot on its TPC (pair fences): drawn by the leader; the peer
+  // reads it from the leader's shared memory after the cluster barrier below
+  // (no distributed-shared-memory access before both CTAs have started).
+  if (tid == 0 && rank == 0) sh.pair_slot = atomicAdd(p.pair_seq + tpc, 1u);
   // TMEM for the pair's GEMM accumulators: allocated once for the CTA's
   // lifetime by warp 1 of both CTAs (cta_group::2: same columns in both),
   // 512 / W columns so the W workers of an SM never contend.
@@ -1172,7 +1169,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   gemm.tmem = gemv.tmem = sh.tmem_base;
-  const unsigned pslot = sh.pair_slot;
+  unsigned pslot = sh.pair_slot;
+  if (rank != 0) {
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(pslot) : "r"(map_rank(&sh.pair_slot, 0)) : "memory");
+  }
   unsigned long long n_blocks = 0, busy = 0, retries = 0;
   unsigned long long first_start = ~0ull;
   // Remote addresses inside the pair.

@@ -163,6 +163,40 @@ const B200Runtime::TensorBody& B200Runtime::tensor_body(const BodyRef& b) {
     check(gpuos_dev_gemv_desc(dev_, W, X, Y, N, K, GPUOS_GEMV_OUT_BF16, static_cast<int32_t>(splits),
                               &t.desc, &t.blocks),
           "gemv descriptor");
+  } else if (b.kind == BodyKind::RmsNormBf16 || b.kind == BodyKind::SiluMulBf16) {
+    // Tenant bodies (csrc/bodies/llama_elementwise.cu), by name.
+    const bool rms = b.kind == BodyKind::RmsNormBf16;
+    check(gpuos_dev_body_id(body_kind_name(b.kind), &t.body), "tenant body lookup");
+    if (rms) {
+      const std::int64_t rows = b.p0, d = b.p1;
+      if (rows <= 0 || d <= 0 || d % 8 != 0) throw ConfigError("rmsnorm_bf16 needs p = [rows, d], d % 8 == 0");
+      void* X = tensor(static_cast<std::uint64_t>(rows) * d, true);
+      void* Wn = tensor(static_cast<std::uint64_t>(d), true);
+      void* Y = tensor(static_cast<std::uint64_t>(rows) * d, false);
+      const float eps = 1e-5f;
+      std::uint32_t eb;
+      std::memcpy(&eb, &eps, 4);
+      t.args[0] = reinterpret_cast<std::uint64_t>(X);
+      t.args[1] = reinterpret_cast<std::uint64_t>(Wn);
+      t.args[2] = reinterpret_cast<std::uint64_t>(Y);
+      t.args[3] = static_cast<std::uint64_t>(d) | (static_cast<std::uint64_t>(eb) << 32);
+      t.args[4] = static_cast<std::uint64_t>(rows);  // GPUOS_GRID(rows)
+      t.blocks = rows;
+    } else {
+      const std::int64_t n = b.p0, chunk = b.p1;
+      if (n <= 0 || n > 0xffffffffll || chunk <= 0 || chunk % 8 != 0)
+        throw ConfigError("silu_mul_bf16 needs p = [n, chunk], chunk % 8 == 0");
+      void* G = tensor(static_cast<std::uint64_t>(n) + 8, true);
+      void* U = tensor(static_cast<std::uint64_t>(n) + 8, true);
+      void* O = tensor(static_cast<std::uint64_t>(n) + 8, false);
+      t.blocks = (n + chunk - 1) / chunk;
+      t.args[0] = reinterpret_cast<std::uint64_t>(G);
+      t.args[1] = reinterpret_cast<std::uint64_t>(U);
+      t.args[2] = reinterpret_cast<std::uint64_t>(O);
+      t.args[3] = static_cast<std::uint64_t>(n) | (static_cast<std::uint64_t>(chunk) << 32);
+      t.args[4] = static_cast<std::uint64_t>(t.blocks);
+    }
+    t.desc = reinterpret_cast<void*>(t.args[2]);  // (verify key: the output buffer)
   } else {
     const std::int64_t n = b.p0, h = b.p1, w = b.p2, c = b.param(3), k = b.param(4), r = b.param(5),
                        sd = b.param(6), pad = b.param(7), st = std::max<std::int64_t>(1, b.param(8));
@@ -213,6 +247,37 @@ void B200Runtime::verify_tensor(const TensorBody& t, VerifyReport& rep) {
   std::vector<std::uint16_t> ra, rb, out1;
   constexpr int kSamples = 48;
   ++rep.tensor_kernels;
+  if (b.kind == BodyKind::RmsNormBf16) {
+    const std::uint64_t rows = static_cast<std::uint64_t>(b.p0), d = static_cast<std::uint64_t>(b.p1);
+    fetch(t.bufs[1], 0, d, rb);  // w
+    for (int i = 0; i < kSamples / 8; ++i) {
+      const std::uint64_t row = next(rows);
+      fetch(t.bufs[0], row * d, d, ra);
+      fetch(t.bufs[2], row * d, d, out1);
+      double ss = 0;
+      for (std::uint64_t k = 0; k < d; ++k) ss += static_cast<double>(bf16_to_float(ra[k])) * bf16_to_float(ra[k]);
+      const double scale = 1.0 / std::sqrt(ss / static_cast<double>(d) + 1e-5);
+      for (int j = 0; j < 8; ++j) {
+        const std::uint64_t k = next(d);
+        const double ref = bf16_to_float(ra[k]) * scale * bf16_to_float(rb[k]);
+        judge(bf16_to_float(out1[k]), ref, std::fabs(ref) * 8.0);
+      }
+    }
+    return;
+  }
+  if (b.kind == BodyKind::SiluMulBf16) {
+    const std::uint64_t n = static_cast<std::uint64_t>(b.p0);
+    for (int i = 0; i < kSamples; ++i) {
+      const std::uint64_t e = next(n);
+      fetch(t.bufs[0], e, 1, ra);
+      fetch(t.bufs[1], e, 1, rb);
+      fetch(t.bufs[2], e, 1, out1);
+      const double g = bf16_to_float(ra[0]);
+      const double ref = g / (1.0 + std::exp(-g)) * bf16_to_float(rb[0]);
+      judge(bf16_to_float(out1[0]), ref, std::fabs(ref) * 8.0);
+    }
+    return;
+  }
   if (b.kind == BodyKind::GemmBf16 || b.kind == BodyKind::GemvBf16) {
     const bool gemm = b.kind == BodyKind::GemmBf16;
     const std::uint64_t M = gemm ? static_cast<std::uint64_t>(b.p0) : 1;
@@ -348,6 +413,17 @@ B200Runtime::Resolved B200Runtime::resolve_body(const SimKernelSpec& spec) {
       r.args[0] = reinterpret_cast<std::uint64_t>(t.desc);
       break;
     }
+    case BodyKind::RmsNormBf16:
+    case BodyKind::SiluMulBf16: {
+      const TensorBody& t = tensor_body(b);
+      if (spec.total_blocks != t.blocks)
+        throw ConfigError(std::string(body_kind_name(b.kind)) + " kernel of this shape has " +
+                          std::to_string(t.blocks) + " blocks, the trace says " +
+                          std::to_string(spec.total_blocks));
+      r.body = t.body;
+      for (int i = 0; i < 5; ++i) r.args[i] = t.args[i];
+      break;
+    }
     case BodyKind::None:
       break;
   }
@@ -480,10 +556,13 @@ VerifyReport B200Runtime::verify_kernels(const std::vector<SimKernelSpec>& specs
       }
     }
     // A tensor-core kernel every block of which ran: its output values.
+    // (Tenant bodies: keyed by their output buffer, args[2].)
+    const bool tenant = r.body >= GPUOS_BODY_USER0;
     if (complete && (r.body == GPUOS_BODY_GEMM_BF16 || r.body == GPUOS_BODY_GEMV_BF16 ||
-                     r.body == GPUOS_BODY_CONV_BF16)) {
-      const auto it = tensor_of_desc_.find(r.args[0]);
-      if (it != tensor_of_desc_.end() && verified.insert(r.args[0]).second) verify_tensor(*it->second, rep);
+                     r.body == GPUOS_BODY_CONV_BF16 || tenant)) {
+      const std::uint64_t key = tenant ? r.args[2] : r.args[0];
+      const auto it = tensor_of_desc_.find(key);
+      if (it != tensor_of_desc_.end() && verified.insert(key).second) verify_tensor(*it->second, rep);
     }
   }
   // Body outputs against the CPU restatement.

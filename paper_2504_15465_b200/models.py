@@ -106,6 +106,20 @@ class Builder:
             "blocks": blocks, "block_us": round(per_block / (TPC_GBS * 1e3), 3), "s": 0.2, "occ": 1,
             "body": {"kind": "gemv_bf16", "ws": self._next(), "p": [n, k, splits]}})
 
+    def rmsnorm(self, rows, d) -> None:
+        """RMSNorm as the tenant body rmsnorm_bf16 (csrc/bodies): one row per
+        block, 256 threads, HBM-bound (x and y: 4 d bytes per row)."""
+        self.kernels.append({
+            "blocks": rows, "block_us": round(max(1.0, 4.0 * d / (TPC_GBS / 4 * 1e3)), 3), "s": 0.2, "occ": 4,
+            "body": {"kind": "rmsnorm_bf16", "ws": self._next(), "p": [rows, d]}})
+
+    def silu_mul(self, n, chunk=2048) -> None:
+        """SiLU(gate) * up as the tenant body silu_mul_bf16: `chunk` elements
+        per block (6 bytes each: gate, up, out)."""
+        self.kernels.append({
+            "blocks": -(-n // chunk), "block_us": round(max(1.0, 6.0 * chunk / (TPC_GBS / 4 * 1e3)), 3),
+            "s": 0.2, "occ": 4, "body": {"kind": "silu_mul_bf16", "ws": self._next(), "p": [n, chunk]}})
+
     def stream(self, nbytes) -> None:
         """Elementwise kernel moving `nbytes` (read + written): blocks of at
         most STREAM_WORDS u32, sized (in 1 KiB steps) to the bytes moved, so
@@ -217,15 +231,15 @@ def llama3_8b_decode(context: int = 1024, ws_base: int = 0,
     b = Builder(ws_base)
     d, kv, ffn, vocab = 4096, 1024, 14336, 128256
     for _ in range(32):
-        b.stream(d * 2 * 2)                              # RMSNorm
-        b.gemv(d + 2 * kv, d, splits[0])                 # QKV (144 blocks)
-        b.stream(context * kv * 2 * 2 + d * 2 * 2)       # RoPE + attention over K and V
-        b.gemv(d, d, splits[1])                          # output projection (128 blocks)
-        b.stream(d * 2 * 3)                              # residual + RMSNorm
+        b.rmsnorm(1, d)                                  # RMSNorm (tenant body)
+        b.gemv(d + 2 * kv, d, splits[0])                 # QKV (72 blocks)
+        b.stream(context * kv * 2 * 2 + d * 2 * 2)       # RoPE + attention over K and V (byte-equivalent)
+        b.gemv(d, d, splits[1])                          # output projection (64 blocks)
+        b.rmsnorm(1, d)                                  # residual + RMSNorm (tenant body)
         b.gemv(2 * ffn, d, splits[2])                    # gate + up (112 blocks)
-        b.stream(2 * ffn * 2 + ffn * 2)                  # SiLU(gate) * up
-        b.gemv(d, ffn, splits[3])                        # down projection (144 blocks)
-    b.stream(d * 2 * 2)                                  # final norm
+        b.silu_mul(ffn)                                  # SiLU(gate) * up (tenant body, 7 blocks)
+        b.gemv(d, ffn, splits[3])                        # down projection (64 blocks)
+    b.rmsnorm(1, d)                                      # final norm
     b.gemv(vocab, d, 1)                                  # LM head
     return b.kernels
 
@@ -244,6 +258,10 @@ def summary(kernels: list[dict]) -> dict:
             Q = (w + 2 * pad - s) // st + 1
             flops += 2.0 * n * P * Q * kk * r * s * c
             nbytes += 2.0 * (n * h * w * c + kk * r * s * c + n * P * Q * kk)
+        elif body["kind"] == "rmsnorm_bf16":
+            nbytes += 2.0 * (2 * p[0] * p[1] + p[1])
+        elif body["kind"] == "silu_mul_bf16":
+            nbytes += 6.0 * p[0]
         elif body["kind"] == "gemv_bf16":
             flops += 2.0 * p[0] * p[1]
             nbytes += 2.0 * (p[0] * p[1] + p[1] + p[0])
