@@ -813,6 +813,7 @@ __device__ __forceinline__ unsigned atom_exch_acq_rel32(unsigned* p, unsigned v)
 // __syncwarp.
 __device__ __forceinline__ void write_done(const Params& p, PendingDone& d, unsigned lane) {
   const DevAtom* a = p.atoms + d.slot;
+  __syncwarp();  // every lane has read d.slot before lane 0 retires the record (d.flags)
   if (lane == 0) {
     // Completion record (the host is waiting on it), in the slot's own
     // record: four 16-byte chunks, each three data words and the ticket
