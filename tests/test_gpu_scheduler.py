@@ -100,7 +100,7 @@ def test_live_fig7_verified(api, cuda_device):
 def test_live_mechanisms_lc_tail_and_be_throughput(api, cuda_device):
     """Block-granular revocation + 25 us preemption quanta: the LC tenant's
     p99 stays near its alone p99 while BE runs far faster than a static
-    partition (north-star targets 1.2x and 1.3x; asserted with margin)."""
+    partition (the north-star targets, 1.2x and 1.3x, asserted as such)."""
     import sys
 
     sys.path.insert(0, os.path.dirname(GOLDEN))
@@ -126,9 +126,9 @@ def test_live_mechanisms_lc_tail_and_be_throughput(api, cuda_device):
         return live, static, p_live, p_alone
 
     live, static, p_live, p_alone = measure()
-    if p_live > 1.35 * p_alone:  # one re-measurement: the host loop shares the CPU with the test
+    if p_live > 1.2 * p_alone:  # one re-measurement: the host loop shares the CPU with the test
         live, static, p_live, p_alone = measure()
-    assert p_live <= 1.35 * p_alone, (p_live, p_alone)
+    assert p_live <= 1.2 * p_alone, (p_live, p_alone)
     be = sum(r["blocks_per_app"][1] for r in live) / sum(r["b200"]["kernel_ms"] for r in live)
     be_static = sum(r["blocks_per_app"][1] for r in static) / sum(r["b200"]["kernel_ms"] for r in static)
     assert be >= 1.3 * be_static, (be, be_static)
@@ -148,3 +148,23 @@ def test_baseline_policies_run_live(api, cuda_device):
     for row in r.values():
         assert row["lc_completed"] > 0 and row["be_atoms"] > 0
     assert r["full_system"]["lc_p99_ms"] < r["mps_like"]["lc_p99_ms"]
+
+
+def test_inference_stacking_keeps_every_lc_tail(api, cuda_device):
+    """BASELINE config #2 under contention (configs.run("infer4")): four LC
+    inference tenants beside a training tenant, TPC utilisation >= 0.5, every
+    LC tenant's p99 within 1.2x of its alone p99 (~400-600 requests each), 100 %
+    SLO attainment."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(GOLDEN))
+    from paper_2504_15465_b200 import configs
+
+    r = configs.run("infer4", horizon_ms=2000.0, reps=2)
+    assert r["tpc_utilization"] >= 0.5, r["tpc_utilization"]
+    for app, row in r["apps"].items():
+        if row["priority"] != "hp":
+            continue
+        assert row["stacked"]["completed"] >= 350, (app, row["stacked"]["completed"])
+        assert row["p99_vs_alone"] <= 1.2, (app, row["p99_vs_alone"])
+        assert row["slo_attainment"] == 1.0, (app, row["slo_attainment"])
