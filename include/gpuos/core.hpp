@@ -88,6 +88,7 @@ enum class BodyKind : std::uint32_t {
   // id comes from gpuos_dev_body_id by name.
   RmsNormBf16 = 6,  // p = [rows, d]: one row per block
   SiluMulBf16 = 7,  // p = [n, chunk]: ceil(n / chunk) blocks
+  AttnDecodeBf16 = 8,  // p = [ctx, chunk]: GQA decode attention, 8 x ceil(ctx / chunk) blocks
 };
 
 struct BodyRef {

@@ -163,6 +163,25 @@ const B200Runtime::TensorBody& B200Runtime::tensor_body(const BodyRef& b) {
     check(gpuos_dev_gemv_desc(dev_, W, X, Y, N, K, GPUOS_GEMV_OUT_BF16, static_cast<int32_t>(splits),
                               &t.desc, &t.blocks),
           "gemv descriptor");
+  } else if (b.kind == BodyKind::AttnDecodeBf16) {
+    // Decode attention (csrc/bodies/llama_attention.cu): q [32][128], K and V
+    // caches [ctx][8][128], workspace (result, counters, chunk partials).
+    check(gpuos_dev_body_id(body_kind_name(b.kind), &t.body), "tenant body lookup");
+    const std::int64_t ctx = b.p0, chunk = b.p1 > 0 ? b.p1 : 128;
+    if (ctx <= 0 || chunk > 256 || chunk <= 0) throw ConfigError("attn_decode_bf16 needs p = [ctx, chunk <= 256]");
+    const std::int64_t chunks = (ctx + chunk - 1) / chunk;
+    void* Q = tensor(32 * 128, true);
+    void* KV = tensor(static_cast<std::uint64_t>(2 * ctx * 8 * 128), true);
+    const std::uint64_t ws_elems = (8448 + 32ull * chunks * 130 * 4) / 2;
+    void* WS = tensor(ws_elems, false);
+    check(gpuos_dev_memset(dev_, WS, 0, ws_elems * 2), "attention workspace");
+    t.blocks = chunks * 8;
+    t.args[0] = reinterpret_cast<std::uint64_t>(Q);
+    t.args[1] = reinterpret_cast<std::uint64_t>(KV);
+    t.args[2] = reinterpret_cast<std::uint64_t>(WS);
+    t.args[3] = static_cast<std::uint64_t>(ctx) | (static_cast<std::uint64_t>(chunk) << 32);
+    t.args[4] = static_cast<std::uint64_t>(chunks) | (8ull << 21);  // GPUOS_GRID(chunks, 8)
+    t.desc = reinterpret_cast<void*>(t.args[2]);  // (verify key: the result buffer)
   } else if (b.kind == BodyKind::RmsNormBf16 || b.kind == BodyKind::SiluMulBf16) {
     // Tenant bodies (csrc/bodies/llama_elementwise.cu), by name.
     const bool rms = b.kind == BodyKind::RmsNormBf16;
@@ -261,6 +280,46 @@ void B200Runtime::verify_tensor(const TensorBody& t, VerifyReport& rep) {
         const std::uint64_t k = next(d);
         const double ref = bf16_to_float(ra[k]) * scale * bf16_to_float(rb[k]);
         judge(bf16_to_float(out1[k]), ref, std::fabs(ref) * 8.0);
+      }
+    }
+    return;
+  }
+  if (b.kind == BodyKind::AttnDecodeBf16) {
+    // Sampled query heads recomputed in float64: RoPE (base 500000,
+    // interleaved pairs) at position ctx, softmax over the whole cache.
+    const std::int64_t ctx = b.p0;
+    std::vector<std::uint16_t> q, kv, out;
+    fetch(t.bufs[0], 0, 32 * 128, q);
+    fetch(t.bufs[1], 0, static_cast<std::uint64_t>(2 * ctx * 8 * 128), kv);
+    fetch(t.bufs[2], 0, 32 * 128, out);
+    for (int i = 0; i < 6; ++i) {
+      const int h = static_cast<int>(next(32)), g = h / 4;
+      double qr[128];
+      for (int j = 0; j < 64; ++j) {
+        const double inv = std::pow(500000.0, -2.0 * j / 128.0), a = static_cast<double>(ctx) * inv;
+        const double x0 = bf16_to_float(q[h * 128 + 2 * j]), x1 = bf16_to_float(q[h * 128 + 2 * j + 1]);
+        qr[2 * j] = x0 * std::cos(a) - x1 * std::sin(a);
+        qr[2 * j + 1] = x0 * std::sin(a) + x1 * std::cos(a);
+      }
+      std::vector<double> s(static_cast<std::size_t>(ctx));
+      double m = -1e300;
+      for (std::int64_t p = 0; p < ctx; ++p) {
+        double d = 0;
+        for (int j = 0; j < 128; ++j) d += qr[j] * bf16_to_float(kv[static_cast<std::size_t>((p * 8 + g) * 128 + j)]);
+        s[static_cast<std::size_t>(p)] = d / std::sqrt(128.0);
+        m = std::max(m, s[static_cast<std::size_t>(p)]);
+      }
+      double l = 0;
+      for (auto& v : s) l += (v = std::exp(v - m));
+      for (int k = 0; k < 4; ++k) {
+        const int j = static_cast<int>(next(128));
+        double o = 0, mag = 0;
+        for (std::int64_t p = 0; p < ctx; ++p) {
+          const double v = bf16_to_float(kv[static_cast<std::size_t>(((ctx + p) * 8 + g) * 128 + j)]);
+          o += s[static_cast<std::size_t>(p)] * v;
+          mag += s[static_cast<std::size_t>(p)] * std::fabs(v);
+        }
+        judge(bf16_to_float(out[static_cast<std::size_t>(h * 128 + j)]), o / l, mag / l * 64.0);
       }
     }
     return;
@@ -414,7 +473,8 @@ B200Runtime::Resolved B200Runtime::resolve_body(const SimKernelSpec& spec) {
       break;
     }
     case BodyKind::RmsNormBf16:
-    case BodyKind::SiluMulBf16: {
+    case BodyKind::SiluMulBf16:
+    case BodyKind::AttnDecodeBf16: {
       const TensorBody& t = tensor_body(b);
       if (spec.total_blocks != t.blocks)
         throw ConfigError(std::string(body_kind_name(b.kind)) + " kernel of this shape has " +

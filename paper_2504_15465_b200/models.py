@@ -120,6 +120,16 @@ class Builder:
             "blocks": -(-n // chunk), "block_us": round(max(1.0, 6.0 * chunk / (TPC_GBS / 4 * 1e3)), 3),
             "s": 0.2, "occ": 4, "body": {"kind": "silu_mul_bf16", "ws": self._next(), "p": [n, chunk]}})
 
+    def attention(self, ctx, chunk=128) -> None:
+        """Decode GQA attention (32 query / 8 KV heads of 128, RoPE on the
+        query) over a `ctx`-long KV cache as the tenant body attn_decode_bf16:
+        block = (context chunk, KV head), chunks merged by the head's last
+        block."""
+        blocks = -(-ctx // chunk) * 8
+        self.kernels.append({
+            "blocks": blocks, "block_us": round(max(1.0, 4.0 * chunk * 128 / (TPC_GBS / 4 * 1e3)), 3),
+            "s": 0.2, "occ": 4, "body": {"kind": "attn_decode_bf16", "ws": self._next(), "p": [ctx, chunk]}})
+
     def stream(self, nbytes) -> None:
         """Elementwise kernel moving `nbytes` (read + written): blocks of at
         most STREAM_WORDS u32, sized (in 1 KiB steps) to the bytes moved, so
@@ -233,7 +243,7 @@ def llama3_8b_decode(context: int = 1024, ws_base: int = 0,
     for _ in range(32):
         b.rmsnorm(1, d)                                  # RMSNorm (tenant body)
         b.gemv(d + 2 * kv, d, splits[0])                 # QKV (72 blocks)
-        b.stream(context * kv * 2 * 2 + d * 2 * 2)       # RoPE + attention over K and V (byte-equivalent)
+        b.attention(context)                             # RoPE + attention over the KV cache (tenant body)
         b.gemv(d, d, splits[1])                          # output projection (64 blocks)
         b.rmsnorm(1, d)                                  # residual + RMSNorm (tenant body)
         b.gemv(2 * ffn, d, splits[2])                    # gate + up (112 blocks)
@@ -262,6 +272,8 @@ def summary(kernels: list[dict]) -> dict:
             nbytes += 2.0 * (2 * p[0] * p[1] + p[1])
         elif body["kind"] == "silu_mul_bf16":
             nbytes += 6.0 * p[0]
+        elif body["kind"] == "attn_decode_bf16":
+            nbytes += 2.0 * (2 * p[0] * 8 * 128 + 2 * 32 * 128)
         elif body["kind"] == "gemv_bf16":
             flops += 2.0 * p[0] * p[1]
             nbytes += 2.0 * (p[0] * p[1] + p[1] + p[0])

@@ -109,3 +109,41 @@ def test_silu_mul_body_matches_reference(api, cuda_device):
     got = O[:n].float().cpu().numpy().astype(np.float64)
     assert (np.abs(got - ref) <= np.abs(ref) * 2.0 ** -8 + 1e-3 * np.abs(ref).max()).all()
     assert torch.isnan(O[n:].float()).all()  # nothing written past n
+
+
+@pytest.mark.parametrize("ctx,chunk", [(1024, 128), (300, 64)])
+def test_attention_body_matches_reference(api, cuda_device, ctx, chunk):
+    """attn_decode_bf16: Llama-3 GQA decode attention (32 query / 8 KV heads of
+    128, RoPE base 500000 on interleaved pairs at position ctx) split over the
+    context in chunks, merged by each KV head's last block; against a float64
+    restatement. The merge is deterministic (chunk order), so a second run of
+    the same kernel reproduces the result bit for bit."""
+    import torch
+
+    chunks = -(-ctx // chunk)
+    blocks = chunks * 8
+    g = torch.Generator().manual_seed(ctx)
+    q = (torch.rand(32, 128, generator=g) * 2 - 1).to(torch.bfloat16)
+    kv = (torch.rand(2, ctx, 8, 128, generator=g) * 2 - 1).to(torch.bfloat16)
+    Q, KV = q.cuda(), kv.cuda()
+    ws = torch.zeros((8448 + 32 * chunks * 130 * 4) // 4, dtype=torch.float32, device="cuda")
+    args = [Q.data_ptr(), KV.data_ptr(), ws.data_ptr(), ctx | (chunk << 32), api.grid(chunks, 8)]
+    outs = []
+    for seed in (4, 5):
+        trace = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+        run(api, api.body_id("attn_decode_bf16"), args, blocks, seed, trace)
+        outs.append(ws[:2048].view(torch.bfloat16)[:4096].cpu().clone())
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    got = outs[0].view(32, 128).double().numpy()
+    qd, k, v = q.double().numpy(), kv[0].double().numpy(), kv[1].double().numpy()
+    j = np.arange(64)
+    ang = ctx * 500000.0 ** (-2.0 * j / 128)
+    qr = np.empty_like(qd)
+    qr[:, 0::2] = qd[:, 0::2] * np.cos(ang) - qd[:, 1::2] * np.sin(ang)
+    qr[:, 1::2] = qd[:, 0::2] * np.sin(ang) + qd[:, 1::2] * np.cos(ang)
+    for h in range(32):
+        s = k[:, h // 4, :] @ qr[h] / np.sqrt(128.0)
+        e = np.exp(s - s.max())
+        ref = (e[:, None] * v[:, h // 4, :]).sum(0) / e.sum()
+        mag = (e[:, None] * np.abs(v[:, h // 4, :])).sum(0) / e.sum()
+        assert (np.abs(got[h] - ref) <= np.abs(ref) * 2.0 ** -8 + 2e-3 * mag + 1e-4).all(), h
