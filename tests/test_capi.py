@@ -105,8 +105,8 @@ def test_ctypes_structs_match_the_header(api, tmp_path):
 
 def test_tenant_body_table(api):
     """The built-in tenant bodies are registered by name (host table, no GPU)."""
-    ids = {n: api.body_id(n) for n in ("grid_probe", "rmsnorm_bf16", "silu_mul_bf16")}
-    assert sorted(ids.values()) == [api.GPUOS_BODY_USER0 + i for i in range(3)]
+    names = ("attn_decode_bf16", "grid_probe", "rmsnorm_bf16", "silu_mul_bf16")  # sorted
+    assert [api.body_id(n) for n in names] == [api.GPUOS_BODY_USER0 + i for i in range(len(names))]
     with pytest.raises(api.GpuosError) as e:
         api.body_id("missing")
     assert e.value.code == -2
