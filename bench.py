@@ -473,8 +473,11 @@ def model_configs(local: int) -> dict:
     out = {}
     # infer4: 2 s x 4 runs = 1200 / 800 requests per ResNet / BERT tenant
     # (nearest-rank p99 over >= 800 samples), alone runs likewise.
-    for name, horizon, reps in (("infer4", 2000.0, 4), ("hybrid", 1000.0, 3)):
-        r = configs.run(name, horizon_ms=horizon, reps=reps, device=local)
+    from paper_2504_15465_b200 import workloads as wl
+
+    for name, horizon, reps, cfg in (("infer4", 2000.0, 4, None), ("hybrid", 1000.0, 3, None),
+                                     ("hybrid_real_attention", 1000.0, 3, wl.hybrid(1000.0, real_attention=True))):
+        r = configs.run("hybrid" if cfg is not None else name, horizon_ms=horizon, reps=reps, device=local, cfg=cfg)
         out[name] = {"tpc_utilization": r["tpc_utilization"], "apps": {
             a: {k: v for k, v in row.items() if k in ("priority", "p99_vs_alone", "slo_attainment",
                                                         "throughput_vs_static", "iterations_vs_static")}
@@ -483,7 +486,9 @@ def model_configs(local: int) -> dict:
             for a, row in r["apps"].items()}, "knobs": r["knobs"]}
     out["note"] = ("#2: 2x ResNet-50 b1 (150 rps) + 2x BERT-base b8 (100 rps), LC, Poisson, beside a "
                    "ResNet-50 b256 training tenant (BE, closed loop), 2 s x 4 runs; #3: Llama-3-8B decode LC "
-                   "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 3 runs; "
+                   "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 3 runs; decode "
+                   "RMSNorm / SiLU-mul as tenant bodies, attention as a byte-equivalent STREAM kernel "
+                   "(hybrid) or the attn_decode_bf16 tenant body (hybrid_real_attention); "
                    "alone = the same scenario with the other tenants silent; static = each tenant on its "
                    "quota (no stealing, atomizer or sharing); BE throughput = executed work (blocks x "
                    "calibrated block time) per second; random-init weights, live on the persistent dispatcher")

@@ -10,7 +10,7 @@
 //   args[2] ws  workspace: o bf16 [32][128] at 0 (the result), arrival
 //               counters u32 [8] at 8192 (zero; self-resetting), partials
 //               fp32 [32][chunks][2 + 128] at 8448
-//   args[3] ctx | chunk << 32 (chunk: positions per block, <= 256)
+//   args[3] ctx | chunk << 32 (chunk: positions per block, <= 32)
 //   args[4] GPUOS_GRID(chunks, 8)
 // Query position = ctx (the cache holds positions 0 .. ctx-1); RoPE base
 // 500000 on interleaved pairs (2i, 2i+1). Each block writes, per query
@@ -24,7 +24,9 @@
 #include "gpuos_body.cuh"
 
 namespace gpuos_bodies_attn {
-constexpr unsigned kHeadDim = 128, kKvHeads = 8, kQPerKv = 4, kQHeads = 32, kMaxChunk = 256;
+constexpr unsigned kHeadDim = 128, kKvHeads = 8, kQPerKv = 4, kQHeads = 32, kMaxChunk = 32;
+constexpr unsigned kPerWarp = kMaxChunk / 8;  // positions per warp
+constexpr unsigned kMaxChunks = 256;          // context chunks merged per head
 constexpr unsigned kWsCounters = 8192, kWsPartials = 8448;
 }  // namespace gpuos_bodies_attn
 
@@ -41,126 +43,167 @@ GPUOS_USER_BODY(attn_decode_bf16) {
   unsigned* counters = reinterpret_cast<unsigned*>(ws + kWsCounters);
   float* part = reinterpret_cast<float*>(ws + kWsPartials);
   const int warp = b.tid >> 5, lane = b.tid & 31;
-  // Shared: scores [4][chunk], per-warp o partials [8 warps][4][128].
-  float* sc = reinterpret_cast<float*>(b.smem);
-  float* ow = sc + kQPerKv * kMaxChunk;
-  __shared__ float red[kQPerKv][8];
-  __shared__ unsigned last;
+  // Shared: per-warp o partials [8 warps][4][128], the per-warp max / sum of
+  // each head, the merge flag; the merge reuses the o area.
+  float* ow = reinterpret_cast<float*>(b.smem);
+  float* wm = ow + 8 * kQPerKv * kHeadDim;  // [8 warps][4 heads][2]
+  unsigned* last = reinterpret_cast<unsigned*>(wm + 8 * kQPerKv * 2);
 
-  // This lane's 4 dims (4 lane .. 4 lane + 3) of the 4 query heads, rotated.
+  // Warp w owns positions p0 + w + 8 i (i < kPerWarp): every K and V row it
+  // needs is loaded up front (one memory latency, not one per position); a
+  // lane holds 4 of the 128 dims (coalesced 256-byte rows).
+  uint2 kr[kPerWarp], vr[kPerWarp];
+#pragma unroll
+  for (unsigned i = 0; i < kPerWarp; ++i) {
+    const unsigned p = p0 + warp + 8 * i;
+    const size_t off = (static_cast<size_t>(p < p1 ? p : p0) * kKvHeads + kvh) * kHeadDim + 4 * lane;
+    kr[i] = *reinterpret_cast<const uint2*>(kc + off);
+    vr[i] = *reinterpret_cast<const uint2*>(vc + off);
+  }
+  // This lane's 4 dims of the 4 query heads, rotated (RoPE at position ctx).
   float qr[kQPerKv][4];
   const float pos = static_cast<float>(ctx);
 #pragma unroll
-  for (unsigned h = 0; h < kQPerKv; ++h) {
-    const __nv_bfloat16* qh = q + (kvh * kQPerKv + h) * kHeadDim + 4 * lane;
+  for (unsigned pr = 0; pr < 2; ++pr) {
+    const unsigned i = 2 * lane + pr;  // pair index 0..63
+    const float inv = exp2f(-2.f * static_cast<float>(i) / static_cast<float>(kHeadDim) * 18.931568569324174f);  // 500000^-2i/128
+    float sn, cs;
+    sincosf(pos * inv, &sn, &cs);
 #pragma unroll
-    for (unsigned pr = 0; pr < 2; ++pr) {
-      const unsigned i = 2 * lane + pr;  // pair index 0..63
-      const float inv = __powf(500000.f, -2.f * static_cast<float>(i) / static_cast<float>(kHeadDim));
-      float sn, cs;
-      sincosf(pos * inv, &sn, &cs);
+    for (unsigned h = 0; h < kQPerKv; ++h) {
+      const __nv_bfloat16* qh = q + (kvh * kQPerKv + h) * kHeadDim + 4 * lane;
       const float x0 = __bfloat162float(qh[2 * pr]), x1 = __bfloat162float(qh[2 * pr + 1]);
       qr[h][2 * pr] = x0 * cs - x1 * sn;
       qr[h][2 * pr + 1] = x0 * sn + x1 * cs;
     }
   }
   const float scale = rsqrtf(static_cast<float>(kHeadDim));
-  // Scores: warp w takes positions p0 + w, p0 + w + 8, ...; a lane holds 4
-  // dims of the key row (coalesced 256-byte row per position).
-  for (unsigned p = p0 + warp; p < p1; p += 8) {
-    const uint2 kv2 = *reinterpret_cast<const uint2*>(kc + (static_cast<size_t>(p) * kKvHeads + kvh) * kHeadDim + 4 * lane);
-    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv2);
+  // Scores (4 heads x kPerWarp positions, warp reductions interleaved).
+  float s[kPerWarp][kQPerKv];
+#pragma unroll
+  for (unsigned i = 0; i < kPerWarp; ++i) {
+    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kr[i]);
     const float2 ka = __bfloat1622float2(k2[0]), kb = __bfloat1622float2(k2[1]);
 #pragma unroll
-    for (unsigned h = 0; h < kQPerKv; ++h) {
-      float d = qr[h][0] * ka.x + qr[h][1] * ka.y + qr[h][2] * kb.x + qr[h][3] * kb.y;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      if (lane == 0) sc[h * kMaxChunk + (p - p0)] = d * scale;
-    }
+    for (unsigned h = 0; h < kQPerKv; ++h) s[i][h] = qr[h][0] * ka.x + qr[h][1] * ka.y + qr[h][2] * kb.x + qr[h][3] * kb.y;
   }
-  __syncthreads();
-  // Chunk max and sum per head (warp h < 4 reduces head h).
-  const unsigned n = p1 - p0;
-  if (warp < static_cast<int>(kQPerKv)) {
-    float m = -INFINITY;
-    for (unsigned i = lane; i < n; i += 32) m = fmaxf(m, sc[warp * kMaxChunk + i]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float l = 0.f;
-    for (unsigned i = lane; i < n; i += 32) {
-      const float e = __expf(sc[warp * kMaxChunk + i] - m);
-      sc[warp * kMaxChunk + i] = e;
-      l += e;
-    }
+  for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) {
-      red[warp][0] = m;
-      red[warp][1] = l;
-    }
+    for (unsigned i = 0; i < kPerWarp; ++i)
+#pragma unroll
+      for (unsigned h = 0; h < kQPerKv; ++h) s[i][h] += __shfl_xor_sync(0xffffffffu, s[i][h], o);
+  float m[kQPerKv], l[kQPerKv];
+#pragma unroll
+  for (unsigned h = 0; h < kQPerKv; ++h) {
+    m[h] = -INFINITY;
+#pragma unroll
+    for (unsigned i = 0; i < kPerWarp; ++i)
+      if (p0 + warp + 8 * i < p1) m[h] = fmaxf(m[h], s[i][h] * scale);
   }
+  if (lane == 0)
+#pragma unroll
+    for (unsigned h = 0; h < kQPerKv; ++h) wm[(warp * kQPerKv + h) * 2] = m[h];
   __syncthreads();
-  // o = sum_p e_p v_p: warp w over positions w, w + 8, ...; lane: 4 dims.
+  // Chunk max per head, then weights e = exp(s - M) and this warp's o.
+  float M[kQPerKv];
+#pragma unroll
+  for (unsigned h = 0; h < kQPerKv; ++h) {
+    M[h] = -INFINITY;
+#pragma unroll
+    for (unsigned w = 0; w < 8; ++w) M[h] = fmaxf(M[h], wm[(w * kQPerKv + h) * 2]);
+    l[h] = 0.f;
+  }
   float acc[kQPerKv][4] = {};
-  for (unsigned p = p0 + warp; p < p1; p += 8) {
-    const uint2 vv = *reinterpret_cast<const uint2*>(vc + (static_cast<size_t>(p) * kKvHeads + kvh) * kHeadDim + 4 * lane);
-    const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vv);
+#pragma unroll
+  for (unsigned i = 0; i < kPerWarp; ++i) {
+    if (p0 + warp + 8 * i >= p1) continue;
+    const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vr[i]);
     const float2 va = __bfloat1622float2(v2[0]), vb = __bfloat1622float2(v2[1]);
 #pragma unroll
     for (unsigned h = 0; h < kQPerKv; ++h) {
-      const float e = sc[h * kMaxChunk + (p - p0)];
+      const float e = __expf(s[i][h] * scale - M[h]);
+      l[h] += e;
       acc[h][0] += e * va.x;
       acc[h][1] += e * va.y;
       acc[h][2] += e * vb.x;
       acc[h][3] += e * vb.y;
     }
   }
+  __syncthreads();  // (every warp has read the maxima before wm is reused)
 #pragma unroll
-  for (unsigned h = 0; h < kQPerKv; ++h)
+  for (unsigned h = 0; h < kQPerKv; ++h) {
 #pragma unroll
     for (unsigned d = 0; d < 4; ++d) ow[(warp * kQPerKv + h) * kHeadDim + 4 * lane + d] = acc[h][d];
+    if (lane == 0) wm[(warp * kQPerKv + h) * 2 + 1] = l[h];
+  }
   __syncthreads();
-  // Partials of this chunk: thread t < 4 x 128 sums its (head, dim) over warps.
+  // This chunk's partials: thread t < 4 x 128 sums its (head, dim) over warps
+  // (all relative to the chunk max M).
   for (unsigned t = b.tid; t < kQPerKv * kHeadDim; t += GPUOS_BLOCK_THREADS) {
     const unsigned h = t / kHeadDim, d = t % kHeadDim;
-    float s = 0.f;
+    float o = 0.f;
 #pragma unroll
-    for (unsigned w = 0; w < 8; ++w) s += ow[(w * kQPerKv + h) * kHeadDim + d];
+    for (unsigned w = 0; w < 8; ++w) o += ow[(w * kQPerKv + h) * kHeadDim + d];
     float* ph = part + (static_cast<size_t>(kvh * kQPerKv + h) * chunks + cx) * (2 + kHeadDim);
-    ph[2 + d] = s;
+    ph[2 + d] = o;
     if (d == 0) {
-      ph[0] = red[h][0];
-      ph[1] = red[h][1];
+      float mm = -INFINITY, ll = 0.f;
+#pragma unroll
+      for (unsigned w = 0; w < 8; ++w) {
+        mm = fmaxf(mm, wm[(w * kQPerKv + h) * 2]);
+        ll += wm[(w * kQPerKv + h) * 2 + 1];
+      }
+      ph[0] = mm;
+      ph[1] = ll;
     }
   }
   // The KV head's last chunk merges (self-resetting counter, as split-K).
   __threadfence();
   __syncthreads();
   if (b.tid == 0) {
-    last = atomicAdd(counters + kvh, 1u) == chunks - 1;
-    if (last) {
+    *last = atomicAdd(counters + kvh, 1u) == chunks - 1;
+    if (*last) {
       __threadfence();
       counters[kvh] = 0u;
     }
   }
   __syncthreads();
-  if (last) {
+  if (*last) {
+    // Merge weights per (head, chunk) in shared memory -- w = exp(m_c - M) /
+    // L with M the head's max and L = sum l_c exp(m_c - M) -- then each
+    // (head, dim) thread sums its chunks' o with the loads in flight
+    // together (a loop of dependent L2 reads cost ~40 us per head group).
+    float* mw = ow;  // [4][kMaxChunks] (the o partials are written out)
+    float* lw = mw + kQPerKv * kMaxChunks;
+    for (unsigned t = b.tid; t < kQPerKv * chunks; t += GPUOS_BLOCK_THREADS) {
+      const unsigned h = t / chunks, c = t % chunks;
+      const float* pc = part + (static_cast<size_t>(kvh * kQPerKv + h) * chunks + c) * (2 + kHeadDim);
+      mw[h * kMaxChunks + c] = __ldcg(pc);
+      lw[h * kMaxChunks + c] = __ldcg(pc + 1);
+    }
+    __syncthreads();
+    if (b.tid < kQPerKv) {
+      const unsigned h = b.tid;
+      float Mx = -INFINITY, L = 0.f;
+      for (unsigned c = 0; c < chunks; ++c) Mx = fmaxf(Mx, mw[h * kMaxChunks + c]);
+      for (unsigned c = 0; c < chunks; ++c) {
+        const float w = __expf(mw[h * kMaxChunks + c] - Mx);
+        mw[h * kMaxChunks + c] = w;
+        L += lw[h * kMaxChunks + c] * w;
+      }
+      for (unsigned c = 0; c < chunks; ++c) mw[h * kMaxChunks + c] /= L;
+    }
+    __syncthreads();
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ws);
     for (unsigned t = b.tid; t < kQPerKv * kHeadDim; t += GPUOS_BLOCK_THREADS) {
       const unsigned h = t / kHeadDim, d = t % kHeadDim;
-      const float* ph = part + static_cast<size_t>(kvh * kQPerKv + h) * chunks * (2 + kHeadDim);
-      float M = -INFINITY;
-      for (unsigned c = 0; c < chunks; ++c) M = fmaxf(M, __ldcg(ph + c * (2 + kHeadDim)));
-      float L = 0.f, O = 0.f;
-      for (unsigned c = 0; c < chunks; ++c) {
-        const float* pc = ph + c * (2 + kHeadDim);
-        const float w = __expf(__ldcg(pc) - M);
-        L += __ldcg(pc + 1) * w;
-        O += __ldcg(pc + 2 + d) * w;
-      }
-      out[(kvh * kQPerKv + h) * kHeadDim + d] = __float2bfloat16_rn(O / L);
+      const float* ph = part + static_cast<size_t>(kvh * kQPerKv + h) * chunks * (2 + kHeadDim) + 2 + d;
+      float O = 0.f;
+#pragma unroll 16
+      for (unsigned c = 0; c < chunks; ++c) O += mw[h * kMaxChunks + c] * __ldcg(ph + c * (2 + kHeadDim));
+      out[(kvh * kQPerKv + h) * kHeadDim + d] = __float2bfloat16_rn(O);
     }
   }
-  __syncthreads();  // (shared scores reused by the worker's next block)
+  __syncthreads();  // (shared memory reused by the worker's next block)
 }

@@ -167,9 +167,10 @@ const B200Runtime::TensorBody& B200Runtime::tensor_body(const BodyRef& b) {
     // Decode attention (csrc/bodies/llama_attention.cu): q [32][128], K and V
     // caches [ctx][8][128], workspace (result, counters, chunk partials).
     check(gpuos_dev_body_id(body_kind_name(b.kind), &t.body), "tenant body lookup");
-    const std::int64_t ctx = b.p0, chunk = b.p1 > 0 ? b.p1 : 128;
-    if (ctx <= 0 || chunk > 256 || chunk <= 0) throw ConfigError("attn_decode_bf16 needs p = [ctx, chunk <= 256]");
+    const std::int64_t ctx = b.p0, chunk = b.p1 > 0 ? b.p1 : 32;
+    if (ctx <= 0 || chunk > 32 || chunk <= 0) throw ConfigError("attn_decode_bf16 needs p = [ctx, chunk <= 32]");
     const std::int64_t chunks = (ctx + chunk - 1) / chunk;
+    if (chunks > 256) throw ConfigError("attn_decode_bf16 merges at most 256 context chunks");
     void* Q = tensor(32 * 128, true);
     void* KV = tensor(static_cast<std::uint64_t>(2 * ctx * 8 * 128), true);
     const std::uint64_t ws_elems = (8448 + 32ull * chunks * 130 * 4) / 2;

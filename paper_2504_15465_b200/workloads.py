@@ -140,7 +140,8 @@ def infer4(horizon_ms: float = 2000.0, rps: tuple = (150.0, 150.0, 100.0, 100.0)
 
 
 def hybrid(horizon_ms: float = 2000.0, tokens_per_s: float = 60.0, slo_ms: float = 25.0,
-           train_batch: int = 256, tpcs: int = 74, decode_splits: tuple = (3, 4, 1, 4)) -> dict:
+           train_batch: int = 256, tpcs: int = 74, decode_splits: tuple = (3, 4, 1, 4),
+           real_attention: bool = False) -> dict:
     """BASELINE config #3, hybrid stacking: Llama-3-8B bf16 decode at batch 1
     (latency-critical, Poisson token requests, one request = one token's 258
     kernels over 15 GB of weights) with ResNet-50 training (best-effort,
@@ -159,7 +160,8 @@ def hybrid(horizon_ms: float = 2000.0, tokens_per_s: float = 60.0, slo_ms: float
         "apps": [
             {"id": "llama_decode", "priority": "hp", "quota": tpcs // 2, "slo_ms": slo_ms,
              "arrival": {"poisson_rps": tokens_per_s, "seed_offset": 0},
-             "kernels": models.llama3_8b_decode(1024, ws_base=0, splits=decode_splits)},
+             "kernels": models.llama3_8b_decode(1024, ws_base=0, splits=decode_splits,
+                                                attention=real_attention)},
             {"id": "rn50_train", "priority": "be", "quota": tpcs - tpcs // 2,
              "arrival": "closed_loop", "kernels": models.resnet50_train(train_batch, ws_base=100_000)},
         ],

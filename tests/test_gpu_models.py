@@ -36,9 +36,10 @@ def test_mirror_resnet50_and_bert_traces(api, cuda_device):
     assert r["log"] == replay["log"]
 
 
-@pytest.mark.parametrize("name", ["infer4", "hybrid"])
+@pytest.mark.parametrize("name", ["infer4", "hybrid", "hybrid_real_attention"])
 def test_live_model_configs_complete(api, cuda_device, name):
-    cfg = workloads.infer4(150.0) if name == "infer4" else workloads.hybrid(150.0)
+    cfg = (workloads.infer4(150.0) if name == "infer4"
+           else workloads.hybrid(150.0, real_attention=name.endswith("attention")))
     req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
            "timeline": True, "verify": True, "b200": {"chunk_cap": 256, "trace": True},
            "set": {"block_revocation": True}}

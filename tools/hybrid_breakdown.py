@@ -134,10 +134,11 @@ def main():
     ap.add_argument("--b200", default="{}", help="extra B200Options (JSON)")
     ap.add_argument("--splits", default="3,4,1,4", help="decode GEMV K splits (QKV, O, gate-up, down)")
     ap.add_argument("--train-alone", action="store_true")
+    ap.add_argument("--attention", action="store_true", help="decode attention as the tenant body")
     args = ap.parse_args()
     splits = tuple(int(x) for x in args.splits.split(","))
-    cfg = workloads.hybrid(args.horizon_ms, decode_splits=splits)
-    trace = models.llama3_8b_decode(1024, ws_base=0, splits=splits)
+    cfg = workloads.hybrid(args.horizon_ms, decode_splits=splits, real_attention=args.attention)
+    trace = models.llama3_8b_decode(1024, ws_base=0, splits=splits, attention=args.attention)
     knobs = {"block_revocation": True, "chain_launches": True} | json.loads(args.set)
     req = {"scenario": {"config": cfg}, "backend": "b200", "device": "b200", "requests": True,
            "b200": {"chunk_cap": 256} | json.loads(args.b200), "set": knobs, "warm_start": True}
