@@ -289,7 +289,7 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     sat_gemv = guarded(lambda: gemv_saturation(api, local, args))
     sat_conv = guarded(lambda: conv_saturation(api, local, args))
     rsz = guarded(lambda: right_sizing_summary(local, args)) if rank == 0 else None
-    cfgs = guarded(lambda: model_configs(local)) if (rank == 0 and not args.skip_configs) else None
+    cfgs = guarded(lambda: isolated("model_configs", local, 900)) if (rank == 0 and not args.skip_configs) else None
     pols = guarded(lambda: policy_rows(local)) if (rank == 0 and not args.skip_configs) else None
     probe = api.probe_dispatch(device=local, workers_per_sm=args.workers_per_sm, serial=2000,
                                pipelined=20000, depth=16)
@@ -397,6 +397,24 @@ def live_traffic(key: str = "dram"):
     except (OSError, KeyError, ValueError):
         return None
     return t["dram_read"] + t["dram_write"] if key == "dram" else t[key]
+
+
+def isolated(fn_name: str, local: int, timeout_s: float):
+    """Runs bench.<fn_name>(local) in a child process bounded by timeout_s
+    (the model-config runs are the longest secondary measurements; a hang
+    there must not cost the bench line). The parent holds no dispatcher
+    meanwhile, so the child has the GPU."""
+    code = (f"import json, sys; sys.path.insert(0, {ROOT!r}); import bench; "
+            f"print('@@' + json.dumps(bench.{fn_name}({local})))")
+    try:
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout_s,
+                           cwd=ROOT)
+    except subprocess.TimeoutExpired:
+        return {"error": f"{fn_name} exceeded {timeout_s:.0f} s"}
+    for line in p.stdout.splitlines()[::-1]:
+        if line.startswith("@@"):
+            return json.loads(line[2:])
+    return {"error": f"{fn_name} failed (rc {p.returncode}): {p.stderr.strip()[-400:]}"}
 
 
 def guarded(fn):

@@ -60,6 +60,9 @@ struct B200Options {
   // power manager's choice. Off by default -- never on a pool whose
   // operator manages clocks.
   bool dvfs_actuate = false;
+  // Live-run watchdog: no atom completion for this long while atoms are in
+  // flight raises InvariantError with the device state (0: off).
+  std::int64_t stall_timeout_ns = 20'000'000'000;
 };
 
 struct AtomTimeline {
@@ -248,6 +251,7 @@ class B200Device final : public Device {
   SimTime host_now() const;
   void pump();
 
+  SimTime last_progress_ns_ = 0;  // host time of the last completion (watchdog)
   double energy_j_ = 0.0;
   unsigned sm_mhz_ = 0, power_mw_ = 0;
   FreqMhz locked_mhz_ = 0;  // dvfs_actuate: clock currently locked (0: none)

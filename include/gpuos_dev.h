@@ -326,6 +326,11 @@ int gpuos_dev_host_free(struct gpuos_dev* dev, void* ptr);
 
 const char* gpuos_dev_last_error(void);
 
+/* Diagnostics: the in-flight atoms' device state (claim offset, done
+ * count, pause / gate bits, chaining) as text into buf (truncated to len);
+ * safe while the dispatcher runs. Returns the full length.               */
+int gpuos_dev_debug_dump(struct gpuos_dev* dev, char* buf, int32_t len);
+
 /* Id of the tenant body GPUOS_USER_BODY(name) compiled into this library
  * (GPUOS_BODY_USER0 + i); GPUOS_E_CONFIG if there is none. Host only.    */
 int gpuos_dev_body_id(const char* name, uint32_t* id);

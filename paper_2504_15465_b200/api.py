@@ -66,7 +66,7 @@ DEV_SYMBOLS = [
     "gpuos_dev_host_alloc", "gpuos_dev_host_free", "gpuos_dev_run_batch", "gpuos_dev_set_fence_mask", "gpuos_dev_set_tpc_owner",
     "gpuos_dev_gemm_desc", "gpuos_dev_gemm_desc_splitk", "gpuos_dev_gemv_desc", "gpuos_dev_conv_desc", "gpuos_dev_fill_bf16",
     "gpuos_dev_gemv_pack", "gpuos_dev_set_pair_fence", "gpuos_power_sample", "gpuos_power_lock_sm_clock",
-    "gpuos_dev_body_id",
+    "gpuos_dev_body_id", "gpuos_dev_debug_dump",
 ]
 SIM_SYMBOLS = [
     "gpuos_session_open", "gpuos_session_run", "gpuos_session_close", "gpuos_run_json",
@@ -171,6 +171,7 @@ def library() -> C.CDLL:
         "gpuos_dev_gemv_pack": (C.c_int, [P, P, P, C.c_int64, C.c_int64]),
         "gpuos_dev_set_pair_fence": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_uint32, C.c_int32]),
         "gpuos_dev_body_id": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint32)]),
+        "gpuos_dev_debug_dump": (C.c_int, [P, C.c_char_p, C.c_int32]),
         "gpuos_dev_gemv_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_uint32, C.c_int32,
                                           C.POINTER(P), C.POINTER(C.c_int64)]),
         "gpuos_dev_gemm_desc": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64,

@@ -158,15 +158,15 @@ GPUOS_USER_BODY(attn_decode_bf16) {
       ph[1] = ll;
     }
   }
-  // The KV head's last chunk merges (self-resetting counter, as split-K).
-  __threadfence();
+  // The KV head's last chunk merges (self-resetting counter, as split-K):
+  // the block's partials precede its count (CTA barrier, then a release
+  // add), and the last block's acquire sees every other block's.
   __syncthreads();
   if (b.tid == 0) {
-    *last = atomicAdd(counters + kvh, 1u) == chunks - 1;
-    if (*last) {
-      __threadfence();
-      counters[kvh] = 0u;
-    }
+    unsigned before;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(before) : "l"(counters + kvh) : "memory");
+    *last = before == chunks - 1;
+    if (*last) counters[kvh] = 0u;  // (ready for the kernel's next run)
   }
   __syncthreads();
   if (*last) {
@@ -183,16 +183,22 @@ GPUOS_USER_BODY(attn_decode_bf16) {
       lw[h * kMaxChunks + c] = __ldcg(pc + 1);
     }
     __syncthreads();
-    if (b.tid < kQPerKv) {
-      const unsigned h = b.tid;
-      float Mx = -INFINITY, L = 0.f;
-      for (unsigned c = 0; c < chunks; ++c) Mx = fmaxf(Mx, mw[h * kMaxChunks + c]);
-      for (unsigned c = 0; c < chunks; ++c) {
+    if (warp < static_cast<int>(kQPerKv)) {  // warp h: head h's weights, a lane per 32 chunks
+      const unsigned h = static_cast<unsigned>(warp);
+      float Mx = -INFINITY;
+      for (unsigned c = lane; c < chunks; c += 32) Mx = fmaxf(Mx, mw[h * kMaxChunks + c]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+      float L = 0.f;
+      for (unsigned c = lane; c < chunks; c += 32) {
         const float w = __expf(mw[h * kMaxChunks + c] - Mx);
         mw[h * kMaxChunks + c] = w;
         L += lw[h * kMaxChunks + c] * w;
       }
-      for (unsigned c = 0; c < chunks; ++c) mw[h * kMaxChunks + c] /= L;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+      const float inv = 1.f / L;
+      for (unsigned c = lane; c < chunks; c += 32) mw[h * kMaxChunks + c] *= inv;
     }
     __syncthreads();
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ws);

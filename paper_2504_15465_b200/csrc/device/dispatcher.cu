@@ -1975,6 +1975,39 @@ int gpuos_dev_get_topology(gpuos_dev* d, gpuos_dev_topology* out) {
 int64_t gpuos_dev_now_ns(gpuos_dev* d) { return d ? steady_ns() - d->t0_ns : 0; }
 int32_t gpuos_dev_in_flight(gpuos_dev* d) { return d ? d->in_flight : 0; }
 
+int gpuos_dev_debug_dump(gpuos_dev* d, char* buf, int32_t len) {
+  if (!d || !buf || len <= 0) return fail(GPUOS_E_CONFIG, "null argument");
+  std::string out;
+  char line[320];
+  std::snprintf(line, sizeof(line), "in_flight %d, ring published %llu consumed %llu\n", d->in_flight,
+                static_cast<unsigned long long>(d->ring_head),
+                static_cast<unsigned long long>(__atomic_load_n(d->consumed_h, __ATOMIC_ACQUIRE)));
+  out += line;
+  int shown = 0;
+  for (const uint32_t slot : d->live) {
+    if (shown++ == 24) {
+      out += "...\n";
+      break;
+    }
+    DevAtom a{};
+    // (side stream: a copy engine read while the persistent kernel runs)
+    if (cudaMemcpyAsync(&a, d->atoms + slot, 128, cudaMemcpyDeviceToHost, d->s_side) != cudaSuccess ||
+        cudaMemcpyAsync(&a.armed, &d->atoms[slot].armed, 4, cudaMemcpyDeviceToHost, d->s_side) != cudaSuccess ||
+        cudaStreamSynchronize(d->s_side) != cudaSuccess)
+      return fail(GPUOS_E_CUDA, "debug dump copy");
+    const HostAtom& h = d->slots[slot];
+    std::snprintf(line, sizeof(line),
+                  "atom %u slot %u seq %u body %u prio %d count %u claimed %u done %u paused 0x%x armed %u "
+                  "chain %u succ 0x%x pred_slot %u tpcs %d\n",
+                  h.atom_id, slot, a.seq, a.body, a.prio, a.count, static_cast<unsigned>(a.claim), a.done,
+                  a.paused, a.armed, a.chain, a.succ, h.pred_seq ? h.pred_slot : 0u,
+                  __builtin_popcountll(a.mask[0]) + __builtin_popcountll(a.mask[1]));
+    out += line;
+  }
+  std::snprintf(buf, static_cast<size_t>(len), "%s", out.c_str());
+  return static_cast<int32_t>(out.size());
+}
+
 int gpuos_dev_start(gpuos_dev* d) {
   if (!d) return fail(GPUOS_E_CONFIG, "null device");
   if (d->running) return fail(GPUOS_E_STATE, "dispatcher already running");

@@ -824,6 +824,7 @@ bool B200Device::step() {
     const AtomCompletion c = ready_.front();
     ready_.pop_front();
     now_ = std::max(now_, c.complete_time);
+    last_progress_ns_ = host_now();
     if (on_complete_) on_complete_(c);
     return true;
   }
@@ -839,6 +840,18 @@ bool B200Device::step() {
   const int in_flight = gpuos_dev_in_flight(rt_->handle());
   if (timers_.empty() && in_flight == 0) return false;
   now_ = std::max(now_, t);
+  // Watchdog: atoms in flight and no completion for stall_timeout_ns -- a
+  // live run that stopped making progress fails loudly (with the device's
+  // view of the in-flight atoms) instead of spinning until the kernel's
+  // 30-minute hang guard.
+  if (in_flight == 0) last_progress_ns_ = t;  // (idle: nothing can be stuck)
+  if (in_flight > 0 && opt_.stall_timeout_ns > 0 && t - last_progress_ns_ > opt_.stall_timeout_ns) {
+    std::string dump(8192, '\0');
+    const int n = gpuos_dev_debug_dump(rt_->handle(), dump.data(), static_cast<int32_t>(dump.size()));
+    dump.resize(n > 0 ? std::min<std::size_t>(static_cast<std::size_t>(n), dump.size() - 1) : 0);
+    throw InvariantError("live run made no progress for " + std::to_string(opt_.stall_timeout_ns / 1000000) +
+                         " ms with " + std::to_string(in_flight) + " atoms in flight:\n" + dump);
+  }
   if (in_flight == 0 && !timers_.empty()) {
     // Nothing on the GPU: sleep towards the next arrival, waking a full
     // millisecond early (OS sleeps overshoot) and spinning the rest.
@@ -856,6 +869,7 @@ void B200Device::run_all() {
   rt_->start();
   origin_ = gpuos_dev_now_ns(rt_->handle());
   now_ = 0;
+  last_progress_ns_ = 0;
   const auto w0 = std::chrono::steady_clock::now();
   try {
     while (step()) {

@@ -155,6 +155,7 @@ B200Options b200_options(const json& o) {
   b.stream_chunk_cap = o.value("chunk_cap", b.stream_chunk_cap);
   b.quantum_ns = static_cast<std::int64_t>(o.value("quantum_us", 0.0) * 1000.0);
   b.dvfs_actuate = o.value("dvfs_actuate", b.dvfs_actuate);
+  b.stall_timeout_ns = static_cast<std::int64_t>(o.value("stall_timeout_s", b.stall_timeout_ns * 1e-9) * 1e9);
   return b;
 }
 

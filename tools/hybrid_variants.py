@@ -34,8 +34,12 @@ ap.add_argument("--only", default=",".join(VARIANTS))
 ap.add_argument("--config", default="hybrid")
 ap.add_argument("--splits", default=None, help="decode GEMV K splits, e.g. 6,8,1,9")
 ap.add_argument("--be-batch", type=int, default=None, help="infer4: best-effort training batch")
+ap.add_argument("--attention", action="store_true", help="hybrid: decode attention as the tenant body")
 args = ap.parse_args()
 cfg = None
+if args.attention:
+    from paper_2504_15465_b200 import workloads  # noqa: E402
+    cfg = workloads.hybrid(args.horizon_ms, real_attention=True)
 if args.be_batch is not None:
     from paper_2504_15465_b200 import workloads  # noqa: E402
     cfg = workloads.infer4(args.horizon_ms, be_batch=args.be_batch)
