@@ -182,6 +182,7 @@ __device__ __forceinline__ void body_conv2(const BlockCmd& c, int tid, unsigned 
     if (blk < 0) break;
     gate = nullptr;
   }
+  cluster_sync_all();  // both CTAs' outputs released before the run is counted (body_gemm2)
 }
 
 }  // namespace gpuos_dev_impl

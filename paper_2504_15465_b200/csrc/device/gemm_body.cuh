@@ -231,13 +231,13 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
-// End of a pair tile: a relaxed arrive, so the epilogue's global stores are
-// not made cluster-visible first (nothing in the pair reads them; the
-// finisher's fence and acq_rel count publish them to other consumers).
-// What the barrier must order -- TMEM reads before the next tile's MMAs
-// (tcgen05 fences around it), shared-memory staging before the next TMA
-// writes, and the posted next tile (NextTile fences its own store) -- does
-// not need the release.
+// End of a pair tile inside a run: a relaxed arrive, so the epilogue's
+// global stores are not drained before the next tile (nothing in the pair
+// reads them). What the barrier must order -- TMEM reads before the next
+// tile's MMAs (tcgen05 fences around it), shared-memory staging before the
+// next TMA writes, and the posted next tile (NextTile fences its own store)
+// -- does not need the release; the run ends with a release barrier before
+// the leader counts it done (body_gemm2), and split-K tiles keep it.
 __device__ __forceinline__ void cluster_sync_tile_end() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
@@ -518,19 +518,22 @@ __device__ __forceinline__ void gemm2_tile(const GemmDesc* D, unsigned blk_in, i
   G.accum_used += 1;
   // Both halves of the tile are written (and both TMEMs read) before the
   // leader records the tile or issues the next tile's MMAs; the posted next
-  // tile is visible in both CTAs after it.
-  cluster_sync_tile_end();
+  // tile is visible in both CTAs after it. Split-K keeps the release: the
+  // peer's reductions into the fp32 accumulator must precede the leader's
+  // count below.
+  if (D->splits > 1) cluster_sync_all();
+  else cluster_sync_tile_end();
   if (D->splits > 1 && rank == 0) {
     // Split-K: the tile's last split converts the accumulator.
     __shared__ int last_split;
     if (tid == 0) {
-      __threadfence();  // this split's reductions (both CTAs, via the cluster barrier)
-      const unsigned before = atomicAdd(D->arrivals + blk, 1u);
+      // acq_rel: this split's reductions (both CTAs, observed through the
+      // cluster barrier: the release is cumulative) precede the count, and
+      // the last split acquires every other split's.
+      unsigned before;
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(before) : "l"(D->arrivals + blk) : "memory");
       last_split = before == D->splits - 1;
-      if (last_split) {
-        __threadfence();
-        D->arrivals[blk] = 0u;  // ready for the kernel's next run
-      }
+      if (last_split) D->arrivals[blk] = 0u;  // ready for the kernel's next run
     }
     __syncthreads();
     if (last_split) gemm_reduce_tile(D, blk, mt, nt, tid);
@@ -550,6 +553,10 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
     if (blk < 0) break;
     gate = nullptr;  // (open: the run's first tile waited for it)
   }
+  // Tiles end with a relaxed arrive; before the leader counts the run done
+  // (which releases C to a chained successor) both CTAs' C stores must be
+  // released: one release barrier per run.
+  cluster_sync_all();
 }
 
 }  // namespace gpuos_dev_impl

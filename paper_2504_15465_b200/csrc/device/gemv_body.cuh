@@ -223,13 +223,13 @@ __device__ __forceinline__ void gemv2_tile(const GemvDesc* D, unsigned block, in
     __shared__ int last_split;
     if (rank == 0) {
       if (tid == 0) {
-        __threadfence();  // this tile's partials (both CTAs, via the cluster barrier)
-        const unsigned before = atomicAdd(D->arrivals + blk, 1u);
+        // acq_rel: this tile's partials (both CTAs, observed through the
+        // cluster barrier: the release is cumulative) precede the count, and
+        // the last split acquires every other split's.
+        unsigned before;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(before) : "l"(D->arrivals + blk) : "memory");
         last_split = before == D->splits - 1;
-        if (last_split) {
-          __threadfence();
-          D->arrivals[blk] = 0u;  // ready for the kernel's next run
-        }
+        if (last_split) D->arrivals[blk] = 0u;  // ready for the kernel's next run
       }
       __syncthreads();
       if (last_split) {
