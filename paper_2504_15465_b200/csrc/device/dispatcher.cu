@@ -620,6 +620,7 @@ struct PairRun {
   unsigned extra;               // tiles claimed inside the body (beyond the first)
   unsigned spread;              // GEMM / conv: the spreading rule applies (not GEMV)
   long long next;               // posted next block, -1: end of run (leader writes both CTAs')
+  unsigned posts;               // posts so far (leader writes both CTAs', with release: next_block)
 };
 
 // A finished atom's bookkeeping held back while its handed-off successor
@@ -748,6 +749,7 @@ struct NextTile {
   const Params& p;
   PairRun& run;
   unsigned peer_next;  // shared::cluster address of the peer's run.next
+  unsigned peer_posts;  // ... and of its run.posts
   int tpc;
   unsigned sm;
   __device__ __forceinline__ void operator()(bool stop = false) const {
@@ -771,11 +773,13 @@ struct NextTile {
         }
       }
     }
+    // The post: the block, then the count with release (next_block waits
+    // for it with acquire in every thread of both CTAs).
     run.next = nb;
     st_cluster_u64(peer_next, static_cast<unsigned long long>(nb));
-    // (the tile-end barrier arrives relaxed: publish the post here, before
-    // this thread's epilogue stores)
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    const unsigned posts = run.posts + 1u;
+    asm volatile("st.release.cluster.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(&run.posts)), "r"(posts) : "memory");
+    asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(peer_posts), "r"(posts) : "memory");
   }
 };
 
@@ -1056,10 +1060,11 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
 
 __device__ __forceinline__ void run_body(const RoundCmd& rc, int tid, unsigned rank,
                                          StreamPipe& pipe, GemmPipe& gemm, GemvPipe& gemv,
-                                         const DevAtom* atoms, PairRun& run, const NextTile& nt) {
+                                         const DevAtom* atoms, PairRun& run, const NextTile& nt,
+                                         unsigned& posts_seen) {
   // Only an early-started atom's blocks check its gate (weights first).
   const unsigned* gate = rc.gated ? &atoms[rc.slot].paused : nullptr;
-  const PairTiles tiles{&run.next};
+  const PairTiles tiles{&run.next, &run.posts, &posts_seen};
   switch (rc.cmd.body) {
     case GPUOS_BODY_STREAM: body_stream(rc.cmd, tid, pipe); break;
     case GPUOS_BODY_GEMV_BF16: body_gemv2(rc.cmd, tid, rank, gemv, gate, tiles, nt); break;
@@ -1150,6 +1155,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
   if (tid == 0) {
     sh.guard = WaitGuard{&p.ctl->fault, &p.ctl->quit, p.wait_bound_ns};
     sh.pend.flags = 0u;
+    sh.run.posts = 0u;
   }
   gemm.guard = gemv.guard = &sh.guard;
   if (tid == 0) {
@@ -1181,6 +1187,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
   const unsigned peer_join_full = map_rank(&sh.join_full, 1);
   const unsigned leader_joined = map_rank(&sh.joined, 0);
   const unsigned peer_run_next = map_rank(&sh.run.next, 1);
+  const unsigned peer_run_posts = map_rank(&sh.run.posts, 1);
+  unsigned posts_seen = 0;  // pair-tile posts this thread has consumed (next_block)
   unsigned joins = 0;  // pair tiles this CTA has run (join_full / joined parity)
   // Warp 0's draining state: the atom it last claimed from and the TPC's
   // candidate-set version at that time. While the version is unchanged no
@@ -1493,8 +1501,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
     const int go = sh.go;
     if (go == kGoExit) break;
     {
-      const NextTile nt{p, sh.run, peer_run_next, tpc, sm};
-      run_body(sh.rc, tid, rank, pipe, gemm, gemv, p.atoms, sh.run, nt);  // pair tiles end with a cluster barrier
+      const NextTile nt{p, sh.run, peer_run_next, peer_run_posts, tpc, sm};
+      run_body(sh.rc, tid, rank, pipe, gemm, gemv, p.atoms, sh.run, nt, posts_seen);  // pair tiles end with a cluster barrier
     }
     if (go == kGoPair || go == kGoJoin) ++joins;
     if (tc_hold && tid == 0) {

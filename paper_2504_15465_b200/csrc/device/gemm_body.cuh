@@ -346,7 +346,26 @@ __device__ __forceinline__ void epilogue_staged(const GemmPipe& G, int tid, unsi
 // `run_next`: this CTA's copy of the posted block.
 struct PairTiles {
   volatile long long* run_next;
+  const unsigned* run_posts;  // posts received (NextTile writes it with release)
+  unsigned* seen;             // this thread's count of posts consumed (per worker)
 };
+
+// Every thread of both CTAs, after a pair tile: the run's next block as the
+// leader posted it for this tile. The post (run.next, then the count with a
+// release store, NextTile) is awaited with an acquire load of the count, so
+// the value read is this tile's whatever barrier ends the tile (a relaxed
+// arrive orders nothing); it was posted before the epilogue, so the wait is
+// normally free.
+__device__ __forceinline__ long long next_block(const PairTiles& run) {
+  const unsigned want = ++*run.seen;
+  unsigned v;
+  for (;;) {
+    asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v)
+                 : "r"(static_cast<unsigned>(__cvta_generic_to_shared(run.run_posts))) : "memory");
+    if (static_cast<int>(v - want) >= 0) break;
+  }
+  return *run.run_next;
+}
 
 // Both CTAs of the pair, all threads; rank 0 is the leader.
 // `gate`: the atom's early-start gate (dispatcher.cu): while it is 1 the
@@ -549,7 +568,7 @@ __device__ __forceinline__ void body_gemm2(const BlockCmd& c, int tid, unsigned 
   long long blk = c.block;
   for (;;) {
     gemm2_tile(D, static_cast<unsigned>(blk), tid, rank, G, gate, next_tile);
-    blk = *run.run_next;
+    blk = next_block(run);
     if (blk < 0) break;
     gate = nullptr;  // (open: the run's first tile waited for it)
   }

@@ -272,7 +272,7 @@ __device__ __forceinline__ void body_gemv2(const BlockCmd& c, int tid, unsigned 
   long long blk = c.block;
   for (;;) {
     gemv2_tile(D, static_cast<unsigned>(blk), tid, rank, G, gate, next_tile);
-    blk = *run.run_next;
+    blk = next_block(run);
     if (blk < 0) break;
     gate = nullptr;  // (open: the run's first block waited for it)
   }
