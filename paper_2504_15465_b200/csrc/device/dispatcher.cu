@@ -100,6 +100,11 @@ static_assert(offsetof(DevAtom, chain) % 8 == 0 && offsetof(DevAtom, succ) == of
 // successor: exactly one does, and a successor registered after the
 // predecessor finished is armed by the ingest warp itself.
 constexpr unsigned kSuccDone = 0xffffffffu;
+// DevAtom::succ: a look-ahead (the finisher that armed this atom) claimed
+// the right to arm the registered successor early, behind a closed gate;
+// this atom's finisher then opens that gate once the successor is armed
+// (account_block). Set by CAS, so it never races the finisher's swap.
+constexpr unsigned kSuccLook = 0x80000000u;
 constexpr unsigned kGatedBit = 2u;  // DevAtom::paused: early start, gate closed
 
 // Opens an early-started atom's gate (release: the predecessor's outputs,
@@ -952,9 +957,12 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   if (chain & kChainHead) {
     unsigned next = 0;
     if (lane == 0) {
-      // Registered before we looked: nothing to race with (registration
-      // happens once), and the acquire above ordered its fields.
-      next = pre != 0u ? pre : atom_exch_acq_rel32(&a->succ, kSuccDone);
+      // Always swapped (never taken from an earlier read): a look-ahead may
+      // mark the registration (kSuccLook) until this swap.
+      (void)pre;
+      next = atom_exch_acq_rel32(&a->succ, kSuccDone);
+      const bool look_armed = (next & kSuccLook) != 0u;
+      next &= ~kSuccLook;
       // The successor's hot line, this TPC's fence and b's own registered
       // successor are loaded together (one L2 round trip, not four in a
       // row): this chain is the gap between two dependent kernels.
@@ -965,9 +973,13 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
         cn = ld_acquire_gpu(&p.atoms[next - 1u].succ);
       }
-      if (next != 0u && ((bf.count_paused >> 32) & kGatedBit)) {
-        // Early-started successor: our outputs, acquired through the count
+      if (next != 0u && (look_armed || ((bf.count_paused >> 32) & kGatedBit))) {
+        // Early-started successor (at ingest, or by a look-ahead -- wait for
+        // its gated arming to land): our outputs, acquired through the count
         // above, are released to its gate waiters.
+        if (look_armed)
+          while (ld_acquire_gpu(&p.atoms[next - 1u].armed) == 0u) {
+          }
         open_gate(&p.atoms[next - 1u].paused);
         next = 0;
       }
@@ -985,10 +997,12 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         b->armed = 1u;
         // Lookahead: b's own registered successor, if a GEMV that may start
         // early, is armed now behind a closed gate (b opens it).
-        if (cn != 0u && cn != kSuccDone) {
+        if (cn != 0u && cn != kSuccDone && !(cn & kSuccLook)) {
           DevAtom* c = p.atoms + (cn - 1u);
+          // The mark on b's registration decides against b's own finisher:
+          // if b already finished (swapped in DONE), it armed c itself.
           if (body_is_pair(c->body) && !(c->chain & kNoEarly) && c->prio <= bprio &&
-              ld_relaxed_gpu(&c->armed) == 0u) {
+              ld_relaxed_gpu(&c->armed) == 0u && atomicCAS(&b->succ, cn, cn | kSuccLook) == cn) {
             // Armed claim and closed gate in one 16-byte store: a claimer
             // never sees one without the other.
             const unsigned cpz = (ld_relaxed_gpu(&c->paused) & 0xffff0000u) | kGatedBit;  // (tenant kept)
@@ -998,7 +1012,8 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
                          "l"(static_cast<unsigned long long>(c->seq) << 32), "l"(cc)
                          : "memory");
             c->t_armed = gtimer();
-            c->armed = 1u;
+            // (release: b's finisher opens the gate only after this arming)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&c->armed), "r"(1u) : "memory");
             look = cn;
           }
         }

@@ -327,3 +327,50 @@ def test_no_early_keeps_a_chained_gemv_behind_its_predecessor(api, cuda_device):
     ref = (w2.double().cpu() @ y1.double().cpu()).float()
     err = ((y2.cpu() - ref).abs().max() / ref.abs().max()).item()
     assert err < 1e-3, err
+
+
+def test_look_ahead_races_the_successors_own_finisher(api, cuda_device):
+    """Chains alternating GEMV -> one-block STREAM -> GEMV ...: a GEMV's
+    finisher arms the STREAM and looks ahead to arm the next GEMV behind a
+    gate, while the STREAM -- on a TPC the finisher is not on, so another
+    worker runs it -- may finish first and arm that GEMV itself. Exactly one
+    of them may arm it (kSuccLook / the finisher's swap): arming it twice
+    re-opened its claims behind a gate nobody would open again (a stall a
+    config-#3 run hit once in ~12). Many short chains must all complete, in
+    chain order, every block once."""
+    import torch
+
+    n, k = 1024, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    w = (torch.rand(n, k, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    x = (torch.rand(k, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    y = torch.zeros(n, device="cuda")
+    src = torch.randint(-2**31, 2**31 - 1, (WORDS,), dtype=torch.int32, device="cuda")
+    dst = torch.zeros_like(src)
+    torch.cuda.synchronize()
+    chains, length = 40, 12
+    with api.Device(workers_per_sm=2) as dev:
+        d, blocks = dev.gemv_desc(w.data_ptr(), x.data_ptr(), y.data_ptr(), n, k, k_splits=2)
+        dev.start()
+        ids = []
+        for c in range(chains):
+            prev = None
+            chain = []
+            for j in range(length):
+                head = j + 1 < length
+                if j % 2 == 0:
+                    aid = dev.submit(0, blocks, list(range(8, 74)), 30, api.GPUOS_BODY_GEMV_BF16, [d],
+                                     after=prev, chain_head=head)
+                else:
+                    aid = dev.submit(0, 1, [c % 8], 30, api.GPUOS_BODY_STREAM,
+                                     [src.data_ptr(), dst.data_ptr(), WORDS, 5, 1], after=prev, chain_head=head)
+                chain.append(aid)
+                prev = aid
+            ids.append(chain)
+            if c % 4 == 3:  # keep the atom table and resident lists from filling
+                wait_all(dev, 4 * length, timeout=30.0)
+        rest = chains % 4
+        if rest:
+            wait_all(dev, rest * length, timeout=30.0)
+        dev.stop()
+        dev.free(d)
