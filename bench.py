@@ -493,8 +493,8 @@ def model_configs(local: int) -> dict:
     # (nearest-rank p99 over >= 800 samples), alone runs likewise.
     from paper_2504_15465_b200 import workloads as wl
 
-    for name, horizon, reps, cfg in (("infer4", 2000.0, 4, None), ("hybrid", 1000.0, 3, None),
-                                     ("hybrid_real_attention", 1000.0, 3, wl.hybrid(1000.0, real_attention=True))):
+    for name, horizon, reps, cfg in (("infer4", 2000.0, 4, None), ("hybrid", 1000.0, 6, None),
+                                     ("hybrid_real_attention", 1000.0, 6, wl.hybrid(1000.0, real_attention=True))):
         r = configs.run("hybrid" if cfg is not None else name, horizon_ms=horizon, reps=reps, device=local, cfg=cfg)
         out[name] = {"tpc_utilization": r["tpc_utilization"], "apps": {
             a: {k: v for k, v in row.items() if k in ("priority", "p99_vs_alone", "slo_attainment",
@@ -504,7 +504,7 @@ def model_configs(local: int) -> dict:
             for a, row in r["apps"].items()}, "knobs": r["knobs"]}
     out["note"] = ("#2: 2x ResNet-50 b1 (150 rps) + 2x BERT-base b8 (100 rps), LC, Poisson, beside a "
                    "ResNet-50 b256 training tenant (BE, closed loop), 2 s x 4 runs; #3: Llama-3-8B decode LC "
-                   "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 3 runs; decode "
+                   "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 6 runs (~340 tokens); decode "
                    "RMSNorm / SiLU-mul as tenant bodies, attention as a byte-equivalent STREAM kernel "
                    "(hybrid) or the attn_decode_bf16 tenant body (hybrid_real_attention); "
                    "alone = the same scenario with the other tenants silent; static = each tenant on its "
@@ -538,7 +538,7 @@ def gemm_saturation(api, local: int, args) -> dict:
         # start is ~2 %; two back-to-back copies measured lower (1484 vs
         # 1540 TF/s: the second atom's tiles interleave with the first's and
         # break the grouped raster's L2 reuse -- DRAM 2.07 GB for 0.81 GB).
-        kernels = 1
+        kernels = int(os.environ.get("GPUOS_BENCH_GEMM_KERNELS", "1"))
         descs = [api.Device.desc(i * blocks // n_atoms, (i + 1) * blocks // n_atoms, range(74), 20,
                                  api.GPUOS_BODY_GEMM_BF16, [desc]) for i in range(n_atoms)] * kernels
         for _ in range(5):  # best of 5 (MEASURED_PEAKS' cuBLAS figure is a best of 10)

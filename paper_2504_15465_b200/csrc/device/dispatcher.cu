@@ -884,19 +884,17 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   const bool single = rc.count == 1u;
   unsigned long long s_t0 = t_start, s_t1 = 0;
   // Fields fixed for the atom's lifetime, read by its finisher (for a
-  // single-slice atom up front, overlapping the accounting). For a chain
-  // head, a successor already registered (set once) is read with them,
-  // with acquire: the finisher then arms it without the swap.
+  // single-slice atom up front, overlapping the accounting). A chain head's
+  // registered successor is always taken by the swap below (a look-ahead
+  // may mark the registration until then).
   unsigned long long tag = 0, ts = 0, ta = 0;
-  unsigned chain = 0, pre = 0;
+  unsigned chain = 0;
   SuccFields bf;
   auto finisher_fields = [&] {
     tag = a->tag;
     ts = ld_relaxed_gpu64(&a->t_seen);
     ta = ld_relaxed_gpu64(&a->t_armed);
-    const unsigned long long cs = ld_acquire_gpu64(reinterpret_cast<unsigned long long*>(&a->chain));
-    chain = static_cast<unsigned>(cs);
-    pre = (chain & kChainHead) ? static_cast<unsigned>(cs >> 32) : 0u;
+    chain = ld_acquire_gpu(&a->chain);
   };
   if (lane == 0) {
     const unsigned long long t_end = gtimer();
@@ -959,7 +957,6 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
     if (lane == 0) {
       // Always swapped (never taken from an earlier read): a look-ahead may
       // mark the registration (kSuccLook) until this swap.
-      (void)pre;
       next = atom_exch_acq_rel32(&a->succ, kSuccDone);
       const bool look_armed = (next & kSuccLook) != 0u;
       next &= ~kSuccLook;

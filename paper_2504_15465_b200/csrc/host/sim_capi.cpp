@@ -85,6 +85,7 @@ void apply_knob(ScenarioConfig& c, const std::string& k, const json& v) {
   else if (k == "be_coexist") s.be_coexist = flag();
   else if (k == "hp_pair_reserve") s.hp_pair_reserve = flag();
   else if (k == "hp_quota_full") s.hp_quota_full = flag();
+  else if (k == "hp_steal_busy_be") s.hp_steal_busy_be = flag();
   else if (k == "atom_duration_us") s.atom_duration = duration_from_us(v.get<double>());
   else if (k == "steal_horizon_us") s.steal_horizon = duration_from_us(v.get<double>());
   else if (k == "max_outstanding_atoms") s.max_outstanding_atoms = v.get<int>();

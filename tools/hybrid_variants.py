@@ -22,6 +22,8 @@ VARIANTS = {
     "I": ({"be_coexist": True, "hp_pair_reserve": True, "atom_lookahead": True}, {}),
     "J": ({"be_coexist": True, "hp_pair_reserve": True, "hp_quota_full": True}, {}),
     "L": ({"chain_best_effort": True}, {}),
+    "P": ({"hp_steal_busy_be": False}, {}),
+    "Q": ({"hp_steal_busy_be": False, "atom_lookahead": True}, {}),
     "N": ({"atom_duration_us": 500.0}, {}),
     "O": ({"atom_duration_us": 2000.0}, {}),
     "K": ({"be_coexist": True, "hp_pair_reserve": True, "hp_quota_full": True, "chain_best_effort": True}, {}),
