@@ -23,6 +23,8 @@ VARIANTS = {
     "J": ({"be_coexist": True, "hp_pair_reserve": True, "hp_quota_full": True}, {}),
     "L": ({"chain_best_effort": True}, {}),
     "P": ({"hp_steal_busy_be": False}, {}),
+    "R": ({"hp_pair_reserve": True, "hp_quota_full": True}, {}),
+    "S": ({"hp_pair_reserve": True}, {}),
     "Q": ({"hp_steal_busy_be": False, "atom_lookahead": True}, {}),
     "N": ({"atom_duration_us": 500.0}, {}),
     "O": ({"atom_duration_us": 2000.0}, {}),
