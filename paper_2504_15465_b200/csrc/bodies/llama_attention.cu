@@ -33,7 +33,10 @@ constexpr unsigned kWsCounters = 8192, kWsPartials = 8448;
 GPUOS_USER_BODY(attn_decode_bf16) {
   using namespace gpuos_bodies_attn;
   const unsigned ctx = static_cast<unsigned>(args[3]);
-  const unsigned chunk = static_cast<unsigned>(args[3] >> 32);
+  const unsigned chunk = static_cast<unsigned>((args[3] >> 32) & 0x7fffffffu);
+  // Profiling (args[3] bit 63): 4 globaltimer stamps per block after the
+  // partials (start, K/V loaded, partials written, end).
+  unsigned long long* stamps = nullptr;
   const unsigned chunks = b.gx, kvh = b.y, cx = b.x;
   const unsigned p0 = cx * chunk, p1 = p0 + chunk < ctx ? p0 + chunk : ctx;
   const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(args[0]);
@@ -42,6 +45,17 @@ GPUOS_USER_BODY(attn_decode_bf16) {
   unsigned char* ws = reinterpret_cast<unsigned char*>(args[2]);
   unsigned* counters = reinterpret_cast<unsigned*>(ws + kWsCounters);
   float* part = reinterpret_cast<float*>(ws + kWsPartials);
+  if (args[3] >> 63)
+    stamps = reinterpret_cast<unsigned long long*>(ws + kWsPartials + 4ull * kQHeads * chunks * (2 + kHeadDim)) +
+             4ull * static_cast<unsigned long long>(b.block);
+  auto stamp = [&](int i) {
+    if (stamps && b.tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      stamps[i] = t;
+    }
+  };
+  stamp(0);
   const int warp = b.tid >> 5, lane = b.tid & 31;
   // Shared: per-warp o partials [8 warps][4][128], the per-warp max / sum of
   // each head, the merge flag; the merge reuses the o area.
@@ -60,6 +74,7 @@ GPUOS_USER_BODY(attn_decode_bf16) {
     kr[i] = *reinterpret_cast<const uint2*>(kc + off);
     vr[i] = *reinterpret_cast<const uint2*>(vc + off);
   }
+  stamp(1);  // (loads issued; their latency lands on the first use below)
   // This lane's 4 dims of the 4 query heads, rotated (RoPE at position ctx).
   float qr[kQPerKv][4];
   const float pos = static_cast<float>(ctx);
@@ -158,6 +173,7 @@ GPUOS_USER_BODY(attn_decode_bf16) {
       ph[1] = ll;
     }
   }
+  stamp(2);
   // The KV head's last chunk merges (self-resetting counter, as split-K):
   // the block's partials precede its count (CTA barrier, then a release
   // add), and the last block's acquire sees every other block's.
@@ -170,46 +186,88 @@ GPUOS_USER_BODY(attn_decode_bf16) {
   }
   __syncthreads();
   if (*last) {
-    // Merge weights per (head, chunk) in shared memory -- w = exp(m_c - M) /
-    // L with M the head's max and L = sum l_c exp(m_c - M) -- then each
-    // (head, dim) thread sums its chunks' o with the loads in flight
-    // together (a loop of dependent L2 reads cost ~40 us per head group).
-    float* mw = ow;  // [4][kMaxChunks] (the o partials are written out)
-    float* lw = mw + kQPerKv * kMaxChunks;
-    for (unsigned t = b.tid; t < kQPerKv * chunks; t += GPUOS_BLOCK_THREADS) {
-      const unsigned h = t / chunks, c = t % chunks;
-      const float* pc = part + (static_cast<size_t>(kvh * kQPerKv + h) * chunks + c) * (2 + kHeadDim);
-      mw[h * kMaxChunks + c] = __ldcg(pc);
-      lw[h * kMaxChunks + c] = __ldcg(pc + 1);
-    }
-    __syncthreads();
-    if (warp < static_cast<int>(kQPerKv)) {  // warp h: head h's weights, a lane per 32 chunks
-      const unsigned h = static_cast<unsigned>(warp);
-      float Mx = -INFINITY;
-      for (unsigned c = lane; c < chunks; c += 32) Mx = fmaxf(Mx, mw[h * kMaxChunks + c]);
+    // Merge. The KV head's partials -- [4 heads][chunks][m, l, o[128]],
+    // contiguous -- are copied into shared memory with cp.async (every
+    // 16-byte piece in flight at once: one L2 round trip on the critical
+    // path, no registers held); warp h turns head h's (m, l) into weights
+    // w = exp(m_c - M) / L (M the head's max, L = sum l_c exp(m_c - M)),
+    // then each thread sums its two (head, dim) outputs over the chunks.
+    const unsigned row = 2 + kHeadDim;
+    const unsigned long long bytes = 4ull * kQPerKv * chunks * row;
+    float* P = reinterpret_cast<float*>(b.smem);  // [4][chunks][row]
+    float* W = P + kQPerKv * chunks * row;        // [4][chunks] weights
+    if (bytes + 4ull * kQPerKv * chunks <= b.smem_bytes) {
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(part + static_cast<size_t>(kvh) * kQPerKv * chunks * row);
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(P));
+      for (unsigned q16 = b.tid; q16 < bytes / 16; q16 += GPUOS_BLOCK_THREADS)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * q16), "l"(src + 16ull * q16) : "memory");
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+      __syncthreads();
+      if (warp < static_cast<int>(kQPerKv)) {  // warp h: head h's weights
+        const unsigned h = static_cast<unsigned>(warp);
+        float Mx = -INFINITY;
+        for (unsigned c = lane; c < chunks; c += 32) Mx = fmaxf(Mx, P[(h * chunks + c) * row]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
-      float L = 0.f;
-      for (unsigned c = lane; c < chunks; c += 32) {
-        const float w = __expf(mw[h * kMaxChunks + c] - Mx);
-        mw[h * kMaxChunks + c] = w;
-        L += lw[h * kMaxChunks + c] * w;
+        for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+        float L = 0.f;
+        for (unsigned c = lane; c < chunks; c += 32) {
+          const float w = __expf(P[(h * chunks + c) * row] - Mx);
+          W[h * chunks + c] = w;
+          L += P[(h * chunks + c) * row + 1] * w;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        const float inv = 1.f / L;
+        for (unsigned c = lane; c < chunks; c += 32) W[h * chunks + c] *= inv;
       }
+      __syncthreads();
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ws) + kvh * kQPerKv * kHeadDim;
+      for (unsigned t = b.tid; t < kQPerKv * kHeadDim; t += GPUOS_BLOCK_THREADS) {
+        const unsigned h = t / kHeadDim, d = t % kHeadDim;
+        float O = 0.f;
+        for (unsigned c = 0; c < chunks; ++c) O += W[h * chunks + c] * P[(h * chunks + c) * row + 2 + d];
+        out[t] = __float2bfloat16_rn(O);
+      }
+    } else {
+      // (more chunks than shared memory holds: the same merge from L2)
+      float* mw = ow;  // [4][kMaxChunks]
+      float* lw = mw + kQPerKv * kMaxChunks;
+      for (unsigned t = b.tid; t < kQPerKv * chunks; t += GPUOS_BLOCK_THREADS) {
+        const unsigned h = t / chunks, c = t % chunks;
+        const float* pc = part + (static_cast<size_t>(kvh * kQPerKv + h) * chunks + c) * row;
+        mw[h * kMaxChunks + c] = __ldcg(pc);
+        lw[h * kMaxChunks + c] = __ldcg(pc + 1);
+      }
+      __syncthreads();
+      if (warp < static_cast<int>(kQPerKv)) {
+        const unsigned h = static_cast<unsigned>(warp);
+        float Mx = -INFINITY;
+        for (unsigned c = lane; c < chunks; c += 32) Mx = fmaxf(Mx, mw[h * kMaxChunks + c]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-      const float inv = 1.f / L;
-      for (unsigned c = lane; c < chunks; c += 32) mw[h * kMaxChunks + c] *= inv;
-    }
-    __syncthreads();
-    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ws);
-    for (unsigned t = b.tid; t < kQPerKv * kHeadDim; t += GPUOS_BLOCK_THREADS) {
-      const unsigned h = t / kHeadDim, d = t % kHeadDim;
-      const float* ph = part + static_cast<size_t>(kvh * kQPerKv + h) * chunks * (2 + kHeadDim) + 2 + d;
-      float O = 0.f;
+        for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+        float L = 0.f;
+        for (unsigned c = lane; c < chunks; c += 32) {
+          const float w = __expf(mw[h * kMaxChunks + c] - Mx);
+          mw[h * kMaxChunks + c] = w;
+          L += lw[h * kMaxChunks + c] * w;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        const float inv = 1.f / L;
+        for (unsigned c = lane; c < chunks; c += 32) mw[h * kMaxChunks + c] *= inv;
+      }
+      __syncthreads();
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ws);
+      for (unsigned t = b.tid; t < kQPerKv * kHeadDim; t += GPUOS_BLOCK_THREADS) {
+        const unsigned h = t / kHeadDim, d = t % kHeadDim;
+        const float* ph = part + static_cast<size_t>(kvh * kQPerKv + h) * chunks * row + 2 + d;
+        float O = 0.f;
 #pragma unroll 16
-      for (unsigned c = 0; c < chunks; ++c) O += mw[h * kMaxChunks + c] * __ldcg(ph + c * (2 + kHeadDim));
-      out[(kvh * kQPerKv + h) * kHeadDim + d] = __float2bfloat16_rn(O);
+        for (unsigned c = 0; c < chunks; ++c) O += mw[h * kMaxChunks + c] * __ldcg(ph + c * row);
+        out[(kvh * kQPerKv + h) * kHeadDim + d] = __float2bfloat16_rn(O);
+      }
     }
   }
+  stamp(3);
   __syncthreads();  // (shared memory reused by the worker's next block)
 }
