@@ -493,7 +493,7 @@ def model_configs(local: int) -> dict:
     # (nearest-rank p99 over >= 800 samples), alone runs likewise.
     from paper_2504_15465_b200 import workloads as wl
 
-    for name, horizon, reps, cfg in (("infer4", 2000.0, 4, None), ("hybrid", 1000.0, 6, None),
+    for name, horizon, reps, cfg in (("infer4", 2000.0, 4, None), ("hybrid", 1000.0, 10, None),
                                      ("hybrid_real_attention", 1000.0, 6, wl.hybrid(1000.0, real_attention=True))):
         r = configs.run("hybrid" if cfg is not None else name, horizon_ms=horizon, reps=reps, device=local, cfg=cfg)
         out[name] = {"tpc_utilization": r["tpc_utilization"], "apps": {
@@ -504,7 +504,7 @@ def model_configs(local: int) -> dict:
             for a, row in r["apps"].items()}, "knobs": r["knobs"]}
     out["note"] = ("#2: 2x ResNet-50 b1 (150 rps) + 2x BERT-base b8 (100 rps), LC, Poisson, beside a "
                    "ResNet-50 b256 training tenant (BE, closed loop), 2 s x 4 runs; #3: Llama-3-8B decode LC "
-                   "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 6 runs (~340 tokens); decode "
+                   "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 10 runs (~580 tokens; 6 for the real-attention line); decode "
                    "RMSNorm / SiLU-mul as tenant bodies, attention as a byte-equivalent STREAM kernel "
                    "(hybrid) or the attn_decode_bf16 tenant body (hybrid_real_attention); "
                    "alone = the same scenario with the other tenants silent; static = each tenant on its "
