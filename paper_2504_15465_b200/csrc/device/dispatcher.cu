@@ -57,6 +57,18 @@ namespace gpuos_dev_impl {
 constexpr int kResident = GPUOS_RESIDENT_PER_TPC;  // keys per TPC (one per lane)
 static_assert(kResident == 32, "one resident key per lane");
 
+// Handoff probe (GPUOS_PROBE_HANDOFF builds only, tools/chain_gap_probe.py):
+// SM clock stamps along a finisher's path into the block it handed itself.
+#ifdef GPUOS_PROBE_HANDOFF
+constexpr int kProbeStamps = 12;
+__device__ unsigned long long g_probe_cur[1184][kProbeStamps];
+__device__ unsigned long long g_probe_ring[4096][kProbeStamps];
+__device__ unsigned g_probe_n;
+#define PROBE_AT(i) (g_probe_cur[blockIdx.x][i] = clock64())
+#else
+#define PROBE_AT(i) ((void)0)
+#endif
+
 enum Op : unsigned { kOpSubmit = 1, kOpPause = 2, kOpResume = 3, kOpFence = 4,
                      kOpDrain = 5, kOpShutdown = 6, kOpFenceMask = 7 };
 
@@ -135,6 +147,7 @@ __device__ __forceinline__ unsigned tenant_of(unsigned long long count_paused) {
 constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head | no early
 constexpr unsigned kAuxNoEarly = 0x40000000u;
 constexpr unsigned kNoEarly = 2u;                 // DevAtom::chain: GPUOS_ATOM_NO_EARLY
+constexpr unsigned kRcTraced = 0x80000000u;       // RoundCmd::chain only: the atom has a trace buffer
 
 struct DevCtl {
   unsigned quit;
@@ -592,7 +605,7 @@ struct RoundCmd {
   unsigned slot;
   unsigned count;               // slices of the atom (1: single-block fast path)
   unsigned gated;               // the atom was early-started: its body checks the gate
-  unsigned pad;
+  unsigned chain;               // DevAtom::chain (kChainHead | kNoEarly), read with the fields
 };
 constexpr int kRoundCmdWords64 = sizeof(RoundCmd) / 8;
 static_assert(sizeof(RoundCmd) % 8 == 0, "RoundCmd copied as 64-bit words");
@@ -631,7 +644,7 @@ struct PairRun {
 // A finished atom's bookkeeping held back while its handed-off successor
 // runs (account_block / write_done).
 struct PendingDone {
-  unsigned long long t0, t1, m0, m1, tag, ts, ta;  // t0, m0, m1: single-slice atoms (else read here)
+  unsigned long long t0, t1, m0, m1;  // t0, m0, m1: single-slice atoms (else read here)
   unsigned slot, tk, n, flags;                     // flags: kPendValid | kPendSingle
 };
 constexpr unsigned kPendValid = 1u, kPendSingle = 2u;
@@ -794,7 +807,7 @@ struct NextTile {
 // now holds block 0 of its chained successor, claimed for this worker).
 // A chained successor's hot-line fields (account_block).
 struct SuccFields {
-  unsigned long long count_paused, lo, body_parts, args[5], seq_prio, mask[2];
+  unsigned long long count_paused, lo, body_parts, args[5], seq_prio, mask[2], trace;
   __device__ __forceinline__ void load(const DevAtom* b) {
     unsigned long long claim;
     ld_relaxed_gpu_v2(b, claim, count_paused);
@@ -804,6 +817,7 @@ struct SuccFields {
     ld_relaxed_gpu_v2(&b->args[4], args[4], seq_prio);
     mask[0] = ld_relaxed_gpu64(&b->mask[0]);  // (+104: 8-byte aligned)
     mask[1] = ld_relaxed_gpu64(&b->mask[1]);
+    trace = ld_relaxed_gpu64(reinterpret_cast<const unsigned long long*>(&b->trace));
   }
 };
 
@@ -833,17 +847,21 @@ __device__ __forceinline__ void write_done(const Params& p, PendingDone& d, unsi
     const unsigned long long t0 = single ? d.t0 : ld_relaxed_gpu64(&a->t_first);
     const unsigned long long m0 = single ? d.m0 : ld_relaxed_gpu64(&a->touched[0]);
     const unsigned long long m1 = single ? d.m1 : ld_relaxed_gpu64(&a->touched[1]);
+    // (fixed for the atom's lifetime; loaded here, off the finisher's path)
+    const unsigned long long tag = a->tag;
+    const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
+    const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
     const unsigned tk = d.tk;
     const unsigned long long span = d.t1 - t0;
-    st_relaxed_sys_v4(rec->w + 0, d.n, static_cast<unsigned>(d.tag), static_cast<unsigned>(d.tag >> 32), tk);
+    st_relaxed_sys_v4(rec->w + 0, d.n, static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32), tk);
     st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
                       span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
     st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
                       static_cast<unsigned>(m1), tk);
     // t_seen / t_armed as ns before t_first (0 in batch mode).
     st_relaxed_sys_v4(rec->w + 12, static_cast<unsigned>(m1 >> 32),
-                      d.ts ? static_cast<unsigned>(t0 - d.ts) : 0u,
-                      d.ta ? static_cast<unsigned>(t0 - d.ta) : 0u, tk);
+                      ts ? static_cast<unsigned>(t0 - ts) : 0u,
+                      ta ? static_cast<unsigned>(t0 - ta) : 0u, tk);
   }
   // Device-side bookkeeping after the record; the host recycles this slot
   // only after thousands of others, long after these land. Our key still
@@ -883,24 +901,17 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   // round trips less on every small kernel).
   const bool single = rc.count == 1u;
   unsigned long long s_t0 = t_start, s_t1 = 0;
-  // Fields fixed for the atom's lifetime, read by its finisher (for a
-  // single-slice atom up front, overlapping the accounting). A chain head's
-  // registered successor is always taken by the swap below (a look-ahead
-  // may mark the registration until then).
-  unsigned long long tag = 0, ts = 0, ta = 0;
-  unsigned chain = 0;
+  // The chain word came with the atom's fields (RoundCmd::chain): a
+  // finisher goes from its count straight to the successor swap. (A chain
+  // head's registered successor is always taken by that swap; a look-ahead
+  // may mark the registration until then.)
+  unsigned chain = rc.chain;
   SuccFields bf;
-  auto finisher_fields = [&] {
-    tag = a->tag;
-    ts = ld_relaxed_gpu64(&a->t_seen);
-    ta = ld_relaxed_gpu64(&a->t_armed);
-    chain = ld_acquire_gpu(&a->chain);
-  };
   if (lane == 0) {
     const unsigned long long t_end = gtimer();
+    PROBE_AT(0);
     s_t1 = t_end;
-    if (single) finisher_fields();
-    if (a->trace != nullptr)
+    if (chain & kRcTraced)
       atomicAdd(a->trace + rc.cmd.block * rc.cmd.parts + rc.cmd.part, 0x10000u + sm + 1u);
     busy += t_end - t_start;
     n_blocks += 1u + extra;
@@ -908,6 +919,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       // The body's output (and trace) precede the completion record; a
       // chain head fences after arming its successor (off its path).
       if (!(chain & kChainHead)) __threadfence();
+      PROBE_AT(1);
       last = 1;
     } else {
       // Per-block records kept off the atom's hot line (every worker of
@@ -929,7 +941,6 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       last = atom_add_acq_rel32(&a->done, 1u + extra) + 1u + extra == rc.count;
       if (last) {
         s_t1 = gtimer();  // every block has ended (each counted after its end)
-        finisher_fields();
       }
     }
   }
@@ -951,24 +962,28 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   RoundCmd ho;
   int handoff = 0;
   unsigned look = 0;  // lane 0: successor's successor armed early (slot + 1)
-  chain = __shfl_sync(0xffffffffu, chain, 0);
+  unsigned long long look_m0 = 0, look_m1 = 0;  // lane 0: its TPC set
   if (chain & kChainHead) {
     unsigned next = 0;
     if (lane == 0) {
       // Always swapped (never taken from an earlier read): a look-ahead may
       // mark the registration (kSuccLook) until this swap.
       next = atom_exch_acq_rel32(&a->succ, kSuccDone);
+      if (next != 0u) PROBE_AT(2);
       const bool look_armed = (next & kSuccLook) != 0u;
       next &= ~kSuccLook;
       // The successor's hot line, this TPC's fence and b's own registered
       // successor are loaded together (one L2 round trip, not four in a
       // row): this chain is the gap between two dependent kernels.
       int floor_prio = 0;
-      unsigned cn = 0;
+      unsigned cn = 0, b_chain = 0;
       if (next != 0u) {
         bf.load(p.atoms + (next - 1u));
         floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
-        cn = ld_acquire_gpu(&p.atoms[next - 1u].succ);
+        const unsigned long long b_cs =
+            ld_acquire_gpu64(reinterpret_cast<const unsigned long long*>(&p.atoms[next - 1u].chain));
+        cn = static_cast<unsigned>(b_cs >> 32);  // b's registered successor
+        b_chain = static_cast<unsigned>(b_cs);
       }
       if (next != 0u && (look_armed || ((bf.count_paused >> 32) & kGatedBit))) {
         // Early-started successor (at ingest, or by a look-ahead -- wait for
@@ -989,31 +1004,45 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
         const bool here = (((tpc < 64 ? bf.mask[0] : bf.mask[1]) >> (tpc & 63)) & 1ull) && ((bf.count_paused >> 32) & 1ull) == 0u &&
                           fence_admits(floor_prio, bprio, tenant_of(bf.count_paused), pair_slot) &&
                           (!body_is_pair(bbody) || rank == 0u);
+        PROBE_AT(3);
         st_relaxed_gpu64(&b->claim, (static_cast<unsigned long long>(bseq) << 32) | (here ? 1u : 0u));
         b->t_armed = gtimer();
         b->armed = 1u;
         // Lookahead: b's own registered successor, if a GEMV that may start
-        // early, is armed now behind a closed gate (b opens it).
+        // early, is armed now behind a closed gate (b opens it). Every field
+        // of c this needs is loaded in one round trip (fixed since c's
+        // registration, which the acquire of cn ordered before these loads).
         if (cn != 0u && cn != kSuccDone && !(cn & kSuccLook)) {
           DevAtom* c = p.atoms + (cn - 1u);
+          unsigned long long c_claim, c_cp, c_lo, c_bp;
+          ld_relaxed_gpu_v2(c, c_claim, c_cp);      // claim, count | paused
+          ld_relaxed_gpu_v2(&c->lo, c_lo, c_bp);    // lo, body | parts
+          const unsigned long long c_sp = ld_relaxed_gpu64(reinterpret_cast<const unsigned long long*>(&c->seq));  // seq | prio
+          const unsigned long long c_m0 = ld_relaxed_gpu64(&c->mask[0]);
+          const unsigned long long c_m1 = ld_relaxed_gpu64(&c->mask[1]);
+          const unsigned long long c_cs = ld_relaxed_gpu64(reinterpret_cast<const unsigned long long*>(&c->chain));  // chain | succ
+          const unsigned c_armed = ld_relaxed_gpu(&c->armed);
           // The mark on b's registration decides against b's own finisher:
           // if b already finished (swapped in DONE), it armed c itself.
-          if (body_is_pair(c->body) && !(c->chain & kNoEarly) && c->prio <= bprio &&
-              ld_relaxed_gpu(&c->armed) == 0u && atomicCAS(&b->succ, cn, cn | kSuccLook) == cn) {
+          if (body_is_pair(static_cast<unsigned>(c_bp)) && !(static_cast<unsigned>(c_cs) & kNoEarly) &&
+              static_cast<int>(c_sp >> 32) <= bprio && c_armed == 0u &&
+              atomicCAS(&b->succ, cn, cn | kSuccLook) == cn) {
             // Armed claim and closed gate in one 16-byte store: a claimer
             // never sees one without the other.
-            const unsigned cpz = (ld_relaxed_gpu(&c->paused) & 0xffff0000u) | kGatedBit;  // (tenant kept)
-            const unsigned long long cc = static_cast<unsigned long long>(c->count) |
-                                          (static_cast<unsigned long long>(cpz) << 32);
+            const unsigned cpz = (static_cast<unsigned>(c_cp >> 32) & 0xffff0000u) | kGatedBit;  // (tenant kept)
+            const unsigned long long cc = (c_cp & 0xffffffffull) | (static_cast<unsigned long long>(cpz) << 32);
             asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(&c->claim),
-                         "l"(static_cast<unsigned long long>(c->seq) << 32), "l"(cc)
+                         "l"(static_cast<unsigned long long>(static_cast<unsigned>(c_sp)) << 32), "l"(cc)
                          : "memory");
             c->t_armed = gtimer();
             // (release: b's finisher opens the gate only after this arming)
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&c->armed), "r"(1u) : "memory");
             look = cn;
+            look_m0 = c_m0;
+            look_m1 = c_m1;
           }
         }
+        PROBE_AT(4);
         if (here) {
           handoff = 1;
 #pragma unroll
@@ -1028,6 +1057,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
           ho.slot = next - 1u;
           ho.count = bcount;
           ho.gated = 0u;  // armed by this finisher: not early
+          ho.chain = b_chain | (bf.trace ? kRcTraced : 0u);
           if (bcount == 1u) next = 0;  // nothing left for other workers: no wake-up
         }
       }
@@ -1036,27 +1066,28 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
     handoff = __shfl_sync(0xffffffffu, handoff, 0);
     look = __shfl_sync(0xffffffffu, look, 0);
     if (next != 0u || look != 0u) {
-      __syncwarp();
+      // The TPC sets to wake (lane 0 loaded them with the fields).
+      const unsigned long long m0 = __shfl_sync(0xffffffffu, (next ? bf.mask[0] : 0ull) | look_m0, 0);
+      const unsigned long long m1 = __shfl_sync(0xffffffffu, (next ? bf.mask[1] : 0ull) | look_m1, 0);
       fence_acq_rel_gpu();  // every lane: the armed claims before the version bumps
-      for (int t = lane; t < p.logical_tpcs; t += 32) {
-        const unsigned long long m = (next ? p.atoms[next - 1u].mask[t >> 6] : 0ull) |
-                                     (look ? p.atoms[look - 1u].mask[t >> 6] : 0ull);
-        if ((m >> (t & 63)) & 1ull) red_relaxed_gpu_add(p.version + t, 1u);
-      }
+      for (int t = lane; t < p.logical_tpcs; t += 32)
+        if ((((t < 64) ? m0 : m1) >> (t & 63)) & 1ull) red_relaxed_gpu_add(p.version + t, 1u);
     }
   }
   // The previous handoff's bookkeeping (its successor -- this block -- is
   // past its own chain work now), then this atom's: written at once, or
   // held back while the successor handed off here runs.
+  if (lane == 0) PROBE_AT(5);
   flush_pending(p, pend, lane);
   if (lane == 0) {
-    if (single && (chain & kChainHead)) __threadfence();  // outputs before the record
+    PROBE_AT(6);
+    // Outputs before the record. A handed-off successor's accounting
+    // writes this record later, after its own acq_rel count / swap or
+    // fence, which orders these outputs too.
+    if (single && (chain & kChainHead) && !handoff) __threadfence();
     pend.slot = rc.slot;
     pend.tk = ~static_cast<unsigned>(rc.key >> 24);
     pend.n = rc.count / rc.cmd.parts;
-    pend.tag = tag;
-    pend.ts = ts;
-    pend.ta = ta;
     pend.t0 = s_t0;
     pend.t1 = s_t1;
     pend.m0 = tpc < 64 ? 1ull << tpc : 0ull;
@@ -1067,6 +1098,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   if (!handoff) write_done(p, pend, lane);
   if (lane == 0 && handoff) rc = ho;  // (rc's old contents are no longer needed)
   __syncwarp();
+  if (lane == 0) PROBE_AT(7);
   return 1 + handoff;
 }
 
@@ -1235,6 +1267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
         // Block 0 of a chained successor, claimed when its predecessor ended
         // here (account_block); a pair tile takes the tensor reservation.
         handoff = false;
+        if (lane == 0) PROBE_AT(8);
         cur_key = 0ull;
         cur_body = lane0_field(sh.rc.cmd.body, lane);
         go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
@@ -1287,6 +1320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
             const unsigned long long k = ld_acquire_gpu64(list + lane);
             bool eligible = false;
             unsigned long long f_lo = 0, f_bp = 0, f_cp = 0, f_cw = 0, f_a[5] = {0, 0, 0, 0, 0};
+            unsigned f_ch = 0;
             if (k != 0ull) {
               const DevAtom* a = p.atoms + (k & 0xffffffull);
               unsigned long long cw, cp;
@@ -1297,6 +1331,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
               ld_relaxed_gpu_v2(&a->args[0], f_a[0], f_a[1]);
               ld_relaxed_gpu_v2(&a->args[2], f_a[2], f_a[3]);
               f_a[4] = ld_relaxed_gpu64(&a->args[4]);
+              f_ch = ld_relaxed_gpu(&a->chain) |
+                     (ld_relaxed_gpu64(reinterpret_cast<const unsigned long long*>(&a->trace)) ? kRcTraced : 0u);
               eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
                          static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
                          ((cp >> 32) & 1ull) == 0u &&
@@ -1375,6 +1411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
               unsigned long long wa5[5];
 #pragma unroll
               for (int k2 = 0; k2 < 5; ++k2) wa5[k2] = __shfl_sync(0xffffffffu, f_a[k2], win);
+              const unsigned wch = __shfl_sync(0xffffffffu, f_ch, win);
               if (lane == 0) {
                 if (stale) {
                   sh.rc.key = 0ull;  // recycled slot: fields reloaded below
@@ -1388,6 +1425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
                   sh.rc.slot = static_cast<unsigned>(key & 0xffffffull);
                   sh.rc.count = wcount;
                   sh.rc.gated = wgated;
+                  sh.rc.chain = wch;
                 }
               }
               break;
@@ -1409,6 +1447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
                 sh.rc.key = key;
                 sh.rc.count = ld_relaxed_gpu(&a->count);
                 sh.rc.gated = ld_relaxed_gpu(&a->paused) & kGatedBit;
+                sh.rc.chain = ld_relaxed_gpu(&a->chain) | (a->trace != nullptr ? kRcTraced : 0u);
               }
               const unsigned parts = sh.rc.cmd.parts;
               sh.rc.cmd.block = sh.rc.lo + off / parts;
@@ -1503,6 +1542,16 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
         }
         sh.go = go;
         sh.t_start = gtimer();
+#ifdef GPUOS_PROBE_HANDOFF
+        if (g_probe_cur[blockIdx.x][8] != 0ull) {
+          PROBE_AT(9);
+          const unsigned r = atomicAdd(&g_probe_n, 1u) & 4095u;
+          for (int i = 0; i < kProbeStamps; ++i) {
+            g_probe_ring[r][i] = g_probe_cur[blockIdx.x][i];
+            g_probe_cur[blockIdx.x][i] = 0ull;
+          }
+        }
+#endif
         if (go != kGoExit) {
           if (first_start == ~0ull) first_start = sh.t_start;
           red_relaxed_gpu_add(p.tpc_occ + tpc, 1u);  // utilisation sampler (OccSampler)
@@ -1522,6 +1571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
       tc_hold = false;
     }
     __syncthreads();
+    if (tid == 0) PROBE_AT(10);
     if (tid == 0) red_relaxed_gpu_add(p.tpc_occ + tpc, ~0u);  // -1: the block has ended
     // The leader records pair tiles (the peer's half is complete: cluster
     // barrier at the end of the body).
@@ -1548,6 +1598,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
 }
 
 __global__ void k_gtimer(unsigned long long* out) { *out = gtimer(); }
+
+#ifdef GPUOS_PROBE_HANDOFF
+extern "C" int gpuos_dev_probe_read(unsigned long long* out, unsigned* n) {
+  if (cudaMemcpyFromSymbol(n, g_probe_n, sizeof(unsigned)) != cudaSuccess) return -1;
+  return cudaMemcpyFromSymbol(out, g_probe_ring, sizeof(g_probe_ring)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // Packed GEMV weights (kGemvPacked): rows of 64 bf16; packed row
 // ((h nk + j) 128 + i) = W row 128 h + i, columns 64 j .. 64 j + 63, zero
