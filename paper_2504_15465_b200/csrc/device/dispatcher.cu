@@ -147,7 +147,6 @@ __device__ __forceinline__ unsigned tenant_of(unsigned long long count_paused) {
 constexpr unsigned kAuxChainHead = 0x80000000u;  // ring kFAux: parts | chain head | no early
 constexpr unsigned kAuxNoEarly = 0x40000000u;
 constexpr unsigned kNoEarly = 2u;                 // DevAtom::chain: GPUOS_ATOM_NO_EARLY
-constexpr unsigned kRcTraced = 0x80000000u;       // RoundCmd::chain only: the atom has a trace buffer
 
 struct DevCtl {
   unsigned quit;
@@ -605,7 +604,7 @@ struct RoundCmd {
   unsigned slot;
   unsigned count;               // slices of the atom (1: single-block fast path)
   unsigned gated;               // the atom was early-started: its body checks the gate
-  unsigned chain;               // DevAtom::chain (kChainHead | kNoEarly), read with the fields
+  unsigned pad;
 };
 constexpr int kRoundCmdWords64 = sizeof(RoundCmd) / 8;
 static_assert(sizeof(RoundCmd) % 8 == 0, "RoundCmd copied as 64-bit words");
@@ -644,7 +643,7 @@ struct PairRun {
 // A finished atom's bookkeeping held back while its handed-off successor
 // runs (account_block / write_done).
 struct PendingDone {
-  unsigned long long t0, t1, m0, m1;  // t0, m0, m1: single-slice atoms (else read here)
+  unsigned long long t0, t1, m0, m1, tag, ts, ta;  // t0, m0, m1: single-slice atoms (else read here)
   unsigned slot, tk, n, flags;                     // flags: kPendValid | kPendSingle
 };
 constexpr unsigned kPendValid = 1u, kPendSingle = 2u;
@@ -807,7 +806,7 @@ struct NextTile {
 // now holds block 0 of its chained successor, claimed for this worker).
 // A chained successor's hot-line fields (account_block).
 struct SuccFields {
-  unsigned long long count_paused, lo, body_parts, args[5], seq_prio, mask[2], trace;
+  unsigned long long count_paused, lo, body_parts, args[5], seq_prio, mask[2];
   __device__ __forceinline__ void load(const DevAtom* b) {
     unsigned long long claim;
     ld_relaxed_gpu_v2(b, claim, count_paused);
@@ -817,7 +816,6 @@ struct SuccFields {
     ld_relaxed_gpu_v2(&b->args[4], args[4], seq_prio);
     mask[0] = ld_relaxed_gpu64(&b->mask[0]);  // (+104: 8-byte aligned)
     mask[1] = ld_relaxed_gpu64(&b->mask[1]);
-    trace = ld_relaxed_gpu64(reinterpret_cast<const unsigned long long*>(&b->trace));
   }
 };
 
@@ -847,21 +845,17 @@ __device__ __forceinline__ void write_done(const Params& p, PendingDone& d, unsi
     const unsigned long long t0 = single ? d.t0 : ld_relaxed_gpu64(&a->t_first);
     const unsigned long long m0 = single ? d.m0 : ld_relaxed_gpu64(&a->touched[0]);
     const unsigned long long m1 = single ? d.m1 : ld_relaxed_gpu64(&a->touched[1]);
-    // (fixed for the atom's lifetime; loaded here, off the finisher's path)
-    const unsigned long long tag = a->tag;
-    const unsigned long long ts = ld_relaxed_gpu64(&a->t_seen);
-    const unsigned long long ta = ld_relaxed_gpu64(&a->t_armed);
     const unsigned tk = d.tk;
     const unsigned long long span = d.t1 - t0;
-    st_relaxed_sys_v4(rec->w + 0, d.n, static_cast<unsigned>(tag), static_cast<unsigned>(tag >> 32), tk);
+    st_relaxed_sys_v4(rec->w + 0, d.n, static_cast<unsigned>(d.tag), static_cast<unsigned>(d.tag >> 32), tk);
     st_relaxed_sys_v4(rec->w + 4, static_cast<unsigned>(t0), static_cast<unsigned>(t0 >> 32),
                       span > 0xffffffffull ? 0xffffffffu : static_cast<unsigned>(span), tk);
     st_relaxed_sys_v4(rec->w + 8, static_cast<unsigned>(m0), static_cast<unsigned>(m0 >> 32),
                       static_cast<unsigned>(m1), tk);
     // t_seen / t_armed as ns before t_first (0 in batch mode).
     st_relaxed_sys_v4(rec->w + 12, static_cast<unsigned>(m1 >> 32),
-                      ts ? static_cast<unsigned>(t0 - ts) : 0u,
-                      ta ? static_cast<unsigned>(t0 - ta) : 0u, tk);
+                      d.ts ? static_cast<unsigned>(t0 - d.ts) : 0u,
+                      d.ta ? static_cast<unsigned>(t0 - d.ta) : 0u, tk);
   }
   // Device-side bookkeeping after the record; the host recycles this slot
   // only after thousands of others, long after these land. Our key still
@@ -901,17 +895,25 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   // round trips less on every small kernel).
   const bool single = rc.count == 1u;
   unsigned long long s_t0 = t_start, s_t1 = 0;
-  // The chain word came with the atom's fields (RoundCmd::chain): a
-  // finisher goes from its count straight to the successor swap. (A chain
-  // head's registered successor is always taken by that swap; a look-ahead
-  // may mark the registration until then.)
-  unsigned chain = rc.chain;
+  // Fields fixed for the atom's lifetime, read by its finisher (for a
+  // single-slice atom up front, overlapping the accounting). A chain head's
+  // registered successor is always taken by the swap below (a look-ahead
+  // may mark the registration until then).
+  unsigned long long tag = 0, ts = 0, ta = 0;
+  unsigned chain = 0;
   SuccFields bf;
+  auto finisher_fields = [&] {
+    tag = a->tag;
+    ts = ld_relaxed_gpu64(&a->t_seen);
+    ta = ld_relaxed_gpu64(&a->t_armed);
+    chain = ld_acquire_gpu(&a->chain);
+  };
   if (lane == 0) {
     const unsigned long long t_end = gtimer();
     PROBE_AT(0);
     s_t1 = t_end;
-    if (chain & kRcTraced)
+    if (single) finisher_fields();
+    if (a->trace != nullptr)
       atomicAdd(a->trace + rc.cmd.block * rc.cmd.parts + rc.cmd.part, 0x10000u + sm + 1u);
     busy += t_end - t_start;
     n_blocks += 1u + extra;
@@ -941,6 +943,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       last = atom_add_acq_rel32(&a->done, 1u + extra) + 1u + extra == rc.count;
       if (last) {
         s_t1 = gtimer();  // every block has ended (each counted after its end)
+        finisher_fields();
       }
     }
   }
@@ -963,6 +966,7 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   int handoff = 0;
   unsigned look = 0;  // lane 0: successor's successor armed early (slot + 1)
   unsigned long long look_m0 = 0, look_m1 = 0;  // lane 0: its TPC set
+  chain = __shfl_sync(0xffffffffu, chain, 0);
   if (chain & kChainHead) {
     unsigned next = 0;
     if (lane == 0) {
@@ -976,14 +980,11 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
       // successor are loaded together (one L2 round trip, not four in a
       // row): this chain is the gap between two dependent kernels.
       int floor_prio = 0;
-      unsigned cn = 0, b_chain = 0;
+      unsigned cn = 0;
       if (next != 0u) {
         bf.load(p.atoms + (next - 1u));
         floor_prio = ld_relaxed_gpu_s32(p.fence + tpc);
-        const unsigned long long b_cs =
-            ld_acquire_gpu64(reinterpret_cast<const unsigned long long*>(&p.atoms[next - 1u].chain));
-        cn = static_cast<unsigned>(b_cs >> 32);  // b's registered successor
-        b_chain = static_cast<unsigned>(b_cs);
+        cn = ld_acquire_gpu(&p.atoms[next - 1u].succ);
       }
       if (next != 0u && (look_armed || ((bf.count_paused >> 32) & kGatedBit))) {
         // Early-started successor (at ingest, or by a look-ahead -- wait for
@@ -1057,7 +1058,6 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
           ho.slot = next - 1u;
           ho.count = bcount;
           ho.gated = 0u;  // armed by this finisher: not early
-          ho.chain = b_chain | (bf.trace ? kRcTraced : 0u);
           if (bcount == 1u) next = 0;  // nothing left for other workers: no wake-up
         }
       }
@@ -1081,11 +1081,11 @@ __device__ __forceinline__ int account_block(const Params& p, RoundCmd& rc,
   flush_pending(p, pend, lane);
   if (lane == 0) {
     PROBE_AT(6);
-    // Outputs before the record. A handed-off successor's accounting
-    // writes this record later, after its own acq_rel count / swap or
-    // fence, which orders these outputs too.
-    if (single && (chain & kChainHead) && !handoff) __threadfence();
+    if (single && (chain & kChainHead)) __threadfence();  // outputs before the record
     pend.slot = rc.slot;
+    pend.tag = tag;
+    pend.ts = ts;
+    pend.ta = ta;
     pend.tk = ~static_cast<unsigned>(rc.key >> 24);
     pend.n = rc.count / rc.cmd.parts;
     pend.t0 = s_t0;
@@ -1320,7 +1320,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
             const unsigned long long k = ld_acquire_gpu64(list + lane);
             bool eligible = false;
             unsigned long long f_lo = 0, f_bp = 0, f_cp = 0, f_cw = 0, f_a[5] = {0, 0, 0, 0, 0};
-            unsigned f_ch = 0;
             if (k != 0ull) {
               const DevAtom* a = p.atoms + (k & 0xffffffull);
               unsigned long long cw, cp;
@@ -1331,8 +1330,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
               ld_relaxed_gpu_v2(&a->args[0], f_a[0], f_a[1]);
               ld_relaxed_gpu_v2(&a->args[2], f_a[2], f_a[3]);
               f_a[4] = ld_relaxed_gpu64(&a->args[4]);
-              f_ch = ld_relaxed_gpu(&a->chain) |
-                     (ld_relaxed_gpu64(reinterpret_cast<const unsigned long long*>(&a->trace)) ? kRcTraced : 0u);
               eligible = static_cast<unsigned>(cw >> 32) == ~static_cast<unsigned>(k >> 24) &&
                          static_cast<unsigned>(cw) < static_cast<unsigned>(cp) &&
                          ((cp >> 32) & 1ull) == 0u &&
@@ -1411,7 +1408,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
               unsigned long long wa5[5];
 #pragma unroll
               for (int k2 = 0; k2 < 5; ++k2) wa5[k2] = __shfl_sync(0xffffffffu, f_a[k2], win);
-              const unsigned wch = __shfl_sync(0xffffffffu, f_ch, win);
               if (lane == 0) {
                 if (stale) {
                   sh.rc.key = 0ull;  // recycled slot: fields reloaded below
@@ -1425,7 +1421,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
                   sh.rc.slot = static_cast<unsigned>(key & 0xffffffull);
                   sh.rc.count = wcount;
                   sh.rc.gated = wgated;
-                  sh.rc.chain = wch;
                 }
               }
               break;
@@ -1447,7 +1442,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
                 sh.rc.key = key;
                 sh.rc.count = ld_relaxed_gpu(&a->count);
                 sh.rc.gated = ld_relaxed_gpu(&a->paused) & kGatedBit;
-                sh.rc.chain = ld_relaxed_gpu(&a->chain) | (a->trace != nullptr ? kRcTraced : 0u);
               }
               const unsigned parts = sh.rc.cmd.parts;
               sh.rc.cmd.block = sh.rc.lo + off / parts;
