@@ -337,6 +337,12 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
             "serial_roundtrip_us_p50": probe["serial_roundtrip_ns"]["p50"] / 1e3,
             "publish_to_first_block_us_p50": probe["publish_to_first_block_ns"]["p50"] / 1e3,
             "pipelined_ns_per_atom": probe["pipelined_ns_per_atom"],
+            # publish -> first block split on the device clock: ring entry seen by
+            # the ingest warp -> armed (slot, keys, wake-ups) -> first block start
+            "ingest_to_armed_us_p50": probe["device_ingest_to_armed_ns_p50"] / 1e3,
+            "armed_to_first_block_us_p50": probe["device_armed_to_first_block_ns_p50"] / 1e3,
+            "publish_to_ingest_us_p50": probe["host_submit_to_device_ingest_ns_p50_offset_sensitive"] / 1e3,
+            "last_block_to_host_us_p50": probe["last_block_to_host_ns"]["p50"] / 1e3,
             "note": "empty one-block atoms through the live ring (gpuos_probe_dispatch)"},
         "cpu_baseline": cpu_baseline([cfg]) if world == 1 else None,
         "e2e": {"value": e2e_atoms_all / e2e_s_max, "unit": "BE atoms/s",

@@ -481,6 +481,7 @@ int gpuos_probe_dispatch(const char* opts_json, char** result_json) {
     gpuos_dev_config cfg{};
     cfg.device_ordinal = o.value("device", 0);
     cfg.workers_per_sm = o.value("workers_per_sm", 2);
+    cfg.idle_sleep_ns = o.value("idle_sleep_ns", 0);  // 0: the default
     gpuos_dev* d = nullptr;
     if (gpuos_dev_open(&cfg, &d) != GPUOS_OK) throw InvariantError(gpuos_dev_last_error());
     std::unique_ptr<gpuos_dev, int (*)(gpuos_dev*)> guard(d, gpuos_dev_close);
