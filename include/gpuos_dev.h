@@ -181,7 +181,8 @@ typedef struct gpuos_dev_stats {
                                 tpc_busy_integral, device.cpp:264-275),
                                 sampled on the device by the ingest warp  */
   uint32_t fault;            /* last run's device fault code (0: none;
-                                1: a pipeline wait expired)               */
+                                1: a pipeline wait expired; 2: a 2-SM
+                                block claimed by a pair's second CTA)     */
   uint32_t reserved;
 } gpuos_dev_stats;
 

@@ -1465,8 +1465,15 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
             spread_since = 0;
             go = body_is_pair(cur_body) ? kGoPair : kGoOwn;
             // A peer reaches a 2-SM block only by adopting a recycled slot
-            // (stale claim, see claim_block): it cannot run it alone.
-            if (go == kGoPair && rank != 0) asm volatile("trap;");
+            // (stale claim, see claim_block): it cannot run it alone. A device
+            // fault the host's stop reports, not a context-killing trap.
+            if (go == kGoPair && rank != 0) {
+              if (lane == 0) {
+                atomicCAS(&p.ctl->fault, 0u, kFaultAdoptedPair);
+                atomicExch(&p.ctl->quit, 1u);
+              }
+              go = kGoExit;
+            }
             break;
           }
           // Idle: wait for this TPC's candidate set to change (acquire: a
@@ -1854,7 +1861,9 @@ int collect_run(gpuos_dev* d, float ms, DevCtl& ctl) {
 }
 
 const char* fault_name(unsigned f) {
-  return f == 1u ? "a tensor-core pipeline wait expired (pipeline_timeout_ms)" : "unknown fault";
+  return f == kFaultPipeline      ? "a tensor-core pipeline wait expired (pipeline_timeout_ms)"
+         : f == kFaultAdoptedPair ? "a 2-SM block was claimed by a pair's second CTA (recycled atom slot)"
+                                  : "unknown fault";
 }
 
 // UMMA N for a pair tile over `cols` output columns: 64, 128 or 256.

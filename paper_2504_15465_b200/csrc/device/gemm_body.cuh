@@ -71,7 +71,8 @@ struct WaitGuard {
   unsigned* quit;               // DevCtl::quit
   unsigned long long bound_ns;  // per wait
 };
-constexpr unsigned kFaultPipeline = 1u;  // an mbarrier wait expired
+constexpr unsigned kFaultPipeline = 1u;     // an mbarrier wait expired
+constexpr unsigned kFaultAdoptedPair = 2u;  // a peer CTA claimed a 2-SM block (dispatcher.cu)
 __device__ __forceinline__ void raise_fault(const WaitGuard& g, unsigned code) {
   atomicCAS(g.fault, 0u, code);
   atomicExch(g.quit, 1u);
