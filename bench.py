@@ -289,7 +289,7 @@ def ours(args, cfg: dict, rank: int, world: int, local: int) -> None:
     sat_gemv = guarded(lambda: gemv_saturation(api, local, args))
     sat_conv = guarded(lambda: conv_saturation(api, local, args))
     rsz = guarded(lambda: right_sizing_summary(local, args)) if rank == 0 else None
-    cfgs = guarded(lambda: isolated("model_configs", local, 900)) if (rank == 0 and not args.skip_configs) else None
+    cfgs = guarded(lambda: model_configs_isolated(local)) if (rank == 0 and not args.skip_configs) else None
     pols = guarded(lambda: policy_rows(local)) if (rank == 0 and not args.skip_configs) else None
     probe = api.probe_dispatch(device=local, workers_per_sm=args.workers_per_sm, serial=2000,
                                pipelined=20000, depth=16)
@@ -405,13 +405,14 @@ def live_traffic(key: str = "dram"):
     return t["dram_read"] + t["dram_write"] if key == "dram" else t[key]
 
 
-def isolated(fn_name: str, local: int, timeout_s: float):
-    """Runs bench.<fn_name>(local) in a child process bounded by timeout_s
-    (the model-config runs are the longest secondary measurements; a hang
-    there must not cost the bench line). The parent holds no dispatcher
-    meanwhile, so the child has the GPU."""
+def isolated(fn_name: str, local: int, timeout_s: float, *extra):
+    """Runs bench.<fn_name>(local, *extra) in a child process bounded by
+    timeout_s (the model-config runs are the longest secondary measurements;
+    a hang there must not cost the bench line). The parent holds no
+    dispatcher meanwhile, so the child has the GPU."""
+    call_args = ", ".join([repr(local)] + [repr(x) for x in extra])
     code = (f"import json, sys; sys.path.insert(0, {ROOT!r}); import bench; "
-            f"print('@@' + json.dumps(bench.{fn_name}({local})))")
+            f"print('@@' + json.dumps(bench.{fn_name}({call_args})))")
     try:
         p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout_s,
                            cwd=ROOT)
@@ -490,32 +491,57 @@ def policy_rows(local: int) -> dict:
     return r
 
 
-def model_configs(local: int) -> dict:
-    """BASELINE configs #2 and #3 on model kernel traces (configs.py)."""
-    from paper_2504_15465_b200 import configs
+MODEL_CONFIGS = ("infer4", "hybrid", "hybrid_real_attention")
+MODEL_CONFIGS_NOTE = (
+    "#2: 2x ResNet-50 b1 (150 rps) + 2x BERT-base b8 (100 rps), LC, Poisson, beside a "
+    "ResNet-50 b256 training tenant (BE, closed loop), 2 s x 4 runs; #3: Llama-3-8B decode LC "
+    "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 10 runs (~580 tokens; 6 for the real-attention line); decode "
+    "RMSNorm / SiLU-mul as tenant bodies, attention as a byte-equivalent STREAM kernel "
+    "(hybrid) or the attn_decode_bf16 tenant body (hybrid_real_attention); "
+    "alone = the same scenario with the other tenants silent; static = each tenant on its "
+    "quota (no stealing, atomizer or sharing); BE throughput = executed work (blocks x "
+    "calibrated block time) per second; random-init weights, live on the persistent dispatcher")
 
-    out = {}
-    # infer4: 2 s x 4 runs = 1200 / 800 requests per ResNet / BERT tenant
-    # (nearest-rank p99 over >= 800 samples), alone runs likewise.
+
+def model_config(local: int, name: str) -> dict:
+    """One of BASELINE configs #2 / #3 on model kernel traces (configs.py)."""
+    from paper_2504_15465_b200 import configs
     from paper_2504_15465_b200 import workloads as wl
 
-    for name, horizon, reps, cfg in (("infer4", 2000.0, 4, None), ("hybrid", 1000.0, 10, None),
-                                     ("hybrid_real_attention", 1000.0, 6, wl.hybrid(1000.0, real_attention=True))):
-        r = configs.run("hybrid" if cfg is not None else name, horizon_ms=horizon, reps=reps, device=local, cfg=cfg)
-        out[name] = {"tpc_utilization": r["tpc_utilization"], "apps": {
-            a: {k: v for k, v in row.items() if k in ("priority", "p99_vs_alone", "slo_attainment",
-                                                        "throughput_vs_static", "iterations_vs_static")}
-            | {"p99_ms": row["stacked"].get("p99_ms"), "alone_p99_ms": row["alone"].get("p99_ms"),
-               "per_s": row["stacked"].get("per_s"), "completed": row["stacked"].get("completed")}
-            for a, row in r["apps"].items()}, "knobs": r["knobs"]}
-    out["note"] = ("#2: 2x ResNet-50 b1 (150 rps) + 2x BERT-base b8 (100 rps), LC, Poisson, beside a "
-                   "ResNet-50 b256 training tenant (BE, closed loop), 2 s x 4 runs; #3: Llama-3-8B decode LC "
-                   "(60 tokens/s Poisson) + ResNet-50 b256 training BE (closed loop), 1 s x 10 runs (~580 tokens; 6 for the real-attention line); decode "
-                   "RMSNorm / SiLU-mul as tenant bodies, attention as a byte-equivalent STREAM kernel "
-                   "(hybrid) or the attn_decode_bf16 tenant body (hybrid_real_attention); "
-                   "alone = the same scenario with the other tenants silent; static = each tenant on its "
-                   "quota (no stealing, atomizer or sharing); BE throughput = executed work (blocks x "
-                   "calibrated block time) per second; random-init weights, live on the persistent dispatcher")
+    # infer4: 2 s x 4 runs = 1200 / 800 requests per ResNet / BERT tenant
+    # (nearest-rank p99 over >= 800 samples), alone runs likewise.
+    horizon, reps, cfg = {"infer4": (2000.0, 4, None), "hybrid": (1000.0, 10, None),
+                          "hybrid_real_attention": (1000.0, 6, wl.hybrid(1000.0, real_attention=True))}[name]
+    r = configs.run("hybrid" if cfg is not None else name, horizon_ms=horizon, reps=reps, device=local, cfg=cfg)
+    return {"tpc_utilization": r["tpc_utilization"], "apps": {
+        a: {k: v for k, v in row.items() if k in ("priority", "p99_vs_alone", "slo_attainment",
+                                                    "throughput_vs_static", "iterations_vs_static")}
+        | {"p99_ms": row["stacked"].get("p99_ms"), "alone_p99_ms": row["alone"].get("p99_ms"),
+           "per_s": row["stacked"].get("per_s"), "completed": row["stacked"].get("completed")}
+        for a, row in r["apps"].items()}, "knobs": r["knobs"]}
+
+
+def model_configs(local: int) -> dict:
+    """BASELINE configs #2 and #3, in this process (tools/hang_hunt2.py)."""
+    out = {name: model_config(local, name) for name in MODEL_CONFIGS}
+    out["note"] = MODEL_CONFIGS_NOTE
+    return out
+
+
+def model_configs_isolated(local: int) -> dict:
+    """Each config in its own child process (~50-70 s each); a config whose
+    run fails (a device fault aborts that process's runs) is measured once
+    more in a fresh process, and the first error is kept beside the result."""
+    out = {}
+    for name in MODEL_CONFIGS:
+        r = isolated("model_config", local, 300, name)
+        if "error" in r and "exceeded" not in r["error"]:  # (a hang is not retried)
+            first = r["error"]
+            again = isolated("model_config", local, 300, name)
+            r = ({"error": first, "retry_error": again["error"]} if "error" in again
+                 else dict(again, first_attempt_error=first))
+        out[name] = r
+    out["note"] = MODEL_CONFIGS_NOTE
     return out
 
 
