@@ -164,6 +164,7 @@ struct DevCtl {
   unsigned idle_leaders;               // leaders waiting with nothing eligible
   unsigned fault;                      // first device fault (kFault*; 0: none)
   unsigned pad2;
+  unsigned long long fault_info[5];    // raise_fault (gemm_body.cuh): where it was raised
 };
 
 // 128-byte submit-ring entry: four 32-byte sectors, each = 7 data words +
@@ -1197,7 +1198,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
   GemvPipe gemv;
   gemv_pipe_init(gemv, dsmem, p.smem_bytes, p.tmem_cols, tid);
   if (tid == 0) {
-    sh.guard = WaitGuard{&p.ctl->fault, &p.ctl->quit, p.wait_bound_ns};
+    sh.guard = WaitGuard{&p.ctl->fault, &p.ctl->quit, p.wait_bound_ns, p.ctl->fault_info,
+                         reinterpret_cast<const unsigned long long*>(&sh.rc)};
     sh.pend.flags = 0u;
     sh.run.posts = 0u;
   }
@@ -1468,10 +1470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(104) k_worker(const __grid
             // (stale claim, see claim_block): it cannot run it alone. A device
             // fault the host's stop reports, not a context-killing trap.
             if (go == kGoPair && rank != 0) {
-              if (lane == 0) {
-                atomicCAS(&p.ctl->fault, 0u, kFaultAdoptedPair);
-                atomicExch(&p.ctl->quit, 1u);
-              }
+              if (lane == 0) raise_fault(sh.guard, kFaultAdoptedPair);
               go = kGoExit;
             }
             break;
@@ -1864,6 +1863,19 @@ const char* fault_name(unsigned f) {
   return f == kFaultPipeline      ? "a tensor-core pipeline wait expired (pipeline_timeout_ms)"
          : f == kFaultAdoptedPair ? "a 2-SM block was claimed by a pair's second CTA (recycled atom slot)"
                                   : "unknown fault";
+}
+
+// The fault and where the device raised it (DevCtl::fault_info).
+std::string fault_text(const DevCtl& c) {
+  char where[256];
+  std::snprintf(where, sizeof where,
+                " [sm %u rank %u thread %u, barrier smem+0x%x parity %u, block %lld of desc 0x%llx, body %u slice %u]",
+                static_cast<unsigned>(c.fault_info[0] & 0xffffu), static_cast<unsigned>((c.fault_info[0] >> 16) & 0xffffu),
+                static_cast<unsigned>(c.fault_info[0] >> 32), static_cast<unsigned>(c.fault_info[1] & 0xffffffffu),
+                static_cast<unsigned>(c.fault_info[1] >> 32), static_cast<long long>(c.fault_info[3]),
+                static_cast<unsigned long long>(c.fault_info[2]), static_cast<unsigned>(c.fault_info[4] & 0xffffffffu),
+                static_cast<unsigned>(c.fault_info[4] >> 32));
+  return std::string(fault_name(c.fault)) + where;
 }
 
 // UMMA N for a pair tile over `cols` output columns: 64, 128 or 256.
@@ -2288,7 +2300,7 @@ int gpuos_dev_stop(gpuos_dev* d, int drain, float* elapsed_ms) {
   if (const int crc = collect_run(d, ms, ctl); crc != GPUOS_OK) return crc;
   d->stats.ingest_entries += static_cast<int64_t>(*d->consumed_h);
   if (ctl.fault != 0u)
-    return fail(GPUOS_E_TIMEOUT, std::string("device fault: ") + fault_name(ctl.fault));
+    return fail(GPUOS_E_TIMEOUT, std::string("device fault: ") + fault_text(ctl));
   if (drain && ctl.outstanding != 0)
     return fail(GPUOS_E_INVARIANT, "drained with atoms outstanding");
   return GPUOS_OK;
@@ -2431,7 +2443,7 @@ int gpuos_dev_run_batch(gpuos_dev* d, const gpuos_atom_desc* descs, int32_t n, f
   DevCtl after{};
   if (const int crc = collect_run(d, ms, after); crc != GPUOS_OK) return crc;
   if (after.fault != 0u)
-    return fail(GPUOS_E_TIMEOUT, std::string("device fault: ") + fault_name(after.fault));
+    return fail(GPUOS_E_TIMEOUT, std::string("device fault: ") + fault_text(after));
   if (after.outstanding != 0) return fail(GPUOS_E_INVARIANT, "batch finished with atoms outstanding");
   return GPUOS_OK;
 }
@@ -2654,10 +2666,10 @@ int gpuos_dev_poll(gpuos_dev* d, gpuos_completion* out, int32_t max) {
       d->exit_check_ns = now;
       const cudaError_t q = cudaStreamQuery(d->s_work);
       if (q != cudaErrorNotReady) {
-        unsigned fault = 0;
-        cudaMemcpy(&fault, &d->ctl->fault, sizeof fault, cudaMemcpyDeviceToHost);
-        if (fault != 0u)
-          return fail(GPUOS_E_TIMEOUT, std::string("dispatcher stopped on a device fault: ") + fault_name(fault));
+        DevCtl c{};
+        cudaMemcpy(&c, d->ctl, sizeof c, cudaMemcpyDeviceToHost);
+        if (c.fault != 0u)
+          return fail(GPUOS_E_TIMEOUT, std::string("dispatcher stopped on a device fault: ") + fault_text(c));
         return fail(GPUOS_E_INVARIANT, q == cudaSuccess ? "dispatcher exited with atoms in flight"
                                                         : std::string("dispatcher failed: ") + cudaGetErrorString(q));
       }

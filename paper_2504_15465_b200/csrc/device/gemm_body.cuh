@@ -70,11 +70,28 @@ struct WaitGuard {
   unsigned* fault;              // DevCtl::fault (0: none)
   unsigned* quit;               // DevCtl::quit
   unsigned long long bound_ns;  // per wait
+  unsigned long long* info;     // DevCtl::fault_info: where the first fault was raised
+  const unsigned long long* ctx;  // the CTA's current block command (RoundCmd words)
 };
 constexpr unsigned kFaultPipeline = 1u;     // an mbarrier wait expired
 constexpr unsigned kFaultAdoptedPair = 2u;  // a peer CTA claimed a 2-SM block (dispatcher.cu)
-__device__ __forceinline__ void raise_fault(const WaitGuard& g, unsigned code) {
-  atomicCAS(g.fault, 0u, code);
+// The first fault also records where it was raised (host error text):
+// SM, cluster rank, thread, the barrier's shared-memory offset and parity,
+// and the block being run (descriptor args[0], block index, body | slice).
+__device__ __noinline__ void raise_fault(const WaitGuard& g, unsigned code, unsigned bar = 0u,
+                                            unsigned parity = 0u) {
+  if (atomicCAS(g.fault, 0u, code) == 0u && g.info != nullptr) {
+    unsigned sm, crank;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    g.info[0] = sm | (static_cast<unsigned long long>(crank) << 16) |
+                (static_cast<unsigned long long>(threadIdx.x) << 32);
+    g.info[1] = bar | (static_cast<unsigned long long>(parity) << 32);
+    g.info[2] = g.ctx ? g.ctx[0] : 0ull;
+    g.info[3] = g.ctx ? g.ctx[5] : 0ull;
+    g.info[4] = g.ctx ? g.ctx[6] : 0ull;
+    __threadfence();
+  }
   atomicExch(g.quit, 1u);
 }
 struct GemmPipe {
@@ -114,7 +131,7 @@ __device__ __forceinline__ void mbar_wait_bounded(unsigned long long* b, unsigne
       if (t0 == 0) {
         t0 = t;
       } else if (t - t0 > g.bound_ns) {
-        raise_fault(g, kFaultPipeline);
+        raise_fault(g, kFaultPipeline, a, parity);
         return;
       }
     }
