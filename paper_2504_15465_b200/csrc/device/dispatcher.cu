@@ -771,6 +771,9 @@ struct NextTile {
   int tpc;
   unsigned sm;
   __device__ __forceinline__ void operator()(bool stop = false) const {
+#ifdef GPUOS_NO_PAIR_RUNS
+    stop = true;  // diagnostic builds: every pair tile is a run of one
+#endif
     long long nb = -1;
     DevAtom* a = run.atom;
     if (!stop && a != nullptr && ld_acquire_gpu(p.version + tpc) == run.ver) {
